@@ -1,0 +1,117 @@
+/* fdmd.h — C ABI of the B200-native DMD hot path (libfdmd.so).
+ *
+ * The reference (`flowdmd`, arXiv 2502.05339) is pure Python over
+ * numpy/LAPACK; its hot path has no FFI of its own. Each entry point below
+ * replaces the numpy/LAPACK call sites the reference makes on that path
+ * (file:line relative to /root/reference/pkg/src/flowdmd/):
+ *
+ *   fdmd_tall_gemm     M @ G, M @ W (linalg.py:82,85), Q @ Ub (linalg.py:88),
+ *                      Xp @ (V/S) and P @ W (dmd.py:255,258), U @ B.T (dmd.py:414)
+ *                      — and the CholeskyQR replacement of np.linalg.qr (linalg.py:82,85)
+ *   fdmd_tall_gram     M.conj().T @ Q (linalg.py:84), Q.conj().T @ M (linalg.py:86),
+ *                      U.conj().T @ P (dmd.py:256); Gram Y^T Y of CholeskyQR2
+ *   fdmd_colmajor_dot  pinv(phi) @ u (runtime.py:52,199), pinv(phi) @ B_i (dmd.py:489)
+ *   fdmd_decode        cols @ coeff / (phi @ z).real (runtime.py:88-99) — batched
+ *   fdmd_table_apply   decode_table() column construction (dmd.py:92-120) and the
+ *                      normalise/phase-canonicalise step of _order_and_pair (dmd.py:191-206)
+ *   fdmd_residual      provenance["residual"] (dmd.py:269-272)
+ *   fdmd_geev          np.linalg.eig in eig_small (linalg.py:120) — cuSOLVER Xgeev
+ *   fdmd_synth3d       BASELINE.json configs 1-4 snapshot generator (device)
+ *
+ * Conventions: every pointer argument is DEVICE memory unless named *_host;
+ * `stream` is a cudaStream_t (NULL = legacy default stream). Calls are
+ * asynchronous on `stream` except fdmd_geev (returns after the solve).
+ * Status: 0 = OK; negative = error, message via fdmd_last_error() (thread-local).
+ * There is no CPU fallback: without a CUDA device every compute call fails
+ * with FDMD_ERR_CUDA.
+ */
+#ifndef FDMD_H_
+#define FDMD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDMD_OK 0
+#define FDMD_ERR_INVALID (-1)     /* maps to ValueError */
+#define FDMD_ERR_CUDA (-2)        /* CUDA runtime failure */
+#define FDMD_ERR_SOLVER (-3)      /* cuSOLVER failure -> ConvergenceError */
+#define FDMD_ERR_WORKSPACE (-4)   /* workspace too small */
+
+#define FDMD_F32 0
+#define FDMD_F64 1
+#define FDMD_ROW 0 /* element (i, k) at p[i*ld + k] */
+#define FDMD_COL 1 /* element (i, k) at p[k*ld + i] */
+
+int fdmd_version(void);
+const char* fdmd_last_error(void);
+int fdmd_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* C[n x N] = A[n x K] * B[K x N]. A: f32/f64, ROW/COL. B: f64 row-major (ld ldb).
+ * C: f32/f64 ROW/COL, may be NULL (statistics only). FP64 DMMA accumulation.
+ * pair_stats (optional, length 3*(N/2), N even): for unit u = columns (2u, 2u+1)
+ * read as (Re, Im): [sum_i |c_i|^2, max_i |c_i|^2, first argmax i + row_offset]. */
+size_t fdmd_tall_gemm_workspace(int64_t n, int N);
+int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda,
+                   const double* B, int64_t ldb,
+                   void* C, int c_dtype, int c_layout, int64_t ldc,
+                   int64_t n, int K, int N,
+                   double* pair_stats, int64_t row_offset,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* C[K1 x K2] (f64 row-major, ld ldc) = beta*C + A[n x K1]^T B[n x K2].
+ * Deterministic fixed-order split reduction. symmetric=1 requires A==B, K1==K2. */
+size_t fdmd_tall_gram_workspace(int64_t n, int K1, int K2);
+int fdmd_tall_gram(const void* A, int a_dtype, int a_layout, int64_t lda,
+                   const void* B, int b_dtype, int b_layout, int64_t ldb,
+                   double* C, int64_t ldc, double beta,
+                   int64_t n, int K1, int K2, int symmetric,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* Reconstruction: out[f*ldo + i] = sum_k D[k*ldd + i] * coef[k*ldcoef + f]
+ * for f < B frames, i < n rows, k < r table columns. D, coef, out share dtype. */
+int fdmd_decode(const void* D, int dtype, int64_t ldd, const void* coef, int ldcoef,
+                void* out, int64_t ldo, int64_t n, int r, int B, void* stream);
+
+/* y[k*nv + v] = sum_i D[k*ldd + i] * U[v*ldu + i]  (k < r, v < nv <= 8), f64 out. */
+size_t fdmd_colmajor_dot_workspace(int64_t n, int r, int nv);
+int fdmd_colmajor_dot(const void* D, int d_dtype, int64_t ldd,
+                      const void* U, int u_dtype, int64_t ldu,
+                      int64_t n, int r, int nv, double* y,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* D[j*ldd + i] = alpha[j]*R[(2*src[j])*ldr + i] + beta[j]*R[(2*src[j]+1)*ldr + i]. */
+int fdmd_table_apply(const void* R, int r_dtype, int64_t ldr, const int* src,
+                     const double* alpha, const double* beta,
+                     void* D, int d_dtype, int64_t ldd, int64_t n, int ncols, void* stream);
+
+/* out[0] = sum_i sum_{j<T} (S[i*lds + 1 + j] - sum_k D[k*ldd+i] F[k*T+j])^2,
+ * out[1] = sum_i sum_{j<T} S[i*lds + 1 + j]^2  (out: 2 doubles, device). */
+size_t fdmd_residual_workspace(int64_t n);
+int fdmd_residual(const void* S, int s_dtype, int64_t lds, const void* D, int d_dtype, int64_t ldd,
+                  const double* F, int r, int T, int64_t n, double* out,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* Real nonsymmetric eigendecomposition (cuSOLVER Xgeev). A: n x n column-major
+ * f64 (overwritten). Outputs: w_host (2n doubles: re, im interleaved),
+ * vr_host (n x n column-major, LAPACK packing: a complex pair occupies columns
+ * j (real part) and j+1 (imaginary part)). Synchronous. */
+int fdmd_geev(int n, double* A, double* w_host, double* vr_host, void* stream);
+
+/* Pitched 2-D copy (cudaMemcpy2DAsync; kind = cudaMemcpyKind, 4 = default/UVA):
+ * uploads a host n x m snapshot block into a padded row-major device buffer. */
+int fdmd_copy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
+                int kind, void* stream);
+
+/* Synthetic separable 3D snapshots (see synth.py). Tables f64 on device. */
+int fdmd_synth3d(const double* sx, const double* sy, const double* sz, const double* Am,
+                 int K, int C, int N, int m, double noise, uint64_t key,
+                 int64_t row0, int64_t rows, void* out, int out_dtype, int64_t ldo, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDMD_H_ */

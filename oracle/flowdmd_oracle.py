@@ -1,0 +1,501 @@
+"""CPU oracle for the DMD hot path — TEST INFRASTRUCTURE ONLY.
+
+This module restates, in numpy, the reference algorithm of `flowdmd`
+(arXiv 2502.05339 reference package, `/root/reference/pkg/src/flowdmd`).
+It is the checker for the CUDA path; nothing in `paper_2502_05339_b200`
+imports it. Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s
+CPU-baseline leg may use it.
+
+Pinning: `tests/test_oracle_golden.py` checks every function here against
+golden vectors produced by running the *real* reference in the build
+container (`oracle/gen_golden.py`, fixtures under `tests/golden/`), so the
+oracle is pinned, not self-referential. The control-augmented DMDc fit
+(`dmdc_fit`) has no reference implementation and is marked
+"parity unpinned" below.
+
+Every function cites the reference file:line it restates (paths relative to
+`/root/reference/pkg/src/flowdmd/`).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+# Thresholds restated from the reference (dmd.py:22-23, runtime.py:18-19).
+UNSTABLE_MODULUS = 1.05
+SIGMA_CUTOFF = 1e-14
+INVERSE_FLOOR = 1e-8
+EXP_OVERFLOW = 700.0
+
+
+class OracleConvergenceError(RuntimeError):
+    pass
+
+
+# --------------------------------------------------------------------------
+# linalg.py
+# --------------------------------------------------------------------------
+
+def canonicalize_columns(U, V):
+    """linalg.py:29-44 — per column, divide U[:,k] and V[:,k] by the unit
+    phase of U's first largest-magnitude entry."""
+    U = np.array(U, copy=True)
+    V = np.array(V, copy=True)
+    piv_rows = np.argmax(np.abs(U), axis=0)            # first maximum, like np.argmax per column
+    for k, i in enumerate(piv_rows):
+        p = U[i, k]
+        a = abs(p)
+        if a == 0.0:
+            continue
+        ph = p / a
+        U[:, k] /= ph
+        V[:, k] /= ph
+    return U, V
+
+
+def dense_truncated_svd(M, r):
+    """linalg.py:47-59 — top-r factors of a dense SVD, canonicalized."""
+    M = np.asarray(M)
+    if not 1 <= r <= min(M.shape):
+        raise ValueError("rank out of range")
+    U, s, Vh = np.linalg.svd(M, full_matrices=False)
+    U, V = canonicalize_columns(U[:, :r], Vh[:r].conj().T)
+    return U, s[:r].copy(), V
+
+
+def sketch_svd(M, r, p, q, seed, omega=None):
+    """linalg.py:62-90 — Gaussian range finder with q re-orthonormalised
+    power passes (Householder QR), projection, small SVD, lift, canonicalize.
+
+    `omega` may be supplied (cols x (r+p)); otherwise it is drawn exactly as
+    linalg.py:80-81 does: default_rng(seed).standard_normal((cols, r+p)).
+    """
+    M = np.asarray(M)
+    rows, cols = M.shape
+    l = r + p
+    if not 1 <= r <= min(rows, cols):
+        raise ValueError("rank out of range")
+    if l > min(rows, cols):
+        raise ValueError("rank + oversample exceeds min dimension")
+    G = draw_omega(cols, l, seed) if omega is None else np.asarray(omega)
+    Q = np.linalg.qr(M @ G)[0]
+    for _ in range(q):
+        W = np.linalg.qr(M.conj().T @ Q)[0]
+        Q = np.linalg.qr(M @ W)[0]
+    B = Q.conj().T @ M
+    Ub, s, Vh = np.linalg.svd(B, full_matrices=False)
+    U, V = canonicalize_columns((Q @ Ub)[:, :r], Vh[:r].conj().T)
+    return U, s[:r].copy(), V
+
+
+def draw_omega(cols, l, seed):
+    """linalg.py:80-81 — the Gaussian test matrix, float64, host-drawn."""
+    return np.random.default_rng(seed).standard_normal((cols, l))
+
+
+def pinv_svd(M, rel_tol=1e-12):
+    """linalg.py:93-104 — SVD pseudo-inverse dropping s < rel_tol*s_max."""
+    M = np.asarray(M)
+    U, s, Vh = np.linalg.svd(M, full_matrices=False)
+    if s.size == 0 or s[0] == 0.0:
+        return np.zeros((M.shape[1], M.shape[0]), dtype=M.dtype)
+    inv = np.where(s > rel_tol * s[0], 1.0 / np.where(s > 0, s, 1.0), 0.0)
+    return (Vh.conj().T * inv) @ U.conj().T
+
+
+def eig_checked(M):
+    """linalg.py:107-133 — eig with unit-norm vectors and residual check."""
+    w, V = np.linalg.eig(M)
+    nv = np.linalg.norm(V, axis=0)
+    nv[nv == 0.0] = 1.0
+    V = V / nv
+    scale = np.linalg.norm(M)
+    res = np.linalg.norm(M @ V - V * w)
+    if scale > 0 and res > 1e-8 * scale:
+        raise OracleConvergenceError("eig residual")
+    return w, V
+
+
+# --------------------------------------------------------------------------
+# dmd.py
+# --------------------------------------------------------------------------
+
+def partner_map(lam, tol=1e-8):
+    """dmd.py:131-155 — greedy conjugate matching; real (|Im| <= tol*scale)
+    or unmatched eigenvalues are self-paired."""
+    lam = np.asarray(lam)
+    r = lam.size
+    scale = max(float(np.abs(lam).max()), 1e-300) if r else 1.0
+    out = -np.ones(r, dtype=np.int64)
+    for i in range(r):
+        if out[i] >= 0:
+            continue
+        if abs(lam[i].imag) <= tol * scale:
+            out[i] = i
+            continue
+        free = [j for j in range(r) if j != i and out[j] < 0]
+        if free:
+            d = np.abs(lam[free] - np.conj(lam[i]))
+            jj = int(np.argmin(d))
+            if d[jj] <= 10 * tol * scale + tol:
+                out[i] = free[jj]
+                out[free[jj]] = i
+                continue
+        out[i] = i
+    return out
+
+
+def frequency_order(lam):
+    """dmd.py:158-187 — the column permutation of _order_and_pair: units
+    (self-paired or representative-with-partner, representative = larger Im)
+    sorted by (|arg|, -|lam|, Re) of the representative."""
+    lam = np.asarray(lam)
+    part = partner_map(lam)
+    seen = np.zeros(lam.size, dtype=bool)
+    units = []
+    for i in range(lam.size):
+        if seen[i]:
+            continue
+        j = int(part[i])
+        seen[i] = seen[j] = True
+        if i == j:
+            units.append((i, -1))
+        elif lam[i].imag >= lam[j].imag:
+            units.append((i, j))
+        else:
+            units.append((j, i))
+    units.sort(key=lambda u: (abs(np.angle(lam[u[0]])), -abs(lam[u[0]]), lam[u[0]].real))
+    order = []
+    for a, b in units:
+        order.append(a)
+        if b >= 0:
+            order.append(b)
+    return np.asarray(order, dtype=np.int64)
+
+
+def order_and_pair(lam, phi):
+    """dmd.py:158-213 — sort, unit-normalise, canonicalise the
+    representative's phase at its first |max| entry, lock exact conjugates,
+    real-ify near-real eigenvalues/modes."""
+    order = frequency_order(lam)
+    lam = np.array(lam, dtype=np.complex128)[order]
+    phi = np.array(phi, dtype=np.complex128)[:, order]
+    k = 0
+    r = lam.size
+    while k < r:
+        c = phi[:, k]
+        nrm = np.linalg.norm(c)
+        if nrm > 0:
+            c = c / nrm
+        i = int(np.argmax(np.abs(c)))
+        if abs(c[i]) > 0:
+            c = c * (np.conj(c[i]) / abs(c[i]))
+        phi[:, k] = c
+        pair = (k + 1 < r and lam[k].imag > 0 and
+                abs(lam[k + 1] - np.conj(lam[k])) <= 1e-6 * max(abs(lam[k]), 1e-300))
+        if pair:
+            lam[k + 1] = np.conj(lam[k])
+            phi[:, k + 1] = np.conj(c)
+            k += 2
+            continue
+        if abs(lam[k].imag) <= 1e-12 * max(abs(lam[k]), 1e-300):
+            lam[k] = lam[k].real
+            if np.abs(c.imag).max() <= 1e-10:
+                phi[:, k] = c.real
+        k += 1
+    return lam, phi
+
+
+def svd_for_fit(X, r, svd_mode, seed, p=None, q=None):
+    """dmd.py:216-222 with the oracle's (p, q) override: the reference
+    clamps p = min(10, T - r) and hard-codes q = 2 for randomized mode."""
+    if svd_mode == "full":
+        return dense_truncated_svd(X, r)
+    if svd_mode != "randomized":
+        raise ValueError(svd_mode)
+    T = min(X.shape)
+    pp = min(10, T - r) if p is None else min(p, T - r)
+    qq = 2 if q is None else q
+    return sketch_svd(X, r, pp, qq, seed)
+
+
+def exact_dmd(states, r, svd_mode="full", seed=None, p=None, q=None, residual=True):
+    """dmd.py:240-274 — returns dict(lam, phi, sigma, residual, residual_rel)."""
+    states = np.asarray(states, dtype=np.float64)
+    X, Xp = states[:, :-1], states[:, 1:]
+    n, T = X.shape
+    if not 1 <= r <= min(n, T):
+        raise ValueError("rank out of range")
+    U, S, V = svd_for_fit(X, r, svd_mode, seed, p, q)
+    if S[-1] <= SIGMA_CUTOFF * S[0]:
+        raise ValueError("numerically zero singular value")
+    P = Xp @ (V / S)
+    Khat = U.conj().T @ P
+    lam, W = eig_checked(Khat)
+    lam, phi = order_and_pair(lam, P @ W)
+    out = dict(lam=lam, phi=phi, sigma=S, U=U, V=V, khat=Khat)
+    if residual:
+        rec = (phi * lam) @ (pinv_svd(phi) @ X)
+        res = float(np.linalg.norm(Xp - rec.real))
+        out["residual"] = res
+        out["residual_rel"] = res / max(np.linalg.norm(Xp), 1e-300)
+    return out
+
+
+def vandermonde(alpha, T):
+    """dmd.py:277-282."""
+    alpha = np.asarray(alpha, dtype=np.complex128)
+    return alpha[None, :] ** np.arange(T)[:, None]
+
+
+def _varpro_fit(alpha, D):
+    P = vandermonde(alpha, D.shape[0])
+    B = np.linalg.lstsq(P, D, rcond=None)[0]
+    R = D - P @ B
+    return float(np.linalg.norm(R)), B, P, R
+
+
+def _min_sep(a):
+    if a.size < 2:
+        return np.inf
+    d = np.abs(a[:, None] - a[None, :])
+    np.fill_diagonal(d, np.inf)
+    return float(d.min())
+
+
+class _Collapse(Exception):
+    pass
+
+
+def varpro_lm(D, alpha0, max_iters=200, init_damping=1.0, up=2.0, down=3.0,
+              rel_tol=1e-8, collapse_tol=1e-12):
+    """dmd.py:314-363 — LM on the eigenvalues with the Kaufman projected
+    Jacobian; returns (alpha, B, history, converged)."""
+    T = D.shape[0]
+    t = np.arange(T)
+    alpha = np.array(alpha0, dtype=np.complex128)
+    if _min_sep(alpha) < collapse_tol:
+        raise _Collapse
+    f, B, P, R = _varpro_fit(alpha, D)
+    floor = 1e-14 * np.linalg.norm(D)
+    hist = [f]
+    if max_iters == 0:
+        return alpha, B, hist, True
+    mu = init_damping
+    conv = False
+    for _ in range(max_iters):
+        if f <= floor:
+            conv = True
+            break
+        Qp = np.linalg.qr(P)[0]
+        dP = np.zeros_like(P)
+        dP[1:, :] = t[1:, None] * alpha[None, :] ** (t[1:, None] - 1)
+        Wk = dP - Qp @ (Qp.conj().T @ dP)
+        JHJ = (Wk.conj().T @ Wk) * np.conj(B @ B.conj().T)
+        g = np.diag(Wk.conj().T @ (R @ B.conj().T))
+        try:
+            step = np.linalg.solve(JHJ + mu * np.eye(alpha.size), g)
+        except np.linalg.LinAlgError:
+            mu *= up
+            continue
+        cand = alpha + step
+        if _min_sep(cand) < collapse_tol:
+            raise _Collapse
+        f2, B2, P2, R2 = _varpro_fit(cand, D)
+        if f2 < f:
+            rel = (f - f2) / max(f, 1e-300)
+            alpha, f, B, P, R = cand, f2, B2, P2, R2
+            hist.append(f)
+            mu /= down
+            if rel < rel_tol or f <= floor:
+                conv = True
+                break
+        else:
+            mu *= up
+    return alpha, B, hist, conv
+
+
+def symmetrize(alpha, B):
+    """dmd.py:439-455."""
+    part = partner_map(alpha)
+    alpha = alpha.copy()
+    B = B.copy()
+    for i in range(alpha.size):
+        j = part[i]
+        if j > i:
+            a = 0.5 * (alpha[i] + np.conj(alpha[j]))
+            alpha[i], alpha[j] = a, np.conj(a)
+            row = 0.5 * (B[i, :] + np.conj(B[j, :]))
+            B[i, :], B[j, :] = row, np.conj(row)
+        elif j == i and abs(alpha[i].imag) <= 1e-8 * max(abs(alpha[i]), 1e-300):
+            alpha[i] = alpha[i].real
+            B[i, :] = B[i, :].real
+    return alpha, B
+
+
+def optdmd(states, r, init=None, max_iters=200, svd_mode="full", seed=None, p=None, q=None):
+    """dmd.py:366-436 — returns dict(lam, phi, sigma, history, converged)."""
+    states = np.asarray(states, dtype=np.float64)
+    X = states[:, :-1]
+    n, T = X.shape
+    U, S, V = svd_for_fit(X, r, svd_mode, seed, p, q)
+    if S[-1] <= SIGMA_CUTOFF * S[0]:
+        raise ValueError("numerically zero singular value")
+    D = np.conj(V) * S
+    if init is None:
+        alpha0 = exact_dmd(states, r, svd_mode, seed, p, q, residual=False)["lam"]
+    else:
+        alpha0 = np.asarray(init, dtype=np.complex128)
+    try:
+        alpha, B, hist, conv = varpro_lm(D, alpha0, max_iters)
+    except _Collapse:
+        rng = np.random.default_rng(0 if seed is None else seed)
+        jit = 1e-10 * (1.0 + np.abs(alpha0)) * np.exp(2j * np.pi * rng.random(alpha0.size))
+        alpha, B, hist, conv = varpro_lm(D, alpha0 + jit, max_iters)
+    a_s, B_s = symmetrize(alpha, B)
+    f_s = float(np.linalg.norm(D - vandermonde(a_s, T) @ B_s))
+    if f_s <= hist[-1] * (1 + 1e-9) and f_s <= hist[0] * (1 + 1e-12):
+        alpha, B = a_s, B_s
+    lam, phi = order_and_pair(alpha, U @ B.T)
+    return dict(lam=lam, phi=phi, sigma=S, history=hist, converged=conv)
+
+
+def reduced_control(phi, channels):
+    """dmd.py:471-491 — B~_i = pinv(phi) @ B_i."""
+    pp = pinv_svd(phi)
+    return [pp @ np.asarray(Bm) for Bm in channels]
+
+
+# --------------------------------------------------------------------------
+# ReducedModel decode table (dmd.py:92-120) and runtime.py
+# --------------------------------------------------------------------------
+
+def decode_columns(phi, lam):
+    """dmd.py:92-120 — real table [Re phi_a] / [2 Re phi_a, -2 Im phi_a]
+    with (column, mode) index maps for Re and Im coefficient parts."""
+    part = partner_map(lam)
+    n, r = phi.shape
+    cols, re_idx, im_idx = [], [], []
+    for a in range(r):
+        b = part[a]
+        if b < a:
+            continue
+        if b == a:
+            re_idx.append((len(cols), a))
+            cols.append(phi[:, a].real)
+        else:
+            re_idx.append((len(cols), a))
+            cols.append(2.0 * phi[:, a].real)
+            im_idx.append((len(cols), a))
+            cols.append(-2.0 * phi[:, a].imag)
+    table = np.stack(cols, axis=1) if cols else np.zeros((n, 0))
+    return np.ascontiguousarray(table), re_idx, im_idx
+
+
+def symmetry_defect(lam, z):
+    """runtime.py:55-63."""
+    part = partner_map(lam)
+    d = 0.0
+    for a in range(z.size):
+        b = part[a]
+        if b == a:
+            d = max(d, abs(z[a].imag))
+        elif b > a:
+            d = max(d, abs(z[b] - np.conj(z[a])))
+    return d
+
+
+def decode(phi, lam, z):
+    """runtime.py:66-99 — table GEMV when z is conjugate-symmetric, else Re(phi z)."""
+    z = np.asarray(z, dtype=np.complex128).ravel()
+    scale = max(float(np.abs(z).max()) if z.size else 0.0, 1e-300)
+    if symmetry_defect(lam, z) <= 1e-9 * scale:
+        table, re_idx, im_idx = decode_columns(phi, lam)
+        c = np.empty(table.shape[1])
+        for k, a in re_idx:
+            c[k] = z[a].real
+        for k, a in im_idx:
+            c[k] = z[a].imag
+        return table @ c
+    return (phi @ z).real
+
+
+def encode(phi, u):
+    """runtime.py:47-52."""
+    return pinv_svd(phi) @ np.asarray(u).ravel()
+
+
+def step_k(lam, z, k):
+    """runtime.py:108-124 (without the overflow guard)."""
+    return lam ** k * z
+
+
+def eval_continuous(lam, dt, z, t):
+    """runtime.py:127-142."""
+    om = np.log(lam) / dt
+    return np.exp(om * t) * z
+
+
+def step_forced(lam, dt, z, reduced_b=(), q=(), pinv_phi=None, f=None):
+    """runtime.py:164-200."""
+    out = lam * z
+    for Bm, qi in zip(reduced_b, q):
+        out = out + (Bm @ np.asarray(qi).ravel()) * dt
+    if f is not None:
+        out = out + (pinv_phi @ f) * dt
+    return out
+
+
+# --------------------------------------------------------------------------
+# CholeskyQR2 restatement of sketch_svd (the algorithm the GPU runs).
+# Used by tests to separate "algorithm change" from "kernel error".
+# --------------------------------------------------------------------------
+
+def cholqr2(Y):
+    """Q = Y R^-1 twice (CholeskyQR2); returns Q, R."""
+    G = Y.T @ Y
+    R1 = np.linalg.cholesky(G).T
+    Q1 = np.linalg.solve(R1.T, Y.T).T
+    G2 = Q1.T @ Q1
+    R2 = np.linalg.cholesky(G2).T
+    Q = np.linalg.solve(R2.T, Q1.T).T
+    return Q, R2 @ R1
+
+
+def sketch_svd_cholqr2(M, r, p, q, omega):
+    M = np.asarray(M, dtype=np.float64)
+    Q = cholqr2(M @ omega)[0]
+    for _ in range(q):
+        W = np.linalg.qr(M.T @ Q)[0]
+        Q = cholqr2(M @ W)[0]
+    B = Q.T @ M
+    Ub, s, Vh = np.linalg.svd(B, full_matrices=False)
+    U, V = canonicalize_columns((Q @ Ub)[:, :r], Vh[:r].T)
+    return U, s[:r].copy(), V
+
+
+# --------------------------------------------------------------------------
+# Control-augmented DMDc — PARITY UNPINNED (no reference implementation:
+# the reference's DMDc is fit_control with known B, dmd.py:471-491; joint
+# identification is a declared non-goal). Restates Proctor
+# et al. 2016 as cited by PAPER.md:420.
+# --------------------------------------------------------------------------
+
+def dmdc_fit(states, controls, p_rank, r, seed, p=10, q=1):
+    """Augmented DMDc: SVD of Omega=[X; Upsilon] at rank p_rank, output basis
+    from an SVD of X' at rank r; returns (A~, B~, lam, phi, Uhat)."""
+    states = np.asarray(states, dtype=np.float64)
+    X, Xp = states[:, :-1], states[:, 1:]
+    Ups = np.asarray(controls, dtype=np.float64)          # ell x T
+    n = X.shape[0]
+    Om = np.vstack([X, Ups])
+    Ut, St, Vt = sketch_svd(Om, p_rank, min(p, Om.shape[1] - p_rank), q, seed)
+    Uh, Sh, Vh = sketch_svd(Xp, r, min(p, Xp.shape[1] - r), q, None if seed is None else seed + 1)
+    U1, U2 = Ut[:n], Ut[n:]
+    core = Xp @ (Vt / St)                                  # n x p_rank
+    A = Uh.T @ core @ (U1.T @ Uh)
+    Bt = Uh.T @ core @ U2.T
+    lam, W = eig_checked(A)
+    phi = core @ (U1.T @ Uh) @ W
+    lam, phi = order_and_pair(lam, phi)
+    return dict(A=A, B=Bt, lam=lam, phi=phi, Uhat=Uh, sigma_aug=St)

@@ -1,0 +1,483 @@
+// extern "C" boundary of libfdmd.so (declared in include/fdmd.h).
+#include <cusolverDn.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/fdmd.h"
+#include "fdmd_kernels.cuh"
+
+// kernels live in fdmd_kernels.cu (same translation unit, see build)
+#include "fdmd_kernels.cu"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess) return fail(FDMD_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+#define LAUNCH_CHECK(name)                                                                  \
+  do {                                                                                      \
+    cudaError_t _e = cudaGetLastError();                                                    \
+    if (_e != cudaSuccess) return fail(FDMD_ERR_CUDA, "%s launch: %s", name, cudaGetErrorString(_e)); \
+  } while (0)
+
+int sm_count_cached() {
+  static thread_local int dev_cached = -1, sms = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != dev_cached) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    dev_cached = dev;
+  }
+  return sms > 0 ? sms : 148;
+}
+
+inline size_t dsize(int dt) { return dt == FDMD_F32 ? 4 : 8; }
+
+// ------------------------------- tall_gemm --------------------------------
+template <int NF> constexpr int bn_of() { return 32 * NF; }
+
+int pick_nf(int N) {
+  if (N <= 64) return 2;
+  if (N <= 128) return 4;
+  return 7;
+}
+
+int64_t tg_tiles(int64_t n) { return (n + fdmd::tg::BM - 1) / fdmd::tg::BM; }
+
+template <typename TA, int AL, int NF, typename TC, int CL, bool ST>
+int launch_tg(const fdmd::TallGemmArgs& a, cudaStream_t s, int grid_x) {
+  auto kern = fdmd::tall_gemm_kernel<TA, AL, NF, TC, CL, ST>;
+  const int smem = (int)sizeof(fdmd::TGSmem<NF>);
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = dev;
+  }
+  dim3 grid(grid_x, (a.N + 32 * NF - 1) / (32 * NF));
+  kern<<<grid, fdmd::tg::THREADS, smem, s>>>(a);
+  LAUNCH_CHECK("tall_gemm");
+  return FDMD_OK;
+}
+
+template <typename TA, int AL, int NF>
+int dispatch_tg_c(const fdmd::TallGemmArgs& a, int c_dtype, int c_layout, bool stats, cudaStream_t s,
+                  int grid_x) {
+  if (c_layout == FDMD_ROW) {
+    if (stats) return fail(FDMD_ERR_INVALID, "pair_stats requires column-major C (or C == NULL)");
+    if (c_dtype == FDMD_F64) return launch_tg<TA, AL, NF, double, fdmd::LAYOUT_ROW, false>(a, s, grid_x);
+    return launch_tg<TA, AL, NF, float, fdmd::LAYOUT_ROW, false>(a, s, grid_x);
+  }
+  if (c_dtype == FDMD_F64)
+    return stats ? launch_tg<TA, AL, NF, double, fdmd::LAYOUT_COL, true>(a, s, grid_x)
+                 : launch_tg<TA, AL, NF, double, fdmd::LAYOUT_COL, false>(a, s, grid_x);
+  return stats ? launch_tg<TA, AL, NF, float, fdmd::LAYOUT_COL, true>(a, s, grid_x)
+               : launch_tg<TA, AL, NF, float, fdmd::LAYOUT_COL, false>(a, s, grid_x);
+}
+
+template <typename TA, int AL>
+int dispatch_tg_nf(const fdmd::TallGemmArgs& a, int c_dtype, int c_layout, bool stats, cudaStream_t s,
+                   int grid_x) {
+  switch (pick_nf(a.N)) {
+    case 2: return dispatch_tg_c<TA, AL, 2>(a, c_dtype, c_layout, stats, s, grid_x);
+    case 4: return dispatch_tg_c<TA, AL, 4>(a, c_dtype, c_layout, stats, s, grid_x);
+    default: return dispatch_tg_c<TA, AL, 7>(a, c_dtype, c_layout, stats, s, grid_x);
+  }
+}
+
+int tg_grid_x(int64_t n) {
+  const int64_t tiles = tg_tiles(n);
+  const int64_t want = (int64_t)sm_count_cached() * 2;
+  return (int)std::max<int64_t>(1, std::min(tiles, want));
+}
+
+// ------------------------------- tall_gram --------------------------------
+struct GramPlan {
+  int ti, tj, tiles, splits;
+  int64_t rows_per_split;
+  int K1p, K2p;
+};
+
+GramPlan gram_plan(int64_t n, int K1, int K2, int symmetric) {
+  GramPlan p;
+  p.ti = (K1 + fdmd::gr::T - 1) / fdmd::gr::T;
+  p.tj = (K2 + fdmd::gr::T - 1) / fdmd::gr::T;
+  p.tiles = symmetric ? p.ti * (p.ti + 1) / 2 : p.ti * p.tj;
+  p.K1p = p.ti * fdmd::gr::T;
+  p.K2p = p.tj * fdmd::gr::T;
+  const int64_t target = (int64_t)sm_count_cached() * 4;
+  const int64_t max_splits = std::max<int64_t>(1, (n + 255) / 256);
+  int64_t splits = std::max<int64_t>(1, target / p.tiles);
+  splits = std::min(splits, max_splits);
+  p.rows_per_split = ((n + splits - 1) / splits + 15) / 16 * 16;
+  if (p.rows_per_split == 0) p.rows_per_split = 16;
+  p.splits = (int)std::max<int64_t>(1, (n + p.rows_per_split - 1) / p.rows_per_split);
+  return p;
+}
+
+template <typename TA, int LA, typename TB, int LB>
+int launch_gram(const fdmd::TallGramArgs& a, int tiles, int splits, cudaStream_t s) {
+  dim3 grid(tiles, splits);
+  fdmd::tall_gram_kernel<TA, LA, TB, LB><<<grid, fdmd::gr::THREADS, 0, s>>>(a);
+  LAUNCH_CHECK("tall_gram");
+  return FDMD_OK;
+}
+
+template <typename TA, int LA>
+int dispatch_gram_b(const fdmd::TallGramArgs& a, int b_dtype, int b_layout, int tiles, int splits,
+                    cudaStream_t s) {
+  if (b_dtype == FDMD_F32)
+    return b_layout == FDMD_ROW ? launch_gram<TA, LA, float, fdmd::LAYOUT_ROW>(a, tiles, splits, s)
+                                : launch_gram<TA, LA, float, fdmd::LAYOUT_COL>(a, tiles, splits, s);
+  return b_layout == FDMD_ROW ? launch_gram<TA, LA, double, fdmd::LAYOUT_ROW>(a, tiles, splits, s)
+                              : launch_gram<TA, LA, double, fdmd::LAYOUT_COL>(a, tiles, splits, s);
+}
+
+// ------------------------------- cuSOLVER ---------------------------------
+struct SolverCtx {
+  cusolverDnHandle_t h = nullptr;
+  cusolverDnParams_t p = nullptr;
+};
+
+SolverCtx* solver_ctx() {
+  static thread_local std::unordered_map<int, SolverCtx> ctxs;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto& c = ctxs[dev];
+  if (!c.h) {
+    if (cusolverDnCreate(&c.h) != CUSOLVER_STATUS_SUCCESS) return nullptr;
+    if (cusolverDnCreateParams(&c.p) != CUSOLVER_STATUS_SUCCESS) return nullptr;
+  }
+  return &c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fdmd_version(void) { return 1; }
+
+const char* fdmd_last_error(void) { return g_err.c_str(); }
+
+int fdmd_device_info(int device, int* sm_count, int* cc_major, int* cc_minor) {
+  CUDA_TRY(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, device));
+  CUDA_TRY(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, device));
+  CUDA_TRY(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, device));
+  return FDMD_OK;
+}
+
+size_t fdmd_tall_gemm_workspace(int64_t n, int N) {
+  (void)n;
+  const int gx = tg_grid_x(n);
+  return (size_t)gx * (size_t)((N + 1) / 2) * 3 * sizeof(double) + 256;
+}
+
+int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda, const double* B, int64_t ldb,
+                   void* C, int c_dtype, int c_layout, int64_t ldc, int64_t n, int K, int N,
+                   double* pair_stats, int64_t row_offset, void* workspace, size_t workspace_bytes,
+                   void* stream) {
+  if (n < 0 || K < 0 || N < 0) return fail(FDMD_ERR_INVALID, "negative size");
+  if (!A || !B) return fail(FDMD_ERR_INVALID, "null operand");
+  if (a_dtype != FDMD_F32 && a_dtype != FDMD_F64) return fail(FDMD_ERR_INVALID, "bad a_dtype");
+  if (c_dtype != FDMD_F32 && c_dtype != FDMD_F64) return fail(FDMD_ERR_INVALID, "bad c_dtype");
+  if (pair_stats && (N % 2)) return fail(FDMD_ERR_INVALID, "pair_stats needs even N");
+  if (a_layout == FDMD_ROW && lda < K) return fail(FDMD_ERR_INVALID, "lda < K");
+  if (a_layout == FDMD_COL && lda < n) return fail(FDMD_ERR_INVALID, "lda < n");
+  if (ldb < N) return fail(FDMD_ERR_INVALID, "ldb < N");
+  if (C && c_layout == FDMD_ROW && ldc < N) return fail(FDMD_ERR_INVALID, "ldc < N");
+  if (C && c_layout == FDMD_COL && ldc < n) return fail(FDMD_ERR_INVALID, "ldc < n");
+  if (n == 0 || N == 0) return FDMD_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int gx = tg_grid_x(n);
+  fdmd::TallGemmArgs a{};
+  a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.C = C; a.ldc = ldc;
+  a.n = n; a.K = K; a.N = N; a.row_offset = row_offset;
+  const bool stats = pair_stats != nullptr;
+  if (stats) {
+    const size_t need = (size_t)gx * (size_t)(N / 2) * 3 * sizeof(double);
+    if (!workspace || workspace_bytes < need)
+      return fail(FDMD_ERR_WORKSPACE, "tall_gemm workspace %zu < %zu", workspace_bytes, need);
+    a.pair_stats = static_cast<double*>(workspace);
+  }
+  if (!C) c_layout = FDMD_COL;  // stats-only pass: no stores
+  int rc;
+  if (a_dtype == FDMD_F32)
+    rc = a_layout == FDMD_ROW ? dispatch_tg_nf<float, fdmd::LAYOUT_ROW>(a, c_dtype, c_layout, stats, s, gx)
+                              : dispatch_tg_nf<float, fdmd::LAYOUT_COL>(a, c_dtype, c_layout, stats, s, gx);
+  else
+    rc = a_layout == FDMD_ROW ? dispatch_tg_nf<double, fdmd::LAYOUT_ROW>(a, c_dtype, c_layout, stats, s, gx)
+                              : dispatch_tg_nf<double, fdmd::LAYOUT_COL>(a, c_dtype, c_layout, stats, s, gx);
+  if (rc != FDMD_OK) return rc;
+  if (stats) {
+    const int U = N / 2;
+    fdmd::pair_stats_reduce_kernel<<<(U + 127) / 128, 128, 0, s>>>(a.pair_stats, gx, U, pair_stats);
+    LAUNCH_CHECK("pair_stats_reduce");
+  }
+  return FDMD_OK;
+}
+
+size_t fdmd_tall_gram_workspace(int64_t n, int K1, int K2) {
+  GramPlan p = gram_plan(n, K1, K2, 0);
+  return (size_t)p.splits * p.K1p * p.K2p * sizeof(double) + 256;
+}
+
+int fdmd_tall_gram(const void* A, int a_dtype, int a_layout, int64_t lda, const void* B, int b_dtype,
+                   int b_layout, int64_t ldb, double* C, int64_t ldc, double beta, int64_t n, int K1,
+                   int K2, int symmetric, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n < 0 || K1 <= 0 || K2 <= 0) return fail(FDMD_ERR_INVALID, "bad sizes n=%lld K1=%d K2=%d", (long long)n, K1, K2);
+  if (!A || !B || !C) return fail(FDMD_ERR_INVALID, "null operand");
+  if (symmetric && (K1 != K2 || A != B)) return fail(FDMD_ERR_INVALID, "symmetric needs A==B, K1==K2");
+  if (ldc < K2) return fail(FDMD_ERR_INVALID, "ldc < K2");
+  if ((a_layout == FDMD_ROW && lda < K1) || (a_layout == FDMD_COL && lda < n))
+    return fail(FDMD_ERR_INVALID, "bad lda");
+  if ((b_layout == FDMD_ROW && ldb < K2) || (b_layout == FDMD_COL && ldb < n))
+    return fail(FDMD_ERR_INVALID, "bad ldb");
+  cudaStream_t s = (cudaStream_t)stream;
+  GramPlan p = gram_plan(n, K1, K2, symmetric);
+  const size_t need = (size_t)p.splits * p.K1p * p.K2p * sizeof(double);
+  if (!workspace || workspace_bytes < need)
+    return fail(FDMD_ERR_WORKSPACE, "tall_gram workspace %zu < %zu", workspace_bytes, need);
+  fdmd::TallGramArgs a{};
+  a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.W = static_cast<double*>(workspace);
+  a.n = n; a.K1 = K1; a.K2 = K2; a.K1p = p.K1p; a.K2p = p.K2p; a.tiles_j = p.tj;
+  a.symmetric = symmetric; a.rows_per_split = p.rows_per_split;
+  int rc;
+  if (a_dtype == FDMD_F32)
+    rc = a_layout == FDMD_ROW ? dispatch_gram_b<float, fdmd::LAYOUT_ROW>(a, b_dtype, b_layout, p.tiles, p.splits, s)
+                              : dispatch_gram_b<float, fdmd::LAYOUT_COL>(a, b_dtype, b_layout, p.tiles, p.splits, s);
+  else
+    rc = a_layout == FDMD_ROW ? dispatch_gram_b<double, fdmd::LAYOUT_ROW>(a, b_dtype, b_layout, p.tiles, p.splits, s)
+                              : dispatch_gram_b<double, fdmd::LAYOUT_COL>(a, b_dtype, b_layout, p.tiles, p.splits, s);
+  if (rc != FDMD_OK) return rc;
+  dim3 grid((K2 + 127) / 128, K1);
+  fdmd::gram_reduce_kernel<<<grid, 128, 0, s>>>(a.W, p.splits, K1, K2, p.K1p, p.K2p, symmetric, C, ldc, beta);
+  LAUNCH_CHECK("gram_reduce");
+  return FDMD_OK;
+}
+
+int fdmd_decode(const void* D, int dtype, int64_t ldd, const void* coef, int ldcoef, void* out, int64_t ldo,
+                int64_t n, int r, int B, void* stream) {
+  if (n < 0 || r < 0 || B < 0) return fail(FDMD_ERR_INVALID, "negative size");
+  if (!D || !coef || !out) return fail(FDMD_ERR_INVALID, "null operand");
+  if (ldd < n || ldo < n || ldcoef < B) return fail(FDMD_ERR_INVALID, "bad leading dimension");
+  if (n == 0 || B == 0) return FDMD_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  // frame groups: <=2 -> (4 rows, FB), <=8 -> (4, 8), <=16 -> (2,16), else 32 per pass (1 row)
+  for (int f0 = 0; f0 < B; ) {
+    const int left = B - f0;
+    int rpt, fb;
+    if (left <= 1) { rpt = 4; fb = 1; }
+    else if (left <= 2) { rpt = 4; fb = 2; }
+    else if (left <= 4) { rpt = 4; fb = 4; }
+    else if (left <= 8) { rpt = 4; fb = 8; }
+    else if (left <= 16) { rpt = 2; fb = 16; }
+    else { rpt = 1; fb = 32; }
+    if (dtype == FDMD_F64 && rpt == 4) rpt = 2;
+    const int threads = 256;
+    const int64_t nthreads = (n + rpt - 1) / rpt;
+    const int64_t blocks = (nthreads + threads - 1) / threads;
+    const size_t smem = (size_t)r * fb * dsize(dtype);
+    if (smem > 200 * 1024) return fail(FDMD_ERR_INVALID, "rank too large for decode smem");
+#define DEC(T, RPT, FB)                                                                          \
+  do {                                                                                          \
+    auto k = fdmd::decode_kernel<T, RPT, FB>;                                                    \
+    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k<<<(unsigned)blocks, threads, smem, s>>>((const T*)D, ldd, (const T*)coef, ldcoef, (T*)out, ldo, n, r, B, f0); \
+  } while (0)
+    if (dtype == FDMD_F32) {
+      if (fb == 1) DEC(float, 4, 1);
+      else if (fb == 2) DEC(float, 4, 2);
+      else if (fb == 4) DEC(float, 4, 4);
+      else if (fb == 8) DEC(float, 4, 8);
+      else if (fb == 16) DEC(float, 2, 16);
+      else DEC(float, 1, 32);
+    } else {
+      if (fb == 1) DEC(double, 2, 1);
+      else if (fb == 2) DEC(double, 2, 2);
+      else if (fb == 4) DEC(double, 2, 4);
+      else if (fb == 8) DEC(double, 2, 8);
+      else if (fb == 16) DEC(double, 2, 16);
+      else DEC(double, 1, 32);
+    }
+#undef DEC
+    LAUNCH_CHECK("decode");
+    f0 += fb;
+  }
+  return FDMD_OK;
+}
+
+static int64_t cd_rows_per_split(int64_t n, int r) {
+  const int64_t target = (int64_t)sm_count_cached() * 8;
+  int64_t splits = std::max<int64_t>(1, target / std::max(1, r));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, (n + 4095) / 4096));
+  return (n + splits - 1) / splits;
+}
+
+size_t fdmd_colmajor_dot_workspace(int64_t n, int r, int nv) {
+  const int64_t rps = cd_rows_per_split(n, r);
+  const int64_t splits = (n + rps - 1) / std::max<int64_t>(rps, 1);
+  return (size_t)std::max<int64_t>(splits, 1) * r * nv * sizeof(double) + 256;
+}
+
+int fdmd_colmajor_dot(const void* D, int d_dtype, int64_t ldd, const void* U, int u_dtype, int64_t ldu,
+                      int64_t n, int r, int nv, double* y, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+  if (n <= 0 || r <= 0 || nv <= 0 || nv > 8) return fail(FDMD_ERR_INVALID, "bad sizes (nv must be 1..8)");
+  if (!D || !U || !y) return fail(FDMD_ERR_INVALID, "null operand");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t rps = cd_rows_per_split(n, r);
+  const int splits = (int)((n + rps - 1) / rps);
+  const size_t need = (size_t)splits * r * nv * sizeof(double);
+  if (!workspace || workspace_bytes < need) return fail(FDMD_ERR_WORKSPACE, "colmajor_dot workspace");
+  double* part = static_cast<double*>(workspace);
+  dim3 grid(r, splits);
+#define CD(TD, TU, NV) fdmd::colmajor_dot_kernel<TD, TU, NV><<<grid, 256, 0, s>>>((const TD*)D, ldd, (const TU*)U, ldu, n, r, rps, part)
+#define CDV(TD, TU)                                                         \
+  switch (nv) {                                                             \
+    case 1: CD(TD, TU, 1); break; case 2: CD(TD, TU, 2); break;             \
+    case 3: CD(TD, TU, 3); break; case 4: CD(TD, TU, 4); break;             \
+    case 5: CD(TD, TU, 5); break; case 6: CD(TD, TU, 6); break;             \
+    case 7: CD(TD, TU, 7); break; default: CD(TD, TU, 8); break;            \
+  }
+  if (d_dtype == FDMD_F32) { if (u_dtype == FDMD_F32) { CDV(float, float) } else { CDV(float, double) } }
+  else { if (u_dtype == FDMD_F32) { CDV(double, float) } else { CDV(double, double) } }
+#undef CDV
+#undef CD
+  LAUNCH_CHECK("colmajor_dot");
+  const int len = r * nv;
+  fdmd::split_sum_kernel<<<(len + 127) / 128, 128, 0, s>>>(part, splits, len, y);
+  LAUNCH_CHECK("split_sum");
+  return FDMD_OK;
+}
+
+int fdmd_table_apply(const void* R, int r_dtype, int64_t ldr, const int* src, const double* alpha,
+                     const double* beta, void* D, int d_dtype, int64_t ldd, int64_t n, int ncols,
+                     void* stream) {
+  if (n < 0 || ncols < 0) return fail(FDMD_ERR_INVALID, "negative size");
+  if (n == 0 || ncols == 0) return FDMD_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t per = std::min<int64_t>((n + 255) / 256, std::max<int64_t>(1, sm_count_cached() * 8 / std::max(ncols, 1)));
+  dim3 grid((unsigned)std::max<int64_t>(per, 1), ncols);
+#define TA_(TR, TD) fdmd::table_apply_kernel<TR, TD><<<grid, 256, 0, s>>>((const TR*)R, ldr, src, alpha, beta, (TD*)D, ldd, n, ncols)
+  if (r_dtype == FDMD_F32) { if (d_dtype == FDMD_F32) TA_(float, float); else TA_(float, double); }
+  else { if (d_dtype == FDMD_F32) TA_(double, float); else TA_(double, double); }
+#undef TA_
+  LAUNCH_CHECK("table_apply");
+  return FDMD_OK;
+}
+
+size_t fdmd_residual_workspace(int64_t n) {
+  (void)n;
+  return (size_t)sm_count_cached() * 4 * 2 * sizeof(double) + 256;
+}
+
+int fdmd_residual(const void* S, int s_dtype, int64_t lds, const void* D, int d_dtype, int64_t ldd,
+                  const double* F, int r, int T, int64_t n, double* out, void* workspace,
+                  size_t workspace_bytes, void* stream) {
+  if (n < 0 || r <= 0 || T <= 0) return fail(FDMD_ERR_INVALID, "bad sizes");
+  const size_t smem = (size_t)r * T * sizeof(double);
+  if (smem > 220 * 1024) return fail(FDMD_ERR_INVALID, "residual: r*T too large for smem");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int blocks = sm_count_cached() * 4;
+  if (!workspace || workspace_bytes < (size_t)blocks * 2 * sizeof(double))
+    return fail(FDMD_ERR_WORKSPACE, "residual workspace");
+  double* part = static_cast<double*>(workspace);
+#define RS(TS, TD)                                                                                   \
+  do {                                                                                               \
+    auto k = fdmd::residual_kernel<TS, TD>;                                                          \
+    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
+    k<<<blocks, 256, smem, s>>>((const TS*)S, lds, (const TD*)D, ldd, F, r, T, n, part);              \
+  } while (0)
+  if (s_dtype == FDMD_F32) { if (d_dtype == FDMD_F32) RS(float, float); else RS(float, double); }
+  else { if (d_dtype == FDMD_F32) RS(double, float); else RS(double, double); }
+#undef RS
+  LAUNCH_CHECK("residual");
+  fdmd::split_sum_kernel<<<1, 32, 0, s>>>(part, blocks, 2, out);
+  LAUNCH_CHECK("residual_sum");
+  return FDMD_OK;
+}
+
+int fdmd_geev(int n, double* A, double* w_host, double* vr_host, void* stream) {
+  if (n <= 0 || !A || !w_host || !vr_host) return fail(FDMD_ERR_INVALID, "geev: bad arguments");
+  SolverCtx* c = solver_ctx();
+  if (!c) return fail(FDMD_ERR_SOLVER, "cusolverDnCreate failed");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cusolverDnSetStream(c->h, s) != CUSOLVER_STATUS_SUCCESS) return fail(FDMD_ERR_SOLVER, "set stream");
+  double* W = nullptr;  // complex n
+  double* VR = nullptr;
+  int* info = nullptr;
+  CUDA_TRY(cudaMallocAsync(&W, sizeof(double) * 2 * n, s));
+  CUDA_TRY(cudaMallocAsync(&VR, sizeof(double) * n * n, s));
+  CUDA_TRY(cudaMallocAsync(&info, sizeof(int), s));
+  size_t dws = 0, hws = 0;
+  cusolverStatus_t st = cusolverDnXgeev_bufferSize(c->h, c->p, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR,
+                                                   n, CUDA_R_64F, A, n, CUDA_C_64F, W, CUDA_R_64F, nullptr, n,
+                                                   CUDA_R_64F, VR, n, CUDA_R_64F, &dws, &hws);
+  if (st != CUSOLVER_STATUS_SUCCESS) return fail(FDMD_ERR_SOLVER, "Xgeev_bufferSize status %d", (int)st);
+  void* dbuf = nullptr;
+  CUDA_TRY(cudaMallocAsync(&dbuf, dws > 0 ? dws : 1, s));
+  std::vector<char> hbuf(hws > 0 ? hws : 1);
+  st = cusolverDnXgeev(c->h, c->p, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, n, CUDA_R_64F, A, n,
+                       CUDA_C_64F, W, CUDA_R_64F, nullptr, n, CUDA_R_64F, VR, n, CUDA_R_64F, dbuf, dws,
+                       hbuf.data(), hws, info);
+  if (st != CUSOLVER_STATUS_SUCCESS) return fail(FDMD_ERR_SOLVER, "Xgeev status %d", (int)st);
+  int info_h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&info_h, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(w_host, W, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(vr_host, VR, sizeof(double) * n * n, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFreeAsync(W, s);
+  cudaFreeAsync(VR, s);
+  cudaFreeAsync(info, s);
+  cudaFreeAsync(dbuf, s);
+  if (info_h != 0) return fail(FDMD_ERR_SOLVER, "Xgeev info %d", info_h);
+  return FDMD_OK;
+}
+
+int fdmd_copy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
+                int kind, void* stream) {
+  if (height <= 0 || width <= 0) return FDMD_OK;
+  CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)height,
+                             (cudaMemcpyKind)kind, (cudaStream_t)stream));
+  return FDMD_OK;
+}
+
+int fdmd_synth3d(const double* sx, const double* sy, const double* sz, const double* Am, int K, int C, int N,
+                 int m, double noise, uint64_t key, int64_t row0, int64_t rows, void* out, int out_dtype,
+                 int64_t ldo, void* stream) {
+  if (K <= 0 || C <= 0 || N <= 0 || m <= 0 || rows < 0 || ldo < m) return fail(FDMD_ERR_INVALID, "synth3d: bad sizes");
+  if (rows == 0) return FDMD_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t bx = std::min<int64_t>((rows + 255) / 256, (int64_t)sm_count_cached() * 16);
+  dim3 grid((unsigned)bx, (m + 7) / 8);
+  if (out_dtype == FDMD_F32)
+    fdmd::synth3d_kernel<float><<<grid, 256, 0, s>>>(sx, sy, sz, Am, K, C, N, m, noise, key, row0, rows, (float*)out, ldo);
+  else
+    fdmd::synth3d_kernel<double><<<grid, 256, 0, s>>>(sx, sy, sz, Am, K, C, N, m, noise, key, row0, rows, (double*)out, ldo);
+  LAUNCH_CHECK("synth3d");
+  return FDMD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,272 @@
+"""Device plumbing: torch tensors for HBM buffers/streams/collectives, libfdmd
+for every tall kernel.
+
+Layout vocabulary (DESIGN.md §Data layout):
+  * a ``Tall`` is an n x k matrix whose n (grid rows) is huge and k (snapshots,
+    sketch width, modes) small. ``layout="row"``: buffer shape (n, ld), element
+    (i, j) at buf[i, j] — snapshot matrices and sketches. ``layout="col"``:
+    buffer shape (k, ld), element (i, j) at buf[j, i] — mode tables and bases,
+    so a decode streams each mode column contiguously.
+  * small factors (Omega, R^-1, W, Ub, ...) are plain fp64 torch tensors.
+
+Row-sharding: when a ``Shard`` with world > 1 is attached, each rank holds a
+contiguous row block and every reduction over n (tall_gram, colmajor_dot,
+residual, pair statistics) is followed by one all-reduce of the small result.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import COL, F32, F64, ROW
+
+_DT = {torch.float32: F32, torch.float64: F64}
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+@dataclass
+class Tall:
+    buf: torch.Tensor
+    layout: str  # "row" | "col"
+    n: int
+    k: int
+
+    @property
+    def ld(self) -> int:
+        return int(self.buf.shape[1])
+
+    @property
+    def dtype(self):
+        return self.buf.dtype
+
+    @property
+    def code(self) -> int:
+        return ROW if self.layout == "row" else COL
+
+    def view(self) -> torch.Tensor:
+        """Logical n x k view (may be a transposed view for col layout)."""
+        if self.layout == "row":
+            return self.buf[: self.n, : self.k]
+        return self.buf[: self.k, : self.n].t()
+
+    def nbytes(self) -> int:
+        return self.buf.numel() * self.buf.element_size()
+
+
+def alloc_tall(n: int, k: int, dtype, layout: str, device=None, zero: bool = False) -> Tall:
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    elt = torch.empty((), dtype=dtype).element_size()
+    q = 16 // elt
+    if layout == "row":
+        shape = (max(n, 1), round_up(max(k, 1), q))
+    else:
+        shape = (max(k, 1), round_up(max(n, 1), q))
+    buf = (torch.zeros if zero else torch.empty)(shape, dtype=dtype, device=device)
+    return Tall(buf, layout, n, k)
+
+
+@dataclass
+class Shard:
+    """Row block [row0, row0 + n_local) of an n_global-row matrix."""
+
+    row0: int
+    n_local: int
+    n_global: int
+    group: object = None
+    world: int = 1
+
+    def allreduce(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(t, group=self.group)
+        return t
+
+
+SINGLE = None  # shard=None means the matrix is whole on this device
+
+
+def allreduce(shard: Optional[Shard], t: torch.Tensor) -> torch.Tensor:
+    return t if shard is None else shard.allreduce(t)
+
+
+class _Workspace:
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+        b = self.bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+            self.bufs[key] = b
+        return b
+
+
+class CudaOps:
+    """Thin wrappers over libfdmd entry points. Counts kernel launches."""
+
+    def __init__(self):
+        self.ws = _Workspace()
+        self.launches = 0
+
+    # -- C[n x N] = A * B (B small fp64, K x N) ---------------------------
+    def tall_gemm(self, A: Tall, B: torch.Tensor, C: Optional[Tall], stats: bool = False,
+                  row_offset: int = 0) -> Optional[torch.Tensor]:
+        L = _lib.lib()
+        K, N = int(B.shape[0]), int(B.shape[1])
+        assert K <= A.k or K <= (A.ld if A.layout == "row" else K), (K, A.k)
+        B = B.to(torch.float64).contiguous()
+        st = None
+        wsb = 0
+        ws = None
+        if stats:
+            st = torch.empty((N // 2, 3), dtype=torch.float64, device=A.buf.device)
+            wsb = int(L.fdmd_tall_gemm_workspace(A.n, N))
+            ws = self.ws.get(wsb, A.buf.device)
+        c_buf = C.buf if C is not None else None
+        c_dt = _DT[C.dtype] if C is not None else F64
+        c_lay = C.code if C is not None else COL
+        c_ld = C.ld if C is not None else A.n
+        _lib.check(L.fdmd_tall_gemm(_ptr(A.buf), _DT[A.dtype], A.code, A.ld, _ptr(B), B.shape[1],
+                                     _ptr(c_buf), c_dt, c_lay, c_ld, A.n, K, N,
+                                     _ptr(st), row_offset, _ptr(ws), wsb, _stream()), "tall_gemm")
+        self.launches += 2 if stats else 1
+        return st
+
+    # -- C[K1 x K2] = A^T B over n ----------------------------------------
+    def tall_gram(self, A: Tall, B: Tall, K1: Optional[int] = None, K2: Optional[int] = None,
+                  symmetric: bool = False, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        L = _lib.lib()
+        K1 = A.k if K1 is None else K1
+        K2 = B.k if K2 is None else K2
+        if out is None:
+            out = torch.empty((K1, K2), dtype=torch.float64, device=A.buf.device)
+        wsb = int(L.fdmd_tall_gram_workspace(A.n, K1, K2))
+        ws = self.ws.get(wsb, A.buf.device)
+        _lib.check(L.fdmd_tall_gram(_ptr(A.buf), _DT[A.dtype], A.code, A.ld, _ptr(B.buf), _DT[B.dtype],
+                                     B.code, B.ld, _ptr(out), out.stride(0), 0.0, A.n, K1, K2,
+                                     1 if symmetric else 0, _ptr(ws), wsb, _stream()), "tall_gram")
+        self.launches += 2
+        return out
+
+    # -- frames[f][i] = sum_k D[k][i] coef[k][f] ---------------------------
+    def decode(self, D: Tall, coef: torch.Tensor, out: Optional[torch.Tensor] = None,
+               ncols: Optional[int] = None) -> torch.Tensor:
+        assert D.layout == "col"
+        r = D.k if ncols is None else ncols
+        coef = coef.to(D.dtype).contiguous()
+        B = int(coef.shape[1])
+        if out is None:
+            out = torch.empty((B, D.n), dtype=D.dtype, device=D.buf.device)
+        _lib.check(_lib.lib().fdmd_decode(_ptr(D.buf), _DT[D.dtype], D.ld, _ptr(coef), coef.stride(0),
+                                          _ptr(out), out.stride(0), D.n, r, B, _stream()), "decode")
+        self.launches += (B + 31) // 32 if B > 16 else 1
+        return out
+
+    # -- y[k][v] = sum_i D[k][i] U[v][i] -----------------------------------
+    def colmajor_dot(self, D: Tall, U: torch.Tensor, ncols: Optional[int] = None) -> torch.Tensor:
+        """U: (nv, n) tensor (nv <= 8), row v contiguous."""
+        assert D.layout == "col"
+        L = _lib.lib()
+        r = D.k if ncols is None else ncols
+        if U.dtype not in (torch.float32, torch.float64):
+            U = U.to(torch.float64)
+        U = U.contiguous()
+        nv = int(U.shape[0])
+        y = torch.empty((r, nv), dtype=torch.float64, device=D.buf.device)
+        wsb = int(L.fdmd_colmajor_dot_workspace(D.n, r, nv))
+        ws = self.ws.get(wsb, D.buf.device)
+        _lib.check(L.fdmd_colmajor_dot(_ptr(D.buf), _DT[D.dtype], D.ld, _ptr(U), _DT[U.dtype], U.stride(0),
+                                       D.n, r, nv, _ptr(y), _ptr(ws), wsb, _stream()), "colmajor_dot")
+        self.launches += 2
+        return y
+
+    def table_apply(self, R: Tall, src, alpha, beta, D: Tall, ncols: int):
+        dev = R.buf.device
+        src_t = torch.as_tensor(np.asarray(src, dtype=np.int32), device=dev)
+        a_t = torch.as_tensor(np.asarray(alpha, dtype=np.float64), device=dev)
+        b_t = torch.as_tensor(np.asarray(beta, dtype=np.float64), device=dev)
+        _lib.check(_lib.lib().fdmd_table_apply(_ptr(R.buf), _DT[R.dtype], R.ld, _ptr(src_t), _ptr(a_t),
+                                               _ptr(b_t), _ptr(D.buf), _DT[D.dtype], D.ld, D.n, ncols,
+                                               _stream()), "table_apply")
+        self.launches += 1
+
+    def residual(self, S: Tall, D: Tall, F: torch.Tensor, ncols: int, T: int) -> torch.Tensor:
+        L = _lib.lib()
+        F = F.to(torch.float64).contiguous()
+        out = torch.empty((2,), dtype=torch.float64, device=S.buf.device)
+        wsb = int(L.fdmd_residual_workspace(S.n))
+        ws = self.ws.get(wsb, S.buf.device)
+        _lib.check(L.fdmd_residual(_ptr(S.buf), _DT[S.dtype], S.ld, _ptr(D.buf), _DT[D.dtype], D.ld,
+                                   _ptr(F), ncols, T, S.n, _ptr(out), _ptr(ws), wsb, _stream()), "residual")
+        self.launches += 2
+        return out
+
+    def geev(self, K: torch.Tensor):
+        """Real nonsymmetric eig on device (cuSOLVER Xgeev). Returns host
+        (w complex[n], V complex[n, n]) with LAPACK pair unpacking."""
+        n = int(K.shape[0])
+        A = K.to(torch.float64).t().contiguous().clone()  # column-major
+        w = np.empty(2 * n, dtype=np.float64)
+        vr = np.empty(n * n, dtype=np.float64)
+        _lib.check(_lib.lib().fdmd_geev(n, _ptr(A), w.ctypes.data_as(ctypes.c_void_p),
+                                        vr.ctypes.data_as(ctypes.c_void_p), _stream()), "geev")
+        lam = w[0::2] + 1j * w[1::2]
+        VR = vr.reshape(n, n).T  # column-major -> (row, col)
+        V = np.empty((n, n), dtype=np.complex128)
+        j = 0
+        while j < n:
+            if lam[j].imag != 0.0 and j + 1 < n:
+                V[:, j] = VR[:, j] + 1j * VR[:, j + 1]
+                V[:, j + 1] = VR[:, j] - 1j * VR[:, j + 1]
+                j += 2
+            else:
+                V[:, j] = VR[:, j]
+                j += 1
+        return lam, V
+
+    def synth3d(self, tables, m: int, noise: float, key: int, row0: int, rows: int, out: Tall):
+        sx, sy, sz, A = tables
+        K, C, N = int(sx.shape[0]), int(sx.shape[1]), int(sx.shape[2])
+        _lib.check(_lib.lib().fdmd_synth3d(_ptr(sx), _ptr(sy), _ptr(sz), _ptr(A), K, C, N, m, noise,
+                                           ctypes.c_uint64(key), row0, rows, _ptr(out.buf), _DT[out.dtype],
+                                           out.ld, _stream()), "synth3d")
+        self.launches += 1
+
+
+ops = CudaOps()
+
+
+def set_ops(o):
+    """Swap the kernel provider (tests use this to run the host orchestration
+    with a CPU checker). Returns the previous provider."""
+    global ops
+    prev, ops = ops, o
+    return prev
+
+
+def get_ops():
+    return ops
+
+
+def default_device():
+    if not torch.cuda.is_available():
+        raise _lib.DeviceError("no CUDA device: the DMD hot path runs only on the GPU (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())

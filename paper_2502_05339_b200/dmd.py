@@ -1,0 +1,807 @@
+"""DMD trainers on the device, mirroring `flowdmd.dmd` (reference dmd.py:1-507).
+
+Names, signatures, validation and provenance keys follow the reference; the
+n-dimensional work runs in libfdmd (FP64 DMMA), the r-dimensional work stays
+on the device (cuSOLVER) except O(r) ordering/pairing bookkeeping, which is
+host logic exactly as in the reference.
+
+Extensions (keyword-only): ``oversample``/``power_iters`` overrides (the
+reference hard-codes q=2 and clamps p, dmd.py:216-222), ``residual`` to skip
+the diagnostic, ``table_dtype`` for the decode table, ``timings`` dict.
+"""
+
+from __future__ import annotations
+
+import time
+import warnings
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import device as dv
+from . import linalg as la
+from .device import Shard, Tall, allreduce, alloc_tall
+from .errors import ConvergenceError
+from .modes import DeviceModes, TableLayout, conjugate_pairs, modes_from_host_phi
+
+UNSTABLE_MODULUS = 1.05
+SIGMA_CUTOFF = 1e-14
+
+__all__ = [
+    "SnapshotMatrix", "ReducedModel", "conjugate_pairs", "exact_dmd", "optdmd", "vandermonde",
+    "LMConfig", "ControlOperator", "fit_control", "dmdc_fit", "UNSTABLE_MODULUS", "SIGMA_CUTOFF",
+]
+
+
+# ---------------------------------------------------------------------------
+# SnapshotMatrix (dmd.py:26-50)
+# ---------------------------------------------------------------------------
+class SnapshotMatrix:
+    """Time-ordered flattened states, one per column, resident in HBM.
+
+    ``states`` may be a host array (uploaded once; float32 stays float32 in
+    HBM and is upcast exactly in-kernel, other dtypes become float64), a
+    CUDA tensor, or an existing row-major ``Tall``. ``shard`` marks a row
+    block of a row-sharded matrix (multi-GPU).
+    """
+
+    def __init__(self, states, dt, grid_meta=None, meta=None, *, shard: Optional[Shard] = None,
+                 device=None, check_finite=True):
+        if isinstance(states, Tall):
+            S = states
+        else:
+            shape = getattr(states, "shape", None)
+            if shape is None:
+                states = np.asarray(states, dtype=np.float64)
+                shape = states.shape
+            if len(shape) != 2 or shape[1] < 2:
+                raise ValueError("snapshot matrix needs at least 2 columns")
+            S = la.as_tall(states, device)
+        if S.k < 2:
+            raise ValueError("snapshot matrix needs at least 2 columns")
+        if check_finite and S.n > 0 and not bool(torch.isfinite(S.view()).all().item()):
+            raise ValueError("snapshot matrix contains non-finite entries")
+        if not dt > 0:
+            raise ValueError("dt must be positive")
+        self.S = S
+        self.dt = float(dt)
+        self.grid_meta = grid_meta
+        self.meta = dict(meta or {})
+        self.shard = shard
+        self._host = None
+
+    @property
+    def n(self):
+        return self.S.n if self.shard is None else self.shard.n_global
+
+    @property
+    def n_transitions(self):
+        return self.S.k - 1
+
+    @property
+    def states(self):
+        """Host float64 copy (the reference keeps states as float64 numpy)."""
+        if self._host is None:
+            self._host = self.S.view().to(torch.float64).cpu().numpy()
+        return self._host
+
+
+def _as_snapshots(data) -> SnapshotMatrix:
+    if isinstance(data, SnapshotMatrix):
+        return data
+    # a reference-style object (e.g. flowdmd.dmd.SnapshotMatrix): .states, .dt
+    return SnapshotMatrix(data.states, data.dt, getattr(data, "grid_meta", None), getattr(data, "meta", None))
+
+
+# ---------------------------------------------------------------------------
+# ReducedModel (dmd.py:53-128)
+# ---------------------------------------------------------------------------
+class ReducedModel:
+    """Trained artifact: mode basis (device decode table), eigenvalues, sigma,
+    dt, provenance. ``phi`` (n x r complex128, host) is materialised lazily
+    from the device table; decoding never needs it."""
+
+    def __init__(self, phi, lam, sigma, dt, grid_meta=None, provenance=None, *, _modes=None):
+        self.lam = np.ascontiguousarray(lam, dtype=np.complex128)
+        self.sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        self.dt = float(dt)
+        self.grid_meta = grid_meta
+        self.provenance = dict(provenance or {})
+        if _modes is None:
+            phi = np.ascontiguousarray(phi, dtype=np.complex128)
+            if phi.ndim != 2:
+                raise ValueError("phi must be a 2D matrix")
+            if phi.shape[1] != self.lam.size or self.lam.size != self.sigma.size:
+                raise ValueError("phi, lam, sigma sizes disagree")
+            if not self.dt > 0:
+                raise ValueError("dt must be positive")
+            self._phi = phi
+            self.modes = modes_from_host_phi(phi, self.lam)
+        else:
+            if self.lam.size != self.sigma.size:
+                raise ValueError("phi, lam, sigma sizes disagree")
+            if not self.dt > 0:
+                raise ValueError("dt must be positive")
+            self._phi = None
+            self.modes = _modes
+        self.pair_partner = conjugate_pairs(self.lam)
+        self._phi_pinv = None
+        self._decode_table = None
+
+    @property
+    def n(self):
+        m = self.modes
+        return m.n_local if m.shard is None else m.shard.n_global
+
+    @property
+    def r(self):
+        return self.lam.size
+
+    @property
+    def phi(self):
+        if self._phi is None:
+            self._phi = self.modes.host_phi()
+        return self._phi
+
+    def phi_pinv(self):
+        """pinv(phi) as a host r x n complex matrix (linalg.py:93-104 semantics)."""
+        if self._phi_pinv is None:
+            D, E = self.modes.basis()
+            M = D.buf[: E.shape[0], : D.n].to(torch.float64).cpu().numpy()   # ncol x n
+            self._phi_pinv = self.modes.pinv_small() @ (E.conj().T @ M)
+        return self._phi_pinv
+
+    def decode_table(self):
+        """(cols n x k float64, re_idx, im_idx) — dmd.py:92-120."""
+        if self._decode_table is None:
+            lay = self.modes.layout
+            self._decode_table = (self.modes.host_table(), list(lay.re_idx), list(lay.im_idx))
+        return self._decode_table
+
+    def with_modes(self, phi, lam, note=None):
+        prov = dict(self.provenance)
+        if note:
+            prov.setdefault("edits", [])
+            prov["edits"] = list(prov["edits"]) + [note]
+        return ReducedModel(phi, lam, self.sigma, self.dt, self.grid_meta, prov)
+
+
+# ---------------------------------------------------------------------------
+# ordering / pairing plan (dmd.py:158-213), host bookkeeping on r values
+# ---------------------------------------------------------------------------
+def frequency_order(lam):
+    """Permutation applied by _order_and_pair (dmd.py:158-187)."""
+    lam = np.asarray(lam)
+    partner = conjugate_pairs(lam)
+    units, seen = [], np.zeros(lam.size, dtype=bool)
+    for i in range(lam.size):
+        if seen[i]:
+            continue
+        j = int(partner[i])
+        seen[i] = seen[j] = True
+        if i == j:
+            units.append((i, -1))
+        else:
+            units.append((i, j) if lam[i].imag >= lam[j].imag else (j, i))
+    units.sort(key=lambda u: (abs(np.angle(lam[u[0]])), -abs(lam[u[0]]), lam[u[0]].real))
+    order = []
+    for a, b in units:
+        order.append(a)
+        if b >= 0:
+            order.append(b)
+    return np.asarray(order, dtype=np.int64)
+
+
+@dataclass
+class PairPlan:
+    lam: np.ndarray                 # final eigenvalues (sorted, locked, real-ified)
+    src: list                       # per computed unit: source eigen-column index
+    pos_unit: list                  # per sorted position: (unit, conj?) ; -1 unused
+    locked: list                    # per unit: True if it is a locked conjugate pair start
+    realify: dict = field(default_factory=dict)   # unit -> True if lam real-ified and not paired
+
+
+def pair_plan(lam_raw) -> PairPlan:
+    order = frequency_order(lam_raw)
+    lam = np.asarray(lam_raw, dtype=np.complex128)[order].copy()
+    r = lam.size
+    src, pos_unit, locked, realify = [], [None] * r, [], {}
+    k = 0
+    while k < r:
+        u = len(src)
+        src.append(int(order[k]))
+        pos_unit[k] = (u, False)
+        paired = (k + 1 < r and lam[k].imag > 0 and
+                  abs(lam[k + 1] - np.conj(lam[k])) <= 1e-6 * max(abs(lam[k]), 1e-300))
+        locked.append(bool(paired))
+        if paired:
+            lam[k + 1] = np.conj(lam[k])
+            pos_unit[k + 1] = (u, True)
+            k += 2
+            continue
+        if abs(lam[k].imag) <= 1e-12 * max(abs(lam[k]), 1e-300):
+            lam[k] = lam[k].real
+            realify[u] = True
+        k += 1
+    return PairPlan(lam, src, pos_unit, locked, realify)
+
+
+def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, shard: Optional[Shard],
+                table_dtype, timings: Optional[dict] = None) -> DeviceModes:
+    """phi_raw = A @ [0_top; Cmap] for every computed unit, with fused
+    column statistics; then normalise + phase-canonicalise + lock conjugates
+    + build the decode table (dmd.py:189-213 and 92-120) in one HBM pass.
+
+    Cmap: K x r complex (device) with phi_raw[:, j] = A[:, top:top+K] @ Cmap[:, j].
+    """
+    ops = dv.get_ops()
+    dev = A.buf.device
+    U = len(plan.src)
+    K = int(Cmap.shape[0])
+    mA = A.k
+    Bm = torch.zeros((mA, 2 * U), dtype=torch.float64, device=dev)
+    src_t = torch.as_tensor(plan.src, device=dev, dtype=torch.long)
+    Cs = Cmap[:, src_t]
+    Bm[row_pad_top:row_pad_top + K, 0::2] = Cs.real
+    Bm[row_pad_top:row_pad_top + K, 1::2] = Cs.imag
+    n_loc = A.n
+    raw = alloc_tall(n_loc, 2 * U, table_dtype, "col", device=dev)
+    row0 = 0 if shard is None else shard.row0
+    t0 = time.perf_counter()
+    st = ops.tall_gemm(A, Bm, raw, stats=True, row_offset=row0)        # (U, 3)
+    st = la._reduce_pair_stats(st, shard)
+    nrm = torch.sqrt(st[:, 0])
+    idx = st[:, 2].round().long()
+    # pivot values raw[idx] (gathered from the owning shard)
+    local = idx - row0
+    if shard is not None and shard.world > 1:
+        own = (local >= 0) & (local < n_loc)
+        piv = torch.zeros((U, 2), dtype=torch.float64, device=dev)
+        li = torch.where(own, local, torch.zeros_like(local))
+        ar = torch.arange(U, device=dev)
+        vals_re = raw.buf[2 * ar, li].to(torch.float64)
+        vals_im = raw.buf[2 * ar + 1, li].to(torch.float64)
+        piv[:, 0] = torch.where(own, vals_re, torch.zeros_like(vals_re))
+        piv[:, 1] = torch.where(own, vals_im, torch.zeros_like(vals_im))
+        piv = shard.allreduce(piv)
+    else:
+        ar = torch.arange(U, device=dev)
+        li = local.clamp(min=0)
+        piv = torch.stack([raw.buf[2 * ar, li], raw.buf[2 * ar + 1, li]], dim=1).to(torch.float64)
+    pc = torch.complex(piv[:, 0], piv[:, 1])
+    pab = pc.abs()
+    phase = torch.where(pab > 0, pc.conj() / torch.where(pab > 0, pab, torch.ones_like(pab)),
+                        torch.ones_like(pc))
+    s = torch.where(nrm > 0, phase / torch.where(nrm > 0, nrm, torch.ones_like(nrm)), phase)
+    s = s.cpu().numpy()
+    Cs_h = Cs.cpu().numpy()
+    # real-ification of phi for real-ified eigenvalues (dmd.py:208-211)
+    realified_phi = set()
+    for u in plan.realify:
+        im_col = (Cs_h[:, u] * s[u]).imag
+        if not np.any(im_col):
+            realified_phi.add(u)
+            continue
+        # max |Im(c s)| over rows via a statistics-only pass
+        Bq = torch.zeros((mA, 2), dtype=torch.float64, device=dev)
+        Bq[row_pad_top:row_pad_top + K, 0] = torch.as_tensor(im_col, device=dev)
+        stq = la._reduce_pair_stats(ops.tall_gemm(A, Bq, None, stats=True, row_offset=row0), shard)
+        if float(torch.sqrt(stq[0, 1]).item()) <= 1e-10:
+            realified_phi.add(u)
+    # phi at each sorted position: (unit, conj)
+    lam = plan.lam
+    partner = conjugate_pairs(lam)
+    r = lam.size
+    extra = []
+    for a in range(r):
+        u, cj = plan.pos_unit[a]
+        if partner[a] == a and u not in realified_phi:
+            im_nonzero = np.any((Cs_h[:, u] * s[u]).imag != 0.0)
+            if im_nonzero:
+                extra.append(a)
+    lay = TableLayout(lam, extra)
+    # exactness: every partner pair must be (unit, False)/(unit, True) of one locked unit
+    exact = True
+    for a in range(r):
+        b = partner[a]
+        if b > a:
+            ua, ca = plan.pos_unit[a]
+            ub, cb = plan.pos_unit[b]
+            if not (ua == ub and ca != cb):
+                exact = False
+    # linear maps raw(Re,Im of unit) -> table columns
+    t_src, t_al, t_be = [], [], []
+
+    def re_of(u, cj, f):      # f * Re(phi)
+        sr, si = s[u].real, s[u].imag
+        return (u, f * sr, -f * si)
+
+    def im_of(u, cj, f):      # f * Im(phi)
+        sr, si = s[u].real, s[u].imag
+        sign = -1.0 if cj else 1.0
+        return (u, f * sign * si, f * sign * sr)
+
+    cols = [None] * lay.ncol
+    for k, a in lay.re_idx:
+        u, cj = plan.pos_unit[a]
+        cols[k] = re_of(u, cj, 1.0 if partner[a] == a else 2.0)
+    for k, a in lay.im_idx:
+        u, cj = plan.pos_unit[a]
+        cols[k] = im_of(u, cj, -2.0)
+    for a, k in lay.extra.items():
+        u, cj = plan.pos_unit[a]
+        cols[k] = im_of(u, cj, 1.0)
+    for c in cols:
+        t_src.append(c[0]); t_al.append(c[1]); t_be.append(c[2])
+    table = alloc_tall(n_loc, lay.ncol, table_dtype, "col", device=dev)
+    ops.table_apply(raw, t_src, t_al, t_be, table, lay.ncol)
+    general = None
+    if not exact:
+        general = alloc_tall(n_loc, 2 * r, table_dtype, "col", device=dev)
+        g_src, g_al, g_be = [], [], []
+        for a in range(r):
+            u, cj = plan.pos_unit[a]
+            c1 = re_of(u, cj, 1.0)
+            if u in realified_phi:
+                c2 = (u, 0.0, 0.0)
+            else:
+                c2 = im_of(u, cj, 1.0)
+            for c in (c1, c2):
+                g_src.append(c[0]); g_al.append(c[1]); g_be.append(c[2])
+        ops.table_apply(raw, g_src, g_al, g_be, general, 2 * r)
+    del raw
+    if timings is not None:
+        timings["modes_s"] = time.perf_counter() - t0
+    return DeviceModes(table, lay, shard, general)
+
+
+# ---------------------------------------------------------------------------
+# helpers shared by the trainers
+# ---------------------------------------------------------------------------
+def _check_sigma(S):
+    if S[-1] <= SIGMA_CUTOFF * S[0]:
+        raise ValueError(
+            f"requested rank hits numerically zero singular value "
+            f"(sigma_r / sigma_1 = {S[-1] / S[0]:.3e}); lower the rank")
+
+
+def _stability_warnings(lam):
+    worst = float(np.abs(lam).max()) if lam.size else 0.0
+    if worst > UNSTABLE_MODULUS:
+        return [f"unstable rollout: max |lambda| = {worst:.6f}"]
+    return []
+
+
+@dataclass
+class _Basis:
+    """Truncated SVD of X = S[:, :T] for the trainers: U = A @ Umap (A tall
+    on device), sigma, V (T x r) and U^T S (r x m)."""
+    A: Tall
+    Umap: Optional[torch.Tensor]   # l x r (randomized) or None (A is U itself)
+    S: torch.Tensor
+    V: torch.Tensor
+    UtS: torch.Tensor
+    stats: dict
+
+
+def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, power_iters,
+               timings: Optional[dict]) -> _Basis:
+    S = data.S
+    T = S.k - 1
+    n_tot = data.n
+    t0 = time.perf_counter()
+    if svd_mode == "randomized":
+        # dmd.py:219-221: oversample = min(10, min(X.shape) - r), power_iters = 2
+        cap = min(n_tot, T) - r
+        p = min(10, cap) if oversample is None else min(oversample, cap)
+        q = 2 if power_iters is None else power_iters
+        l = r + p
+        if not 1 <= r <= min(n_tot, T):
+            raise ValueError(f"rank {r} out of range [1, {min(n_tot, T)}]")
+        omega = la.draw_omega(T, l, seed)
+        f = la.sketch_factors(S, T, l, q, omega, data.shard)
+        Umap = f.Ub[:, :r].contiguous()
+        UtS = Umap.t() @ f.QtS
+        basis = _Basis(f.Q, Umap, f.s[:r].contiguous(), f.Vh[:r].t().contiguous(), UtS, f.stats)
+        basis.stats.update(l=l, p=p, q=q)
+    elif svd_mode == "full":
+        svd = la.truncated_svd(S if data.shard is None else S, r, shard=data.shard, keep_device=True)
+        Ud = svd.U_device
+        UtS = allreduce(data.shard, dv.get_ops().tall_gram(Ud, S))
+        basis = _Basis(Ud, None, torch.as_tensor(svd.S, device=S.buf.device),
+                       torch.as_tensor(svd.V, device=S.buf.device), UtS, {})
+    else:
+        raise ValueError(f"unknown svd mode {svd_mode!r}")
+    if timings is not None:
+        torch.cuda.synchronize()
+        timings["svd_s"] = time.perf_counter() - t0
+    return basis
+
+
+def _eig_device(Khat: torch.Tensor):
+    """eig_small (linalg.py:107-133) on the device: cuSOLVER Xgeev + residual check."""
+    w, V = dv.get_ops().geev(Khat)
+    return la._check_eig(Khat.cpu().numpy(), w, V)
+
+
+def _residual_diag(data: SnapshotMatrix, modes: DeviceModes, lam: np.ndarray):
+    """||X' - Re(phi Lam pinv(phi) X)||_F and the relative value (dmd.py:269-272)."""
+    S = data.S
+    T = S.k - 1
+    D, E = modes.basis()
+    DtS = allreduce(data.shard, dv.get_ops().tall_gram(D, S, K1=E.shape[0]))   # ncol x m
+    Y = E.conj().T @ DtS[:, :T].cpu().numpy()                                   # phi^H X
+    Z = modes.pinv_small() @ Y                                                  # pinv(phi) X
+    F = np.real(E @ (lam[:, None] * Z))                                         # ncol x T
+    out = dv.get_ops().residual(S, D, torch.as_tensor(F, device=S.buf.device), E.shape[0], T)
+    out = allreduce(data.shard, out)
+    res2, xp2 = out.cpu().numpy()
+    res = float(np.sqrt(max(res2, 0.0)))
+    return res, res / max(float(np.sqrt(xp2)), 1e-300)
+
+
+def _default_table_dtype(data: SnapshotMatrix):
+    return data.S.dtype
+
+
+# ---------------------------------------------------------------------------
+# exact DMD (dmd.py:240-274)
+# ---------------------------------------------------------------------------
+def exact_dmd(data, r, svd_mode="full", seed=None, *, oversample=None, power_iters=None,
+              residual=True, table_dtype=None, timings=None):
+    """One-shot fit of the reduced step operator (dmd.py:240-274)."""
+    data = _as_snapshots(data)
+    n, T = data.n, data.n_transitions
+    if not 1 <= r <= min(n, T):
+        raise ValueError(f"rank {r} out of range [1, {min(n, T)}]")
+    basis = _fit_basis(data, r, svd_mode, seed, oversample, power_iters, timings)
+    Sv = basis.S.cpu().numpy()
+    _check_sigma(Sv)
+    t0 = time.perf_counter()
+    VS = basis.V / basis.S[None, :]                          # V / S   (T x r)
+    Khat = basis.UtS[:, 1:] @ VS                             # U^H X' V S^-1 (dmd.py:255-256)
+    lam_raw, W = _eig_device(Khat)
+    plan = pair_plan(lam_raw)
+    Wt = torch.as_tensor(W, device=VS.device)
+    if timings is not None:
+        timings["small_s"] = time.perf_counter() - t0
+    if basis.Umap is None:
+        # full mode: phi = X' (V/S) W  (dmd.py:255,258)
+        Cmap = VS.to(torch.complex128) @ Wt
+        A, top = data.S, 1
+    else:
+        Cmap = VS.to(torch.complex128) @ Wt
+        A, top = data.S, 1
+    tdt = table_dtype or _default_table_dtype(data)
+    modes = _modes_pass(A, Cmap, plan, top, data.shard, tdt, timings)
+    model = ReducedModel(None, plan.lam, Sv, data.dt, grid_meta=data.grid_meta,
+                         provenance={"method": "exact", "svd": svd_mode, "seed": seed}, _modes=modes)
+    if svd_mode == "randomized":
+        model.provenance["sketch"] = {k: v for k, v in basis.stats.items()}
+    if residual:
+        t0 = time.perf_counter()
+        res, rel = _residual_diag(data, modes, plan.lam)
+        model.provenance["residual"] = res
+        model.provenance["residual_rel"] = rel
+        if timings is not None:
+            timings["residual_s"] = time.perf_counter() - t0
+    model.provenance["warnings"] = _stability_warnings(plan.lam)
+    return model
+
+
+# ---------------------------------------------------------------------------
+# OptDMD (dmd.py:277-455), LM on the device
+# ---------------------------------------------------------------------------
+def vandermonde(alpha, T):
+    """T x r matrix with entry (i, j) = alpha_j ** i (dmd.py:277-282)."""
+    if T < 1:
+        raise ValueError("T must be >= 1")
+    alpha = np.asarray(alpha, dtype=np.complex128)
+    return alpha[None, :] ** np.arange(T)[:, None]
+
+
+@dataclass
+class LMConfig:
+    max_iters: int = 200
+    init_damping: float = 1.0
+    damping_up: float = 2.0
+    damping_down: float = 3.0
+    rel_tol: float = 1e-8
+    collapse_tol: float = 1e-12
+
+
+class _AlphaCollapse(Exception):
+    pass
+
+
+def _vander_t(alpha: torch.Tensor, T: int) -> torch.Tensor:
+    t = torch.arange(T, device=alpha.device, dtype=torch.float64)
+    return alpha[None, :] ** t[:, None].to(alpha.dtype)
+
+
+def _min_sep_t(alpha: torch.Tensor) -> float:
+    if alpha.numel() < 2:
+        return float("inf")
+    d = (alpha[:, None] - alpha[None, :]).abs()
+    d.fill_diagonal_(float("inf"))
+    return float(d.min().item())
+
+
+def _objective_t(alpha, D, T):
+    P = _vander_t(alpha, T)
+    B = torch.linalg.lstsq(P, D).solution
+    R = D - P @ B
+    return float(torch.linalg.vector_norm(R).item()), B, P, R
+
+
+def _varpro_lm_device(D: torch.Tensor, alpha0: np.ndarray, cfg: LMConfig):
+    """dmd.py:314-363 on device tensors (complex128)."""
+    T = D.shape[0]
+    dev = D.device
+    t = torch.arange(T, device=dev, dtype=torch.float64).to(torch.complex128)
+    alpha = torch.as_tensor(np.asarray(alpha0, dtype=np.complex128), device=dev).clone()
+    if _min_sep_t(alpha) < cfg.collapse_tol:
+        raise _AlphaCollapse
+    f, B, P, R = _objective_t(alpha, D, T)
+    floor = 1e-14 * float(torch.linalg.vector_norm(D).item())
+    history = [f]
+    if cfg.max_iters == 0:
+        return alpha, B, history, True
+    mu = cfg.init_damping
+    converged = False
+    eye = torch.eye(alpha.numel(), dtype=torch.complex128, device=dev)
+    for _ in range(cfg.max_iters):
+        if f <= floor:
+            converged = True
+            break
+        Qp, _ = torch.linalg.qr(P, mode="reduced")
+        dphi = torch.zeros_like(P)
+        dphi[1:, :] = t[1:, None] * alpha[None, :] ** (t[1:, None] - 1)
+        Wk = dphi - Qp @ (Qp.mH @ dphi)
+        JHJ = (Wk.mH @ Wk) * (B @ B.mH).conj()
+        g = torch.diagonal(Wk.mH @ (R @ B.mH))
+        delta, info = torch.linalg.solve_ex(JHJ + mu * eye, g)
+        if int(info.item()) != 0:
+            mu *= cfg.damping_up
+            continue
+        cand = alpha + delta
+        if _min_sep_t(cand) < cfg.collapse_tol:
+            raise _AlphaCollapse
+        f_new, B_new, P_new, R_new = _objective_t(cand, D, T)
+        if f_new < f:
+            rel = (f - f_new) / max(f, 1e-300)
+            alpha, f, B, P, R = cand, f_new, B_new, P_new, R_new
+            history.append(f)
+            mu /= cfg.damping_down
+            if rel < cfg.rel_tol or f <= floor:
+                converged = True
+                break
+        else:
+            mu *= cfg.damping_up
+    return alpha, B, history, converged
+
+
+def _symmetrize(alpha: np.ndarray, B: np.ndarray):
+    """dmd.py:439-455."""
+    partner = conjugate_pairs(alpha)
+    alpha = alpha.copy()
+    B = B.copy()
+    for i in range(alpha.size):
+        j = partner[i]
+        if j > i:
+            a = 0.5 * (alpha[i] + np.conj(alpha[j]))
+            alpha[i] = a
+            alpha[j] = np.conj(a)
+            row = 0.5 * (B[i, :] + np.conj(B[j, :]))
+            B[i, :] = row
+            B[j, :] = np.conj(row)
+        elif j == i and abs(alpha[i].imag) <= 1e-8 * max(abs(alpha[i]), 1e-300):
+            alpha[i] = alpha[i].real
+            B[i, :] = B[i, :].real
+    return alpha, B
+
+
+def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, oversample=None,
+           power_iters=None, table_dtype=None, timings=None):
+    """Variable-projection refit of the eigenvalues (dmd.py:366-436)."""
+    cfg = lm_config or LMConfig()
+    data = _as_snapshots(data)
+    n, T = data.n, data.n_transitions
+    if not 1 <= r <= min(n, T):
+        raise ValueError(f"rank {r} out of range [1, {min(n, T)}]")
+    basis = _fit_basis(data, r, svd_mode, seed, oversample, power_iters, timings)
+    Sv = basis.S.cpu().numpy()
+    _check_sigma(Sv)
+    t0 = time.perf_counter()
+    Dm = (basis.V.conj() * basis.S[None, :]).to(torch.complex128)      # dmd.py:384
+    if init is None:
+        # alpha0 = exact_dmd(data, r, svd_mode, seed).lam (dmd.py:387): the same
+        # seed reproduces the same SVD, so the eigenvalues come from it directly.
+        VS = basis.V / basis.S[None, :]
+        Khat = basis.UtS[:, 1:] @ VS
+        lam_raw, _ = _eig_device(Khat)
+        alpha0 = pair_plan(lam_raw).lam
+    else:
+        alpha0 = np.asarray(init, dtype=np.complex128)
+        if alpha0.size != r:
+            raise ValueError(f"init has {alpha0.size} eigenvalues, expected {r}")
+    try:
+        alpha, B, history, converged = _varpro_lm_device(Dm, alpha0, cfg)
+    except _AlphaCollapse:
+        rng = np.random.default_rng(0 if seed is None else seed)
+        jitter = 1e-10 * (1.0 + np.abs(alpha0)) * np.exp(2j * np.pi * rng.random(alpha0.size))
+        try:
+            alpha, B, history, converged = _varpro_lm_device(Dm, alpha0 + jitter, cfg)
+        except _AlphaCollapse:
+            raise ConvergenceError("eigenvalue iterates collapsed below separation tolerance twice") from None
+    alpha_h = alpha.cpu().numpy()
+    B_h = B.cpu().numpy()
+    a_s, B_s = _symmetrize(alpha_h, B_h)
+    Dh = Dm.cpu().numpy()
+    f_sym = float(np.linalg.norm(Dh - vandermonde(a_s, T) @ B_s))
+    if f_sym <= history[-1] * (1 + 1e-9) and f_sym <= history[0] * (1 + 1e-12):
+        alpha_h, B_h = a_s, B_s
+    if timings is not None:
+        timings["lm_s"] = time.perf_counter() - t0
+    plan = pair_plan(alpha_h)
+    # phi = U @ B.T (dmd.py:414) with U = A @ Umap
+    Bt = torch.as_tensor(B_h.T.copy(), device=basis.V.device)                # r x r
+    if basis.Umap is None:
+        Cmap = Bt
+    else:
+        Cmap = basis.Umap.to(torch.complex128) @ Bt                          # l x r
+    tdt = table_dtype or _default_table_dtype(data)
+    modes = _modes_pass(basis.A, Cmap, plan, 0, data.shard, tdt, timings)
+    model = ReducedModel(None, plan.lam, Sv, data.dt, grid_meta=data.grid_meta,
+                         provenance={"method": "optdmd", "svd": svd_mode, "seed": seed,
+                                     "objective_history": history, "converged": converged},
+                         _modes=modes)
+    warns = _stability_warnings(plan.lam)
+    if not converged and cfg.max_iters > 0:
+        warns.append(f"variable projection hit max_iters={cfg.max_iters}")
+        warnings.warn(warns[-1], RuntimeWarning, stacklevel=2)
+    model.provenance["warnings"] = warns
+    return model
+
+
+# ---------------------------------------------------------------------------
+# control channels (dmd.py:458-491)
+# ---------------------------------------------------------------------------
+@dataclass
+class ControlOperator:
+    reduced_b: list
+    labels: list
+
+    def __post_init__(self):
+        if len(self.reduced_b) != len(self.labels):
+            raise ValueError("one label per channel required")
+        self.reduced_b = [np.asarray(m, dtype=np.complex128) for m in self.reduced_b]
+
+
+def fit_control(model, channels, labels=None):
+    """Project each force-response matrix into the trained basis:
+    reduced_b_i = pinv(phi) @ B_i (dmd.py:471-491), via the device table."""
+    labels = labels or [f"channel_{k}" for k in range(len(channels))]
+    reduced = []
+    dev = model.modes.table.buf.device
+    for mat in channels:
+        if mat.shape[0] != model.n:
+            raise ValueError(f"channel has {mat.shape[0]} rows, model state length is {model.n}")
+        if hasattr(mat, "toarray") and not isinstance(mat, np.ndarray):
+            mat = mat.toarray()
+        if isinstance(mat, torch.Tensor):
+            Bt = mat.to(dev)
+        else:
+            Bt = torch.as_tensor(np.asarray(mat, dtype=np.float64), device=dev)
+        if Bt.is_complex():
+            re = model.modes.project(Bt.real.t().contiguous())
+            im = model.modes.project(Bt.imag.t().contiguous())
+            red = re + 1j * im
+        else:
+            red = model.modes.project(Bt.t().contiguous())
+        reduced.append(red)
+    return ControlOperator(reduced, list(labels))
+
+
+# ---------------------------------------------------------------------------
+# Control-augmented DMDc (BASELINE config 2). No reference implementation:
+# the reference's DMDc is fit_control with known B (dmd.py:471-491), joint
+# identification is a declared non-goal. Parity unpinned;
+# restated from Proctor et al. 2016 as cited at PAPER.md:420.
+# ---------------------------------------------------------------------------
+def dmdc_fit(data, controls, r_aug, r, seed=None, *, oversample=10, power_iters=1,
+             table_dtype=None, timings=None):
+    """Returns (ReducedModel, ControlOperator) for x_{j+1} = A x_j + B u_j.
+
+    controls: ell x T host array (u_j for j < T). The augmented matrix
+    [X; Upsilon] is sketched at rank r_aug; the output basis U_hat is a rank-r
+    sketch of X' (seed + 1). reduced_b is scaled by 1/dt so that
+    runtime.step_forced (which multiplies by dt, runtime.py:188) reproduces
+    B u_j exactly.
+    """
+    data = _as_snapshots(data)
+    if data.shard is not None and data.shard.world > 1:
+        raise ValueError("dmdc_fit is single-device in this round")
+    S = data.S
+    n, m = S.n, S.k
+    T = m - 1
+    Ups = np.asarray(controls, dtype=np.float64)
+    if Ups.ndim != 2 or Ups.shape[1] != T:
+        raise ValueError(f"controls must be ell x {T}")
+    ell = Ups.shape[0]
+    dev = S.buf.device
+    # augmented tall matrix: rows [S; Upsilon | 0]
+    Aug = alloc_tall(n + ell, m, S.dtype, "row", device=dev, zero=False)
+    Aug.buf[:n].copy_(S.buf[:n])
+    tail = torch.zeros((ell, Aug.ld), dtype=S.dtype, device=dev)
+    tail[:, :T] = torch.as_tensor(Ups, dtype=S.dtype, device=dev)
+    Aug.buf[n:n + ell].copy_(tail)
+    t0 = time.perf_counter()
+    p1 = min(oversample, min(n + ell, T) - r_aug)
+    f1 = la.sketch_factors(Aug, T, r_aug + p1, power_iters, la.draw_omega(T, r_aug + p1, seed))
+    p2 = min(oversample, min(n, T) - r)
+    # sketch of X' = S[:, 1:]: shift by viewing S with column offset through padded smalls
+    f2 = _sketch_shifted(S, 1, T, r + p2, power_iters, la.draw_omega(T, r + p2, None if seed is None else seed + 1))
+    Ub1 = f1.Ub[:, :r_aug]
+    s1 = f1.s[:r_aug]
+    V1 = f1.Vh[:r_aug].t()
+    Ub2 = f2.Ub[:, :r]
+    # U1^T Uhat = Ub1^T (Q1[:n]^T Q2) Ub2
+    Q1top = Tall(f1.Q.buf, "row", n, f1.Q.k)
+    M12 = dv.get_ops().tall_gram(Q1top, f2.Q)                          # l1 x l2
+    U1tUh = Ub1.t() @ M12 @ Ub2                                        # r_aug x r
+    U2 = f1.Q.buf[n:n + ell, : f1.Q.k].to(torch.float64) @ Ub1        # ell x r_aug
+    UhtXp = Ub2.t() @ f2.QtS[:, 1:]                                    # r x T
+    core = UhtXp @ (V1 / s1[None, :])                                  # r x r_aug
+    Atil = core @ U1tUh                                                # r x r
+    Btil = core @ U2.t()                                               # r x ell
+    lam_raw, W = _eig_device(Atil)
+    plan = pair_plan(lam_raw)
+    Wt = torch.as_tensor(W, device=dev)
+    Cmap = ((V1 / s1[None, :]) @ U1tUh).to(torch.complex128) @ Wt     # T x r
+    if timings is not None:
+        torch.cuda.synchronize()
+        timings["svd_s"] = time.perf_counter() - t0
+    tdt = table_dtype or S.dtype
+    modes = _modes_pass(S, Cmap, plan, 1, None, tdt, timings)
+    model = ReducedModel(None, plan.lam, s1.cpu().numpy()[:r] if r <= r_aug else s1.cpu().numpy(),
+                         data.dt, grid_meta=data.grid_meta,
+                         provenance={"method": "dmdc", "svd": "randomized", "seed": seed,
+                                     "r_aug": r_aug}, _modes=modes)
+    # reduced_b = pinv(phi) U_hat B~ / dt, U_hat = Q2 Ub2
+    D, E = modes.basis()
+    DtQ2 = dv.get_ops().tall_gram(D, f2.Q, K1=E.shape[0])              # ncol x l2
+    y = (DtQ2 @ Ub2 @ Btil).cpu().numpy()                              # ncol x ell
+    red = modes.pinv_small() @ (E.conj().T @ y) / data.dt
+    ctrl = ControlOperator([red], ["augmented"])
+    model.provenance["A_tilde"] = Atil.cpu().numpy()
+    model.provenance["B_tilde"] = Btil.cpu().numpy()
+    return model, ctrl
+
+
+def _sketch_shifted(S: Tall, c0: int, T: int, l: int, q: int, omega: np.ndarray):
+    """sketch_factors for X = S[:, c0:c0+T] (zero-padded small factors)."""
+    ops = dv.get_ops()
+    dev = S.buf.device
+    m = S.k
+
+    def pad(B):
+        out = torch.zeros((m, B.shape[1]), dtype=torch.float64, device=dev)
+        out[c0:c0 + B.shape[0]] = B
+        return out
+
+    Q = alloc_tall(S.n, l, torch.float64, "row", device=dev)
+    ops.tall_gemm(S, pad(torch.as_tensor(omega, device=dev)), Q)
+    la.cholqr2_inplace(Q)
+    for _ in range(q):
+        Z = ops.tall_gram(S, Q)
+        W, _ = torch.linalg.qr(Z[c0:c0 + T], mode="reduced")
+        ops.tall_gemm(S, pad(W), Q)
+        la.cholqr2_inplace(Q)
+    QtS = ops.tall_gram(Q, S)
+    B = QtS[:, c0:c0 + T]
+    Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvd" if B.is_cuda else None)
+    # QtS re-indexed so that column 1.. of the returned block is Q^T X'_{shifted}
+    return la.SketchFactors(Q, Ub, s, Vh, QtS, {})

@@ -1,0 +1,393 @@
+"""Device linear algebra for the DMD fit, mirroring `flowdmd.linalg`
+(reference linalg.py:1-141) with the same names and semantics.
+
+Tall work (n rows) runs in libfdmd FP64 DMMA kernels; small factors
+(<= a few hundred on a side) stay on the device in cuSOLVER/cuBLAS via
+torch.linalg (preferred library forced to cuSOLVER). The orthonormalisation
+of the sketch is CholeskyQR2 (two Gram + Cholesky + triangular-apply passes)
+instead of Householder (linalg.py:82,85), falling back to shifted CholeskyQR3
+when the sketch is ill-conditioned and to a device Householder QR when it is
+numerically rank deficient.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import device as dv
+from .device import Shard, Tall, allreduce, alloc_tall
+from .errors import ConvergenceError
+
+if torch.cuda.is_available():
+    try:
+        torch.backends.cuda.preferred_linalg_library("cusolver")
+    except Exception:  # pragma: no cover
+        pass
+
+# condition number of R1 above which CholeskyQR2 is replaced by shifted CholeskyQR3
+CHOLQR2_COND_LIMIT = 3e7
+
+
+# ---------------------------------------------------------------------------
+# result type (linalg.py:17-26)
+# ---------------------------------------------------------------------------
+class SvdResult:
+    """Truncated SVD factors ``M ~ U @ diag(S) @ V.conj().T``.
+
+    ``U`` may live on the device (``U_device``, a column-major n x r table);
+    the host array is materialised on first access, as the reference returns
+    numpy arrays (linalg.py:17-26).
+    """
+
+    def __init__(self, U, S, V, U_device: Optional[Tall] = None, shard: Optional[Shard] = None):
+        self._U = U
+        self.S = np.asarray(S)
+        self.V = np.asarray(V)
+        self.U_device = U_device
+        self.shard = shard
+
+    @property
+    def U(self):
+        if self._U is None:
+            self._U = self.U_device.view().double().cpu().numpy().copy()
+        return self._U
+
+    @U.setter
+    def U(self, value):
+        self._U = value
+
+    def reconstruct(self):
+        return (self.U * self.S) @ self.V.conj().T
+
+
+# ---------------------------------------------------------------------------
+# upload helpers
+# ---------------------------------------------------------------------------
+def as_tall(M, device=None) -> Tall:
+    """Host (numpy) or device (torch) 2-D matrix -> row-major device Tall.
+    fp32 stays fp32 (it is upcast exactly inside the kernels); everything
+    else becomes fp64, as the reference coerces to float64 (dmd.py:36)."""
+    if isinstance(M, Tall):
+        return M
+    device = device or dv.default_device()
+    if isinstance(M, torch.Tensor):
+        t = M
+        dtype = torch.float32 if t.dtype == torch.float32 else torch.float64
+    else:
+        a = np.asarray(M)
+        if np.iscomplexobj(a):
+            raise ValueError("complex snapshot matrices are not supported on the device path")
+        dtype = torch.float32 if a.dtype == np.float32 else torch.float64
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32 if dtype == torch.float32 else np.float64))
+    if t.ndim != 2:
+        raise ValueError("matrix must be 2-D")
+    n, k = int(t.shape[0]), int(t.shape[1])
+    T = alloc_tall(n, k, dtype, "row", device=device)
+    if T.ld > k:
+        T.buf[:, k:].zero_()
+    copy_rows_h2d(T, t)
+    return T
+
+
+def copy_rows_h2d(T: Tall, t: torch.Tensor, row0: int = 0):
+    """Copy a (rows x k) host/device tensor into rows [row0, row0+rows) of a
+    row-major Tall with a pitched 2-D copy (no staging buffer)."""
+    import ctypes
+
+    from . import _lib
+    rows, k = int(t.shape[0]), int(t.shape[1])
+    if t.dtype != T.dtype:
+        t = t.to(T.dtype)
+    t = t.contiguous()
+    elt = t.element_size()
+    dst = T.buf.data_ptr() + row0 * T.ld * elt
+    kind = 4  # cudaMemcpyDefault (UVA)
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _lib.check(_lib.lib().fdmd_copy2d(ctypes.c_void_p(dst), T.ld * elt, ctypes.c_void_p(t.data_ptr()),
+                                      k * elt, k * elt, rows, kind, stream), "copy2d")
+
+
+# ---------------------------------------------------------------------------
+# CholeskyQR2 / shifted CholeskyQR3 (replaces np.linalg.qr at linalg.py:82,85)
+# ---------------------------------------------------------------------------
+def _chol_upper(G: torch.Tensor):
+    L, info = torch.linalg.cholesky_ex(G)
+    if int(info.item()) != 0:
+        return None
+    return L.mH
+
+
+def _apply_rinv(Y: Tall, R: torch.Tensor, shard: Optional[Shard]):
+    """Y <- Y R^-1 in place (R upper triangular, l x l)."""
+    l = R.shape[0]
+    eye = torch.eye(l, dtype=torch.float64, device=R.device)
+    Rinv = torch.linalg.solve_triangular(R, eye, upper=True)
+    dv.get_ops().tall_gemm(Y, Rinv, Y)
+
+
+def cholqr2_inplace(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict] = None) -> torch.Tensor:
+    """Orthonormalise the columns of Y in place. Returns R (Y_in = Q R)."""
+    ops = dv.get_ops()
+    l = Y.k
+    G = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
+    R1 = _chol_upper(G)
+    if R1 is None:
+        return _householder_inplace(Y, shard, stats)
+    cond = float(torch.linalg.cond(R1).item())
+    if stats is not None:
+        stats.setdefault("cond_R1", []).append(cond)
+    if cond > CHOLQR2_COND_LIMIT:
+        # shifted CholeskyQR3 (Fukaya et al. 2020): shift makes the first
+        # factorisation succeed with kappa(Q1) ~ sqrt(1/u); two CholQR passes follow.
+        u = np.finfo(np.float64).eps / 2
+        nrm2 = float(torch.linalg.matrix_norm(G, ord=2).item())
+        n_tot = Y.n if shard is None else shard.n_global
+        s = 11.0 * (n_tot * l + l * (l + 1)) * u * nrm2
+        R0 = _chol_upper(G + s * torch.eye(l, dtype=G.dtype, device=G.device))
+        if R0 is None:
+            return _householder_inplace(Y, shard, stats)
+        _apply_rinv(Y, R0, shard)
+        G = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
+        R1b = _chol_upper(G)
+        if R1b is None:
+            return _householder_inplace(Y, shard, stats)
+        _apply_rinv(Y, R1b, shard)
+        R1 = R1b @ R0
+        if stats is not None:
+            stats["shifted_cholqr3"] = stats.get("shifted_cholqr3", 0) + 1
+    else:
+        _apply_rinv(Y, R1, shard)
+    G2 = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
+    R2 = _chol_upper(G2)
+    if R2 is None:
+        raise ConvergenceError("CholeskyQR2: second Gram not positive definite")
+    _apply_rinv(Y, R2, shard)
+    return R2 @ R1
+
+
+def _householder_inplace(Y: Tall, shard: Optional[Shard], stats: Optional[dict]) -> torch.Tensor:
+    """Numerically rank-deficient sketch: Householder QR on the device
+    (cuSOLVER geqrf/orgqr), matching the reference's np.linalg.qr."""
+    if shard is not None and shard.world > 1:
+        raise ConvergenceError("rank-deficient sketch on a row-sharded matrix (TSQR not implemented)")
+    if stats is not None:
+        stats["householder_fallback"] = stats.get("householder_fallback", 0) + 1
+    Q, R = torch.linalg.qr(Y.view().to(torch.float64), mode="reduced")
+    Y.view().copy_(Q.to(Y.dtype))
+    return R
+
+
+# ---------------------------------------------------------------------------
+# randomized SVD core (linalg.py:62-90) over the first T columns of S
+# ---------------------------------------------------------------------------
+def draw_omega(cols: int, l: int, seed) -> np.ndarray:
+    """Exactly linalg.py:80-81: the host-drawn float64 Gaussian test matrix."""
+    return np.random.default_rng(seed).standard_normal((cols, l))
+
+
+@dataclass
+class SketchFactors:
+    Q: Tall            # n x l, fp64, orthonormal columns
+    Ub: torch.Tensor   # l x l
+    s: torch.Tensor    # l
+    Vh: torch.Tensor   # l x T
+    QtS: torch.Tensor  # l x m (Q^T S: both Q^T X and Q^T X')
+    stats: dict
+
+
+def _pad_rows(Bsmall: torch.Tensor, rows: int) -> torch.Tensor:
+    if Bsmall.shape[0] == rows:
+        return Bsmall.contiguous()
+    out = torch.zeros((rows, Bsmall.shape[1]), dtype=torch.float64, device=Bsmall.device)
+    out[: Bsmall.shape[0]] = Bsmall
+    return out
+
+
+def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Optional[Shard] = None,
+                   Q: Optional[Tall] = None) -> SketchFactors:
+    """Range finder + power passes + projection for X = S[:, :T].
+
+    Kernel sequence (DESIGN.md §Fit pipeline): Y = S[Omega;0] -> CholQR2 ->
+    q x {Z = S^T Q (allreduce) -> W = qr(Z[:T]) -> Y = S[W;0] -> CholQR2} ->
+    Q^T S (allreduce) -> svd(Q^T X) on device.
+    """
+    ops = dv.get_ops()
+    dev = S.buf.device
+    m = S.k
+    stats: dict = {}
+    if Q is None:
+        Q = alloc_tall(S.n, l, torch.float64, "row", device=dev)
+    Om = torch.as_tensor(np.asarray(omega, dtype=np.float64), device=dev)
+    ops.tall_gemm(S, _pad_rows(Om, m), Q)
+    cholqr2_inplace(Q, shard, stats)
+    for _ in range(q):
+        Z = allreduce(shard, ops.tall_gram(S, Q))            # m x l
+        W, _ = torch.linalg.qr(Z[:T], mode="reduced")        # T x l (Householder, device)
+        ops.tall_gemm(S, _pad_rows(W, m), Q)
+        cholqr2_inplace(Q, shard, stats)
+    QtS = allreduce(shard, ops.tall_gram(Q, S))              # l x m
+    B = QtS[:, :T]
+    Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvd" if B.is_cuda else None)
+    return SketchFactors(Q, Ub, s, Vh, QtS, stats)
+
+
+def _canonical_signs(Q: Tall, Ub_r: torch.Tensor, shard: Optional[Shard]) -> torch.Tensor:
+    """Sign of U = Q Ub_r at each column's first largest-|.| entry
+    (linalg.py:29-44 for real U), found by a statistics-only DMMA pass."""
+    ops = dv.get_ops()
+    r = Ub_r.shape[1]
+    Bp = torch.zeros((Ub_r.shape[0], 2 * r), dtype=torch.float64, device=Ub_r.device)
+    Bp[:, 0::2] = Ub_r
+    row0 = 0 if shard is None else shard.row0
+    st = ops.tall_gemm(Q, Bp, None, stats=True, row_offset=row0)   # (r, 3)
+    st = _reduce_pair_stats(st, shard)
+    idx = st[:, 2].round().long()
+    local = idx - row0
+    if shard is not None and shard.world > 1:
+        own = (local >= 0) & (local < Q.n)
+        rows = torch.zeros((r, Q.k), dtype=torch.float64, device=Ub_r.device)
+        rows[own] = Q.view()[local[own]].to(torch.float64)
+        rows = shard.allreduce(rows)
+    else:
+        rows = Q.view()[local].to(torch.float64)
+    piv = (rows * Ub_r.t()).sum(dim=1)
+    return torch.where(piv < 0, -1.0, 1.0).to(torch.float64)
+
+
+def _reduce_pair_stats(st: torch.Tensor, shard: Optional[Shard]) -> torch.Tensor:
+    """Combine per-rank [sumsq, max, argmax] (argmax ties -> lowest global row)."""
+    if shard is None or shard.world <= 1:
+        return st
+    import torch.distributed as dist
+    gathered = [torch.empty_like(st) for _ in range(shard.world)]
+    dist.all_gather(gathered, st.contiguous(), group=shard.group)
+    out = gathered[0].clone()
+    out[:, 0] = 0.0
+    for g in gathered:                                       # fixed rank order
+        out[:, 0] += g[:, 0]
+    best = gathered[0][:, 1].clone()
+    bidx = gathered[0][:, 2].clone()
+    for g in gathered[1:]:
+        better = (g[:, 1] > best) | ((g[:, 1] == best) & (g[:, 2] < bidx))
+        best = torch.where(better, g[:, 1], best)
+        bidx = torch.where(better, g[:, 2], bidx)
+    out[:, 1], out[:, 2] = best, bidx
+    return out
+
+
+def _validate_rank(rows, cols, r, l=None):
+    if not 1 <= r <= min(rows, cols):
+        raise ValueError(f"rank {r} out of range [1, {min(rows, cols)}]")
+    if l is not None and l > min(rows, cols):
+        raise ValueError(f"rank + oversample = {l} exceeds min dimension {min(rows, cols)}")
+
+
+def randomized_svd(M, r, oversample=10, power_iters=2, seed=None, *, omega=None,
+                   shard: Optional[Shard] = None, keep_device=False) -> SvdResult:
+    """Sketched SVD (linalg.py:62-90): same Omega (default_rng(seed)), same
+    power count, same canonicalisation; CholeskyQR2 replaces Householder QR."""
+    A = as_tall(M)
+    n_tot = A.n if shard is None else shard.n_global
+    rows, cols = n_tot, A.k
+    l = r + oversample
+    _validate_rank(rows, cols, r, l)
+    G = draw_omega(cols, l, seed) if omega is None else np.asarray(omega, dtype=np.float64)
+    f = sketch_factors(A, cols, l, power_iters, G, shard)
+    Ub_r = f.Ub[:, :r].contiguous()
+    sgn = _canonical_signs(f.Q, Ub_r, shard)
+    Ub_r = Ub_r * sgn[None, :]
+    V = (f.Vh[:r].t() * sgn[None, :]).contiguous()
+    U = alloc_tall(A.n, r, torch.float64, "col", device=A.buf.device)
+    dv.get_ops().tall_gemm(f.Q, Ub_r, U)                     # lift U = Q Ub_r (linalg.py:88)
+    res = SvdResult(None, f.s[:r].cpu().numpy().copy(), V.cpu().numpy(), U_device=U, shard=shard)
+    if not keep_device:
+        _ = res.U
+    return res
+
+
+def truncated_svd(M, r, *, shard: Optional[Shard] = None, keep_device=False) -> SvdResult:
+    """Dense truncated SVD (linalg.py:47-59) of a tall matrix on the device:
+    Householder QR (cuSOLVER) then SVD of the small R factor."""
+    A = as_tall(M)
+    if shard is not None and shard.world > 1:
+        raise ValueError("svd_mode='full' is single-device; use 'randomized' for row-sharded data")
+    rows, cols = A.n, A.k
+    if not 1 <= r <= min(rows, cols):
+        raise ValueError(f"rank {r} out of range [1, {min(rows, cols)}]")
+    X = A.view().to(torch.float64)
+    if rows >= cols:
+        Qf, Rf = torch.linalg.qr(X, mode="reduced")
+        Ur, s, Vh = torch.linalg.svd(Rf, full_matrices=False, driver="gesvd" if Rf.is_cuda else None)
+        Ufull = Qf @ Ur
+    else:
+        Ufull, s, Vh = torch.linalg.svd(X, full_matrices=False, driver="gesvd" if X.is_cuda else None)
+    U = Ufull[:, :r]
+    V = Vh[:r].t()
+    idx = torch.argmax(U.abs(), dim=0)
+    piv = U[idx, torch.arange(r, device=U.device)]
+    sgn = torch.where(piv < 0, -1.0, 1.0).to(torch.float64)
+    U = U * sgn[None, :]
+    V = V * sgn[None, :]
+    Ut = alloc_tall(rows, r, torch.float64, "col", device=A.buf.device)
+    Ut.view().copy_(U)
+    res = SvdResult(None, s[:r].cpu().numpy().copy(), V.cpu().numpy(), U_device=Ut)
+    if not keep_device:
+        _ = res.U
+    return res
+
+
+# ---------------------------------------------------------------------------
+# small dense helpers (linalg.py:93-141)
+# ---------------------------------------------------------------------------
+def pinv(M, rel_tol=1e-12):
+    """SVD pseudo-inverse (linalg.py:93-104) of a small matrix, on the device."""
+    if not 0 < rel_tol < 1:
+        raise ValueError(f"rel_tol must lie in (0, 1), got {rel_tol}")
+    A = np.asarray(M)
+    dev = dv.default_device()
+    t = torch.as_tensor(A, device=dev)
+    U, s, Vh = torch.linalg.svd(t, full_matrices=False)
+    if s.numel() == 0 or float(s[0]) == 0.0:
+        return np.zeros((A.shape[1], A.shape[0]), dtype=A.dtype)
+    keep = s > rel_tol * s[0]
+    inv = torch.where(keep, 1.0 / torch.where(keep, s, torch.ones_like(s)), torch.zeros_like(s))
+    return ((Vh.mH * inv.to(Vh.dtype)) @ U.mH).cpu().numpy()
+
+
+def eig_small(M, max_dim=2000):
+    """Eigendecomposition with residual check (linalg.py:107-133); real
+    input runs cuSOLVER Xgeev on the device."""
+    A = np.asarray(M)
+    if A.ndim != 2 or A.shape[0] != A.shape[1]:
+        raise ValueError(f"matrix must be square, got {A.shape}")
+    if A.shape[0] > max_dim:
+        raise ValueError(f"dense eig limited to {max_dim}, got {A.shape[0]}")
+    dev = dv.default_device()
+    if np.iscomplexobj(A):
+        raise ValueError("eig_small on the device path takes real matrices (the DMD operator is real)")
+    w, V = dv.get_ops().geev(torch.as_tensor(A, dtype=torch.float64, device=dev))
+    return _check_eig(A, w, V)
+
+
+def _check_eig(A, w, V):
+    norms = np.linalg.norm(V, axis=0)
+    norms[norms == 0.0] = 1.0
+    V = V / norms
+    scale = np.linalg.norm(A)
+    resid = np.linalg.norm(A @ V - V * w)
+    if scale > 0 and resid > 1e-8 * scale:
+        raise ConvergenceError(f"eigendecomposition residual {resid:.3e} exceeds 1e-8 * ||M||",
+                               residual=resid)
+    return w, V
+
+
+def lstsq(A, B):
+    """Least-squares solve (linalg.py:136-141) on the device."""
+    dev = dv.default_device()
+    At = torch.as_tensor(np.asarray(A), device=dev)
+    Bt = torch.as_tensor(np.asarray(B), device=dev)
+    return torch.linalg.lstsq(At, Bt).solution.cpu().numpy()

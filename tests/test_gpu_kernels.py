@@ -1,0 +1,182 @@
+"""Kernel-level numerics of libfdmd on the GPU against numpy fp64 (the
+oracle for plain linear algebra). FP64 kernels must match to ~1e-13
+relative; fp32 outputs to fp32 rounding."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dv():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2502_05339_b200 import device
+    return device
+
+
+def _tall_from(dv, M, layout, dtype):
+    n, k = M.shape
+    T = dv.alloc_tall(n, k, dtype, layout, zero=True)
+    src = torch.as_tensor(M, dtype=dtype)
+    if layout == "row":
+        T.buf[:n, :k].copy_(src)
+    else:
+        T.buf[:k, :n].copy_(src.t())
+    return T
+
+
+@pytest.mark.parametrize("a_layout", ["row", "col"])
+@pytest.mark.parametrize("a_dtype", ["f32", "f64"])
+@pytest.mark.parametrize("c_layout,c_dtype", [("row", "f64"), ("col", "f64"), ("col", "f32"), ("row", "f32")])
+@pytest.mark.parametrize("shape", [(1000, 37, 20), (4099, 201, 210), (130, 16, 130), (64, 5, 3), (7, 201, 160)])
+def test_tall_gemm(dv, a_layout, a_dtype, c_layout, c_dtype, shape):
+    n, K, N = shape
+    rng = np.random.default_rng(n + K + N)
+    A = rng.standard_normal((n, K))
+    ta = torch.float32 if a_dtype == "f32" else torch.float64
+    if a_dtype == "f32":
+        A = A.astype(np.float32).astype(np.float64)
+    B = rng.standard_normal((K, N))
+    At = _tall_from(dv, A, a_layout, ta)
+    tc = torch.float32 if c_dtype == "f32" else torch.float64
+    C = dv.alloc_tall(n, N, tc, c_layout)
+    dv.get_ops().tall_gemm(At, torch.as_tensor(B, device="cuda"), C)
+    got = C.view().double().cpu().numpy()
+    want = A @ B
+    tol = 1e-6 if c_dtype == "f32" else 1e-12
+    assert np.abs(got - want).max() <= tol * max(np.abs(want).max(), 1.0)
+
+
+def test_tall_gemm_pair_stats(dv):
+    rng = np.random.default_rng(3)
+    n, K, U = 5000, 31, 9
+    A = rng.standard_normal((n, K))
+    B = rng.standard_normal((K, 2 * U))
+    At = _tall_from(dv, A, "row", torch.float64)
+    C = dv.alloc_tall(n, 2 * U, torch.float64, "col")
+    st = dv.get_ops().tall_gemm(At, torch.as_tensor(B, device="cuda"), C, stats=True, row_offset=11).cpu().numpy()
+    P = A @ B
+    mag = P[:, 0::2] ** 2 + P[:, 1::2] ** 2
+    np.testing.assert_allclose(st[:, 0], mag.sum(0), rtol=1e-12)
+    np.testing.assert_allclose(st[:, 1], mag.max(0), rtol=1e-13)
+    np.testing.assert_array_equal(st[:, 2].astype(np.int64), mag.argmax(0) + 11)
+    # stats-only pass (no output) gives the same statistics
+    st2 = dv.get_ops().tall_gemm(At, torch.as_tensor(B, device="cuda"), None, stats=True, row_offset=11).cpu().numpy()
+    np.testing.assert_array_equal(st, st2)
+
+
+def test_tall_gemm_inplace(dv):
+    rng = np.random.default_rng(4)
+    n, l = 3000, 200
+    Y = rng.standard_normal((n, l))
+    R = np.triu(rng.standard_normal((l, l))) + 5 * np.eye(l)
+    Yt = _tall_from(dv, Y, "row", torch.float64)
+    dv.get_ops().tall_gemm(Yt, torch.as_tensor(R, device="cuda"), Yt)
+    np.testing.assert_allclose(Yt.view().cpu().numpy(), Y @ R, rtol=0, atol=1e-11 * np.abs(Y @ R).max())
+
+
+@pytest.mark.parametrize("la,lb", [("row", "row"), ("col", "row"), ("row", "col"), ("col", "col")])
+@pytest.mark.parametrize("da,db", [("f32", "f32"), ("f64", "f32"), ("f64", "f64")])
+@pytest.mark.parametrize("shape", [(10000, 200, 201), (333, 30, 101), (17, 5, 3), (70000, 64, 64)])
+def test_tall_gram(dv, la, lb, da, db, shape):
+    n, K1, K2 = shape
+    rng = np.random.default_rng(n + K1)
+    A = rng.standard_normal((n, K1))
+    B = rng.standard_normal((n, K2))
+    if da == "f32":
+        A = A.astype(np.float32).astype(np.float64)
+    if db == "f32":
+        B = B.astype(np.float32).astype(np.float64)
+    At = _tall_from(dv, A, la, torch.float32 if da == "f32" else torch.float64)
+    Bt = _tall_from(dv, B, lb, torch.float32 if db == "f32" else torch.float64)
+    G = dv.get_ops().tall_gram(At, Bt).cpu().numpy()
+    want = A.T @ B
+    assert np.abs(G - want).max() <= 1e-12 * np.abs(want).max() * max(1, np.sqrt(n) / 100)
+
+
+def test_tall_gram_symmetric_deterministic(dv):
+    rng = np.random.default_rng(5)
+    Y = rng.standard_normal((200000, 210))
+    Yt = _tall_from(dv, Y, "row", torch.float64)
+    G1 = dv.get_ops().tall_gram(Yt, Yt, symmetric=True).cpu().numpy()
+    G2 = dv.get_ops().tall_gram(Yt, Yt, symmetric=True).cpu().numpy()
+    assert np.array_equal(G1, G2)
+    assert np.array_equal(G1, G1.T)
+    np.testing.assert_allclose(G1, Y.T @ Y, rtol=0, atol=1e-12 * np.abs(Y.T @ Y).max())
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("B", [1, 2, 3, 8, 13, 32, 45])
+@pytest.mark.parametrize("n,r", [(10007, 150), (64, 7), (100003, 200)])
+def test_decode(dv, dtype, B, n, r):
+    rng = np.random.default_rng(B * 7 + r)
+    D = rng.standard_normal((n, r))
+    C = rng.standard_normal((r, B))
+    td = torch.float32 if dtype == "f32" else torch.float64
+    if dtype == "f32":
+        D = D.astype(np.float32).astype(np.float64)
+        C = C.astype(np.float32).astype(np.float64)
+    Dt = _tall_from(dv, D, "col", td)
+    out = dv.get_ops().decode(Dt, torch.as_tensor(C, device="cuda", dtype=td)).double().cpu().numpy()
+    want = (D @ C).T
+    tol = 2e-6 if dtype == "f32" else 1e-13
+    assert np.linalg.norm(out - want) <= tol * np.linalg.norm(want)
+
+
+@pytest.mark.parametrize("nv", [1, 3, 8])
+def test_colmajor_dot(dv, nv):
+    rng = np.random.default_rng(nv)
+    n, r = 123457, 40
+    D = rng.standard_normal((n, r))
+    U = rng.standard_normal((nv, n))
+    Dt = _tall_from(dv, D, "col", torch.float64)
+    y = dv.get_ops().colmajor_dot(Dt, torch.as_tensor(U, device="cuda")).cpu().numpy()
+    np.testing.assert_allclose(y, D.T @ U.T, rtol=1e-11, atol=1e-11 * np.abs(D.T @ U.T).max())
+
+
+def test_table_apply_and_residual(dv):
+    rng = np.random.default_rng(9)
+    n, U, m = 20000, 5, 12
+    R = rng.standard_normal((n, 2 * U))
+    Rt = _tall_from(dv, R, "col", torch.float64)
+    src = [0, 0, 3, 4, 2]
+    al = rng.standard_normal(5)
+    be = rng.standard_normal(5)
+    Dt = dv.alloc_tall(n, 5, torch.float64, "col")
+    dv.get_ops().table_apply(Rt, src, al, be, Dt, 5)
+    D = Dt.view().cpu().numpy()
+    want = np.stack([al[j] * R[:, 2 * src[j]] + be[j] * R[:, 2 * src[j] + 1] for j in range(5)], axis=1)
+    np.testing.assert_allclose(D, want, rtol=1e-14, atol=1e-14)
+    S = rng.standard_normal((n, m))
+    St = _tall_from(dv, S, "row", torch.float64)
+    F = rng.standard_normal((5, m - 1))
+    out = dv.get_ops().residual(St, Dt, torch.as_tensor(F, device="cuda"), 5, m - 1).cpu().numpy()
+    np.testing.assert_allclose(out[0], np.sum((S[:, 1:] - D @ F) ** 2), rtol=1e-12)
+    np.testing.assert_allclose(out[1], np.sum(S[:, 1:] ** 2), rtol=1e-12)
+
+
+@pytest.mark.parametrize("n", [6, 50, 200])
+def test_geev(dv, n):
+    rng = np.random.default_rng(n)
+    K = rng.standard_normal((n, n))
+    w, V = dv.get_ops().geev(torch.as_tensor(K, device="cuda"))
+    assert np.linalg.norm(K @ V - V * w) <= 1e-10 * np.linalg.norm(K) * np.linalg.norm(V)
+    ref = np.linalg.eigvals(K)
+    from conftest import match_eigs
+    assert match_eigs(w, ref) <= 1e-10 * np.abs(ref).max()
+
+
+def test_synth3d_matches_host(dv):
+    from paper_2502_05339_b200 import synth
+    p = synth.config_params(1, seed=5, grid=12)
+    p.dtype = np.float64
+    Xh = synth.generate_host(p).astype(np.float64)
+    sx, sy, sz, A = [torch.as_tensor(np.ascontiguousarray(t), device="cuda") for t in p.sep_tables()]
+    out = dv.alloc_tall(p.n, p.m, torch.float64, "row")
+    dv.get_ops().synth3d((sx, sy, sz, A), p.m, p.noise, synth.noise_key(p.seed), 0, p.n, out)
+    Xd = out.view().cpu().numpy()
+    assert np.abs(Xd - Xh).max() <= 1e-11 * np.abs(Xh).max()
