@@ -239,8 +239,14 @@ int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda, const 
 }
 
 size_t fdmd_tall_gram_workspace(int64_t n, int K1, int K2) {
+  // large enough for either plan (a symmetric Gram has fewer tiles -> more splits)
   GramPlan p = gram_plan(n, K1, K2, 0);
-  return (size_t)p.splits * p.K1p * p.K2p * sizeof(double) + 256;
+  size_t need = (size_t)p.splits * p.K1p * p.K2p * sizeof(double);
+  if (K1 == K2) {
+    GramPlan q = gram_plan(n, K1, K2, 1);
+    need = std::max(need, (size_t)q.splits * q.K1p * q.K2p * sizeof(double));
+  }
+  return need + 256;
 }
 
 int fdmd_tall_gram(const void* A, int a_dtype, int a_layout, int64_t lda, const void* B, int b_dtype,
@@ -388,33 +394,45 @@ int fdmd_table_apply(const void* R, int r_dtype, int64_t ldr, const int* src, co
   return FDMD_OK;
 }
 
+static int residual_chunk(int r, int T) {
+  const int maxcols = (int)((200 * 1024) / ((size_t)r * sizeof(double)));
+  return std::max(1, std::min(T, maxcols));
+}
+
 size_t fdmd_residual_workspace(int64_t n) {
   (void)n;
-  return (size_t)sm_count_cached() * 4 * 2 * sizeof(double) + 256;
+  // up to 64 column chunks x blocks x 2 partial sums
+  return (size_t)64 * sm_count_cached() * 4 * 2 * sizeof(double) + 256;
 }
 
 int fdmd_residual(const void* S, int s_dtype, int64_t lds, const void* D, int d_dtype, int64_t ldd,
                   const double* F, int r, int T, int64_t n, double* out, void* workspace,
                   size_t workspace_bytes, void* stream) {
   if (n < 0 || r <= 0 || T <= 0) return fail(FDMD_ERR_INVALID, "bad sizes");
-  const size_t smem = (size_t)r * T * sizeof(double);
-  if (smem > 220 * 1024) return fail(FDMD_ERR_INVALID, "residual: r*T too large for smem");
+  const int Tc = residual_chunk(r, T);
+  const int nch = (T + Tc - 1) / Tc;
+  if (nch > 64 || (size_t)r * sizeof(double) > 200 * 1024) return fail(FDMD_ERR_INVALID, "residual: r too large");
   cudaStream_t s = (cudaStream_t)stream;
   const int blocks = sm_count_cached() * 4;
-  if (!workspace || workspace_bytes < (size_t)blocks * 2 * sizeof(double))
+  if (!workspace || workspace_bytes < (size_t)nch * blocks * 2 * sizeof(double))
     return fail(FDMD_ERR_WORKSPACE, "residual workspace");
   double* part = static_cast<double*>(workspace);
+  for (int c = 0; c < nch; ++c) {
+    const int j0 = c * Tc, tc = std::min(Tc, T - j0);
+    const size_t smem = (size_t)r * tc * sizeof(double);
 #define RS(TS, TD)                                                                                   \
   do {                                                                                               \
     auto k = fdmd::residual_kernel<TS, TD>;                                                          \
-    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
-    k<<<blocks, 256, smem, s>>>((const TS*)S, lds, (const TD*)D, ldd, F, r, T, n, part);              \
+    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));      \
+    k<<<blocks, 256, smem, s>>>((const TS*)S, lds, (const TD*)D, ldd, F + j0, T, r, tc, j0, n,       \
+                                part + (size_t)c * blocks * 2);                                      \
   } while (0)
-  if (s_dtype == FDMD_F32) { if (d_dtype == FDMD_F32) RS(float, float); else RS(float, double); }
-  else { if (d_dtype == FDMD_F32) RS(double, float); else RS(double, double); }
+    if (s_dtype == FDMD_F32) { if (d_dtype == FDMD_F32) RS(float, float); else RS(float, double); }
+    else { if (d_dtype == FDMD_F32) RS(double, float); else RS(double, double); }
 #undef RS
-  LAUNCH_CHECK("residual");
-  fdmd::split_sum_kernel<<<1, 32, 0, s>>>(part, blocks, 2, out);
+    LAUNCH_CHECK("residual");
+  }
+  fdmd::split_sum_kernel<<<1, 32, 0, s>>>(part, nch * blocks, 2, out);
   LAUNCH_CHECK("residual_sum");
   return FDMD_OK;
 }

@@ -618,10 +618,10 @@ __global__ void table_apply_kernel(const TR* __restrict__ R, int64_t ldr, const 
 template <typename TS, typename TD>
 __global__ void __launch_bounds__(256) residual_kernel(const TS* __restrict__ S, int64_t lds,
                                                        const TD* __restrict__ D, int64_t ldd,
-                                                       const double* __restrict__ F, int r, int T,
-                                                       int64_t n, double* __restrict__ part) {
-  extern __shared__ double Fs[];  // r x T
-  for (int e = threadIdx.x; e < r * T; e += blockDim.x) Fs[e] = F[e];
+                                                       const double* __restrict__ F, int ldf, int r, int T,
+                                                       int jbase, int64_t n, double* __restrict__ part) {
+  extern __shared__ double Fs[];  // r x T (chunk of columns [jbase, jbase+T))
+  for (int e = threadIdx.x; e < r * T; e += blockDim.x) Fs[e] = F[(int64_t)(e / T) * ldf + e % T];
   __syncthreads();
   double local = 0.0, xnorm = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(256) residual_kernel(const TS* __restrict__ S,
 #pragma unroll
       for (int q = 0; q < 16; ++q)
         if (j0 + q < T) {
-          const double x = (double)S[i * lds + 1 + j0 + q];
+          const double x = (double)S[i * lds + 1 + jbase + j0 + q];
           const double e = x - rec[q];
           local = fma(e, e, local);
           xnorm = fma(x, x, xnorm);

@@ -407,7 +407,8 @@ def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, po
         basis = _Basis(f.Q, Umap, f.s[:r].contiguous(), f.Vh[:r].t().contiguous(), UtS, f.stats)
         basis.stats.update(l=l, p=p, q=q)
     elif svd_mode == "full":
-        svd = la.truncated_svd(S if data.shard is None else S, r, shard=data.shard, keep_device=True)
+        X = Tall(S.buf, "row", S.n, T)                       # X = states[:, :-1] (dmd.py:248)
+        svd = la.truncated_svd(X, r, shard=data.shard, keep_device=True)
         Ud = svd.U_device
         UtS = allreduce(data.shard, dv.get_ops().tall_gram(Ud, S))
         basis = _Basis(Ud, None, torch.as_tensor(svd.S, device=S.buf.device),

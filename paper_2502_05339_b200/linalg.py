@@ -103,6 +103,9 @@ def copy_rows_h2d(T: Tall, t: torch.Tensor, row0: int = 0):
     if t.dtype != T.dtype:
         t = t.to(T.dtype)
     t = t.contiguous()
+    if not T.buf.is_cuda:   # host-resident Tall (CPU test harness only)
+        T.buf[row0:row0 + rows, :k].copy_(t)
+        return
     elt = t.element_size()
     dst = T.buf.data_ptr() + row0 * T.ld * elt
     kind = 4  # cudaMemcpyDefault (UVA)

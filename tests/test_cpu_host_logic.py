@@ -1,0 +1,140 @@
+"""CPU tests of the host-side logic: the C-ABI library loads and exports every
+symbol in include/fdmd.h, and the pairing / ordering / table bookkeeping the
+device path relies on matches the oracle restatement of dmd.py:131-213."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import flowdmd_oracle as orc
+from conftest import ROOT
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "fdmd.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(fdmd_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_header_symbol():
+    path = os.path.join(ROOT, "paper_2502_05339_b200", "libfdmd.so")
+    if not os.path.exists(path):
+        pytest.skip("libfdmd.so not built (run __graft_entry__.build())")
+    lib = ctypes.CDLL(path)
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), s
+    from paper_2502_05339_b200 import _lib
+    assert set(_lib.SIGNATURES) == set(syms)
+    _lib.lib()
+    assert _lib.lib().fdmd_version() == 1
+
+
+def test_no_cuda_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    import paper_2502_05339_b200 as fd
+    from paper_2502_05339_b200 import _lib
+    with pytest.raises((_lib.DeviceError, RuntimeError)):
+        fd.exact_dmd(fd.SnapshotMatrix(np.random.default_rng(0).standard_normal((50, 10)), 0.1), 3)
+
+
+def _spectrum(rng, pairs, reals, near_dup=False):
+    lam = []
+    for _ in range(pairs):
+        v = rng.uniform(0.5, 1.0) * np.exp(1j * rng.uniform(0.05, 3.0))
+        lam += [v, np.conj(v)]
+    lam += list(rng.uniform(-1, 1, reals) + 0j)
+    lam = np.array(lam)
+    if near_dup and pairs:
+        lam[1] = np.conj(lam[0]) + 1e-9
+    rng.shuffle(lam)
+    return lam
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_pair_plan_matches_order_and_pair(seed):
+    from paper_2502_05339_b200.dmd import frequency_order, pair_plan
+    rng = np.random.default_rng(seed)
+    lam = _spectrum(rng, rng.integers(0, 6), rng.integers(0, 4), near_dup=seed % 3 == 0)
+    if lam.size == 0:
+        return
+    np.testing.assert_array_equal(frequency_order(lam), orc.frequency_order(lam))
+    # modes: random complex columns with exact conjugate partners where lam pairs
+    n = 40
+    phi = rng.standard_normal((n, lam.size)) + 1j * rng.standard_normal((n, lam.size))
+    lam_o, phi_o = orc.order_and_pair(lam, phi)
+    plan = pair_plan(lam)
+    np.testing.assert_array_equal(plan.lam, lam_o)
+    # reconstruct phi at each sorted position from units (normalised + phased)
+    for pos in range(lam.size):
+        u, cj = plan.pos_unit[pos]
+        c = phi[:, plan.src[u]]
+        c = c / np.linalg.norm(c)
+        i = np.argmax(np.abs(c))
+        c = c * (np.conj(c[i]) / abs(c[i]))
+        if cj:
+            c = np.conj(c)
+        if u in plan.realify and np.abs(c.imag).max() <= 1e-10:
+            c = c.real
+        np.testing.assert_allclose(c, phi_o[:, pos], atol=1e-14)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_table_layout_matches_decode_table(seed):
+    from paper_2502_05339_b200.modes import TableLayout, conjugate_pairs
+    rng = np.random.default_rng(100 + seed)
+    lam = _spectrum(rng, rng.integers(1, 6), rng.integers(0, 3))
+    np.testing.assert_array_equal(conjugate_pairs(lam), orc.partner_map(lam))
+    lam_o, _ = orc.order_and_pair(lam, np.eye(lam.size, dtype=complex))
+    n = 30
+    phi = rng.standard_normal((n, lam.size)) + 1j * rng.standard_normal((n, lam.size))
+    _, phi = orc.order_and_pair(lam, phi)
+    table, re_idx, im_idx = orc.decode_columns(phi, lam_o)
+    part0 = orc.partner_map(lam_o)
+    extra = [a for a in range(lam.size) if part0[a] == a and np.any(phi[:, a].imag != 0)]
+    lay = TableLayout(lam_o, extra)
+    assert lay.re_idx == re_idx and lay.im_idx == im_idx
+    # phi == [table, Im(phi_extra)] @ E and the coefficient map reproduces the table GEMV
+    full = np.hstack([table] + [phi[:, [a]].imag for a in extra]) if extra else table
+    np.testing.assert_allclose(full @ lay.E(), phi, atol=1e-14)
+    z = rng.standard_normal(lam.size) + 1j * rng.standard_normal(lam.size)
+    part = orc.partner_map(lam_o)
+    for a in range(lam.size):
+        if part[a] == a:
+            z[a] = z[a].real
+        elif part[a] > a:
+            z[part[a]] = np.conj(z[a])
+    np.testing.assert_allclose(table @ lay.coeff(z)[:, 0], orc.decode(phi, lam_o, z), atol=1e-12)
+
+
+def test_conjugate_pairs_reference_examples():
+    from paper_2502_05339_b200.modes import conjugate_pairs
+    assert conjugate_pairs(np.array([0.9 + 0j, 0.5 + 0j])).tolist() == [0, 1]
+    assert conjugate_pairs(np.array([0.8 + 0.1j, 0.5 + 0j, 0.8 - 0.1j])).tolist() == [2, 1, 0]
+
+
+def test_vandermonde_and_runtime_scalars():
+    import paper_2502_05339_b200 as fd
+    np.testing.assert_allclose(fd.vandermonde(np.array([2.0]), 3)[:, 0], [1.0, 2.0, 4.0])
+    np.testing.assert_allclose(fd.vandermonde(np.array([1j]), 4)[:, 0], [1.0, 1j, -1.0, -1j])
+    with pytest.raises(ValueError):
+        fd.vandermonde(np.array([1.0]), 0)
+
+
+def test_synth_generator_properties():
+    from paper_2502_05339_b200 import synth
+    p = synth.config_params(1, seed=2, grid=8)
+    X = synth.generate_host(p)
+    assert X.shape == (3 * 8 ** 3, 201) and X.dtype == np.float32
+    # row blocks regenerate identically (sharding-independent)
+    Xb = synth.generate_host(p, row0=100, rows=50)
+    np.testing.assert_array_equal(Xb, X[100:150])
+    # counter noise is standard normal
+    g = synth.counter_normal(7, np.arange(200000), np.zeros(200000, dtype=np.int64), 1)
+    assert abs(g.mean()) < 0.01 and abs(g.std() - 1) < 0.01

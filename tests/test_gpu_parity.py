@@ -218,7 +218,9 @@ def test_config3_reduced_grid_exact_and_opt(fd, config_golden):
         mo = fd.optdmd(data, 200, lm_config=fd.LMConfig(max_iters=10), svd_mode="randomized", seed=3,
                        oversample=10, power_iters=1)
     assert match_eigs(mo.lam, g["c3s_opt_lam"]) <= LAM_TOL
-    np.testing.assert_allclose(mo.provenance["objective_history"][0], g["c3s_opt_hist"][0], rtol=1e-6)
+    # r = T: the varpro objective starts at round-off level in both implementations
+    assert mo.provenance["objective_history"][0] <= 1e-12 * g["c3s_opt_sigma"][0]
+    assert g["c3s_opt_hist"][0] <= 1e-12 * g["c3s_opt_sigma"][0]
 
 
 # ---------------------------------------------------------------- reconstruct batch APIs
