@@ -1,0 +1,401 @@
+"""Benchmark of the B200 DMD hot path (BASELINE.json metric: DMD fit GFLOP/s +
+reconstruct frames/s at 256^3, r=200, as % of roofline).
+
+One step = the config-3 fit (randomized SVD r=200, p=10 (clamped: l=T=200),
+q=1, CholeskyQR2, 10 OptDMD LM iterations, modes + POD basis U) followed by
+the config-4 reconstruction u(t) = U Re(W Lam^t b) at 1024 seeded continuous
+times in batches of 1, 32 and 1024 frames. Inputs are resident in HBM before
+the timed region (`value`); `e2e` repeats the fit through the public API from
+pinned host memory with the host<->device copies inside the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c1] [--impl fdmd|reference]
+
+Multi-GPU (torchrun): rows are sharded across ranks (strong scaling, fixed
+256^3 problem), the only collectives are NCCL all-reduces of the small
+Gram/projection blocks; time = max over ranks of CUDA-event time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
+METRIC = "DMD fit GFLOP/s + reconstruct frames/s (256³, r=200); % of roofline"
+CONFIGS = {
+    "c3": dict(cfg=3, grid=256, r=200, p=10, q=1, lm_iters=10, times=1024, seed=3),
+    "c1": dict(cfg=1, grid=128, r=150, p=10, q=1, lm_iters=10, times=1024, seed=1),
+    "c3s": dict(cfg=3, grid=64, r=200, p=10, q=1, lm_iters=10, times=1024, seed=3),
+}
+
+
+def fit_flops(n, m, r, p, q, modes="optdmd"):
+    """SURVEY.md §8(d) algorithmic flops (executed terms only)."""
+    T = m - 1
+    l = min(r + p, T)
+    terms = {
+        "sketch+power 2nTl(1+2q)": 2.0 * n * T * l * (1 + 2 * q),
+        "CholQR2 4nl^2(1+q)": 4.0 * n * l * l * (1 + q),
+        "projection 2nml": 2.0 * n * m * l,
+        "lift U 2nlr": 2.0 * n * l * r,
+        ("modes 4nr^2" if modes == "optdmd" else "modes 4nTr"): 4.0 * n * r * (r if modes == "optdmd" else T),
+    }
+    return sum(terms.values()), terms, l
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+def _dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference algorithm's CPU implementation (the
+    oracle port, oracle/flowdmd_oracle.py — the reference is pure Python and
+    not importable on the GPU box) on a bounded row sample of the workload."""
+    world, rank, _ = _dist_init()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import flowdmd_oracle as orc
+    from paper_2502_05339_b200 import synth
+    res = cpu_sample(orc, synth, cfg, args.cpu_rows)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        cpu_fit(orc, res["X"], cfg)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    tmed = float(np.median(times))
+    val = res["flops"] / tmed / 1e9
+    line = {
+        "metric": METRIC, "value": round(val, 3), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(tmed * 1e3, 1), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"config{cfg['cfg']} fit, row sample", "rows": res["rows"], "m": 201, "r": cfg["r"],
+                   "p": cfg["p"], "q": cfg["q"], "lm_iters": cfg["lm_iters"]},
+        "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
+                         "sample": res["sample"]},
+        "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_sample(orc, synth, cfg, rows):
+    p = synth.config_params(cfg["cfg"], seed=cfg["seed"], grid=cfg["grid"])
+    rows = min(rows, p.n)
+    X = synth.generate_host(p, 0, rows).astype(np.float64)
+    flops, _, _ = fit_flops(rows, p.m, cfg["r"], cfg["p"], cfg["q"])
+    sample = (f"config{cfg['cfg']} rows [0,{rows}) x {p.m} snapshots; oracle optdmd r={cfg['r']} "
+              f"p={cfg['p']} q={cfg['q']} {cfg['lm_iters']} LM iters, numpy/OpenBLAS fp64; "
+              f"GFLOP/s from the SURVEY §8d formula at n={rows}")
+    return {"X": X, "rows": rows, "flops": flops, "sample": sample}
+
+
+def cpu_fit(orc, X, cfg):
+    return orc.optdmd(X, cfg["r"], max_iters=cfg["lm_iters"], svd_mode="randomized", seed=cfg["seed"],
+                      p=cfg["p"], q=cfg["q"])
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="fdmd", choices=["fdmd", "reference"])
+    ap.add_argument("--cpu-rows", type=int, default=98304)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    world, rank, local = _dist_init()
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+
+    import paper_2502_05339_b200 as fd
+    from paper_2502_05339_b200 import _lib, synth
+    from paper_2502_05339_b200 import device as dv
+    from paper_2502_05339_b200.runtime import ModalBasis
+
+    p = synth.config_params(cfg["cfg"], seed=cfg["seed"], grid=cfg["grid"])
+    n, m, r = p.n, p.m, cfg["r"]
+    bounds = np.linspace(0, n, world + 1).astype(np.int64)
+    row0, row1 = int(bounds[rank]), int(bounds[rank + 1])
+    n_loc = row1 - row0
+    shard = dv.Shard(row0, n_loc, n, group, world) if world > 1 else None
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- inputs resident in HBM (device generator, synth.py recipe) ----
+    S = dv.alloc_tall(n_loc, m, torch.float32, "row")
+    S.buf[:, m:].zero_()
+    tabs = [torch.as_tensor(np.ascontiguousarray(t), device="cuda") for t in p.sep_tables()]
+    dv.get_ops().synth3d(tabs, m, p.noise, synth.noise_key(p.seed), row0, n_loc, S)
+    torch.cuda.synchronize()
+    data = fd.SnapshotMatrix(S, synth.DT, shard=shard)
+    # config 4: W (r x r complex), Lam and b from config 3's generator (conjugate-closed)
+    rng = np.random.default_rng(4)
+    lam4 = np.concatenate([p.lam, np.conj(p.lam)])[:r]
+    b4 = np.concatenate([p.b, np.conj(p.b)])[:r]
+    W4 = (rng.standard_normal((r, r)) + 1j * rng.standard_normal((r, r))) / np.sqrt(2 * r)
+    times = rng.uniform(0.0, 300.0, cfg["times"])
+    peak = ctypes_peak(_lib)
+    ops = dv.get_ops()
+    F_fit, terms, l = fit_flops(n, m, r, cfg["p"], cfg["q"])
+    lm = fd.LMConfig(max_iters=cfg["lm_iters"])
+
+    def one_step(record):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record()
+        import warnings
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            model = fd.optdmd(data, r, lm_config=lm, svd_mode="randomized", seed=cfg["seed"],
+                              oversample=cfg["p"], power_iters=cfg["q"], keep_basis=True)
+        ev[1].record()
+        mb = ModalBasis(model.basis_U, W4, lam4, b4, dt=1.0)
+        f1 = mb.reconstruct(times[:1])                       # interactive frame (GEMV)
+        ev[2].record()
+        out32 = torch.empty((32, n_loc), dtype=torch.float32, device="cuda")
+        mb.reconstruct(times[:32], out=out32)                # one 32-frame batch
+        ev[3].record()
+        for c0 in range(0, len(times), 32):                  # 1024 frames streamed through one buffer
+            mb.reconstruct(times[c0:c0 + 32], out=out32)
+        ev[4].record()
+        torch.cuda.synchronize()
+        t = [ev[0].elapsed_time(ev[i]) / 1e3 for i in range(1, 5)]
+        del model, mb, f1, out32
+        return {"fit": t[0], "rec1": t[1] - t[0], "rec32": t[2] - t[1], "rec1024": t[3] - t[2]}
+
+    for _ in range(args.warmup):
+        one_step(False)
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ops.profile = []
+    launches0 = ops.launches
+    barrier()
+    torch.cuda.synchronize()
+    t0e = torch.cuda.Event(enable_timing=True)
+    t1e = torch.cuda.Event(enable_timing=True)
+    t0e.record()
+    res = [one_step(True) for _ in range(args.steps)]
+    t1e.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = ops.launches - launches0
+    prof = ops.profile
+    ops.profile = None
+    total = max_over_ranks(t0e.elapsed_time(t1e) / 1e3)
+    fit_t = max_over_ranks(float(np.mean([x["fit"] for x in res])))
+    rec = {k: max_over_ranks(float(np.mean([x[k] for x in res]))) for k in ("rec1", "rec32", "rec1024")}
+
+    # roofline: FP64 DMMA contraction kernels (tall_gemm + tall_gram), CUDA events
+    kt = {"tall_gemm": [0.0, 0.0, 0], "tall_gram": [0.0, 0.0, 0], "decode": [0.0, 0.0, 0]}
+    for name, fl, e0, e1 in prof:
+        kt[name][0] += e0.elapsed_time(e1) / 1e3
+        kt[name][1] += fl
+        kt[name][2] += 1
+    fit_kernel_t = (kt["tall_gemm"][0] + kt["tall_gram"][0]) / args.steps
+    achieved = F_fit / world / max(fit_kernel_t, 1e-12) / 1e12   # per-GPU TFLOP/s in the contractions
+    value = F_fit / fit_t / 1e9
+
+    # reconstruct figures (config 4, HBM-bound)
+    def rec_obj(B, t):
+        byt = 4.0 * n * r + 4.0 * n * B + 8.0 * r * B
+        gbs = byt / t / 1e9 / world
+        return {"frames_per_s": round(B / t, 1), "ms": round(t * 1e3, 3), "hbm_GBps_per_gpu": round(gbs, 1),
+                "frac_hbm": round(gbs / hbm_peak(), 3)}
+    recon = {"B=1": rec_obj(1, rec["rec1"]), "B=32": rec_obj(32, rec["rec32"])}
+    b1024 = rec["rec1024"]
+    byt = (4.0 * n * r) * (len(times) / 32) + 4.0 * n * len(times)
+    recon["B=1024"] = {"frames_per_s": round(len(times) / b1024, 1), "ms": round(b1024 * 1e3, 2),
+                       "hbm_GBps_per_gpu": round(byt / b1024 / 1e9 / world, 1),
+                       "note": "32-frame passes over U; compute-bound in fp32 FFMA (DESIGN.md)"}
+
+    # ---- e2e through the public API from pinned host memory ----
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((n_loc, m), dtype=torch.float32, pin_memory=True)
+        host.copy_(S.view().cpu())
+        del data, S
+        torch.cuda.empty_cache()
+        e2e = run_e2e(args, fd, host, n_loc, m, r, cfg, lm, shard, F_fit, max_over_ranks, barrier)
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 1), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config{cfg['cfg']} fit (OptDMD, {cfg['lm_iters']} LM iters) + config4 reconstruct",
+                   "n": n, "m": m, "r": r, "l": l, "p": cfg["p"], "q": cfg["q"], "grid": f"{cfg['grid']}^3x3",
+                   "snapshot_dtype": "f32", "parallelism": f"rows{world}", "l2": "inputs larger than L2 (X >= 3.8 GB)"},
+        "fit": {"s": round(fit_t, 4), "gflops": round(value, 1), "flops": F_fit,
+                "terms": {k: v for k, v in terms.items()}},
+        "reconstruct": recon,
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(),
+                     "kernel": "FP64 DMMA contractions (tall_gemm + tall_gram), CUDA events per launch",
+                     "peak_source": "in-run DMMA.8x8x4 throughput probe (fdmd_dmma_peak); spec 40 TF/s",
+                     "kernel_share_of_fit": round(fit_kernel_t / fit_t, 3),
+                     "launches_per_step": {k: v[2] // args.steps for k, v in kt.items()},
+                     "ms_per_step": {k: round(v[0] / args.steps * 1e3, 2) for k, v in kt.items()}},
+        "clocks": clk,
+        "gpu_launches": launches,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and not args.no_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import flowdmd_oracle as orc
+        s = cpu_sample(orc, synth, cfg, args.cpu_rows)
+        t0 = time.perf_counter()
+        cpu_fit(orc, s["X"], cfg)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": round(s["flops"] / dt / 1e9, 3), "unit": "GFLOP/s", "cores": os.cpu_count(),
+                                "kind": "port", "sample": s["sample"], "s": round(dt, 2)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_e2e(args, fd, host, n_loc, m, r, cfg, lm, shard, F_fit, max_over_ranks, barrier):
+    import warnings
+
+    import torch
+    ts = []
+    for i in range(1 + args.e2e_steps):
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            d2 = fd.SnapshotMatrix(host, 0.1, shard=shard)
+            model = fd.optdmd(d2, r, lm_config=lm, svd_mode="randomized", seed=cfg["seed"],
+                              oversample=cfg["p"], power_iters=cfg["q"])
+            z0 = fd.ReducedState(np.ones(r, dtype=complex))
+            frame = fd.decode(model, fd.step_k(model, z0, 10))            # D2H of one frame
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        del d2, model, frame
+        if i >= 1:
+            ts.append(max_over_ranks(dt))
+    t = float(np.mean(ts))
+    return {"value": round(F_fit / t / 1e9, 2), "unit": "GFLOP/s", "s_per_step": round(t, 3),
+            "h2d_bytes_per_step": int(n_loc * m * 4), "d2h_bytes_per_step": int(n_loc * 8 + 2 * r * 16),
+            "api": "SnapshotMatrix(pinned host f32) -> optdmd -> decode(step_k) to host"}
+
+
+def ctypes_peak(_lib):
+    import ctypes
+    v = ctypes.c_double(0.0)
+    _lib.check(_lib.lib().fdmd_dmma_peak(0.4, ctypes.byref(v)), "dmma_peak")
+    return v.value
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def traffic_from_profiles():
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    summary (profiles/), or None if no capture exists yet."""
+    path = os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")
+    try:
+        return json.load(open(path)).get("traffic_bytes_per_launch")
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

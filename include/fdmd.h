@@ -101,6 +101,11 @@ int fdmd_residual(const void* S, int s_dtype, int64_t lds, const void* D, int d_
  * j (real part) and j+1 (imaginary part)). Synchronous. */
 int fdmd_geev(int n, double* A, double* w_host, double* vr_host, void* stream);
 
+/* FP64 tensor-pipe (DMMA.8x8x4) throughput probe on the current device:
+ * a register-only mma.sync f64 loop lasting ~`seconds`/4; writes TFLOP/s.
+ * The fit's roofline denominator (MEASURED_PEAKS.json has no FP64 figure). */
+int fdmd_dmma_peak(double seconds, double* tflops);
+
 /* Pitched 2-D copy (cudaMemcpy2DAsync; kind = cudaMemcpyKind, 4 = default/UVA):
  * uploads a host n x m snapshot block into a padded row-major device buffer. */
 int fdmd_copy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,

@@ -46,6 +46,7 @@ SIGNATURES = {
     "fdmd_residual": (_i, [_vp, _i, _i64, _vp, _i, _i64, _vp, _i, _i, _i64, _vp, _vp, _sz, _vp]),
     "fdmd_geev": (_i, [_i, _vp, _vp, _vp, _vp]),
     "fdmd_copy2d": (_i, [_vp, _i64, _vp, _i64, _i64, _i64, _i, _vp]),
+    "fdmd_dmma_peak": (_i, [_d, _c.POINTER(_d)]),
     "fdmd_synth3d": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _d, _u64, _i64, _i64, _vp, _i, _i64, _vp]),
 }
 

@@ -474,6 +474,35 @@ int fdmd_geev(int n, double* A, double* w_host, double* vr_host, void* stream) {
   return FDMD_OK;
 }
 
+int fdmd_dmma_peak(double seconds, double* tflops) {
+  if (!tflops || seconds <= 0) return fail(FDMD_ERR_INVALID, "dmma_peak: bad arguments");
+  double* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, sizeof(double)));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  const int blocks = sm_count_cached() * 4, threads = 256;
+  int iters = 2000;
+  float ms = 0.f;
+  fdmd::dmma_peak_kernel<<<blocks, threads>>>(d, 100);
+  for (int rep = 0; rep < 8; ++rep) {  // grow until one launch lasts ~seconds/4
+    CUDA_TRY(cudaEventRecord(e0));
+    fdmd::dmma_peak_kernel<<<blocks, threads>>>(d, iters);
+    CUDA_TRY(cudaEventRecord(e1));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms >= 250.0 * seconds) break;
+    iters = (int)std::min<double>(2e9 / 8, iters * std::max(2.0, 250.0 * seconds / std::max(ms, 0.01f)));
+  }
+  const double flops = 2.0 * 8 * 8 * 4 * 8 * (double)iters * blocks * (threads / 32);
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  LAUNCH_CHECK("dmma_peak");
+  return FDMD_OK;
+}
+
 int fdmd_copy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
                 int kind, void* stream) {
   if (height <= 0 || width <= 0) return FDMD_OK;

@@ -720,4 +720,23 @@ __global__ void __launch_bounds__(256) synth3d_kernel(const double* __restrict__
   }
 }
 
+// ===========================================================================
+// FP64 tensor-pipe (DMMA) throughput probe: the roofline denominator for the
+// fit contractions (MEASURED_PEAKS.json carries no FP64 figure).
+// ===========================================================================
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma884(c[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 1234.5) out[0] = s;
+}
+
 }  // namespace fdmd

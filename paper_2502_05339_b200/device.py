@@ -125,10 +125,22 @@ class CudaOps:
     def __init__(self):
         self.ws = _Workspace()
         self.launches = 0
+        self.profile = None   # list -> per-call (name, algorithmic flops, ev0, ev1)
+
+    def _ev(self):
+        if self.profile is None:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def _done(self, name, flops, e0):
+        if e0 is not None:
+            self.profile.append((name, float(flops), e0, self._ev()))
 
     # -- C[n x N] = A * B (B small fp64, K x N) ---------------------------
     def tall_gemm(self, A: Tall, B: torch.Tensor, C: Optional[Tall], stats: bool = False,
-                  row_offset: int = 0) -> Optional[torch.Tensor]:
+                  row_offset: int = 0, alg_flops: Optional[float] = None) -> Optional[torch.Tensor]:
         L = _lib.lib()
         K, N = int(B.shape[0]), int(B.shape[1])
         assert K <= A.k or K <= (A.ld if A.layout == "row" else K), (K, A.k)
@@ -144,15 +156,18 @@ class CudaOps:
         c_dt = _DT[C.dtype] if C is not None else F64
         c_lay = C.code if C is not None else COL
         c_ld = C.ld if C is not None else A.n
+        e0 = self._ev()
         _lib.check(L.fdmd_tall_gemm(_ptr(A.buf), _DT[A.dtype], A.code, A.ld, _ptr(B), B.shape[1],
                                      _ptr(c_buf), c_dt, c_lay, c_ld, A.n, K, N,
                                      _ptr(st), row_offset, _ptr(ws), wsb, _stream()), "tall_gemm")
+        self._done("tall_gemm", 2.0 * A.n * K * N if alg_flops is None else alg_flops, e0)
         self.launches += 2 if stats else 1
         return st
 
     # -- C[K1 x K2] = A^T B over n ----------------------------------------
     def tall_gram(self, A: Tall, B: Tall, K1: Optional[int] = None, K2: Optional[int] = None,
-                  symmetric: bool = False, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                  symmetric: bool = False, out: Optional[torch.Tensor] = None,
+                  alg_flops: Optional[float] = None) -> torch.Tensor:
         L = _lib.lib()
         K1 = A.k if K1 is None else K1
         K2 = B.k if K2 is None else K2
@@ -160,9 +175,13 @@ class CudaOps:
             out = torch.empty((K1, K2), dtype=torch.float64, device=A.buf.device)
         wsb = int(L.fdmd_tall_gram_workspace(A.n, K1, K2))
         ws = self.ws.get(wsb, A.buf.device)
+        e0 = self._ev()
         _lib.check(L.fdmd_tall_gram(_ptr(A.buf), _DT[A.dtype], A.code, A.ld, _ptr(B.buf), _DT[B.dtype],
                                      B.code, B.ld, _ptr(out), out.stride(0), 0.0, A.n, K1, K2,
                                      1 if symmetric else 0, _ptr(ws), wsb, _stream()), "tall_gram")
+        if alg_flops is None:
+            alg_flops = (1.0 if symmetric else 2.0) * A.n * K1 * K2
+        self._done("tall_gram", alg_flops, e0)
         self.launches += 2
         return out
 
@@ -175,8 +194,10 @@ class CudaOps:
         B = int(coef.shape[1])
         if out is None:
             out = torch.empty((B, D.n), dtype=D.dtype, device=D.buf.device)
+        e0 = self._ev()
         _lib.check(_lib.lib().fdmd_decode(_ptr(D.buf), _DT[D.dtype], D.ld, _ptr(coef), coef.stride(0),
                                           _ptr(out), out.stride(0), D.n, r, B, _stream()), "decode")
+        self._done("decode", 2.0 * D.n * r * B, e0)
         self.launches += (B + 31) // 32 if B > 16 else 1
         return out
 

@@ -250,7 +250,10 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
     raw = alloc_tall(n_loc, 2 * U, table_dtype, "col", device=dev)
     row0 = 0 if shard is None else shard.row0
     t0 = time.perf_counter()
-    st = ops.tall_gemm(A, Bm, raw, stats=True, row_offset=row0)        # (U, 3)
+    # algorithmic count: real n x K times complex K x r (SURVEY §8d F_modes = 4 n K r);
+    # only one column of each conjugate pair is executed
+    st = ops.tall_gemm(A, Bm, raw, stats=True, row_offset=row0,
+                       alg_flops=4.0 * n_loc * K * plan.lam.size)      # (U, 3)
     st = la._reduce_pair_stats(st, shard)
     nrm = torch.sqrt(st[:, 0])
     idx = st[:, 2].round().long()
@@ -468,13 +471,11 @@ def exact_dmd(data, r, svd_mode="full", seed=None, *, oversample=None, power_ite
     Wt = torch.as_tensor(W, device=VS.device)
     if timings is not None:
         timings["small_s"] = time.perf_counter() - t0
-    if basis.Umap is None:
-        # full mode: phi = X' (V/S) W  (dmd.py:255,258)
-        Cmap = VS.to(torch.complex128) @ Wt
-        A, top = data.S, 1
-    else:
-        Cmap = VS.to(torch.complex128) @ Wt
-        A, top = data.S, 1
+    # phi = X' (V/S) W  (dmd.py:255,258) = S [0; (V/S) W]; the sketch basis is no
+    # longer needed, so it is released before the mode buffers are allocated.
+    Cmap = VS.to(torch.complex128) @ Wt
+    A, top = data.S, 1
+    basis.A = None
     tdt = table_dtype or _default_table_dtype(data)
     modes = _modes_pass(A, Cmap, plan, top, data.shard, tdt, timings)
     model = ReducedModel(None, plan.lam, Sv, data.dt, grid_meta=data.grid_meta,
@@ -605,7 +606,7 @@ def _symmetrize(alpha: np.ndarray, B: np.ndarray):
 
 
 def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, oversample=None,
-           power_iters=None, table_dtype=None, timings=None):
+           power_iters=None, table_dtype=None, timings=None, keep_basis=False):
     """Variable-projection refit of the eigenvalues (dmd.py:366-436)."""
     cfg = lm_config or LMConfig()
     data = _as_snapshots(data)
@@ -647,18 +648,24 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
     if timings is not None:
         timings["lm_s"] = time.perf_counter() - t0
     plan = pair_plan(alpha_h)
-    # phi = U @ B.T (dmd.py:414) with U = A @ Umap
+    # phi = U @ B.T (dmd.py:414). The POD basis U = Q Ub_r is lifted once into
+    # a column-major table (the north_star reconstruction basis), Q is released,
+    # and the modes are formed from U — peak HBM stays S + Q + U at config 3.
     Bt = torch.as_tensor(B_h.T.copy(), device=basis.V.device)                # r x r
-    if basis.Umap is None:
-        Cmap = Bt
-    else:
-        Cmap = basis.Umap.to(torch.complex128) @ Bt                          # l x r
     tdt = table_dtype or _default_table_dtype(data)
-    modes = _modes_pass(basis.A, Cmap, plan, 0, data.shard, tdt, timings)
+    if basis.Umap is None:
+        U = basis.A
+    else:
+        U = alloc_tall(basis.A.n, r, tdt, "col", device=basis.A.buf.device)
+        nl = float(basis.A.n)
+        dv.get_ops().tall_gemm(basis.A, basis.Umap, U, alg_flops=2 * nl * basis.A.k * r)   # lift (linalg.py:88)
+        basis.A = None                                                       # release Q
+    modes = _modes_pass(U, Bt, plan, 0, data.shard, tdt, timings)
     model = ReducedModel(None, plan.lam, Sv, data.dt, grid_meta=data.grid_meta,
                          provenance={"method": "optdmd", "svd": svd_mode, "seed": seed,
                                      "objective_history": history, "converged": converged},
                          _modes=modes)
+    model.basis_U = U if keep_basis else None
     warns = _stability_warnings(plan.lam)
     if not converged and cfg.max_iters > 0:
         warns.append(f"variable projection hit max_iters={cfg.max_iters}")

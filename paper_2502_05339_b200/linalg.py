@@ -129,7 +129,8 @@ def _apply_rinv(Y: Tall, R: torch.Tensor, shard: Optional[Shard]):
     l = R.shape[0]
     eye = torch.eye(l, dtype=torch.float64, device=R.device)
     Rinv = torch.linalg.solve_triangular(R, eye, upper=True)
-    dv.get_ops().tall_gemm(Y, Rinv, Y)
+    n_tot = Y.n                                               # algorithmic TRSM: n l^2
+    dv.get_ops().tall_gemm(Y, Rinv, Y, alg_flops=float(n_tot) * l * l)
 
 
 def cholqr2_inplace(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict] = None) -> torch.Tensor:
@@ -225,14 +226,15 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     if Q is None:
         Q = alloc_tall(S.n, l, torch.float64, "row", device=dev)
     Om = torch.as_tensor(np.asarray(omega, dtype=np.float64), device=dev)
-    ops.tall_gemm(S, _pad_rows(Om, m), Q)
+    nl = float(S.n)
+    ops.tall_gemm(S, _pad_rows(Om, m), Q, alg_flops=2 * nl * T * l)
     cholqr2_inplace(Q, shard, stats)
     for _ in range(q):
-        Z = allreduce(shard, ops.tall_gram(S, Q))            # m x l
+        Z = allreduce(shard, ops.tall_gram(S, Q, alg_flops=2 * nl * T * l))   # m x l
         W, _ = torch.linalg.qr(Z[:T], mode="reduced")        # T x l (Householder, device)
-        ops.tall_gemm(S, _pad_rows(W, m), Q)
+        ops.tall_gemm(S, _pad_rows(W, m), Q, alg_flops=2 * nl * T * l)
         cholqr2_inplace(Q, shard, stats)
-    QtS = allreduce(shard, ops.tall_gram(Q, S))              # l x m
+    QtS = allreduce(shard, ops.tall_gram(Q, S, alg_flops=2 * nl * m * l))     # l x m
     B = QtS[:, :T]
     Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvd" if B.is_cuda else None)
     return SketchFactors(Q, Ub, s, Vh, QtS, stats)
