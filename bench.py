@@ -186,7 +186,7 @@ def main():
         group = dist.group.WORLD
 
     import paper_2502_05339_b200 as fd
-    from paper_2502_05339_b200 import _lib, synth
+    from paper_2502_05339_b200 import _lib, synth, trace
     from paper_2502_05339_b200 import device as dv
     from paper_2502_05339_b200.runtime import ModalBasis
 
@@ -232,7 +232,7 @@ def main():
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()
         import warnings
-        with warnings.catch_warnings():
+        with warnings.catch_warnings(), trace.stage("fit"):
             warnings.simplefilter("ignore")
             model = fd.optdmd(data, r, lm_config=lm, svd_mode="randomized", seed=cfg["seed"],
                               oversample=cfg["p"], power_iters=cfg["q"], keep_basis=True)
@@ -258,6 +258,7 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     ops.profile = []
+    trace.enable()
     launches0 = ops.launches
     barrier()
     torch.cuda.synchronize()
@@ -272,6 +273,7 @@ def main():
     launches = ops.launches - launches0
     prof = ops.profile
     ops.profile = None
+    stages = trace.summarize(trace.disable(), args.steps)
     total = max_over_ranks(t0e.elapsed_time(t1e) / 1e3)
     fit_t = max_over_ranks(float(np.mean([x["fit"] for x in res])))
     rec = {k: max_over_ranks(float(np.mean([x[k] for x in res]))) for k in ("rec1", "rec32", "rec1024")}
@@ -325,6 +327,7 @@ def main():
                      "kernel_share_of_fit": round(fit_kernel_t / fit_t, 3),
                      "launches_per_step": {k: v[2] // args.steps for k, v in kt.items()},
                      "ms_per_step": {k: round(v[0] / args.steps * 1e3, 2) for k, v in kt.items()}},
+        "fit_stages_ms": stages,
         "clocks": clk,
         "gpu_launches": launches,
     }

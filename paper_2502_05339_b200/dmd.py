@@ -25,6 +25,7 @@ from . import linalg as la
 from .device import Shard, Tall, allreduce, alloc_tall
 from .errors import ConvergenceError
 from .modes import DeviceModes, TableLayout, conjugate_pairs, modes_from_host_phi
+from .trace import stage
 
 UNSTABLE_MODULUS = 1.05
 SIGMA_CUTOFF = 1e-14
@@ -247,13 +248,15 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
     Bm[row_pad_top:row_pad_top + K, 0::2] = Cs.real
     Bm[row_pad_top:row_pad_top + K, 1::2] = Cs.imag
     n_loc = A.n
-    raw = alloc_tall(n_loc, 2 * U, table_dtype, "col", device=dev)
+    with stage("modes.alloc_raw"):
+        raw = alloc_tall(n_loc, 2 * U, table_dtype, "col", device=dev)
     row0 = 0 if shard is None else shard.row0
     t0 = time.perf_counter()
     # algorithmic count: real n x K times complex K x r (SURVEY §8d F_modes = 4 n K r);
     # only one column of each conjugate pair is executed
-    st = ops.tall_gemm(A, Bm, raw, stats=True, row_offset=row0,
-                       alg_flops=4.0 * n_loc * K * plan.lam.size)      # (U, 3)
+    with stage("modes.raw+stats"):
+        st = ops.tall_gemm(A, Bm, raw, stats=True, row_offset=row0,
+                           alg_flops=4.0 * n_loc * K * plan.lam.size)  # (U, 3)
     st = la._reduce_pair_stats(st, shard)
     nrm = torch.sqrt(st[:, 0])
     idx = st[:, 2].round().long()
@@ -338,8 +341,10 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
         cols[k] = im_of(u, cj, 1.0)
     for c in cols:
         t_src.append(c[0]); t_al.append(c[1]); t_be.append(c[2])
-    table = alloc_tall(n_loc, lay.ncol, table_dtype, "col", device=dev)
-    ops.table_apply(raw, t_src, t_al, t_be, table, lay.ncol)
+    with stage("modes.alloc_table"):
+        table = alloc_tall(n_loc, lay.ncol, table_dtype, "col", device=dev)
+    with stage("modes.table_apply"):
+        ops.table_apply(raw, t_src, t_al, t_be, table, lay.ncol)
     general = None
     if not exact:
         general = alloc_tall(n_loc, 2 * r, table_dtype, "col", device=dev)
@@ -613,7 +618,8 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
     n, T = data.n, data.n_transitions
     if not 1 <= r <= min(n, T):
         raise ValueError(f"rank {r} out of range [1, {min(n, T)}]")
-    basis = _fit_basis(data, r, svd_mode, seed, oversample, power_iters, timings)
+    with stage("optdmd.basis"):
+        basis = _fit_basis(data, r, svd_mode, seed, oversample, power_iters, timings)
     Sv = basis.S.cpu().numpy()
     _check_sigma(Sv)
     t0 = time.perf_counter()
@@ -621,16 +627,18 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
     if init is None:
         # alpha0 = exact_dmd(data, r, svd_mode, seed).lam (dmd.py:387): the same
         # seed reproduces the same SVD, so the eigenvalues come from it directly.
-        VS = basis.V / basis.S[None, :]
-        Khat = basis.UtS[:, 1:] @ VS
-        lam_raw, _ = _eig_device(Khat)
-        alpha0 = pair_plan(lam_raw).lam
+        with stage("small.eig(Khat)"):
+            VS = basis.V / basis.S[None, :]
+            Khat = basis.UtS[:, 1:] @ VS
+            lam_raw, _ = _eig_device(Khat)
+            alpha0 = pair_plan(lam_raw).lam
     else:
         alpha0 = np.asarray(init, dtype=np.complex128)
         if alpha0.size != r:
             raise ValueError(f"init has {alpha0.size} eigenvalues, expected {r}")
     try:
-        alpha, B, history, converged = _varpro_lm_device(Dm, alpha0, cfg)
+        with stage("small.varpro_lm"):
+            alpha, B, history, converged = _varpro_lm_device(Dm, alpha0, cfg)
     except _AlphaCollapse:
         rng = np.random.default_rng(0 if seed is None else seed)
         jitter = 1e-10 * (1.0 + np.abs(alpha0)) * np.exp(2j * np.pi * rng.random(alpha0.size))
@@ -656,11 +664,13 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
     if basis.Umap is None:
         U = basis.A
     else:
-        U = alloc_tall(basis.A.n, r, tdt, "col", device=basis.A.buf.device)
-        nl = float(basis.A.n)
-        dv.get_ops().tall_gemm(basis.A, basis.Umap, U, alg_flops=2 * nl * basis.A.k * r)   # lift (linalg.py:88)
-        basis.A = None                                                       # release Q
-    modes = _modes_pass(U, Bt, plan, 0, data.shard, tdt, timings)
+        with stage("lift.U=QUb"):
+            U = alloc_tall(basis.A.n, r, tdt, "col", device=basis.A.buf.device)
+            nl = float(basis.A.n)
+            dv.get_ops().tall_gemm(basis.A, basis.Umap, U, alg_flops=2 * nl * basis.A.k * r)   # linalg.py:88
+            basis.A = None                                                   # release Q
+    with stage("optdmd.modes_total"):
+        modes = _modes_pass(U, Bt, plan, 0, data.shard, tdt, timings)
     model = ReducedModel(None, plan.lam, Sv, data.dt, grid_meta=data.grid_meta,
                          provenance={"method": "optdmd", "svd": svd_mode, "seed": seed,
                                      "objective_history": history, "converged": converged},

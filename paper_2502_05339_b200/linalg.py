@@ -21,6 +21,7 @@ import torch
 from . import device as dv
 from .device import Shard, Tall, allreduce, alloc_tall
 from .errors import ConvergenceError
+from .trace import stage
 
 if torch.cuda.is_available():
     try:
@@ -110,6 +111,17 @@ def copy_rows_h2d(T: Tall, t: torch.Tensor, row0: int = 0):
     dst = T.buf.data_ptr() + row0 * T.ld * elt
     kind = 4  # cudaMemcpyDefault (UVA)
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if t.device.type == "cpu" and T.ld != k and rows * k * elt > (64 << 20):
+        # A host->device DMA with a short row pitch is slow (one descriptor per
+        # row); stream contiguous chunks through a staging buffer and re-pitch
+        # them on the device instead.
+        chunk = max(1, (512 << 20) // (k * elt))
+        staging = torch.empty(min(chunk, rows) * k, dtype=T.dtype, device=T.buf.device)
+        for r0 in range(0, rows, chunk):
+            rr = min(chunk, rows - r0)
+            staging[: rr * k].copy_(t[r0:r0 + rr].reshape(-1), non_blocking=True)
+            T.buf[row0 + r0:row0 + r0 + rr, :k].copy_(staging[: rr * k].view(rr, k))
+        return
     _lib.check(_lib.lib().fdmd_copy2d(ctypes.c_void_p(dst), T.ld * elt, ctypes.c_void_p(t.data_ptr()),
                                       k * elt, k * elt, rows, kind, stream), "copy2d")
 
@@ -137,11 +149,13 @@ def cholqr2_inplace(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict
     """Orthonormalise the columns of Y in place. Returns R (Y_in = Q R)."""
     ops = dv.get_ops()
     l = Y.k
-    G = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
-    R1 = _chol_upper(G)
-    if R1 is None:
-        return _householder_inplace(Y, shard, stats)
-    cond = float(torch.linalg.cond(R1).item())
+    with stage("cholqr.gram"):
+        G = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
+    with stage("cholqr.chol+cond"):
+        R1 = _chol_upper(G)
+        if R1 is None:
+            return _householder_inplace(Y, shard, stats)
+        cond = float(torch.linalg.cond(R1).item())
     if stats is not None:
         stats.setdefault("cond_R1", []).append(cond)
     if cond > CHOLQR2_COND_LIMIT:
@@ -224,19 +238,28 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     m = S.k
     stats: dict = {}
     if Q is None:
-        Q = alloc_tall(S.n, l, torch.float64, "row", device=dev)
+        with stage("sketch.alloc_Q"):
+            Q = alloc_tall(S.n, l, torch.float64, "row", device=dev)
     Om = torch.as_tensor(np.asarray(omega, dtype=np.float64), device=dev)
     nl = float(S.n)
-    ops.tall_gemm(S, _pad_rows(Om, m), Q, alg_flops=2 * nl * T * l)
-    cholqr2_inplace(Q, shard, stats)
-    for _ in range(q):
-        Z = allreduce(shard, ops.tall_gram(S, Q, alg_flops=2 * nl * T * l))   # m x l
-        W, _ = torch.linalg.qr(Z[:T], mode="reduced")        # T x l (Householder, device)
-        ops.tall_gemm(S, _pad_rows(W, m), Q, alg_flops=2 * nl * T * l)
+    with stage("sketch.Y=XOmega"):
+        ops.tall_gemm(S, _pad_rows(Om, m), Q, alg_flops=2 * nl * T * l)
+    with stage("sketch.cholqr2"):
         cholqr2_inplace(Q, shard, stats)
-    QtS = allreduce(shard, ops.tall_gram(Q, S, alg_flops=2 * nl * m * l))     # l x m
-    B = QtS[:, :T]
-    Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvd" if B.is_cuda else None)
+    for _ in range(q):
+        with stage("power.Z=XtQ"):
+            Z = allreduce(shard, ops.tall_gram(S, Q, alg_flops=2 * nl * T * l))   # m x l
+        with stage("power.qr(Z)"):
+            W, _ = torch.linalg.qr(Z[:T], mode="reduced")    # T x l (Householder, device)
+        with stage("power.Y=XW"):
+            ops.tall_gemm(S, _pad_rows(W, m), Q, alg_flops=2 * nl * T * l)
+        with stage("power.cholqr2"):
+            cholqr2_inplace(Q, shard, stats)
+    with stage("project.QtS"):
+        QtS = allreduce(shard, ops.tall_gram(Q, S, alg_flops=2 * nl * m * l))     # l x m
+    with stage("small.svd(B)"):
+        B = QtS[:, :T]
+        Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvd" if B.is_cuda else None)
     return SketchFactors(Q, Ub, s, Vh, QtS, stats)
 
 

@@ -15,7 +15,7 @@ class CpuOps:
     def __init__(self):
         self.launches = 0
 
-    def tall_gemm(self, A, B, C, stats=False, row_offset=0):
+    def tall_gemm(self, A, B, C, stats=False, row_offset=0, alg_flops=None):
         K = B.shape[0]
         Av = _logical(A).to(torch.float64)
         if Av.shape[1] < K:  # row-major buffers may be multiplied over padded columns
@@ -31,7 +31,7 @@ class CpuOps:
             _logical(C).copy_(P.to(C.dtype))
         return st
 
-    def tall_gram(self, A, B, K1=None, K2=None, symmetric=False, out=None):
+    def tall_gram(self, A, B, K1=None, K2=None, symmetric=False, out=None, alg_flops=None):
         Av = _logical(A).to(torch.float64)
         Bv = _logical(B).to(torch.float64)
         K1 = A.k if K1 is None else K1
