@@ -50,6 +50,8 @@ int fdmd_version(void);
 const char* fdmd_last_error(void);
 int fdmd_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
 
+#define FDMD_B_UPPER 1 /* tall_gemm flag: B is upper triangular (CholeskyQR's R^-1) */
+
 /* C[n x N] = A[n x K] * B[K x N]. A: f32/f64, ROW/COL. B: f64 row-major (ld ldb).
  * C: f32/f64 ROW/COL, may be NULL (statistics only). FP64 DMMA accumulation.
  * pair_stats (optional, length 3*(N/2), N even): for unit u = columns (2u, 2u+1)
@@ -58,7 +60,7 @@ size_t fdmd_tall_gemm_workspace(int64_t n, int N);
 int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda,
                    const double* B, int64_t ldb,
                    void* C, int c_dtype, int c_layout, int64_t ldc,
-                   int64_t n, int K, int N,
+                   int64_t n, int K, int N, int flags,
                    double* pair_stats, int64_t row_offset,
                    void* workspace, size_t workspace_bytes, void* stream);
 

@@ -33,7 +33,7 @@ SIGNATURES = {
     "fdmd_last_error": (_c.c_char_p, []),
     "fdmd_device_info": (_i, [_i, _c.POINTER(_i), _c.POINTER(_i), _c.POINTER(_i)]),
     "fdmd_tall_gemm_workspace": (_sz, [_i64, _i]),
-    "fdmd_tall_gemm": (_i, [_vp, _i, _i, _i64, _vp, _i64, _vp, _i, _i, _i64, _i64, _i, _i,
+    "fdmd_tall_gemm": (_i, [_vp, _i, _i, _i64, _vp, _i64, _vp, _i, _i, _i64, _i64, _i, _i, _i,
                             _vp, _i64, _vp, _sz, _vp]),
     "fdmd_tall_gram_workspace": (_sz, [_i64, _i, _i]),
     "fdmd_tall_gram": (_i, [_vp, _i, _i, _i64, _vp, _i, _i, _i64, _vp, _i64, _d, _i64, _i, _i, _i,

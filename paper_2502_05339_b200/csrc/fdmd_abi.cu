@@ -68,7 +68,7 @@ int64_t tg_tiles(int64_t n) { return (n + fdmd::tg::BM - 1) / fdmd::tg::BM; }
 template <typename TA, int AL, int NF, typename TC, int CL, bool ST>
 int launch_tg(const fdmd::TallGemmArgs& a, cudaStream_t s, int grid_x) {
   auto kern = fdmd::tall_gemm_kernel<TA, AL, NF, TC, CL, ST>;
-  const int smem = (int)sizeof(fdmd::TGSmem<NF>);
+  const int smem = (int)sizeof(fdmd::TGSmem<NF, AL>);
   static thread_local int configured = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -195,7 +195,7 @@ size_t fdmd_tall_gemm_workspace(int64_t n, int N) {
 }
 
 int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda, const double* B, int64_t ldb,
-                   void* C, int c_dtype, int c_layout, int64_t ldc, int64_t n, int K, int N,
+                   void* C, int c_dtype, int c_layout, int64_t ldc, int64_t n, int K, int N, int flags,
                    double* pair_stats, int64_t row_offset, void* workspace, size_t workspace_bytes,
                    void* stream) {
   if (n < 0 || K < 0 || N < 0) return fail(FDMD_ERR_INVALID, "negative size");
@@ -214,6 +214,7 @@ int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda, const 
   fdmd::TallGemmArgs a{};
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.C = C; a.ldc = ldc;
   a.n = n; a.K = K; a.N = N; a.row_offset = row_offset;
+  a.b_upper = (flags & FDMD_B_UPPER) ? 1 : 0;
   const bool stats = pair_stats != nullptr;
   if (stats) {
     const size_t need = (size_t)gx * (size_t)(N / 2) * 3 * sizeof(double);
@@ -299,7 +300,7 @@ int fdmd_decode(const void* D, int dtype, int64_t ldd, const void* coef, int ldc
     else if (left <= 4) { rpt = 4; fb = 4; }
     else if (left <= 8) { rpt = 4; fb = 8; }
     else if (left <= 16) { rpt = 2; fb = 16; }
-    else { rpt = 1; fb = 32; }
+    else { rpt = (dtype == FDMD_F32) ? 2 : 1; fb = 32; }
     if (dtype == FDMD_F64 && rpt == 4) rpt = 2;
     const int threads = 256;
     const int64_t nthreads = (n + rpt - 1) / rpt;
@@ -318,7 +319,7 @@ int fdmd_decode(const void* D, int dtype, int64_t ldd, const void* coef, int ldc
       else if (fb == 4) DEC(float, 4, 4);
       else if (fb == 8) DEC(float, 4, 8);
       else if (fb == 16) DEC(float, 2, 16);
-      else DEC(float, 1, 32);
+      else DEC(float, 2, 32);
     } else {
       if (fb == 1) DEC(double, 2, 1);
       else if (fb == 2) DEC(double, 2, 2);

@@ -142,7 +142,7 @@ def _apply_rinv(Y: Tall, R: torch.Tensor, shard: Optional[Shard]):
     eye = torch.eye(l, dtype=torch.float64, device=R.device)
     Rinv = torch.linalg.solve_triangular(R, eye, upper=True)
     n_tot = Y.n                                               # algorithmic TRSM: n l^2
-    dv.get_ops().tall_gemm(Y, Rinv, Y, alg_flops=float(n_tot) * l * l)
+    dv.get_ops().tall_gemm(Y, Rinv, Y, alg_flops=float(n_tot) * l * l, upper=True)
 
 
 def cholqr2_inplace(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict] = None) -> torch.Tensor:

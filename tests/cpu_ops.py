@@ -15,7 +15,7 @@ class CpuOps:
     def __init__(self):
         self.launches = 0
 
-    def tall_gemm(self, A, B, C, stats=False, row_offset=0, alg_flops=None):
+    def tall_gemm(self, A, B, C, stats=False, row_offset=0, alg_flops=None, upper=False):
         K = B.shape[0]
         Av = _logical(A).to(torch.float64)
         if Av.shape[1] < K:  # row-major buffers may be multiplied over padded columns

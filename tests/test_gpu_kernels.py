@@ -69,14 +69,27 @@ def test_tall_gemm_pair_stats(dv):
     np.testing.assert_array_equal(st, st2)
 
 
-def test_tall_gemm_inplace(dv):
-    rng = np.random.default_rng(4)
-    n, l = 3000, 200
+@pytest.mark.parametrize("upper", [False, True])
+@pytest.mark.parametrize("l", [200, 37, 160])
+def test_tall_gemm_inplace(dv, upper, l):
+    rng = np.random.default_rng(4 + l)
+    n = 3000
     Y = rng.standard_normal((n, l))
     R = np.triu(rng.standard_normal((l, l))) + 5 * np.eye(l)
     Yt = _tall_from(dv, Y, "row", torch.float64)
-    dv.get_ops().tall_gemm(Yt, torch.as_tensor(R, device="cuda"), Yt)
+    dv.get_ops().tall_gemm(Yt, torch.as_tensor(R, device="cuda"), Yt, upper=upper)
     np.testing.assert_allclose(Yt.view().cpu().numpy(), Y @ R, rtol=0, atol=1e-11 * np.abs(Y @ R).max())
+
+
+@pytest.mark.parametrize("K", [200, 13, 64, 71])
+def test_tall_gram_symmetric_shapes(dv, K):
+    rng = np.random.default_rng(K)
+    n = 5003
+    Y = rng.standard_normal((n, K))
+    for layout in ("row", "col"):
+        Yt = _tall_from(dv, Y, layout, torch.float64)
+        G = dv.get_ops().tall_gram(Yt, Yt, symmetric=True).cpu().numpy()
+        np.testing.assert_allclose(G, Y.T @ Y, rtol=0, atol=1e-12 * np.abs(Y.T @ Y).max())
 
 
 @pytest.mark.parametrize("la,lb", [("row", "row"), ("col", "row"), ("row", "col"), ("col", "col")])
