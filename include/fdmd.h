@@ -90,6 +90,11 @@ int fdmd_table_apply(const void* R, int r_dtype, int64_t ldr, const int* src,
                      const double* alpha, const double* beta,
                      void* D, int d_dtype, int64_t ldd, int64_t n, int ncols, void* stream);
 
+/* In place: R[j*ldr + i] <- alpha[j]*R[(2*src[j])*ldr + i] + beta[j]*R[(2*src[j]+1)*ldr + i]
+ * for j < ncols <= nraw (each block stages its rows of all nraw columns first). */
+int fdmd_table_apply_inplace(void* R, int dtype, int64_t ldr, int nraw, const int* src,
+                             const double* alpha, const double* beta, int ncols, int64_t n, void* stream);
+
 /* out[0] = sum_i sum_{j<T} (S[i*lds + 1 + j] - sum_k D[k*ldd+i] F[k*T+j])^2,
  * out[1] = sum_i sum_{j<T} S[i*lds + 1 + j]^2  (out: 2 doubles, device). */
 size_t fdmd_residual_workspace(int64_t n);

@@ -42,6 +42,7 @@ SIGNATURES = {
     "fdmd_colmajor_dot_workspace": (_sz, [_i64, _i, _i]),
     "fdmd_colmajor_dot": (_i, [_vp, _i, _i64, _vp, _i, _i64, _i64, _i, _i, _vp, _vp, _sz, _vp]),
     "fdmd_table_apply": (_i, [_vp, _i, _i64, _vp, _vp, _vp, _vp, _i, _i64, _i64, _i, _vp]),
+    "fdmd_table_apply_inplace": (_i, [_vp, _i, _i64, _i, _vp, _vp, _vp, _i, _i64, _vp]),
     "fdmd_residual_workspace": (_sz, [_i64]),
     "fdmd_residual": (_i, [_vp, _i, _i64, _vp, _i, _i64, _vp, _i, _i, _i64, _vp, _vp, _sz, _vp]),
     "fdmd_geev": (_i, [_i, _vp, _vp, _vp, _vp]),

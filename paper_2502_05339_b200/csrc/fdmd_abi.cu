@@ -400,6 +400,30 @@ static int residual_chunk(int r, int T) {
   return std::max(1, std::min(T, maxcols));
 }
 
+int fdmd_table_apply_inplace(void* R, int dtype, int64_t ldr, int nraw, const int* src, const double* alpha,
+                             const double* beta, int ncols, int64_t n, void* stream) {
+  if (n < 0 || ncols < 0 || nraw <= 0 || ncols > nraw) return fail(FDMD_ERR_INVALID, "table_apply_inplace: bad sizes");
+  if (n == 0 || ncols == 0) return FDMD_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t elt = dsize(dtype);
+  int rpb = 128;
+  while (rpb > 8 && (size_t)nraw * rpb * elt > 160 * 1024) rpb /= 2;
+  const size_t smem = (size_t)nraw * rpb * elt;
+  if (smem > 200 * 1024) return fail(FDMD_ERR_INVALID, "table_apply_inplace: too many raw columns");
+  const int64_t tiles = (n + rpb - 1) / rpb;
+  const int blocks = (int)std::min<int64_t>(tiles, (int64_t)sm_count_cached() * 8);
+#define TAI(T)                                                                                        \
+  do {                                                                                                \
+    auto k = fdmd::table_apply_inplace_kernel<T>;                                                     \
+    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));       \
+    k<<<blocks, 256, smem, s>>>((T*)R, ldr, nraw, src, alpha, beta, ncols, n, rpb);                  \
+  } while (0)
+  if (dtype == FDMD_F32) TAI(float); else TAI(double);
+#undef TAI
+  LAUNCH_CHECK("table_apply_inplace");
+  return FDMD_OK;
+}
+
 size_t fdmd_residual_workspace(int64_t n) {
   (void)n;
   // up to 64 column chunks x blocks x 2 partial sums

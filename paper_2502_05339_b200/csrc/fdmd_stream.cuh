@@ -171,6 +171,40 @@ __global__ void table_apply_kernel(const TR* __restrict__ R, int64_t ldr, const 
   }
 }
 
+// In-place variant: the table overwrites the raw buffer (column j of the
+// output lands in raw column j). Each block stages ITS rows of all `nraw`
+// raw columns in shared memory before writing, so no block reads a value
+// another block has overwritten. Saves a second n x r buffer (40 GB at
+// config 3) and one HBM allocation per fit.
+template <typename T>
+__global__ void __launch_bounds__(256) table_apply_inplace_kernel(T* __restrict__ R, int64_t ldr, int nraw,
+                                                                  const int* __restrict__ src,
+                                                                  const double* __restrict__ alpha,
+                                                                  const double* __restrict__ beta, int ncols,
+                                                                  int64_t n, int rows_per_block) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* s = reinterpret_cast<T*>(smem_raw);  // nraw x rows_per_block
+  for (int64_t r0 = (int64_t)blockIdx.x * rows_per_block; r0 < n; r0 += (int64_t)gridDim.x * rows_per_block) {
+    const int64_t left = n - r0;
+    const int rows = left < rows_per_block ? (int)left : rows_per_block;
+    for (int e = threadIdx.x; e < nraw * rows_per_block; e += blockDim.x) {
+      const int c = e / rows_per_block, i = e % rows_per_block;
+      if (i < rows) s[e] = R[(int64_t)c * ldr + r0 + i];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < ncols * rows_per_block; e += blockDim.x) {
+      const int j = e / rows_per_block, i = e % rows_per_block;
+      if (i < rows) {
+        const int u = src[j];
+        const double v = alpha[j] * (double)s[(2 * u) * rows_per_block + i] +
+                         beta[j] * (double)s[(2 * u + 1) * rows_per_block + i];
+        R[(int64_t)j * ldr + r0 + i] = (T)v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ===========================================================================
 // Residual: part[b] = (sum_i ||S[i, 1:T+1] - D[:, i]^T F||^2, sum_i ||S[i, 1:T+1]||^2)
 // per block, used for the exact_dmd one-step residual diagnostic

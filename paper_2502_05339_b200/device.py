@@ -230,6 +230,18 @@ class CudaOps:
                                                _stream()), "table_apply")
         self.launches += 1
 
+    def table_apply_inplace(self, R: Tall, src, alpha, beta, ncols: int) -> Tall:
+        """R's first ncols columns become the table (R column-major, 2U >= ncols)."""
+        dev = R.buf.device
+        src_t = torch.as_tensor(np.asarray(src, dtype=np.int32), device=dev)
+        a_t = torch.as_tensor(np.asarray(alpha, dtype=np.float64), device=dev)
+        b_t = torch.as_tensor(np.asarray(beta, dtype=np.float64), device=dev)
+        _lib.check(_lib.lib().fdmd_table_apply_inplace(_ptr(R.buf), _DT[R.dtype], R.ld, R.k, _ptr(src_t),
+                                                       _ptr(a_t), _ptr(b_t), ncols, R.n, _stream()),
+                   "table_apply_inplace")
+        self.launches += 1
+        return Tall(R.buf, "col", R.n, ncols)
+
     def residual(self, S: Tall, D: Tall, F: torch.Tensor, ncols: int, T: int) -> torch.Tensor:
         L = _lib.lib()
         F = F.to(torch.float64).contiguous()

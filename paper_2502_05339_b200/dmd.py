@@ -341,12 +341,9 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
         cols[k] = im_of(u, cj, 1.0)
     for c in cols:
         t_src.append(c[0]); t_al.append(c[1]); t_be.append(c[2])
-    with stage("modes.alloc_table"):
-        table = alloc_tall(n_loc, lay.ncol, table_dtype, "col", device=dev)
-    with stage("modes.table_apply"):
-        ops.table_apply(raw, t_src, t_al, t_be, table, lay.ncol)
     general = None
     if not exact:
+        # only hand-built / degenerate spectra: keep an explicit [Re phi_a, Im phi_a] basis
         general = alloc_tall(n_loc, 2 * r, table_dtype, "col", device=dev)
         g_src, g_al, g_be = [], [], []
         for a in range(r):
@@ -359,6 +356,9 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
             for c in (c1, c2):
                 g_src.append(c[0]); g_al.append(c[1]); g_be.append(c[2])
         ops.table_apply(raw, g_src, g_al, g_be, general, 2 * r)
+    # the decode table overwrites the raw buffer in place (no second n x r allocation)
+    with stage("modes.table_apply"):
+        table = ops.table_apply_inplace(raw, t_src, t_al, t_be, lay.ncol)
     del raw
     if timings is not None:
         timings["modes_s"] = time.perf_counter() - t0

@@ -63,6 +63,14 @@ class CpuOps:
             v = alpha[j] * R.buf[2 * u, : R.n].to(torch.float64) + beta[j] * R.buf[2 * u + 1, : R.n].to(torch.float64)
             D.buf[j, : D.n] = v.to(D.dtype)
 
+    def table_apply_inplace(self, R, src, alpha, beta, ncols):
+        from paper_2502_05339_b200.device import Tall
+        raw = R.buf[: R.k, : R.n].to(torch.float64).clone()
+        for j in range(ncols):
+            u = src[j]
+            R.buf[j, : R.n] = (alpha[j] * raw[2 * u] + beta[j] * raw[2 * u + 1]).to(R.dtype)
+        return Tall(R.buf, "col", R.n, ncols)
+
     def residual(self, S, D, F, ncols, T):
         Sv = _logical(S).to(torch.float64)
         rec = D.buf[:ncols, : D.n].to(torch.float64).t() @ F.to(torch.float64)

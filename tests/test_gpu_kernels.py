@@ -164,6 +164,14 @@ def test_table_apply_and_residual(dv):
     D = Dt.view().cpu().numpy()
     want = np.stack([al[j] * R[:, 2 * src[j]] + be[j] * R[:, 2 * src[j] + 1] for j in range(5)], axis=1)
     np.testing.assert_allclose(D, want, rtol=1e-14, atol=1e-14)
+    for dt in (torch.float64, torch.float32):
+        Ri = _tall_from(dv, R, "col", dt)
+        Ti = dv.get_ops().table_apply_inplace(Ri, src, al, be, 5)
+        assert Ti.k == 5 and Ti.buf.data_ptr() == Ri.buf.data_ptr()
+        Rd = R.astype(np.float32).astype(np.float64) if dt == torch.float32 else R
+        want_i = np.stack([al[j] * Rd[:, 2 * src[j]] + be[j] * Rd[:, 2 * src[j] + 1] for j in range(5)], axis=1)
+        tol = 1e-6 if dt == torch.float32 else 1e-14
+        np.testing.assert_allclose(Ti.view().double().cpu().numpy(), want_i, rtol=tol, atol=tol)
     S = rng.standard_normal((n, m))
     St = _tall_from(dv, S, "row", torch.float64)
     F = rng.standard_normal((5, m - 1))
