@@ -353,25 +353,38 @@ def run_e2e(args, fd, host, n_loc, m, r, cfg, lm, shard, F_fit, max_over_ranks, 
     import warnings
 
     import torch
+    from paper_2502_05339_b200 import trace
     ts = []
+    stages = {}
     for i in range(1 + args.e2e_steps):
         barrier()
         torch.cuda.synchronize()
+        if i >= 1:
+            trace.enable()
         t0 = time.perf_counter()
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
-            d2 = fd.SnapshotMatrix(host, 0.1, shard=shard)
-            model = fd.optdmd(d2, r, lm_config=lm, svd_mode="randomized", seed=cfg["seed"],
-                              oversample=cfg["p"], power_iters=cfg["q"])
-            z0 = fd.ReducedState(np.ones(r, dtype=complex))
-            frame = fd.decode(model, fd.step_k(model, z0, 10))            # D2H of one frame
+            with trace.stage("e2e.upload"):
+                d2 = fd.SnapshotMatrix(host, 0.1, shard=shard)
+            with trace.stage("e2e.fit"):
+                model = fd.optdmd(d2, r, lm_config=lm, svd_mode="randomized", seed=cfg["seed"],
+                                  oversample=cfg["p"], power_iters=cfg["q"])
+            with trace.stage("e2e.frame_d2h"):
+                z0 = fd.ReducedState(np.ones(r, dtype=complex))
+                frame = fd.decode(model, fd.step_k(model, z0, 10))        # D2H of one frame
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        if i >= 1:
+            rec = trace.disable()
+            for k, v in trace.summarize(rec).items():
+                if k.startswith("e2e."):
+                    stages[k] = stages.get(k, 0.0) + v / args.e2e_steps
         del d2, model, frame
         if i >= 1:
             ts.append(max_over_ranks(dt))
     t = float(np.mean(ts))
     return {"value": round(F_fit / t / 1e9, 2), "unit": "GFLOP/s", "s_per_step": round(t, 3),
+            "stages_ms": {k: round(v, 1) for k, v in stages.items()},
             "h2d_bytes_per_step": int(n_loc * m * 4), "d2h_bytes_per_step": int(n_loc * 8 + 2 * r * 16),
             "api": "SnapshotMatrix(pinned host f32) -> optdmd -> decode(step_k) to host"}
 

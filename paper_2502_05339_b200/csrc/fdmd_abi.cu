@@ -58,6 +58,11 @@ inline size_t dsize(int dt) { return dt == FDMD_F32 ? 4 : 8; }
 template <int NF> constexpr int bn_of() { return 32 * NF; }
 
 int pick_nf(int N) {
+  static const int forced = [] {
+    const char* e = getenv("FDMD_TG_NF");  // tuning override: 2, 4 or 7
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 2 || forced == 4 || forced == 7) return forced;
   if (N <= 64) return 2;
   if (N <= 128) return 4;
   return 7;
@@ -68,7 +73,7 @@ int64_t tg_tiles(int64_t n) { return (n + fdmd::tg::BM - 1) / fdmd::tg::BM; }
 template <typename TA, int AL, int NF, typename TC, int CL, bool ST>
 int launch_tg(const fdmd::TallGemmArgs& a, cudaStream_t s, int grid_x) {
   auto kern = fdmd::tall_gemm_kernel<TA, AL, NF, TC, CL, ST>;
-  const int smem = (int)sizeof(fdmd::TGSmem<NF, AL>);
+  const int smem = (int)sizeof(fdmd::TGSmem<TA, AL, NF>);
   static thread_local int configured = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -139,8 +144,17 @@ GramPlan gram_plan(int64_t n, int K1, int K2, int symmetric) {
 
 template <typename TA, int LA, typename TB, int LB>
 int launch_gram(const fdmd::TallGramArgs& a, int tiles, int splits, cudaStream_t s) {
+  auto kern = fdmd::tall_gram_kernel<TA, LA, TB, LB>;
+  const int smem = (int)sizeof(fdmd::GramSmem<TA, LA, TB, LB>);
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = dev;
+  }
   dim3 grid(tiles, splits);
-  fdmd::tall_gram_kernel<TA, LA, TB, LB><<<grid, fdmd::gr::THREADS, 0, s>>>(a);
+  kern<<<grid, fdmd::gr::THREADS, smem, s>>>(a);
   LAUNCH_CHECK("tall_gram");
   return FDMD_OK;
 }
@@ -215,6 +229,8 @@ int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda, const 
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.C = C; a.ldc = ldc;
   a.n = n; a.K = K; a.N = N; a.row_offset = row_offset;
   a.b_upper = (flags & FDMD_B_UPPER) ? 1 : 0;
+  static const int dbg = [] { const char* e = getenv("FDMD_TG_DEBUG"); return e ? atoi(e) : 0; }();
+  a.debug = dbg;
   const bool stats = pair_stats != nullptr;
   if (stats) {
     const size_t need = (size_t)gx * (size_t)(N / 2) * 3 * sizeof(double);

@@ -1,144 +1,147 @@
 // FP64 DMMA contractions for the tall-skinny products of the fit.
 // Included by fdmd_kernels.cu.
 //
-// Shared-memory layout rule (both kernels): a DMMA m8n8k4 fragment read is
-// 4 rows (t = lane&3) x 8 consecutive doubles (g = lane>>2), executed as two
-// half-warp phases of 4 rows x 4 doubles (32 B each). A row stride of 4 mod 16
-// doubles (32 B mod 128 B) puts the four rows of a phase on disjoint bank
-// groups, so every fragment read is the minimum 2 wavefronts. (The first
-// version used 8 mod 16 and measured 2x excess wavefronts in ncu.)
+// Pipeline: a 4-stage cp.async ring streams raw (fp32 or fp64) operand tiles
+// into shared memory; fragments are converted to fp64 at read time, so no
+// register ever waits on HBM at a prefetch point and the loads run three
+// chunks ahead of the DMMA work. Tails are zero-filled by cp.async (src-size),
+// never read from padding.
 //
-// Fragments that are entirely outside the valid output (padding to the tile
-// size), entirely below the diagonal of a symmetric Gram, or entirely zero
-// because the small operand is upper triangular (CholeskyQR's R^-1) are
-// skipped with warp-uniform branches, so the DMMA pipe only executes useful
-// work; the counted flops are the algorithmic ones of SURVEY.md §8d.
+// Shared-memory layout rule: every DMMA m8n8k4 fragment read (4 k x 8 m
+// elements per warp) must hit distinct bank groups. With raw-type staging the
+// required row stride depends on the element size and on which index is
+// contiguous; each stage type below states its stride. Fragments entirely in
+// padding, below the diagonal of a symmetric Gram, or zero because the small
+// operand is upper triangular (CholeskyQR's R^-1) are skipped with warp-
+// uniform branches, so the DMMA pipe executes only algorithmic work.
 #pragma once
 #include "fdmd_kernels.cuh"
 
 namespace fdmd {
 
+// ------------------------------------------------------------- cp.async ----
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_small(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem), "n"(BYTES), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ int clamp_valid(int64_t rem, int V) {
+  return rem <= 0 ? 0 : (rem < V ? (int)rem : V);
+}
+
+// Copy `vlen` consecutive elements starting at gmem (of which `valid` are in
+// bounds) into smem; vectorised (16 B) when `vec`, element-wise otherwise.
+template <typename T>
+__device__ __forceinline__ void cp_vec(T* smem, const T* gmem, int valid, bool vec, const T* safe) {
+  constexpr int V = 16 / sizeof(T);
+  if (vec) {
+    cp_async16(smem, valid > 0 ? gmem : safe, valid > 0 ? valid * (int)sizeof(T) : 0);
+  } else {
+#pragma unroll
+    for (int q = 0; q < V; ++q)
+      cp_async_small<sizeof(T)>(smem + q, q < valid ? gmem + q : safe, q < valid ? (int)sizeof(T) : 0);
+  }
+}
+
 // ===========================================================================
 // tall_gemm: C[n x N] = A[n x K] * B[K x N]
 // CTA = 8 warps (2 along M x 4 along N); warp tile 32 x 8*NF; CTA tile
-// 64 x 32*NF; K streamed in chunks of 16, register double buffering;
-// persistent over row tiles (grid-stride) so the pair-statistics epilogue
-// keeps one partial per CTA.
+// 64 x 32*NF; K in chunks of 16; persistent over row tiles (grid-stride) with
+// one flat (tile, chunk) pipeline, so loads run ahead across tile boundaries
+// and the pair-statistics epilogue keeps one partial per CTA.
 // ===========================================================================
 namespace tg {
 constexpr int BM = 64;
 constexpr int BK = 16;
-constexpr int LDAR = BK + 4;   // row-major A staging: As[m][k], 20 doubles
-constexpr int LDAC = BM + 4;   // k-major A staging:   As[k][m], 68 doubles
+constexpr int STAGES = 4;
 constexpr int THREADS = 256;
 }  // namespace tg
 
-template <int A_LAYOUT> struct ASmem;
-template <> struct ASmem<LAYOUT_ROW> { double a[tg::BM][tg::LDAR]; };
-template <> struct ASmem<LAYOUT_COL> { double a[tg::BK][tg::LDAC]; };
-
-template <int NF, int A_LAYOUT> struct TGSmem {
-  static constexpr int BN = 32 * NF;
-  static constexpr int LDB_S = BN + 4;
-  ASmem<A_LAYOUT> As[2];
-  double Bs[2][tg::BK][LDB_S];
-  double red[2][4][8 * NF / 2][3];  // cross-warp (wm) stats exchange
+// A stage. ROW: a[m][k], stride 20 elements (fp32: 80 B = 16 mod 128 -> the 8
+// rows x 16 B of a fragment read are distinct; fp64: 160 B = 32 mod 128 -> each
+// half-warp's 4 rows x 32 B are distinct). COL: a[k][m], stride 72 floats
+// (288 B) or 68 doubles (544 B), both 32 mod 128 B.
+template <typename TA, int AL> struct AStage;
+template <typename TA> struct AStage<TA, LAYOUT_ROW> {
+  static constexpr int LD = 20;
+  TA a[tg::BM][LD];
+  __device__ __forceinline__ double frag(int m, int k) const { return (double)a[m][k]; }
+};
+template <typename TA> struct AStage<TA, LAYOUT_COL> {
+  static constexpr int LD = sizeof(TA) == 4 ? 72 : 68;
+  TA a[tg::BK][LD];
+  __device__ __forceinline__ double frag(int m, int k) const { return (double)a[k][m]; }
 };
 
-template <typename TA>
-__device__ __forceinline__ void load4(const TA* p, double (&v)[4]) {
-  if (sizeof(TA) == 4) {
-    const float4 f = __ldg(reinterpret_cast<const float4*>(p));
-    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+template <typename TA, int AL, int NF> struct TGSmem {
+  static constexpr int BN = 32 * NF;
+  static constexpr int LDB = BN + 4;  // 4 mod 16 doubles
+  AStage<TA, AL> As[tg::STAGES];
+  double Bs[tg::STAGES][tg::BK][LDB];
+  double red[2][4][8 * NF / 2][3];    // cross-warp (wm) statistics exchange
+};
+
+template <typename TA, int AL>
+__device__ __forceinline__ void tg_load_a(AStage<TA, AL>& st, const TA* __restrict__ A, int64_t lda, int64_t n,
+                                          int K, int64_t row0, int k0, int tid, bool vec) {
+  constexpr int V = 16 / sizeof(TA);
+  if (AL == LAYOUT_ROW) {
+    constexpr int VPR = tg::BK / V;                 // vectors per row
+    constexpr int PER = tg::BM * VPR / tg::THREADS;  // 1 (fp32) or 2 (fp64)
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int e = tid + p * tg::THREADS;
+      const int i = e / VPR, kv = (e % VPR) * V;
+      const int64_t row = row0 + i;
+      const int k = k0 + kv;
+      const int valid = row < n ? max(0, min(V, K - k)) : 0;
+      cp_vec<TA>(&st.a[i][kv], A + row * lda + k, valid, vec, A);
+    }
   } else {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    constexpr int VPR = tg::BM / V;
+    constexpr int PER = tg::BK * VPR / tg::THREADS;
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int e = tid + p * tg::THREADS;
+      const int kk = e / VPR, iv = (e % VPR) * V;
+      const int k = k0 + kk;
+      const int64_t row = row0 + iv;
+      const int valid = k < K ? clamp_valid(n - row, V) : 0;
+      cp_vec<TA>(&st.a[kk][iv], A + (int64_t)k * lda + row, valid, vec, A);
+    }
   }
 }
 
-template <typename TA, int A_LAYOUT>
-struct ATileLoader {
-  // Each thread owns 4 elements of the 64 x 16 chunk.
-  double v[4];
-  __device__ __forceinline__ void load(const TA* __restrict__ A, int64_t lda, int64_t n, int K,
-                                       int64_t row0, int k0, int tid, bool vec_ok) {
-    if (A_LAYOUT == LAYOUT_ROW) {
-      const int i = tid >> 2, j = (tid & 3) * 4;
-      const int64_t row = row0 + i;
-      const int k = k0 + j;
-      if (row < n && vec_ok && k + 3 < K) {
-        load4(A + row * lda + k, v);
-      } else {
+template <int NF, int LDB>
+__device__ __forceinline__ void tg_load_b(double (*Bs)[LDB], const double* __restrict__ B, int64_t ldb, int K,
+                                          int N, int k0, int n0, int tid, bool vec) {
+  constexpr int BN = 32 * NF;
+  constexpr int VPR = BN / 2;
+  constexpr int PER = tg::BK * VPR / tg::THREADS;    // = NF
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          v[q] = (row < n && k + q < K) ? to_f64(__ldg(A + row * lda + k + q)) : 0.0;
-      }
-    } else {
-      const int k = k0 + (tid >> 4);
-      const int i = (tid & 15) * 4;
-      const int64_t row = row0 + i;
-      if (k < K && vec_ok && row + 3 < n) {
-        load4(A + (int64_t)k * lda + row, v);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          v[q] = (k < K && row + q < n) ? to_f64(__ldg(A + (int64_t)k * lda + row + q)) : 0.0;
-      }
-    }
+  for (int p = 0; p < PER; ++p) {
+    const int e = tid + p * tg::THREADS;
+    const int kk = e / VPR, jv = (e % VPR) * 2;
+    const int k = k0 + kk, j = n0 + jv;
+    const int valid = k < K ? max(0, min(2, N - j)) : 0;
+    cp_vec<double>(&Bs[kk][jv], B + (int64_t)k * ldb + j, valid, vec, B);
   }
-  __device__ __forceinline__ void store(ASmem<A_LAYOUT>& s, int tid) {
-    if (A_LAYOUT == LAYOUT_ROW) {
-      const int i = tid >> 2, j = (tid & 3) * 4;
-      double2* p = reinterpret_cast<double2*>(&s.a[i][j]);
-      p[0] = make_double2(v[0], v[1]);
-      p[1] = make_double2(v[2], v[3]);
-    } else {
-      const int k = tid >> 4, i = (tid & 15) * 4;
-      double2* p = reinterpret_cast<double2*>(&s.a[k][i]);
-      p[0] = make_double2(v[0], v[1]);
-      p[1] = make_double2(v[2], v[3]);
-    }
-  }
-};
-
-template <int A_LAYOUT>
-__device__ __forceinline__ double afrag(const ASmem<A_LAYOUT>& s, int m, int k) {
-  if (A_LAYOUT == LAYOUT_ROW) return s.a[m][k];
-  return s.a[k][m];
 }
-
-template <int NF>
-struct BTileLoader {
-  static constexpr int BN = 32 * NF;
-  static constexpr int PER = (tg::BK * BN) / tg::THREADS;  // = 2*NF
-  double v[PER];
-  __device__ __forceinline__ void load(const double* __restrict__ B, int64_t ldb, int K, int N,
-                                       int k0, int n0, int tid) {
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = tid + q * tg::THREADS;
-      const int kk = e / BN, jj = e % BN;
-      const int k = k0 + kk, j = n0 + jj;
-      v[q] = (k < K && j < N) ? __ldg(B + (int64_t)k * ldb + j) : 0.0;
-    }
-  }
-  template <int LDB_S>
-  __device__ __forceinline__ void store(double (*Bs)[LDB_S], int tid) {
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = tid + q * tg::THREADS;
-      Bs[e / BN][e % BN] = v[q];
-    }
-  }
-};
 
 template <typename TA, int A_LAYOUT, int NF, typename TC, int C_LAYOUT, bool STATS>
-__global__ void __launch_bounds__(tg::THREADS, 1) tall_gemm_kernel(TallGemmArgs args) {
-  using S = TGSmem<NF, A_LAYOUT>;
+__global__ void __launch_bounds__(tg::THREADS, (NF <= 4) ? 2 : 1) tall_gemm_kernel(TallGemmArgs args) {
+  using S = TGSmem<TA, A_LAYOUT, NF>;
   constexpr int BN = S::BN;
-  constexpr int LDB_S = S::LDB_S;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int LDB = S::LDB;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
 
   const TA* __restrict__ A = static_cast<const TA*>(args.A);
@@ -149,94 +152,97 @@ __global__ void __launch_bounds__(tg::THREADS, 1) tall_gemm_kernel(TallGemmArgs 
   const int n0 = blockIdx.y * BN;
   const int64_t ntiles = (args.n + tg::BM - 1) / tg::BM;
   const int nk = (args.K + tg::BK - 1) / tg::BK;
-  const bool vec_ok =
-      ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
-      ((args.lda * (int64_t)sizeof(TA)) % 16 == 0);
-  // first output column of each of this warp's fragments; warp-uniform validity
+  const bool vec_a = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((args.lda * (int64_t)sizeof(TA)) % 16 == 0);
+  const bool vec_b = ((reinterpret_cast<uintptr_t>(args.B) & 15) == 0) && ((args.ldb * 8) % 16 == 0);
   const int wcol0 = n0 + wn * 8 * NF;
-  const bool upper = args.b_upper != 0;
+
+  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t total = my_tiles * nk;
+
+  // Producer-side position (row tile, k chunk, ring stage), advanced
+  // incrementally: no 64-bit division on the critical path.
+  int64_t p_it = 0, p_tile = blockIdx.x;
+  int p_kc = 0, p_s = 0;
+  auto issue = [&]() {
+    if (p_it < total && !(args.debug & 1)) {
+      tg_load_a<TA, A_LAYOUT>(sm.As[p_s], A, args.lda, args.n, args.K, p_tile * tg::BM, p_kc * tg::BK, tid, vec_a);
+      tg_load_b<NF, LDB>(sm.Bs[p_s], args.B, args.ldb, args.K, args.N, p_kc * tg::BK, n0, tid, vec_b);
+    }
+    cp_async_commit();
+    ++p_it;
+    p_s = (p_s + 1 == tg::STAGES) ? 0 : p_s + 1;
+    if (++p_kc == nk) { p_kc = 0; p_tile += gridDim.x; }
+  };
 
   double st_sum[NF], st_max[NF];
   int64_t st_idx[NF];
 #pragma unroll
   for (int f = 0; f < NF; ++f) { st_sum[f] = 0.0; st_max[f] = -1.0; st_idx[f] = INT64_MAX; }
 
-  ATileLoader<TA, A_LAYOUT> la;
-  BTileLoader<NF> lb;
+#pragma unroll
+  for (int s = 0; s < tg::STAGES - 1; ++s) issue();
 
+  double acc[4][NF][2];
+  int kc = 0, s = 0;
   int64_t tile = blockIdx.x;
-  if (tile < ntiles) {
-    la.load(A, args.lda, args.n, args.K, tile * tg::BM, 0, tid, vec_ok);
-    lb.load(args.B, args.ldb, args.K, args.N, 0, n0, tid);
-  }
-  int buf = 0;
-  for (; tile < ntiles; tile += gridDim.x) {
-    const int64_t row0 = tile * tg::BM;
-    double acc[4][NF][2];
+  for (int64_t it = 0; it < total; ++it) {
+    cp_async_wait<tg::STAGES - 2>();
+    __syncthreads();
+    issue();
+    if (kc == 0) {
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int f = 0; f < NF; ++f) acc[mi][f][0] = acc[mi][f][1] = 0.0;
-
-    for (int kc = 0; kc < nk; ++kc) {
-      la.store(sm.As[buf], tid);
-      lb.template store<LDB_S>(sm.Bs[buf], tid);
-      __syncthreads();
-      if (kc + 1 < nk) {
-        la.load(A, args.lda, args.n, args.K, row0, (kc + 1) * tg::BK, tid, vec_ok);
-        lb.load(args.B, args.ldb, args.K, args.N, (kc + 1) * tg::BK, n0, tid);
-      } else if (tile + gridDim.x < ntiles) {
-        la.load(A, args.lda, args.n, args.K, (tile + gridDim.x) * tg::BM, 0, tid, vec_ok);
-        lb.load(args.B, args.ldb, args.K, args.N, 0, n0, tid);
-      }
+        for (int f = 0; f < NF; ++f) acc[mi][f][0] = acc[mi][f][1] = 0.0;
+    }
 #pragma unroll
-      for (int ks = 0; ks < tg::BK / 4; ++ks) {
-        const int kb = kc * tg::BK + ks * 4;  // first k of this step (warp-uniform)
-        if (kb >= args.K) break;
-        double a[4], b[NF];
+    for (int ks = 0; ks < tg::BK / 4; ++ks) {
+      // branch-free: tails are zero-filled by cp.async, so padded k-steps and
+      // columns contribute exact zeros (a branch around mma.sync costs a
+      // WARPSYNC/BSSY pair per fragment, measured ~2x slower)
+      double a[4], b[NF];
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi) a[mi] = afrag<A_LAYOUT>(sm.As[buf], wm * 32 + mi * 8 + g, ks * 4 + t);
+      for (int mi = 0; mi < 4; ++mi) a[mi] = sm.As[s].frag(wm * 32 + mi * 8 + g, ks * 4 + t);
 #pragma unroll
-        for (int f = 0; f < NF; ++f) b[f] = sm.Bs[buf][ks * 4 + t][wn * 8 * NF + f * 8 + g];
+      for (int f = 0; f < NF; ++f) b[f] = sm.Bs[s][ks * 4 + t][wn * 8 * NF + f * 8 + g];
+#pragma unroll
+      for (int f = 0; f < NF; ++f)
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) dmma884(acc[mi][f], a[mi], b[f]);
+    }
+    if (kc == nk - 1) {
+      const int64_t row0 = tile * tg::BM;
+      TC* __restrict__ C = static_cast<TC*>(args.C);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int64_t row = row0 + wm * 32 + mi * 8 + g;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-          const int c0 = wcol0 + f * 8;
-          if (c0 >= args.N) continue;                 // padded columns
-          if (upper && kb > c0 + 7) continue;         // B[k][c] = 0 for k > c
-#pragma unroll
-          for (int mi = 0; mi < 4; ++mi) dmma884(acc[mi][f], a[mi], b[f]);
-        }
-      }
-      buf ^= 1;
-    }
-
-    TC* __restrict__ C = static_cast<TC*>(args.C);
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi) {
-      const int64_t row = row0 + wm * 32 + mi * 8 + g;
-#pragma unroll
-      for (int f = 0; f < NF; ++f) {
-        const int col = wcol0 + f * 8 + 2 * t;
-        if (row < args.n) {
-          if (C != nullptr) {
-            if (C_LAYOUT == LAYOUT_ROW) {
-              TC* p = C + row * args.ldc + col;
-              if (col < args.N) p[0] = (TC)acc[mi][f][0];
-              if (col + 1 < args.N) p[1] = (TC)acc[mi][f][1];
-            } else {
-              if (col < args.N) C[(int64_t)col * args.ldc + row] = (TC)acc[mi][f][0];
-              if (col + 1 < args.N) C[(int64_t)(col + 1) * args.ldc + row] = (TC)acc[mi][f][1];
+          const int col = wcol0 + f * 8 + 2 * t;
+          if (row < args.n) {
+            if (C != nullptr && !(args.debug & 2)) {
+              if (C_LAYOUT == LAYOUT_ROW) {
+                TC* p = C + row * args.ldc + col;
+                if (col < args.N) p[0] = (TC)acc[mi][f][0];
+                if (col + 1 < args.N) p[1] = (TC)acc[mi][f][1];
+              } else {
+                if (col < args.N) C[(int64_t)col * args.ldc + row] = (TC)acc[mi][f][0];
+                if (col + 1 < args.N) C[(int64_t)(col + 1) * args.ldc + row] = (TC)acc[mi][f][1];
+              }
+            }
+            if (STATS) {
+              const double v = acc[mi][f][0] * acc[mi][f][0] + acc[mi][f][1] * acc[mi][f][1];
+              st_sum[f] += v;
+              if (v > st_max[f]) { st_max[f] = v; st_idx[f] = row + args.row_offset; }
             }
           }
-          if (STATS) {
-            const double v = acc[mi][f][0] * acc[mi][f][0] + acc[mi][f][1] * acc[mi][f][1];
-            st_sum[f] += v;
-            if (v > st_max[f]) { st_max[f] = v; st_idx[f] = row + args.row_offset; }
-          }
         }
       }
     }
+    s = (s + 1 == tg::STAGES) ? 0 : s + 1;
+    if (++kc == nk) { kc = 0; tile += gridDim.x; }
   }
+  cp_async_wait<0>();
 
   if (STATS) {
 #pragma unroll
@@ -297,64 +303,72 @@ __global__ void pair_stats_reduce_kernel(const double* __restrict__ part, int P,
 }
 
 // ===========================================================================
-// tall_gram: partial[split] = A[rows]^T B[rows], 64x64 output tiles.
-// Rows are the MMA k-dimension, streamed in chunks of 16 with register
-// double-buffering; smem row-major As[row][col] with stride 68 doubles.
+// tall_gram: partial[split] = A[rows]^T B[rows], 64x64 output tiles; rows are
+// the MMA k-dimension, 16 per chunk, 4-stage cp.async ring.
 // ===========================================================================
 namespace gr {
 constexpr int T = 64;   // output tile (both dims)
 constexpr int BR = 16;  // rows per chunk
-constexpr int LD = T + 4;
+constexpr int STAGES = 4;
 constexpr int THREADS = 256;
 }  // namespace gr
 
-template <typename TA, int LAYOUT>
-struct GramLoader {
-  double v[4];
-  __device__ __forceinline__ void load(const TA* __restrict__ A, int64_t lda, int64_t rend, int K,
-                                       int64_t r0, int c0, int tid, bool vec_ok) {
-    if (LAYOUT == LAYOUT_ROW) {
-      const int rr = tid >> 4, cc = (tid & 15) * 4;
-      const int64_t row = r0 + rr;
-      const int col = c0 + cc;
-      if (row < rend && vec_ok && col + 3 < K) {
-        load4(A + row * lda + col, v);
-      } else {
+// Operand stage. ROW (global row-major): s[row][col], stride 72 floats / 68
+// doubles (32 mod 128 B: a fragment's 4 rows x 8 cols are distinct). COL
+// (global column-major): s[col][row], stride 20 elements (fp32 80 B = 16 mod
+// 128: 8 cols x 16 B distinct; fp64 160 B = 32 mod 128 per half-warp).
+template <typename T, int L> struct GStage;
+template <typename T> struct GStage<T, LAYOUT_ROW> {
+  static constexpr int LD = sizeof(T) == 4 ? 72 : 68;
+  T s[gr::BR][LD];
+  __device__ __forceinline__ double frag(int col, int row) const { return (double)s[row][col]; }
+};
+template <typename T> struct GStage<T, LAYOUT_COL> {
+  static constexpr int LD = 20;
+  T s[gr::T][LD];
+  __device__ __forceinline__ double frag(int col, int row) const { return (double)s[col][row]; }
+};
+
+template <typename T, int L>
+__device__ __forceinline__ void gr_load(GStage<T, L>& st, const T* __restrict__ A, int64_t lda, int64_t rend,
+                                        int K, int64_t r0, int c0, int tid, bool vec) {
+  constexpr int V = 16 / sizeof(T);
+  if (L == LAYOUT_ROW) {
+    constexpr int VPR = gr::T / V;
+    constexpr int PER = gr::BR * VPR / gr::THREADS;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          v[q] = (row < rend && col + q < K) ? to_f64(__ldg(A + row * lda + col + q)) : 0.0;
-      }
-    } else {
-      const int cc = tid >> 2, rr = (tid & 3) * 4;
-      const int col = c0 + cc;
+    for (int p = 0; p < PER; ++p) {
+      const int e = tid + p * gr::THREADS;
+      const int rr = e / VPR, cv = (e % VPR) * V;
       const int64_t row = r0 + rr;
-      if (col < K && vec_ok && row + 3 < rend) {
-        load4(A + (int64_t)col * lda + row, v);
-      } else {
+      const int col = c0 + cv;
+      const int valid = row < rend ? max(0, min(V, K - col)) : 0;
+      cp_vec<T>(&st.s[rr][cv], A + row * lda + col, valid, vec, A);
+    }
+  } else {
+    constexpr int VPR = gr::BR / V;
+    constexpr int PER = gr::T * VPR / gr::THREADS;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          v[q] = (col < K && row + q < rend) ? to_f64(__ldg(A + (int64_t)col * lda + row + q)) : 0.0;
-      }
+    for (int p = 0; p < PER; ++p) {
+      const int e = tid + p * gr::THREADS;
+      const int cc = e / VPR, rv = (e % VPR) * V;
+      const int col = c0 + cc;
+      const int64_t row = r0 + rv;
+      const int valid = col < K ? clamp_valid(rend - row, V) : 0;
+      cp_vec<T>(&st.s[cc][rv], A + (int64_t)col * lda + row, valid, vec, A);
     }
   }
-  __device__ __forceinline__ void store(double (*As)[gr::LD], int tid) {
-    if (LAYOUT == LAYOUT_ROW) {
-      const int rr = tid >> 4, cc = (tid & 15) * 4;
-      double2* p = reinterpret_cast<double2*>(&As[rr][cc]);
-      p[0] = make_double2(v[0], v[1]);
-      p[1] = make_double2(v[2], v[3]);
-    } else {
-      const int cc = tid >> 2, rr = (tid & 3) * 4;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) As[rr + q][cc] = v[q];
-    }
-  }
+}
+
+template <typename TA, int LA, typename TB, int LB> struct GramSmem {
+  GStage<TA, LA> a[gr::STAGES];
+  GStage<TB, LB> b[gr::STAGES];
 };
 
 template <typename TA, int LA, typename TB, int LB>
 __global__ void __launch_bounds__(gr::THREADS, 2) tall_gram_kernel(TallGramArgs args) {
-  __shared__ __align__(16) double As[2][gr::BR][gr::LD];
-  __shared__ __align__(16) double Bs[2][gr::BR][gr::LD];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto& sm = *reinterpret_cast<GramSmem<TA, LA, TB, LB>*>(smem_raw);
   const TA* __restrict__ A = static_cast<const TA*>(args.A);
   const TB* __restrict__ B = static_cast<const TB*>(args.B);
 
@@ -382,7 +396,6 @@ __global__ void __launch_bounds__(gr::THREADS, 2) tall_gram_kernel(TallGramArgs 
   const bool vec_a = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((args.lda * (int64_t)sizeof(TA)) % 16 == 0);
   const bool vec_b = ((reinterpret_cast<uintptr_t>(B) & 15) == 0) && ((args.ldb * (int64_t)sizeof(TB)) % 16 == 0);
 
-  // warp-uniform fragment validity: in range, and (symmetric) on/above the diagonal
   bool live[4][2];
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
@@ -398,38 +411,38 @@ __global__ void __launch_bounds__(gr::THREADS, 2) tall_gram_kernel(TallGramArgs 
 #pragma unroll
     for (int f = 0; f < 2; ++f) acc[mi][f][0] = acc[mi][f][1] = 0.0;
 
-  GramLoader<TA, LA> la;
-  GramLoader<TB, LB> lb;
   const int64_t nchunks = rend > rbeg ? (rend - rbeg + gr::BR - 1) / gr::BR : 0;
-  if (nchunks > 0) {
-    la.load(A, args.lda, rend, args.K1, rbeg, c0a, tid, vec_a);
-    lb.load(B, args.ldb, rend, args.K2, rbeg, c0b, tid, vec_b);
-  }
-  int buf = 0;
-  for (int64_t c = 0; c < nchunks; ++c) {
-    la.store(As[buf], tid);
-    lb.store(Bs[buf], tid);
-    __syncthreads();
-    if (c + 1 < nchunks) {
-      const int64_t r0 = rbeg + (c + 1) * gr::BR;
-      la.load(A, args.lda, rend, args.K1, r0, c0a, tid, vec_a);
-      lb.load(B, args.ldb, rend, args.K2, r0, c0b, tid, vec_b);
+  auto issue = [&](int64_t c) {
+    if (c < nchunks) {
+      const int s = (int)(c % gr::STAGES);
+      const int64_t r0 = rbeg + c * gr::BR;
+      gr_load<TA, LA>(sm.a[s], A, args.lda, rend, args.K1, r0, c0a, tid, vec_a);
+      gr_load<TB, LB>(sm.b[s], B, args.ldb, rend, args.K2, r0, c0b, tid, vec_b);
     }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < gr::STAGES - 1; ++s) issue(s);
+  for (int64_t c = 0; c < nchunks; ++c) {
+    cp_async_wait<gr::STAGES - 2>();
+    __syncthreads();
+    issue(c + gr::STAGES - 1);
+    const int s = (int)(c % gr::STAGES);
 #pragma unroll
     for (int ks = 0; ks < gr::BR / 4; ++ks) {
       double a[4], b[2];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = As[buf][ks * 4 + t][wm * 32 + mi * 8 + g];
+      for (int mi = 0; mi < 4; ++mi) a[mi] = sm.a[s].frag(wm * 32 + mi * 8 + g, ks * 4 + t);
 #pragma unroll
-      for (int f = 0; f < 2; ++f) b[f] = Bs[buf][ks * 4 + t][wn * 16 + f * 8 + g];
+      for (int f = 0; f < 2; ++f) b[f] = sm.b[s].frag(wn * 16 + f * 8 + g, ks * 4 + t);
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
         for (int f = 0; f < 2; ++f)
           if (live[mi][f]) dmma884(acc[mi][f], a[mi], b[f]);
     }
-    buf ^= 1;
   }
+  cp_async_wait<0>();
   double* W = args.W + (int64_t)blockIdx.y * args.K1p * args.K2p;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
