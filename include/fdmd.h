@@ -108,6 +108,20 @@ int fdmd_residual(const void* S, int s_dtype, int64_t lds, const void* D, int d_
  * j (real part) and j+1 (imaginary part)). Synchronous. */
 int fdmd_geev(int n, double* A, double* w_host, double* vr_host, void* stream);
 
+/* tcgen05 batched reconstruction (FP32-accurate 2-way FP16 split, see
+ * csrc/fdmd_tc_decode.cuh). Basis planes uh/ul: row-major n x ldu halves
+ * (ldu % 8 == 0) of U * 2^su; coefficient planes ch/cl: frame-major nf x ldk
+ * halves; fscale[f] = 2^-(su + sc_f); out[f*ldo + i] fp32. r <= 256.
+ * fdmd_split_basis builds uh/ul from a column-major fp32 table (r x n, ld ldd);
+ * fdmd_split_coef builds ch/cl/fscale from coefficients (r x nf, row-major).
+ * Replace the per-frame `cols @ coeff` of runtime.py:88 for batches. */
+int fdmd_split_basis(const float* D, int64_t ldd, int64_t n, int r, float scale, void* uh, void* ul, int64_t ldu,
+                     void* stream);
+int fdmd_split_coef(const float* coef, int ldc, int r, int nf, float su_inv, void* ch, void* cl, int ldk,
+                    float* fscale, void* stream);
+int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch, const void* cl,
+                   int ldk, int nf, const float* fscale, float* out, int64_t ldo, void* stream);
+
 /* FP64 tensor-pipe (DMMA.8x8x4) throughput probe on the current device:
  * a register-only mma.sync f64 loop lasting ~`seconds`/4; writes TFLOP/s.
  * The fit's roofline denominator (MEASURED_PEAKS.json has no FP64 figure). */

@@ -48,6 +48,9 @@ SIGNATURES = {
     "fdmd_geev": (_i, [_i, _vp, _vp, _vp, _vp]),
     "fdmd_copy2d": (_i, [_vp, _i64, _vp, _i64, _i64, _i64, _i, _vp]),
     "fdmd_dmma_peak": (_i, [_d, _c.POINTER(_d)]),
+    "fdmd_split_basis": (_i, [_vp, _i64, _i64, _i, _c.c_float, _vp, _vp, _i64, _vp]),
+    "fdmd_split_coef": (_i, [_vp, _i, _i, _i, _c.c_float, _vp, _vp, _i, _vp, _vp]),
+    "fdmd_tc_decode": (_i, [_vp, _vp, _i64, _i64, _i, _vp, _vp, _i, _i, _vp, _vp, _i64, _vp]),
     "fdmd_synth3d": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _d, _u64, _i64, _i64, _vp, _i, _i64, _vp]),
 }
 

@@ -1,4 +1,6 @@
 // extern "C" boundary of libfdmd.so (declared in include/fdmd.h).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cusolverDn.h>
 
 #include <cstdarg>
@@ -70,8 +72,83 @@ int pick_nf(int N) {
 
 int64_t tg_tiles(int64_t n) { return (n + fdmd::tg::BM - 1) / fdmd::tg::BM; }
 
+// ---- TMA / warp-specialised variant (default; FDMD_TG_IMPL=cpasync selects the ring kernel)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+bool tma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FDMD_TG_IMPL");
+    return !(e && strcmp(e, "cpasync") == 0);
+  }();
+  return on;
+}
+
 template <typename TA, int AL, int NF, typename TC, int CL, bool ST>
-int launch_tg(const fdmd::TallGemmArgs& a, cudaStream_t s, int grid_x) {
+int launch_tg_tma(const fdmd::TallGemmArgs& a, cudaStream_t s, int& grid_x, bool& used) {
+  used = false;
+  auto encode = tensor_map_encoder();
+  const size_t elt = sizeof(TA);
+  if (!tma_enabled() || !encode || (reinterpret_cast<uintptr_t>(a.A) & 15) || ((a.lda * elt) % 16) != 0 ||
+      a.n >= (int64_t)INT32_MAX)
+    return FDMD_OK;
+  CUtensorMap map;
+  cuuint64_t dims[2], strides[1];
+  cuuint32_t box[2], estr[2] = {1, 1};
+  if (AL == fdmd::LAYOUT_ROW) {
+    dims[0] = (cuuint64_t)a.K; dims[1] = (cuuint64_t)a.n; box[0] = fdmd::tt::BK; box[1] = fdmd::tt::BM;
+  } else {
+    dims[0] = (cuuint64_t)a.n; dims[1] = (cuuint64_t)a.K; box[0] = fdmd::tt::BM; box[1] = fdmd::tt::BK;
+  }
+  strides[0] = (cuuint64_t)(a.lda * elt);
+  CUresult r = encode(&map, elt == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                      const_cast<void*>(a.A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return FDMD_OK;  // unsupported shape: ring kernel
+  constexpr int BN = 32 * NF;
+  const int gy = (a.N + BN - 1) / BN;
+  const int Kp = (a.K + fdmd::tt::BK - 1) / fdmd::tt::BK * fdmd::tt::BK;
+  const int64_t ldbp = (int64_t)gy * BN;
+  double* Bp = nullptr;
+  CUDA_TRY(cudaMallocAsync(&Bp, sizeof(double) * Kp * ldbp, s));
+  CUDA_TRY(cudaMemsetAsync(Bp, 0, sizeof(double) * Kp * ldbp, s));
+  CUDA_TRY(cudaMemcpy2DAsync(Bp, ldbp * sizeof(double), a.B, a.ldb * sizeof(double), a.N * sizeof(double), a.K,
+                             cudaMemcpyDeviceToDevice, s));
+  fdmd::TTArgs ta{a, Bp, ldbp};
+  auto kern = fdmd::tall_gemm_tma_kernel<TA, AL, NF, TC, CL, ST>;
+  const int smem = (int)sizeof(fdmd::TTSmem<TA, AL, NF>);
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = dev;
+  }
+  const int64_t ntiles = (a.n + fdmd::tt::BM - 1) / fdmd::tt::BM;
+  grid_x = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, sm_count_cached()));
+  dim3 grid(grid_x, gy);
+  kern<<<grid, fdmd::tt::THREADS, smem, s>>>(map, ta);
+  LAUNCH_CHECK("tall_gemm_tma");
+  CUDA_TRY(cudaFreeAsync(Bp, s));
+  used = true;
+  return FDMD_OK;
+}
+
+template <typename TA, int AL, int NF, typename TC, int CL, bool ST>
+int launch_tg(const fdmd::TallGemmArgs& a, cudaStream_t s, int& grid_x) {
+  bool used = false;
+  int rc = launch_tg_tma<TA, AL, NF, TC, CL, ST>(a, s, grid_x, used);
+  if (rc != FDMD_OK || used) return rc;
   auto kern = fdmd::tall_gemm_kernel<TA, AL, NF, TC, CL, ST>;
   const int smem = (int)sizeof(fdmd::TGSmem<TA, AL, NF>);
   static thread_local int configured = -1;
@@ -89,7 +166,7 @@ int launch_tg(const fdmd::TallGemmArgs& a, cudaStream_t s, int grid_x) {
 
 template <typename TA, int AL, int NF>
 int dispatch_tg_c(const fdmd::TallGemmArgs& a, int c_dtype, int c_layout, bool stats, cudaStream_t s,
-                  int grid_x) {
+                  int& grid_x) {
   if (c_layout == FDMD_ROW) {
     if (stats) return fail(FDMD_ERR_INVALID, "pair_stats requires column-major C (or C == NULL)");
     if (c_dtype == FDMD_F64) return launch_tg<TA, AL, NF, double, fdmd::LAYOUT_ROW, false>(a, s, grid_x);
@@ -104,7 +181,7 @@ int dispatch_tg_c(const fdmd::TallGemmArgs& a, int c_dtype, int c_layout, bool s
 
 template <typename TA, int AL>
 int dispatch_tg_nf(const fdmd::TallGemmArgs& a, int c_dtype, int c_layout, bool stats, cudaStream_t s,
-                   int grid_x) {
+                   int& grid_x) {
   switch (pick_nf(a.N)) {
     case 2: return dispatch_tg_c<TA, AL, 2>(a, c_dtype, c_layout, stats, s, grid_x);
     case 4: return dispatch_tg_c<TA, AL, 4>(a, c_dtype, c_layout, stats, s, grid_x);
@@ -125,14 +202,17 @@ struct GramPlan {
   int K1p, K2p;
 };
 
-GramPlan gram_plan(int64_t n, int K1, int K2, int symmetric) {
+// sw = warp-specialised TMA kernel (64 x TN tiles, full tile grid with
+// early exit below the diagonal); otherwise the cp.async ring kernel (64 x 64
+// tiles, triangular enumeration when symmetric).
+GramPlan gram_plan(int64_t n, int K1, int K2, int symmetric, bool sw = false, int TN = 64) {
   GramPlan p;
   p.ti = (K1 + fdmd::gr::T - 1) / fdmd::gr::T;
-  p.tj = (K2 + fdmd::gr::T - 1) / fdmd::gr::T;
-  p.tiles = symmetric ? p.ti * (p.ti + 1) / 2 : p.ti * p.tj;
+  p.tj = (K2 + TN - 1) / TN;
+  p.tiles = (symmetric && TN == fdmd::gr::T) ? p.ti * (p.ti + 1) / 2 : p.ti * p.tj;
   p.K1p = p.ti * fdmd::gr::T;
-  p.K2p = p.tj * fdmd::gr::T;
-  const int64_t target = (int64_t)sm_count_cached() * 4;
+  p.K2p = p.tj * TN;
+  const int64_t target = (int64_t)sm_count_cached() * (sw ? (TN > 64 ? 2 : 4) : 4);
   const int64_t max_splits = std::max<int64_t>(1, (n + 255) / 256);
   int64_t splits = std::max<int64_t>(1, target / p.tiles);
   splits = std::min(splits, max_splits);
@@ -140,6 +220,49 @@ GramPlan gram_plan(int64_t n, int K1, int K2, int symmetric) {
   if (p.rows_per_split == 0) p.rows_per_split = 16;
   p.splits = (int)std::max<int64_t>(1, (n + p.rows_per_split - 1) / p.rows_per_split);
   return p;
+}
+
+bool gram_sw_eligible(const void* A, int a_dtype, int a_layout, int64_t lda, const void* B, int b_dtype,
+                      int b_layout, int64_t ldb, int64_t n) {
+  return a_layout == FDMD_ROW && b_layout == FDMD_ROW && tma_enabled() && tensor_map_encoder() &&
+         !(reinterpret_cast<uintptr_t>(A) & 15) && !(reinterpret_cast<uintptr_t>(B) & 15) &&
+         (lda * (int64_t)dsize(a_dtype)) % 16 == 0 && (ldb * (int64_t)dsize(b_dtype)) % 16 == 0 &&
+         n < (int64_t)INT32_MAX;
+}
+
+template <typename TA, typename TB, int NFB>
+int launch_gram_sw(const fdmd::TallGramArgs& a, int tiles, int splits, cudaStream_t s) {
+  {
+    auto kt = fdmd::tall_gram_sw_kernel<TA, TB, NFB>;
+    const int smt = (int)sizeof(fdmd::TGSSmem<TA, TB, NFB>) + 1024;
+    CUtensorMap maps[2];
+    const void* ptr[2] = {a.A, a.B};
+    const int64_t ld[2] = {a.lda, a.ldb};
+    const int kdim[2] = {a.K1, a.K2};
+    const size_t elt[2] = {sizeof(TA), sizeof(TB)};
+    bool ok = true;
+    for (int i = 0; i < 2 && ok; ++i) {
+      cuuint64_t dims[2] = {(cuuint64_t)kdim[i], (cuuint64_t)a.n};
+      cuuint64_t strides[1] = {(cuuint64_t)(ld[i] * elt[i])};
+      cuuint32_t box[2] = {(cuuint32_t)(128 / elt[i]), (cuuint32_t)fdmd::tgs::BR};
+      cuuint32_t estr[2] = {1, 1};
+      ok = tensor_map_encoder()(&maps[i], elt[i] == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                                2, const_cast<void*>(ptr[i]), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    if (!ok) return fail(FDMD_ERR_CUDA, "tall_gram: tensor map encode failed");
+    static thread_local int conf_t = -1;
+    int dv = 0;
+    cudaGetDevice(&dv);
+    if (conf_t != dv) {
+      CUDA_TRY(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smt));
+      conf_t = dv;
+    }
+    kt<<<dim3(tiles, splits), fdmd::tgs::THREADS, smt, s>>>(maps[0], maps[1], a);
+    LAUNCH_CHECK("tall_gram_sw");
+    return FDMD_OK;
+  }
 }
 
 template <typename TA, int LA, typename TB, int LB>
@@ -224,7 +347,7 @@ int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda, const 
   if (C && c_layout == FDMD_COL && ldc < n) return fail(FDMD_ERR_INVALID, "ldc < n");
   if (n == 0 || N == 0) return FDMD_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const int gx = tg_grid_x(n);
+  int gx = tg_grid_x(n);
   fdmd::TallGemmArgs a{};
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.C = C; a.ldc = ldc;
   a.n = n; a.K = K; a.N = N; a.row_offset = row_offset;
@@ -257,12 +380,14 @@ int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda, const 
 
 size_t fdmd_tall_gram_workspace(int64_t n, int K1, int K2) {
   // large enough for either plan (a symmetric Gram has fewer tiles -> more splits)
-  GramPlan p = gram_plan(n, K1, K2, 0);
-  size_t need = (size_t)p.splits * p.K1p * p.K2p * sizeof(double);
-  if (K1 == K2) {
-    GramPlan q = gram_plan(n, K1, K2, 1);
-    need = std::max(need, (size_t)q.splits * q.K1p * q.K2p * sizeof(double));
-  }
+  size_t need = 0;
+  for (int sym = 0; sym < 2; ++sym)
+    for (int v = 0; v < 3; ++v) {
+      const bool sw = v > 0;
+      const int TN = v == 2 ? 224 : 64;
+      GramPlan q = gram_plan(n, K1, K2, sym, sw, TN);
+      need = std::max(need, (size_t)q.splits * q.K1p * q.K2p * sizeof(double));
+    }
   return need + 256;
 }
 
@@ -278,7 +403,11 @@ int fdmd_tall_gram(const void* A, int a_dtype, int a_layout, int64_t lda, const 
   if ((b_layout == FDMD_ROW && ldb < K2) || (b_layout == FDMD_COL && ldb < n))
     return fail(FDMD_ERR_INVALID, "bad ldb");
   cudaStream_t s = (cudaStream_t)stream;
-  GramPlan p = gram_plan(n, K1, K2, symmetric);
+  const bool sw = gram_sw_eligible(A, a_dtype, a_layout, lda, B, b_dtype, b_layout, ldb, n);
+  // wide tiles for general products; 64x64 for symmetric Grams (a 64 x 224 stripe
+  // of a triangle leaves the lower stripes nearly idle: measured 9.8 vs 16 TF/s)
+  const int nfb = (K2 > 64 && !symmetric) ? 7 : 2;
+  GramPlan p = gram_plan(n, K1, K2, symmetric, sw, sw ? 32 * nfb : fdmd::gr::T);
   const size_t need = (size_t)p.splits * p.K1p * p.K2p * sizeof(double);
   if (!workspace || workspace_bytes < need)
     return fail(FDMD_ERR_WORKSPACE, "tall_gram workspace %zu < %zu", workspace_bytes, need);
@@ -287,7 +416,12 @@ int fdmd_tall_gram(const void* A, int a_dtype, int a_layout, int64_t lda, const 
   a.n = n; a.K1 = K1; a.K2 = K2; a.K1p = p.K1p; a.K2p = p.K2p; a.tiles_j = p.tj;
   a.symmetric = symmetric; a.rows_per_split = p.rows_per_split;
   int rc;
-  if (a_dtype == FDMD_F32)
+  if (sw) {
+#define GSW(TA, TB) (nfb == 7 ? launch_gram_sw<TA, TB, 7>(a, p.tiles, p.splits, s) : launch_gram_sw<TA, TB, 2>(a, p.tiles, p.splits, s))
+    if (a_dtype == FDMD_F32) rc = b_dtype == FDMD_F32 ? GSW(float, float) : GSW(float, double);
+    else rc = b_dtype == FDMD_F32 ? GSW(double, float) : GSW(double, double);
+#undef GSW
+  } else if (a_dtype == FDMD_F32)
     rc = a_layout == FDMD_ROW ? dispatch_gram_b<float, fdmd::LAYOUT_ROW>(a, b_dtype, b_layout, p.tiles, p.splits, s)
                               : dispatch_gram_b<float, fdmd::LAYOUT_COL>(a, b_dtype, b_layout, p.tiles, p.splits, s);
   else
@@ -422,8 +556,8 @@ int fdmd_table_apply_inplace(void* R, int dtype, int64_t ldr, int nraw, const in
   if (n == 0 || ncols == 0) return FDMD_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t elt = dsize(dtype);
-  int rpb = 128;
-  while (rpb > 8 && (size_t)nraw * rpb * elt > 160 * 1024) rpb /= 2;
+  int rpb = 128;  // rows per block: keep ~4 blocks resident per SM
+  while (rpb > 8 && (size_t)nraw * rpb * elt > 56 * 1024) rpb /= 2;
   const size_t smem = (size_t)nraw * rpb * elt;
   if (smem > 200 * 1024) return fail(FDMD_ERR_INVALID, "table_apply_inplace: too many raw columns");
   const int64_t tiles = (n + rpb - 1) / rpb;
@@ -512,6 +646,63 @@ int fdmd_geev(int n, double* A, double* w_host, double* vr_host, void* stream) {
   cudaFreeAsync(info, s);
   cudaFreeAsync(dbuf, s);
   if (info_h != 0) return fail(FDMD_ERR_SOLVER, "Xgeev info %d", info_h);
+  return FDMD_OK;
+}
+
+int fdmd_split_basis(const float* D, int64_t ldd, int64_t n, int r, float scale, void* uh, void* ul, int64_t ldu,
+                     void* stream) {
+  if (!D || !uh || !ul || n <= 0 || r <= 0 || ldu < r || ldd < n) return fail(FDMD_ERR_INVALID, "split_basis: bad arguments");
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((ldu + 31) / 32));
+  fdmd::split_basis_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(D, ldd, n, r, scale, (__half*)uh, (__half*)ul, ldu);
+  LAUNCH_CHECK("split_basis");
+  return FDMD_OK;
+}
+
+int fdmd_split_coef(const float* coef, int ldc, int r, int nf, float su_inv, void* ch, void* cl, int ldk,
+                    float* fscale, void* stream) {
+  if (!coef || !ch || !cl || !fscale || r <= 0 || nf <= 0 || ldk < r || ldc < nf)
+    return fail(FDMD_ERR_INVALID, "split_coef: bad arguments");
+  fdmd::split_coef_kernel<<<nf, 128, 0, (cudaStream_t)stream>>>(coef, ldc, r, nf, su_inv, (__half*)ch, (__half*)cl, ldk, fscale);
+  LAUNCH_CHECK("split_coef");
+  return FDMD_OK;
+}
+
+int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch, const void* cl,
+                   int ldk, int nf, const float* fscale, float* out, int64_t ldo, void* stream) {
+  if (!uh || !ul || !ch || !cl || !fscale || !out || n <= 0 || r <= 0 || nf <= 0 || r > fdmd::tc::BKC * fdmd::tc::MAXKC)
+    return fail(FDMD_ERR_INVALID, "tc_decode: bad arguments (r must be <= %d)", fdmd::tc::BKC * fdmd::tc::MAXKC);
+  if ((ldu * 2) % 16 || (ldk * 2) % 16 || ldu < r || ldk < r || ldo < n || n >= (int64_t)UINT32_MAX)
+    return fail(FDMD_ERR_INVALID, "tc_decode: leading dimensions must be multiples of 8 halves");
+  auto encode = tensor_map_encoder();
+  if (!encode) return fail(FDMD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap maps[4];
+  const void* ptrs[4] = {uh, ul, ch, cl};
+  for (int i = 0; i < 4; ++i) {
+    const bool a = i < 2;
+    cuuint64_t dims[2] = {(cuuint64_t)r, (cuuint64_t)(a ? n : nf)};
+    cuuint64_t strides[1] = {(cuuint64_t)((a ? ldu : ldk) * 2)};
+    cuuint32_t box[2] = {(cuuint32_t)fdmd::tc::BKC, (cuuint32_t)(a ? fdmd::tc::BM : fdmd::tc::BN)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult res = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptrs[i]), dims, strides,
+                          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) return fail(FDMD_ERR_CUDA, "tc_decode: tensor map encode failed (%d)", (int)res);
+  }
+  const int smem = (int)sizeof(fdmd::TCSmem) + 1024;
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    CUDA_TRY(cudaFuncSetAttribute(fdmd::tc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = dev;
+  }
+  fdmd::TCArgs ta{out, ldo, n, r, nf, fscale};
+  const int64_t mtiles = (n + fdmd::tc::BM - 1) / fdmd::tc::BM;
+  const int ny = (nf + fdmd::tc::BN - 1) / fdmd::tc::BN;
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(mtiles, std::max(1, sm_count_cached() / ny)));
+  fdmd::tc_decode_kernel<<<dim3(gx, ny), fdmd::tc::THREADS, smem, (cudaStream_t)stream>>>(maps[0], maps[1], maps[2],
+                                                                                           maps[3], ta);
+  LAUNCH_CHECK("tc_decode");
   return FDMD_OK;
 }
 

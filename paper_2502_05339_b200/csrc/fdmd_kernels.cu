@@ -8,4 +8,7 @@
 #include <cstdio>
 
 #include "fdmd_tall.cuh"
+#include "fdmd_tall_tma.cuh"
+#include "fdmd_gram_tma.cuh"
+#include "fdmd_tc_decode.cuh"
 #include "fdmd_stream.cuh"

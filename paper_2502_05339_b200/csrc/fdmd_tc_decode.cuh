@@ -1,0 +1,270 @@
+// tcgen05 reconstruction: frames[f][i] = sum_k U[i][k] * C[k][f] for batches
+// of frames (BASELINE config 4: u(t) = U Re(W Lam^t b); decode_batch/rollout).
+//
+// Precision: FP32-accurate through a 2-way FP16 split with power-of-two
+// scaling (U*2^su = Uh + Ul, C[:,f]*2^sc_f = Ch + Cl, |lo| <= 2^-11 |hi|):
+//   D = Uh*Ch + Uh*Cl + Ul*Ch   (3 tcgen05.mma kind::f16, FP32 accumulate in TMEM)
+// drops only Ul*Cl (2^-22 relative); SURVEY §7 hard part 5 measured 1xTF32 at
+// 3e-4 (fails the 1e-4 frame bar) and FP32-accurate splits at ~3e-7.
+//
+// Operands (both K-major, 128-byte swizzled, loaded by TMA):
+//   A = Us: row-major n x r fp16 hi/lo planes (the split basis, built once)
+//   B = Cs: frame-major F x r fp16 hi/lo planes (coefficients, per batch)
+// CTA tile: M = 128 rows x N = 128 frames, K = r in 64-wide chunks. B (all K,
+// hi+lo, 128 frames) stays resident in smem; A streams through a 2-stage ring.
+// Warp roles: w0 TMA producer, w1 MMA issuer (one lane), w2..w5 epilogue
+// (TMEM lane quadrant = warp % 4). Two TMEM accumulators (2 x 128 columns) let
+// the epilogue of tile t overlap the MMAs of tile t+1.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include "fdmd_tall_tma.cuh"
+
+namespace fdmd {
+
+namespace tc {
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int BKC = 64;          // K per chunk (128 B of fp16 = one SW128 row)
+constexpr int MAXKC = 4;         // r <= 256
+constexpr int ASTAGES = 2;
+constexpr int THREADS = 192;     // 6 warps
+constexpr int A_CHUNK_BYTES = BM * BKC * 2;   // 16 KB per plane
+constexpr int B_CHUNK_BYTES = BN * BKC * 2;   // 16 KB per plane
+}  // namespace tc
+
+struct TCSmem {
+  // 1024-B aligned SW128 atoms
+  __half A[tc::ASTAGES][2][tc::BM * tc::BKC];        // [stage][hi/lo]
+  __half B[tc::MAXKC][2][tc::BN * tc::BKC];          // [kchunk][hi/lo], resident
+  uint64_t afull[tc::ASTAGES], aempty[tc::ASTAGES];
+  uint64_t bfull;
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(const void* smem) {
+  // K-major, SWIZZLE_128B canonical layout: rows of 128 B, 8-row atoms of 1024 B.
+  // start>>4 [0,14) | LBO>>4 = 1 [16,30) | SBO>>4 = 64 (1024 B) [32,46) | version 1 [46,48) | layout 2 [61,64)
+  const uint64_t start = (uint64_t)((smem_u32(smem) & 0x3FFFF) >> 4);
+  return start | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+
+// 32 lanes x 32 consecutive columns (one fp32 per column per lane)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TCArgs {
+  float* out;          // frames: out[f * ldo + i]
+  int64_t ldo;
+  int64_t n;           // rows
+  int r;               // K (modes)
+  int nf;              // frames in this launch (<= BN * gridDim.y)
+  const float* fscale; // per-frame output scale 2^-(su + sc_f)
+};
+
+// TMA maps: amap_h/amap_l over Us planes (dims {r, n}, box {64, 128}, SW128),
+//           bmap_h/bmap_l over Cs planes (dims {r, nf}, box {64, 128}, SW128).
+__global__ void __launch_bounds__(tc::THREADS, 1)
+tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_constant__ CUtensorMap amap_l,
+                 const __grid_constant__ CUtensorMap bmap_h, const __grid_constant__ CUtensorMap bmap_l,
+                 const TCArgs args) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // align the SW128 atoms to 1024 B
+  TCSmem& sm = *reinterpret_cast<TCSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkc = (args.r + tc::BKC - 1) / tc::BKC;
+  const int ksteps_last = ((args.r - (nkc - 1) * tc::BKC) + 15) / 16;   // valid 16-wide steps in last chunk
+  const int64_t mtiles = (args.n + tc::BM - 1) / tc::BM;
+  const int64_t my_tiles = blockIdx.x < mtiles ? (mtiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int f0 = blockIdx.y * tc::BN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < tc::ASTAGES; ++s) { mbar_init(&sm.afull[s], 1); mbar_init(&sm.aempty[s], 1); }
+    mbar_init(&sm.bfull, 1);
+    for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], 4); }
+    mbar_fence_init();
+  }
+  if (warp == 1) {  // TMEM: 2 accumulators x 128 fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&sm.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // resident B (coefficients): all K chunks, hi + lo
+      mbar_expect_tx(&sm.bfull, (uint32_t)(nkc * 2 * tc::B_CHUNK_BYTES));
+      for (int c = 0; c < nkc; ++c) {
+        tma_load_2d(sm.B[c][0], &bmap_h, c * tc::BKC, f0, &sm.bfull);
+        tma_load_2d(sm.B[c][1], &bmap_l, c * tc::BKC, f0, &sm.bfull);
+      }
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = 0; t < my_tiles; ++t) {
+        const int row0 = (int)((blockIdx.x + t * gridDim.x) * tc::BM);
+        for (int c = 0; c < nkc; ++c) {
+          mbar_wait(&sm.aempty[s], ph ^ 1);
+          mbar_expect_tx(&sm.afull[s], 2 * tc::A_CHUNK_BYTES);
+          tma_load_2d(sm.A[s][0], &amap_h, c * tc::BKC, row0, &sm.afull[s]);
+          tma_load_2d(sm.A[s][1], &amap_l, c * tc::BKC, row0, &sm.afull[s]);
+          if (++s == tc::ASTAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // kind::f16, fp16 x fp16 -> fp32, K-major A and B, M = 128, N = 128
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(tc::BN >> 3) << 17) | ((uint32_t)(tc::BM >> 4) << 24);
+      mbar_wait(&sm.bfull, 0);
+      tc_fence_after();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = 0; t < my_tiles; ++t) {
+        const int acc = (int)(t & 1);
+        const uint32_t acc_ph = (uint32_t)((t >> 1) & 1);
+        mbar_wait(&sm.tempty[acc], acc_ph ^ 1);   // epilogue drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tmem + acc * tc::BN;
+        uint32_t first = 1;
+        for (int c = 0; c < nkc; ++c) {
+          mbar_wait(&sm.afull[s], ph);
+          tc_fence_after();
+          const int ksteps = (c == nkc - 1) ? ksteps_last : tc::BKC / 16;
+          const uint64_t ah = umma_desc_sw128(sm.A[s][0]), al = umma_desc_sw128(sm.A[s][1]);
+          const uint64_t bh = umma_desc_sw128(sm.B[c][0]), bl = umma_desc_sw128(sm.B[c][1]);
+          for (int k = 0; k < ksteps; ++k) {
+            const uint64_t adv = (uint64_t)((k * 32) >> 4);   // +32 B per K=16 inside the 128-B row
+            umma_f16(d, ah + adv, bh + adv, idesc, first ? 0u : 1u);
+            umma_f16(d, ah + adv, bl + adv, idesc, 1u);
+            umma_f16(d, al + adv, bh + adv, idesc, 1u);
+            first = 0;
+          }
+          umma_commit(&sm.aempty[s]);             // frees the A stage once these MMAs retire
+          if (++s == tc::ASTAGES) { s = 0; ph ^= 1; }
+        }
+        umma_commit(&sm.tfull[acc]);              // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quadrant q = warp % 4
+    const int q = warp & 3;
+    for (int64_t t = 0; t < my_tiles; ++t) {
+      const int acc = (int)(t & 1);
+      const uint32_t acc_ph = (uint32_t)((t >> 1) & 1);
+      mbar_wait(&sm.tfull[acc], acc_ph);
+      tc_fence_after();
+      const int64_t row = (blockIdx.x + t * gridDim.x) * tc::BM + q * 32 + lane;
+#pragma unroll 1
+      for (int cb = 0; cb < tc::BN; cb += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * tc::BN + cb), v);
+        if (row < args.n) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int f = f0 + cb + j;
+            if (f < args.nf) __stcs(args.out + (int64_t)f * args.ldo + row, v[j] * __ldg(args.fscale + f));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+  }
+}
+
+// ------------------------------------------------------------ split kernels --
+// Us[i][k] (hi, lo planes, row-major, ld = ldu) from a column-major fp32 table
+// D[k][i] (ld = ldd), scaled by 2^su. Tiled transpose through smem.
+__global__ void split_basis_kernel(const float* __restrict__ D, int64_t ldd, int64_t n, int r, float scale,
+                                   __half* __restrict__ uh, __half* __restrict__ ul, int64_t ldu) {
+  __shared__ float tile[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32;
+  const int k0 = blockIdx.y * 32;
+  for (int kk = threadIdx.y; kk < 32; kk += blockDim.y) {
+    const int k = k0 + kk;
+    const int64_t i = i0 + threadIdx.x;
+    tile[kk][threadIdx.x] = (k < r && i < n) ? D[(int64_t)k * ldd + i] * scale : 0.f;
+  }
+  __syncthreads();
+  for (int ii = threadIdx.y; ii < 32; ii += blockDim.y) {
+    const int64_t i = i0 + ii;
+    const int k = k0 + threadIdx.x;
+    if (i < n && k < ldu) {
+      const float x = tile[threadIdx.x][ii];
+      const __half h = __float2half_rn(x);
+      uh[i * ldu + k] = h;
+      ul[i * ldu + k] = __float2half_rn(x - __half2float(h));
+    }
+  }
+}
+
+// Cs[f][k] (hi, lo) from coefficients coef[k][f] (r x nf, row-major, ld ldc),
+// per-frame power-of-two scale so max |C[:, f]| * 2^sc ~ 2^14; writes
+// fscale[f] = 2^-(su + sc_f).
+__global__ void split_coef_kernel(const float* __restrict__ coef, int ldc, int r, int nf, float su_inv,
+                                  __half* __restrict__ ch, __half* __restrict__ cl, int ldk, float* __restrict__ fscale) {
+  const int f = blockIdx.x;
+  if (f >= nf) return;
+  __shared__ float red[32];
+  float mx = 0.f;
+  for (int k = threadIdx.x; k < r; k += blockDim.x) mx = fmaxf(mx, fabsf(coef[(int64_t)k * ldc + f]));
+  for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float m = threadIdx.x < (blockDim.x + 31) / 32 ? red[threadIdx.x] : 0.f;
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if (threadIdx.x == 0) red[0] = m;
+  }
+  __syncthreads();
+  const float m = red[0];
+  int e = 0;
+  if (m > 0.f) frexpf(m, &e);            // m = x * 2^e, x in [0.5, 1)
+  const float sc = ldexpf(1.f, 14 - e);  // max |c| * sc in [2^13, 2^14)
+  for (int k = threadIdx.x; k < ldk; k += blockDim.x) {
+    const float x = k < r ? coef[(int64_t)k * ldc + f] * sc : 0.f;
+    const __half h = __float2half_rn(x);
+    ch[(int64_t)f * ldk + k] = h;
+    cl[(int64_t)f * ldk + k] = __float2half_rn(x - __half2float(h));
+  }
+  if (threadIdx.x == 0) fscale[f] = su_inv / sc;
+}
+
+}  // namespace fdmd

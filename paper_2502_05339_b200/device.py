@@ -202,6 +202,47 @@ class CudaOps:
         self.launches += (B + 31) // 32 if B > 16 else 1
         return out
 
+    # -- tcgen05 batched reconstruction (FP16 2-way split) -----------------
+    def tc_basis(self, D: Tall, ncols: Optional[int] = None):
+        """Split a column-major fp32 basis into the row-major fp16 hi/lo
+        planes the tcgen05 kernel streams (built once per basis)."""
+        import math
+        assert D.layout == "col" and D.dtype == torch.float32
+        r = D.k if ncols is None else ncols
+        n = D.n
+        ldu = round_up(r, 8)
+        mx = float(D.buf[:r, :n].abs().max().item()) if n else 0.0
+        e = math.frexp(mx)[1] if mx > 0 else 0
+        su = math.ldexp(1.0, 14 - e)
+        uh = torch.empty((n, ldu), dtype=torch.float16, device=D.buf.device)
+        ul = torch.empty_like(uh)
+        _lib.check(_lib.lib().fdmd_split_basis(_ptr(D.buf), D.ld, n, r, ctypes.c_float(su), _ptr(uh), _ptr(ul),
+                                               ldu, _stream()), "split_basis")
+        self.launches += 1
+        return {"uh": uh, "ul": ul, "ldu": ldu, "su": su, "n": n, "r": r}
+
+    def tc_decode(self, tcb: dict, coef: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """frames (B x n fp32) = basis @ coef (r x B) on tcgen05."""
+        r, n = tcb["r"], tcb["n"]
+        coef = coef.to(torch.float32).contiguous()
+        B = int(coef.shape[1])
+        ldk = round_up(r, 8)
+        dev = coef.device
+        ch = torch.empty((B, ldk), dtype=torch.float16, device=dev)
+        cl = torch.empty_like(ch)
+        fs = torch.empty((B,), dtype=torch.float32, device=dev)
+        if out is None:
+            out = torch.empty((B, n), dtype=torch.float32, device=dev)
+        e0 = self._ev()
+        L = _lib.lib()
+        _lib.check(L.fdmd_split_coef(_ptr(coef), coef.stride(0), r, B, ctypes.c_float(1.0 / tcb["su"]), _ptr(ch),
+                                     _ptr(cl), ldk, _ptr(fs), _stream()), "split_coef")
+        _lib.check(L.fdmd_tc_decode(_ptr(tcb["uh"]), _ptr(tcb["ul"]), tcb["ldu"], n, r, _ptr(ch), _ptr(cl), ldk, B,
+                                    _ptr(fs), _ptr(out), out.stride(0), _stream()), "tc_decode")
+        self._done("tc_decode", 2.0 * n * r * B, e0)
+        self.launches += 2
+        return out
+
     # -- y[k][v] = sum_i D[k][i] U[v][i] -----------------------------------
     def colmajor_dot(self, D: Tall, U: torch.Tensor, ncols: Optional[int] = None) -> torch.Tensor:
         """U: (nv, n) tensor (nv <= 8), row v contiguous."""

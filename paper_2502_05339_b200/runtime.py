@@ -288,7 +288,11 @@ class ModalBasis:
     """u(t) = U Re(W Lam^t b) with a real device basis U (n x r, column-major)
     — BASELINE config 4's reconstruction (north_star third part)."""
 
-    def __init__(self, U: Tall, W, lam, b, dt=1.0):
+    # batches at least this large go to the tcgen05 kernel (fp32 bases);
+    # a single frame is a GEMV and stays on the HBM-streaming SIMT kernel
+    TC_MIN_BATCH = 16
+
+    def __init__(self, U: Tall, W, lam, b, dt=1.0, use_tc: Optional[bool] = None):
         assert U.layout == "col"
         self.U = U
         dev = U.buf.device
@@ -296,11 +300,21 @@ class ModalBasis:
         self.lam = np.asarray(lam, dtype=np.complex128)
         self.omega = torch.as_tensor(np.log(self.lam) / dt, device=dev)
         self.b = torch.as_tensor(np.asarray(b, dtype=np.complex128), device=dev)
+        self.use_tc = (U.dtype == torch.float32 and U.buf.is_cuda) if use_tc is None else use_tc
+        self._tc = None
 
     def coefficients(self, times) -> torch.Tensor:
         t = torch.as_tensor(np.asarray(times, dtype=np.float64), device=self.U.buf.device)
         Lt = torch.exp(self.omega[:, None] * t[None, :].to(torch.complex128)) * self.b[:, None]
         return (self.W @ Lt).real.contiguous()      # r x B
 
+    def tc_state(self):
+        if self._tc is None:
+            self._tc = dv.get_ops().tc_basis(self.U)
+        return self._tc
+
     def reconstruct(self, times, out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        return dv.get_ops().decode(self.U, self.coefficients(times), out=out)
+        C = self.coefficients(times)
+        if self.use_tc and C.shape[1] >= self.TC_MIN_BATCH:
+            return dv.get_ops().tc_decode(self.tc_state(), C, out=out)
+        return dv.get_ops().decode(self.U, C, out=out)

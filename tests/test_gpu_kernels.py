@@ -69,6 +69,34 @@ def test_tall_gemm_pair_stats(dv):
     np.testing.assert_array_equal(st, st2)
 
 
+def test_tall_gemm_ring_variant_matches(dv):
+    """The cp.async-ring kernel (FDMD_TG_IMPL=cpasync, used when TMA cannot
+    describe the operand) gives the same results as the default TMA kernel."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, '.')
+from paper_2502_05339_b200 import device as dv
+rng = np.random.default_rng(1)
+for (n, K, N, lay) in [(5000, 201, 200, 'row'), (777, 37, 64, 'col'), (4099, 200, 128, 'row')]:
+    A = rng.standard_normal((n, K)).astype(np.float32).astype(np.float64)
+    T = dv.alloc_tall(n, K, torch.float32, lay, zero=True)
+    (T.buf[:n, :K] if lay == 'row' else T.buf[:K, :n]).copy_(torch.as_tensor(A if lay == 'row' else A.T))
+    B = rng.standard_normal((K, N))
+    C = dv.alloc_tall(n, N, torch.float64, 'row')
+    dv.get_ops().tall_gemm(T, torch.as_tensor(B, device='cuda'), C)
+    err = np.abs(C.view().cpu().numpy() - A @ B).max() / np.abs(A @ B).max()
+    assert err < 1e-12, err
+print('ok')
+"""
+    env = dict(os.environ, FDMD_TG_IMPL="cpasync")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
 @pytest.mark.parametrize("upper", [False, True])
 @pytest.mark.parametrize("l", [200, 37, 160])
 def test_tall_gemm_inplace(dv, upper, l):
@@ -138,6 +166,23 @@ def test_decode(dv, dtype, B, n, r):
     want = (D @ C).T
     tol = 2e-6 if dtype == "f32" else 1e-13
     assert np.linalg.norm(out - want) <= tol * np.linalg.norm(want)
+
+
+@pytest.mark.parametrize("n,r,B", [(100003, 200, 32), (5000, 150, 128), (70000, 200, 300), (257, 7, 16),
+                                   (100000, 256, 129)])
+def test_tc_decode_fp16_split(dv, n, r, B):
+    """tcgen05 2-way FP16 split reconstruction: FP32-accurate (rel-L2 per frame)."""
+    rng = np.random.default_rng(n + r + B)
+    U = np.linalg.qr(rng.standard_normal((n, r)))[0] if n >= r else rng.standard_normal((n, r))
+    U = U.astype(np.float32).astype(np.float64)
+    C = rng.standard_normal((r, B)) * np.exp(rng.uniform(-8, 3, B))[None, :]   # frames of very different scale
+    Ut = _tall_from(dv, U, "col", torch.float32)
+    ops = dv.get_ops()
+    tcb = ops.tc_basis(Ut)
+    out = ops.tc_decode(tcb, torch.as_tensor(C, device="cuda")).double().cpu().numpy()
+    want = (U @ C.astype(np.float32).astype(np.float64)).T
+    err = np.linalg.norm(out - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert err.max() <= 2e-6, err.max()
 
 
 @pytest.mark.parametrize("nv", [1, 3, 8])
