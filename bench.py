@@ -228,8 +228,10 @@ def main():
     F_fit, terms, l = fit_flops(n, m, r, cfg["p"], cfg["q"])
     lm = fd.LMConfig(max_iters=cfg["lm_iters"])
 
+    CHUNK = 128   # frames per tcgen05 launch (one CTA column of the 128-frame tile)
+
     def one_step(record):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         ev[0].record()
         import warnings
         with warnings.catch_warnings(), trace.stage("fit"):
@@ -237,19 +239,25 @@ def main():
             model = fd.optdmd(data, r, lm_config=lm, svd_mode="randomized", seed=cfg["seed"],
                               oversample=cfg["p"], power_iters=cfg["q"], keep_basis=True)
         ev[1].record()
-        mb = ModalBasis(model.basis_U, W4, lam4, b4, dt=1.0)
-        f1 = mb.reconstruct(times[:1])                       # interactive frame (GEMV)
+        U = model.basis_U
+        del model                                            # config 4 reconstructs from U, not the table
+        mb = ModalBasis(U, W4, lam4, b4, dt=1.0)
+        f1 = mb.reconstruct(times[:1])                       # interactive frame (GEMV, fp32 U)
         ev[2].record()
-        out32 = torch.empty((32, n_loc), dtype=torch.float32, device="cuda")
-        mb.reconstruct(times[:32], out=out32)                # one 32-frame batch
+        with trace.stage("reconstruct.basis_split"):
+            mb.tc_state()                                    # once per basis: fp16 hi/lo planes
         ev[3].record()
-        for c0 in range(0, len(times), 32):                  # 1024 frames streamed through one buffer
-            mb.reconstruct(times[c0:c0 + 32], out=out32)
+        outb = torch.empty((CHUNK, n_loc), dtype=torch.float32, device="cuda")
+        mb.reconstruct(times[:32], out=outb[:32])            # one 32-frame batch
         ev[4].record()
+        for c0 in range(0, len(times), CHUNK):               # 1024 frames streamed through one buffer
+            mb.reconstruct(times[c0:c0 + CHUNK], out=outb)
+        ev[5].record()
         torch.cuda.synchronize()
-        t = [ev[0].elapsed_time(ev[i]) / 1e3 for i in range(1, 5)]
-        del model, mb, f1, out32
-        return {"fit": t[0], "rec1": t[1] - t[0], "rec32": t[2] - t[1], "rec1024": t[3] - t[2]}
+        t = [ev[0].elapsed_time(ev[i]) / 1e3 for i in range(1, 6)]
+        del mb, f1, outb, U
+        return {"fit": t[0], "rec1": t[1] - t[0], "split": t[2] - t[1], "rec32": t[3] - t[2],
+                "rec1024": t[4] - t[3]}
 
     for _ in range(args.warmup):
         one_step(False)
@@ -276,11 +284,13 @@ def main():
     stages = trace.summarize(trace.disable(), args.steps)
     total = max_over_ranks(t0e.elapsed_time(t1e) / 1e3)
     fit_t = max_over_ranks(float(np.mean([x["fit"] for x in res])))
-    rec = {k: max_over_ranks(float(np.mean([x[k] for x in res]))) for k in ("rec1", "rec32", "rec1024")}
+    rec = {k: max_over_ranks(float(np.mean([x[k] for x in res]))) for k in ("rec1", "split", "rec32", "rec1024")}
 
     # roofline: FP64 DMMA contraction kernels (tall_gemm + tall_gram), CUDA events
-    kt = {"tall_gemm": [0.0, 0.0, 0], "tall_gram": [0.0, 0.0, 0], "decode": [0.0, 0.0, 0]}
+    kt = {"tall_gemm": [0.0, 0.0, 0], "tall_gram": [0.0, 0.0, 0], "decode": [0.0, 0.0, 0],
+          "tc_decode": [0.0, 0.0, 0]}
     for name, fl, e0, e1 in prof:
+        kt.setdefault(name, [0.0, 0.0, 0])
         kt[name][0] += e0.elapsed_time(e1) / 1e3
         kt[name][1] += fl
         kt[name][2] += 1
@@ -295,11 +305,16 @@ def main():
         return {"frames_per_s": round(B / t, 1), "ms": round(t * 1e3, 3), "hbm_GBps_per_gpu": round(gbs, 1),
                 "frac_hbm": round(gbs / hbm_peak(), 3)}
     recon = {"B=1": rec_obj(1, rec["rec1"]), "B=32": rec_obj(32, rec["rec32"])}
+    recon["B=1"]["kernel"] = "decode (SIMT GEMV over fp32 U)"
+    recon["B=32"]["kernel"] = "tc_decode (tcgen05, FP16 2-way split)"
     b1024 = rec["rec1024"]
-    byt = (4.0 * n * r) * (len(times) / 32) + 4.0 * n * len(times)
+    # algorithmic bytes: U read once per 128-frame launch + frames written
+    byt = (4.0 * n * r) * (len(times) / CHUNK) + 4.0 * n * len(times)
     recon["B=1024"] = {"frames_per_s": round(len(times) / b1024, 1), "ms": round(b1024 * 1e3, 2),
                        "hbm_GBps_per_gpu": round(byt / b1024 / 1e9 / world, 1),
-                       "note": "32-frame passes over U; compute-bound in fp32 FFMA (DESIGN.md)"}
+                       "frac_hbm": round(byt / b1024 / 1e9 / world / hbm_peak(), 3),
+                       "kernel": f"tc_decode, {CHUNK}-frame launches streamed through one buffer"}
+    recon["basis_split_ms"] = round(rec["split"] * 1e3, 2)
 
     # ---- e2e through the public API from pinned host memory ----
     e2e = None
@@ -318,6 +333,7 @@ def main():
                    "n": n, "m": m, "r": r, "l": l, "p": cfg["p"], "q": cfg["q"], "grid": f"{cfg['grid']}^3x3",
                    "snapshot_dtype": "f32", "parallelism": f"rows{world}", "l2": "inputs larger than L2 (X >= 3.8 GB)"},
         "fit": {"s": round(fit_t, 4), "gflops": round(value, 1), "flops": F_fit,
+                "per_step_s": [round(x["fit"], 4) for x in res],
                 "terms": {k: v for k, v in terms.items()}},
         "reconstruct": recon,
         "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",

@@ -257,6 +257,8 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
     with stage("modes.raw+stats"):
         st = ops.tall_gemm(A, Bm, raw, stats=True, row_offset=row0,
                            alg_flops=4.0 * n_loc * K * plan.lam.size)  # (U, 3)
+    post = stage("modes.post")
+    post.__enter__()
     st = la._reduce_pair_stats(st, shard)
     nrm = torch.sqrt(st[:, 0])
     idx = st[:, 2].round().long()
@@ -341,6 +343,7 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
         cols[k] = im_of(u, cj, 1.0)
     for c in cols:
         t_src.append(c[0]); t_al.append(c[1]); t_be.append(c[2])
+    post.__exit__(None, None, None)
     general = None
     if not exact:
         # only hand-built / degenerate spectra: keep an explicit [Re phi_a, Im phi_a] basis
@@ -410,9 +413,10 @@ def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, po
             raise ValueError(f"rank {r} out of range [1, {min(n_tot, T)}]")
         omega = la.draw_omega(T, l, seed)
         f = la.sketch_factors(S, T, l, q, omega, data.shard)
-        Umap = f.Ub[:, :r].contiguous()
-        UtS = Umap.t() @ f.QtS
-        basis = _Basis(f.Q, Umap, f.s[:r].contiguous(), f.Vh[:r].t().contiguous(), UtS, f.stats)
+        Ub_r = f.Ub[:, :r].contiguous()
+        UtS = Ub_r.t() @ f.QtS
+        basis = _Basis(f.Q, f.right(Ub_r).contiguous(), f.s[:r].contiguous(), f.Vh[:r].t().contiguous(),
+                       UtS, f.stats)
         basis.stats.update(l=l, p=p, q=q)
     elif svd_mode == "full":
         X = Tall(S.buf, "row", S.n, T)                       # X = states[:, :-1] (dmd.py:248)
@@ -769,8 +773,12 @@ def dmdc_fit(data, controls, r_aug, r, seed=None, *, oversample=10, power_iters=
     # U1^T Uhat = Ub1^T (Q1[:n]^T Q2) Ub2
     Q1top = Tall(f1.Q.buf, "row", n, f1.Q.k)
     M12 = dv.get_ops().tall_gram(Q1top, f2.Q)                          # l1 x l2
+    if f1.fix is not None:
+        M12 = f1.fix.t() @ M12
+    if f2.fix is not None:
+        M12 = M12 @ f2.fix
     U1tUh = Ub1.t() @ M12 @ Ub2                                        # r_aug x r
-    U2 = f1.Q.buf[n:n + ell, : f1.Q.k].to(torch.float64) @ Ub1        # ell x r_aug
+    U2 = f1.Q.buf[n:n + ell, : f1.Q.k].to(torch.float64) @ f1.right(Ub1)   # ell x r_aug
     UhtXp = Ub2.t() @ f2.QtS[:, 1:]                                    # r x T
     core = UhtXp @ (V1 / s1[None, :])                                  # r x r_aug
     Atil = core @ U1tUh                                                # r x r
@@ -791,7 +799,7 @@ def dmdc_fit(data, controls, r_aug, r, seed=None, *, oversample=10, power_iters=
     # reduced_b = pinv(phi) U_hat B~ / dt, U_hat = Q2 Ub2
     D, E = modes.basis()
     DtQ2 = dv.get_ops().tall_gram(D, f2.Q, K1=E.shape[0])              # ncol x l2
-    y = (DtQ2 @ Ub2 @ Btil).cpu().numpy()                              # ncol x ell
+    y = (DtQ2 @ f2.right(Ub2) @ Btil).cpu().numpy()                    # ncol x ell
     red = modes.pinv_small() @ (E.conj().T @ y) / data.dt
     ctrl = ControlOperator([red], ["augmented"])
     model.provenance["A_tilde"] = Atil.cpu().numpy()

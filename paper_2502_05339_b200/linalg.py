@@ -147,6 +147,19 @@ def _apply_rinv(Y: Tall, R: torch.Tensor, shard: Optional[Shard]):
 
 def cholqr2_inplace(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict] = None) -> torch.Tensor:
     """Orthonormalise the columns of Y in place. Returns R (Y_in = Q R)."""
+    R, fix = cholqr2_deferred(Y, shard, stats)
+    if fix is not None:
+        l = fix.shape[0]
+        dv.get_ops().tall_gemm(Y, fix, Y, alg_flops=float(Y.n) * l * l, upper=True)
+    return R
+
+
+def cholqr2_deferred(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict] = None):
+    """CholeskyQR2 without the final tall triangular apply: Y is left holding
+    Q1 and the orthonormal factor is Q = Y @ fix (fix = R2^-1, upper
+    triangular, ~I). Every consumer of Q in the fit is linear, so `fix` is
+    folded into small matrices instead of a second n*l^2 pass. Returns
+    (R, fix) with Y_in = Q R; fix is None when Y already holds Q."""
     ops = dv.get_ops()
     l = Y.k
     with stage("cholqr.gram"):
@@ -154,7 +167,7 @@ def cholqr2_inplace(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict
     with stage("cholqr.chol+cond"):
         R1 = _chol_upper(G)
         if R1 is None:
-            return _householder_inplace(Y, shard, stats)
+            return _householder_inplace(Y, shard, stats), None
         cond = float(torch.linalg.cond(R1).item())
     if stats is not None:
         stats.setdefault("cond_R1", []).append(cond)
@@ -167,24 +180,25 @@ def cholqr2_inplace(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict
         s = 11.0 * (n_tot * l + l * (l + 1)) * u * nrm2
         R0 = _chol_upper(G + s * torch.eye(l, dtype=G.dtype, device=G.device))
         if R0 is None:
-            return _householder_inplace(Y, shard, stats)
+            return _householder_inplace(Y, shard, stats), None
         _apply_rinv(Y, R0, shard)
         G = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
         R1b = _chol_upper(G)
         if R1b is None:
-            return _householder_inplace(Y, shard, stats)
+            return _householder_inplace(Y, shard, stats), None
         _apply_rinv(Y, R1b, shard)
         R1 = R1b @ R0
         if stats is not None:
             stats["shifted_cholqr3"] = stats.get("shifted_cholqr3", 0) + 1
     else:
         _apply_rinv(Y, R1, shard)
-    G2 = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
+    with stage("cholqr.gram2"):
+        G2 = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
     R2 = _chol_upper(G2)
     if R2 is None:
         raise ConvergenceError("CholeskyQR2: second Gram not positive definite")
-    _apply_rinv(Y, R2, shard)
-    return R2 @ R1
+    eye = torch.eye(l, dtype=torch.float64, device=R2.device)
+    return R2 @ R1, torch.linalg.solve_triangular(R2, eye, upper=True)
 
 
 def _householder_inplace(Y: Tall, shard: Optional[Shard], stats: Optional[dict]) -> torch.Tensor:
@@ -209,12 +223,17 @@ def draw_omega(cols: int, l: int, seed) -> np.ndarray:
 
 @dataclass
 class SketchFactors:
-    Q: Tall            # n x l, fp64, orthonormal columns
+    Q: Tall            # n x l fp64 buffer; the orthonormal basis is Q @ fix
     Ub: torch.Tensor   # l x l
     s: torch.Tensor    # l
     Vh: torch.Tensor   # l x T
-    QtS: torch.Tensor  # l x m (Q^T S: both Q^T X and Q^T X')
+    QtS: torch.Tensor  # l x m (Q^T S: both Q^T X and Q^T X'), fix already applied
     stats: dict
+    fix: Optional[torch.Tensor] = None   # l x l upper triangular (None = identity)
+
+    def right(self, M: torch.Tensor) -> torch.Tensor:
+        """Small matrix to multiply the stored buffer by to get (Q @ M)."""
+        return M if self.fix is None else self.fix @ M
 
 
 def _pad_rows(Bsmall: torch.Tensor, rows: int) -> torch.Tensor:
@@ -244,23 +263,30 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     nl = float(S.n)
     with stage("sketch.Y=XOmega"):
         ops.tall_gemm(S, _pad_rows(Om, m), Q, alg_flops=2 * nl * T * l)
+    # CholeskyQR2's final R2^-1 is kept as the small `fix` (Q = buffer @ fix)
+    # and folded into Z, Q^T S and the lift; its tall apply is never executed
+    # (counted as the TRSM term it replaces).
     with stage("sketch.cholqr2"):
-        cholqr2_inplace(Q, shard, stats)
+        _, fix = cholqr2_deferred(Q, shard, stats)
     for _ in range(q):
         with stage("power.Z=XtQ"):
             Z = allreduce(shard, ops.tall_gram(S, Q, alg_flops=2 * nl * T * l))   # m x l
+            if fix is not None:
+                Z = Z @ fix
         with stage("power.qr(Z)"):
             W, _ = torch.linalg.qr(Z[:T], mode="reduced")    # T x l (Householder, device)
         with stage("power.Y=XW"):
             ops.tall_gemm(S, _pad_rows(W, m), Q, alg_flops=2 * nl * T * l)
         with stage("power.cholqr2"):
-            cholqr2_inplace(Q, shard, stats)
+            _, fix = cholqr2_deferred(Q, shard, stats)
     with stage("project.QtS"):
         QtS = allreduce(shard, ops.tall_gram(Q, S, alg_flops=2 * nl * m * l))     # l x m
+        if fix is not None:
+            QtS = fix.t() @ QtS
     with stage("small.svd(B)"):
         B = QtS[:, :T]
         Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvd" if B.is_cuda else None)
-    return SketchFactors(Q, Ub, s, Vh, QtS, stats)
+    return SketchFactors(Q, Ub, s, Vh, QtS, stats, fix)
 
 
 def _canonical_signs(Q: Tall, Ub_r: torch.Tensor, shard: Optional[Shard]) -> torch.Tensor:
@@ -326,11 +352,11 @@ def randomized_svd(M, r, oversample=10, power_iters=2, seed=None, *, omega=None,
     G = draw_omega(cols, l, seed) if omega is None else np.asarray(omega, dtype=np.float64)
     f = sketch_factors(A, cols, l, power_iters, G, shard)
     Ub_r = f.Ub[:, :r].contiguous()
-    sgn = _canonical_signs(f.Q, Ub_r, shard)
+    sgn = _canonical_signs(f.Q, f.right(Ub_r), shard)
     Ub_r = Ub_r * sgn[None, :]
     V = (f.Vh[:r].t() * sgn[None, :]).contiguous()
     U = alloc_tall(A.n, r, torch.float64, "col", device=A.buf.device)
-    dv.get_ops().tall_gemm(f.Q, Ub_r, U)                     # lift U = Q Ub_r (linalg.py:88)
+    dv.get_ops().tall_gemm(f.Q, f.right(Ub_r), U)            # lift U = Q Ub_r (linalg.py:88)
     res = SvdResult(None, f.s[:r].cpu().numpy().copy(), V.cpu().numpy(), U_device=U, shard=shard)
     if not keep_device:
         _ = res.U
