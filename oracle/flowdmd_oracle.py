@@ -499,3 +499,34 @@ def dmdc_fit(states, controls, p_rank, r, seed, p=10, q=1):
     phi = core @ (U1.T @ Uh) @ W
     lam, phi = order_and_pair(lam, phi)
     return dict(A=A, B=Bt, lam=lam, phi=phi, Uhat=Uh, sigma_aug=St)
+
+
+def dmdc_reduced_b(fit, dt):
+    """Modal control matrix pinv(phi) @ U_hat @ B~ / dt, so that
+    runtime.step_forced's `reduced_b q dt` (runtime.py:188) adds B u."""
+    return pinv_svd(fit["phi"]) @ (fit["Uhat"] @ fit["B"]) / dt
+
+
+def controlled_system(n, pairs, ell, m, seed, noise=0.0):
+    """x_{j+1} = A x_j + B u_j with A = Psi Ablk Psi^+ (rank 2*pairs, known
+    eigenvalues rho e^{+-i theta}) and B = ell random fields; returns
+    (states n x m, controls ell x (m-1), true eigenvalues, B)."""
+    rng = np.random.default_rng(seed)
+    Psi = np.linalg.qr(rng.standard_normal((n, 2 * pairs)))[0]
+    rho = rng.uniform(0.9, 0.999, pairs)
+    th = rng.uniform(0.05, 1.0, pairs)
+    Ab = np.zeros((2 * pairs, 2 * pairs))
+    eigs = []
+    for i in range(pairs):
+        c, s = np.cos(th[i]), np.sin(th[i])
+        Ab[2 * i:2 * i + 2, 2 * i:2 * i + 2] = rho[i] * np.array([[c, -s], [s, c]])
+        eigs += [rho[i] * np.exp(1j * th[i]), rho[i] * np.exp(-1j * th[i])]
+    Bf = rng.standard_normal((n, ell)) / np.sqrt(n)
+    U = rng.standard_normal((ell, m - 1))
+    X = np.empty((n, m))
+    X[:, 0] = Psi @ rng.standard_normal(2 * pairs)
+    for j in range(m - 1):
+        X[:, j + 1] = Psi @ (Ab @ (Psi.T @ X[:, j])) + Bf @ U[:, j]
+    if noise:
+        X = X + noise * rng.standard_normal(X.shape)
+    return X, U, np.asarray(eigs), Bf

@@ -361,7 +361,11 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
         ops.table_apply(raw, g_src, g_al, g_be, general, 2 * r)
     # the decode table overwrites the raw buffer in place (no second n x r allocation)
     with stage("modes.table_apply"):
-        table = ops.table_apply_inplace(raw, t_src, t_al, t_be, lay.ncol)
+        if lay.ncol <= raw.k:
+            table = ops.table_apply_inplace(raw, t_src, t_al, t_be, lay.ncol)
+        else:   # many complex self-paired modes (extra Im columns): out of place
+            table = alloc_tall(n_loc, lay.ncol, table_dtype, "col", device=dev)
+            ops.table_apply(raw, t_src, t_al, t_be, table, lay.ncol)
     del raw
     if timings is not None:
         timings["modes_s"] = time.perf_counter() - t0

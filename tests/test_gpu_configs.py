@@ -1,0 +1,111 @@
+"""BASELINE configs on the GPU beyond the reduced-grid goldens:
+* config 1 at FULL size (n = 6,291,456, device generator) through
+  size-independent properties (the oracle cannot run there: ~105 GB RAM);
+* config 2 (augmented DMDc) against the oracle restatement — parity
+  UNPINNED (no reference implementation) — and against the
+  known controlled system it was generated from."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import match_eigs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fd():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2502_05339_b200 as fd
+    return fd
+
+
+def _device_config(cfg, seed, grid=None):
+    from paper_2502_05339_b200 import device as dv
+    from paper_2502_05339_b200 import synth
+    p = synth.config_params(cfg, seed=seed, grid=grid)
+    S = dv.alloc_tall(p.n, p.m, torch.float32, "row", zero=True)
+    tabs = [torch.as_tensor(np.ascontiguousarray(t), device="cuda") for t in p.sep_tables()]
+    dv.get_ops().synth3d(tabs, p.m, p.noise, synth.noise_key(p.seed), 0, p.n, S)
+    return p, S
+
+
+def test_config1_full_size_properties(fd):
+    from paper_2502_05339_b200 import synth
+    p, S = _device_config(1, seed=1)
+    assert p.n == 6291456
+    data = fd.SnapshotMatrix(S, synth.DT)
+    model = fd.exact_dmd(data, 150, svd_mode="randomized", seed=1, oversample=10, power_iters=1)
+    again = fd.exact_dmd(data, 150, svd_mode="randomized", seed=1, oversample=10, power_iters=1, residual=False)
+    assert np.array_equal(model.lam, again.lam)                      # bitwise per seed (test_dmd.py:105)
+    lam = model.lam
+    # conjugate closure and exact conjugate partners (dmd.py:199-206)
+    assert max(np.abs(lam - np.conj(v)).min() for v in lam) <= 1e-12
+    # 75 random frequencies in a 20 s window are not all resolvable (SURVEY
+    # App. A: ~27 singular values above the noise floor), so individual
+    # generator eigenvalues are not a parity target here; the spectrum must
+    # stay physical (the generator decays: |lambda| <= 1) up to noise modes.
+    assert np.abs(lam).max() < 1.05
+    assert np.sort(model.sigma)[::-1][0] > 1e3 * model.sigma[-1]
+    # unit-norm modes (on the device table: ||phi_a||^2 from the Gram)
+    D, E = model.modes.basis()
+    from paper_2502_05339_b200 import device as dv
+    Gm = dv.get_ops().tall_gram(D, D, symmetric=True).cpu().numpy()
+    norms = np.real(np.einsum("ka,kl,la->a", E.conj(), Gm, E))
+    np.testing.assert_allclose(norms, 1.0, atol=1e-5)
+    # the one-step residual sits at the noise floor (noise 1e-3 per entry)
+    assert model.provenance["residual_rel"] < 5e-3
+    # encode/decode round trip of snapshot 0 reproduces it to the noise level
+    x0 = S.buf[:, 0].double()
+    z0 = fd.encode(model, S.buf[:, 0].contiguous())
+    rec = fd.decode(model, z0, to_host=False).double()
+    rel = float(torch.linalg.vector_norm(rec - x0) / torch.linalg.vector_norm(x0))
+    assert rel < 5e-3, rel
+
+
+def test_config3_reduced_grid_device_generator_matches_host(fd):
+    from paper_2502_05339_b200 import synth
+    p, S = _device_config(3, seed=3, grid=16)
+    Xh = synth.generate_host(p).astype(np.float64)
+    Xd = S.view().double().cpu().numpy()
+    assert np.abs(Xd - Xh).max() <= 1e-6 * np.abs(Xh).max()   # fp32 storage of the same fp64 values
+
+
+@pytest.mark.parametrize("noise", [0.0, 1e-4])
+def test_dmdc_against_oracle_and_truth(fd, noise):
+    import flowdmd_oracle as orc
+    n, pairs, ell, m = 6000, 5, 3, 61
+    X, U, true_eigs, Bf = orc.controlled_system(n, pairs, ell, m, seed=7, noise=noise)
+    # [X; Upsilon] spans span(Psi, B) (+) R^ell; X' spans span(Psi, B)
+    r_aug, r = 2 * pairs + 2 * ell, 2 * pairs + ell
+    ref = orc.dmdc_fit(X, U, r_aug, r, seed=5, p=10, q=1)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        model, ctrl = fd.dmdc_fit(fd.SnapshotMatrix(X, 1.0), U, r_aug, r, seed=5, oversample=10, power_iters=1)
+    # parity with the (unpinned) restatement
+    assert match_eigs(model.lam, ref["lam"]) <= 1e-8
+    # modes of the dynamic eigenvalues agree up to phase (the ell eigenvalues at
+    # ~0 form a degenerate cluster whose eigenvectors are not unique)
+    from conftest import phase_aligned_error
+    dyn = np.abs(ref["lam"]) > 0.5
+    order = [int(np.argmin(np.abs(model.lam - v))) for v in ref["lam"][dyn]]
+    assert phase_aligned_error(model.phi[:, order], ref["phi"][:, dyn]) <= 1e-6
+    assert ctrl.reduced_b[0].shape == (r, ell) and np.isfinite(ctrl.reduced_b[0]).all()
+    # physics: the generator's eigenvalues and B are recovered
+    if noise == 0.0:
+        # every generator eigenvalue is identified (the B-directions add eigenvalues ~0)
+        d = np.array([np.abs(model.lam - t).min() for t in true_eigs])
+        assert d.max() <= 1e-7, d.max()
+        # the reduced pair (A~, B~) reproduces the data in the output basis:
+        # x~_{j+1} = A~ x~_j + B~ u_j with x~ = U_hat^T x (U_hat from the oracle,
+        # whose column signs may differ from the GPU's -> compare via the
+        # similarity-invariant spectrum of A~ and the response norms of B~)
+        At = model.provenance["A_tilde"]
+        np.testing.assert_allclose(np.sort(np.abs(np.linalg.eigvals(At))), np.sort(np.abs(ref["lam"])),
+                                   atol=1e-8)
+        np.testing.assert_allclose(np.linalg.norm(model.provenance["B_tilde"], axis=0),
+                                   np.linalg.norm(ref["B"], axis=0), rtol=1e-8)
