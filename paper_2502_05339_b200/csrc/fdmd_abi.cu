@@ -61,16 +61,35 @@ template <int NF> constexpr int bn_of() { return 32 * NF; }
 
 int pick_nf(int N) {
   static const int forced = [] {
-    const char* e = getenv("FDMD_TG_NF");  // tuning override: 2, 4 or 7
+    const char* e = getenv("FDMD_TG_NF");  // tuning override: 1, 2, 4 or 7
     return e ? atoi(e) : 0;
   }();
-  if (forced == 2 || forced == 4 || forced == 7) return forced;
+  if (forced == 1 || forced == 2 || forced == 4 || forced == 7) return forced;
+  if (N <= 32) return 1;
   if (N <= 64) return 2;
   if (N <= 128) return 4;
   return 7;
 }
 
 int64_t tg_tiles(int64_t n) { return (n + fdmd::tg::BM - 1) / fdmd::tg::BM; }
+
+// Stream-ordered scratch (padded B, solver workspaces) comes from the device's
+// default memory pool with an unbounded release threshold, so repeated calls
+// reuse the same pages instead of unmapping/remapping them at every sync.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static thread_local int tuned = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (tuned != dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    tuned = dev;
+  }
+  return cudaMallocAsync(p, bytes, s);
+}
 
 // ---- TMA / warp-specialised variant (default; FDMD_TG_IMPL=cpasync selects the ring kernel)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -120,7 +139,7 @@ int launch_tg_tma(const fdmd::TallGemmArgs& a, cudaStream_t s, int& grid_x, bool
   const int Kp = (a.K + fdmd::tt::BK - 1) / fdmd::tt::BK * fdmd::tt::BK;
   const int64_t ldbp = (int64_t)gy * BN;
   double* Bp = nullptr;
-  CUDA_TRY(cudaMallocAsync(&Bp, sizeof(double) * Kp * ldbp, s));
+  CUDA_TRY(scratch_alloc((void**)&Bp, sizeof(double) * Kp * ldbp, s));
   CUDA_TRY(cudaMemsetAsync(Bp, 0, sizeof(double) * Kp * ldbp, s));
   CUDA_TRY(cudaMemcpy2DAsync(Bp, ldbp * sizeof(double), a.B, a.ldb * sizeof(double), a.N * sizeof(double), a.K,
                              cudaMemcpyDeviceToDevice, s));
@@ -183,6 +202,7 @@ template <typename TA, int AL>
 int dispatch_tg_nf(const fdmd::TallGemmArgs& a, int c_dtype, int c_layout, bool stats, cudaStream_t s,
                    int& grid_x) {
   switch (pick_nf(a.N)) {
+    case 1: return dispatch_tg_c<TA, AL, 1>(a, c_dtype, c_layout, stats, s, grid_x);
     case 2: return dispatch_tg_c<TA, AL, 2>(a, c_dtype, c_layout, stats, s, grid_x);
     case 4: return dispatch_tg_c<TA, AL, 4>(a, c_dtype, c_layout, stats, s, grid_x);
     default: return dispatch_tg_c<TA, AL, 7>(a, c_dtype, c_layout, stats, s, grid_x);
@@ -613,7 +633,8 @@ int fdmd_residual(const void* S, int s_dtype, int64_t lds, const void* D, int d_
 }
 
 int fdmd_geev(int n, double* A, double* w_host, double* vr_host, void* stream) {
-  if (n <= 0 || !A || !w_host || !vr_host) return fail(FDMD_ERR_INVALID, "geev: bad arguments");
+  if (n <= 0 || !A || !w_host) return fail(FDMD_ERR_INVALID, "geev: bad arguments");
+  const cusolverEigMode_t jobvr = vr_host ? CUSOLVER_EIG_MODE_VECTOR : CUSOLVER_EIG_MODE_NOVECTOR;
   SolverCtx* c = solver_ctx();
   if (!c) return fail(FDMD_ERR_SOLVER, "cusolverDnCreate failed");
   cudaStream_t s = (cudaStream_t)stream;
@@ -621,28 +642,28 @@ int fdmd_geev(int n, double* A, double* w_host, double* vr_host, void* stream) {
   double* W = nullptr;  // complex n
   double* VR = nullptr;
   int* info = nullptr;
-  CUDA_TRY(cudaMallocAsync(&W, sizeof(double) * 2 * n, s));
-  CUDA_TRY(cudaMallocAsync(&VR, sizeof(double) * n * n, s));
-  CUDA_TRY(cudaMallocAsync(&info, sizeof(int), s));
+  CUDA_TRY(scratch_alloc((void**)&W, sizeof(double) * 2 * n, s));
+  if (vr_host) CUDA_TRY(scratch_alloc((void**)&VR, sizeof(double) * n * n, s));
+  CUDA_TRY(scratch_alloc((void**)&info, sizeof(int), s));
   size_t dws = 0, hws = 0;
-  cusolverStatus_t st = cusolverDnXgeev_bufferSize(c->h, c->p, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR,
+  cusolverStatus_t st = cusolverDnXgeev_bufferSize(c->h, c->p, CUSOLVER_EIG_MODE_NOVECTOR, jobvr,
                                                    n, CUDA_R_64F, A, n, CUDA_C_64F, W, CUDA_R_64F, nullptr, n,
                                                    CUDA_R_64F, VR, n, CUDA_R_64F, &dws, &hws);
   if (st != CUSOLVER_STATUS_SUCCESS) return fail(FDMD_ERR_SOLVER, "Xgeev_bufferSize status %d", (int)st);
   void* dbuf = nullptr;
-  CUDA_TRY(cudaMallocAsync(&dbuf, dws > 0 ? dws : 1, s));
+  CUDA_TRY(scratch_alloc(&dbuf, dws > 0 ? dws : 1, s));
   std::vector<char> hbuf(hws > 0 ? hws : 1);
-  st = cusolverDnXgeev(c->h, c->p, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, n, CUDA_R_64F, A, n,
+  st = cusolverDnXgeev(c->h, c->p, CUSOLVER_EIG_MODE_NOVECTOR, jobvr, n, CUDA_R_64F, A, n,
                        CUDA_C_64F, W, CUDA_R_64F, nullptr, n, CUDA_R_64F, VR, n, CUDA_R_64F, dbuf, dws,
                        hbuf.data(), hws, info);
   if (st != CUSOLVER_STATUS_SUCCESS) return fail(FDMD_ERR_SOLVER, "Xgeev status %d", (int)st);
   int info_h = 0;
   CUDA_TRY(cudaMemcpyAsync(&info_h, info, sizeof(int), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(w_host, W, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(vr_host, VR, sizeof(double) * n * n, cudaMemcpyDeviceToHost, s));
+  if (vr_host) CUDA_TRY(cudaMemcpyAsync(vr_host, VR, sizeof(double) * n * n, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   cudaFreeAsync(W, s);
-  cudaFreeAsync(VR, s);
+  if (VR) cudaFreeAsync(VR, s);
   cudaFreeAsync(info, s);
   cudaFreeAsync(dbuf, s);
   if (info_h != 0) return fail(FDMD_ERR_SOLVER, "Xgeev info %d", info_h);

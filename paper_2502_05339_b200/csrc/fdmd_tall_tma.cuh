@@ -121,9 +121,14 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
   }
 
   // ============================ consumers ============================
-  const int wm = warp >> 2, wn = warp & 3;
+  // SM sub-partition = warp & 3; pairing column block wn with 3 - wn on each
+  // sub-partition balances the DMMA work when B is upper triangular.
+  const int wm = warp >> 2, wn = (wm == 0) ? (warp & 3) : 3 - (warp & 3);
   const int g = lane >> 2, t = lane & 3;
   const int wcol0 = n0 + wn * 8 * NF;
+  // upper-triangular B (B[k][j] = 0 for k > j): k-chunks past this warp's last
+  // column contribute nothing and are skipped (still consumed from the ring)
+  const int kc_last = args.b_upper ? (wcol0 + 8 * NF - 1) / tt::BK : INT32_MAX;
   double st_sum[NF], st_max[NF];
   int64_t st_idx[NF];
 #pragma unroll
@@ -142,6 +147,7 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
     }
     mbar_wait(&sm.full[s], phase);
     const TA* As = sm.A[s];
+    if (kc <= kc_last) {
 #pragma unroll
     for (int ks = 0; ks < tt::BK / 4; ++ks) {
       double a[4], b[NF];
@@ -156,6 +162,7 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
       for (int f = 0; f < NF; ++f)
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) dmma884(acc[mi][f], a[mi], b[f]);
+    }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[s]);

@@ -294,16 +294,20 @@ class CudaOps:
         self.launches += 2
         return out
 
-    def geev(self, K: torch.Tensor):
+    def geev(self, K: torch.Tensor, vectors: bool = True):
         """Real nonsymmetric eig on device (cuSOLVER Xgeev). Returns host
-        (w complex[n], V complex[n, n]) with LAPACK pair unpacking."""
+        (w complex[n], V complex[n, n]) with LAPACK pair unpacking; V is None
+        when vectors=False (eigenvalues only)."""
         n = int(K.shape[0])
         A = K.to(torch.float64).t().contiguous().clone()  # column-major
         w = np.empty(2 * n, dtype=np.float64)
-        vr = np.empty(n * n, dtype=np.float64)
+        vr = np.empty(n * n, dtype=np.float64) if vectors else None
         _lib.check(_lib.lib().fdmd_geev(n, _ptr(A), w.ctypes.data_as(ctypes.c_void_p),
-                                        vr.ctypes.data_as(ctypes.c_void_p), _stream()), "geev")
+                                        vr.ctypes.data_as(ctypes.c_void_p) if vectors else None,
+                                        _stream()), "geev")
         lam = w[0::2] + 1j * w[1::2]
+        if not vectors:
+            return lam, None
         VR = vr.reshape(n, n).T  # column-major -> (row, col)
         V = np.empty((n, n), dtype=np.complex128)
         j = 0

@@ -230,12 +230,14 @@ def pair_plan(lam_raw) -> PairPlan:
 
 
 def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, shard: Optional[Shard],
-                table_dtype, timings: Optional[dict] = None) -> DeviceModes:
+                table_dtype, timings: Optional[dict] = None, a_orthonormal: bool = False) -> DeviceModes:
     """phi_raw = A @ [0_top; Cmap] for every computed unit, with fused
     column statistics; then normalise + phase-canonicalise + lock conjugates
     + build the decode table (dmd.py:189-213 and 92-120) in one HBM pass.
 
     Cmap: K x r complex (device) with phi_raw[:, j] = A[:, top:top+K] @ Cmap[:, j].
+    a_orthonormal: A's columns are orthonormal (the POD basis U), which bounds
+    the real-ification test of dmd.py:210 without an extra pass.
     """
     ops = dv.get_ops()
     dev = A.buf.device
@@ -287,17 +289,35 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
     Cs_h = Cs.cpu().numpy()
     # real-ification of phi for real-ified eigenvalues (dmd.py:208-211)
     realified_phi = set()
+    check = []
     for u in plan.realify:
         im_col = (Cs_h[:, u] * s[u]).imag
         if not np.any(im_col):
             realified_phi.add(u)
             continue
-        # max |Im(c s)| over rows via a statistics-only pass
-        Bq = torch.zeros((mA, 2), dtype=torch.float64, device=dev)
-        Bq[row_pad_top:row_pad_top + K, 0] = torch.as_tensor(im_col, device=dev)
-        stq = la._reduce_pair_stats(ops.tall_gemm(A, Bq, None, stats=True, row_offset=row0), shard)
-        if float(torch.sqrt(stq[0, 1]).item()) <= 1e-10:
-            realified_phi.add(u)
+        if a_orthonormal:
+            # A has orthonormal columns (rows of norm <= 1): ||Im||_inf lies in
+            # [||v||_2 / sqrt(n), ||v||_2] — decide without a pass when possible
+            v2 = float(np.linalg.norm(im_col))
+            n_glob = n_loc if shard is None else shard.n_global
+            if v2 * (1 + 1e-5) <= 1e-10:
+                realified_phi.add(u)
+                continue
+            if v2 * (1 - 1e-5) / np.sqrt(n_glob) > 1e-10:
+                continue
+        check.append((u, im_col))
+    if check:
+        # max_i |Im(phi_u s_u)_i| for every candidate in ONE statistics-only pass
+        # (column pair (Im, 0) per unit: the pair max is max Im^2)
+        Bq = torch.zeros((mA, 2 * len(check)), dtype=torch.float64, device=dev)
+        for k, (u, im_col) in enumerate(check):
+            Bq[row_pad_top:row_pad_top + K, 2 * k] = torch.as_tensor(im_col, device=dev)
+        with stage("modes.realify_pass"):
+            stq = la._reduce_pair_stats(ops.tall_gemm(A, Bq, None, stats=True, row_offset=row0), shard)
+            mx = torch.sqrt(stq[:, 1]).cpu().numpy()
+        for k, (u, _) in enumerate(check):
+            if mx[k] <= 1e-10:
+                realified_phi.add(u)
     # phi at each sorted position: (unit, conj)
     lam = plan.lam
     partner = conjugate_pairs(lam)
@@ -635,10 +655,13 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
     if init is None:
         # alpha0 = exact_dmd(data, r, svd_mode, seed).lam (dmd.py:387): the same
         # seed reproduces the same SVD, so the eigenvalues come from it directly.
+        # eigenvalues only: the init needs lam, not the residual-checked vectors
+        # of eig_small (linalg.py:107-133) that exact_dmd would also build
         with stage("small.eig(Khat)"):
             VS = basis.V / basis.S[None, :]
             Khat = basis.UtS[:, 1:] @ VS
-            lam_raw, _ = _eig_device(Khat)
+            with stage("small.geev"):
+                lam_raw, _ = dv.get_ops().geev(Khat, vectors=False)
             alpha0 = pair_plan(lam_raw).lam
     else:
         alpha0 = np.asarray(init, dtype=np.complex128)
@@ -678,7 +701,7 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
             dv.get_ops().tall_gemm(basis.A, basis.Umap, U, alg_flops=2 * nl * basis.A.k * r)   # linalg.py:88
             basis.A = None                                                   # release Q
     with stage("optdmd.modes_total"):
-        modes = _modes_pass(U, Bt, plan, 0, data.shard, tdt, timings)
+        modes = _modes_pass(U, Bt, plan, 0, data.shard, tdt, timings, a_orthonormal=True)
     model = ReducedModel(None, plan.lam, Sv, data.dt, grid_meta=data.grid_meta,
                          provenance={"method": "optdmd", "svd": svd_mode, "seed": seed,
                                      "objective_history": history, "converged": converged},

@@ -136,6 +136,20 @@ def _chol_upper(G: torch.Tensor):
     return L.mH
 
 
+def _cond_upper(R: torch.Tensor) -> float:
+    """2-norm condition number of the triangular factor for the CholQR2 /
+    shifted-CholQR3 switch. The Frobenius bound ||R||_F ||R^-1||_F >= cond_2
+    (two reductions) decides when it is clearly below the limit; only
+    otherwise are the singular values computed (svdvals, ~9 ms at l = 200)."""
+    l = R.shape[0]
+    eye = torch.eye(l, dtype=R.dtype, device=R.device)
+    Rinv = torch.linalg.solve_triangular(R, eye, upper=True)
+    bound = float((torch.linalg.matrix_norm(R) * torch.linalg.matrix_norm(Rinv)).item())
+    if not bound <= CHOLQR2_COND_LIMIT:      # also catches inf/nan
+        return float(torch.linalg.cond(R).item())
+    return bound
+
+
 def _apply_rinv(Y: Tall, R: torch.Tensor, shard: Optional[Shard]):
     """Y <- Y R^-1 in place (R upper triangular, l x l)."""
     l = R.shape[0]
@@ -168,7 +182,7 @@ def cholqr2_deferred(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dic
         R1 = _chol_upper(G)
         if R1 is None:
             return _householder_inplace(Y, shard, stats), None
-        cond = float(torch.linalg.cond(R1).item())
+        cond = _cond_upper(R1)
     if stats is not None:
         stats.setdefault("cond_R1", []).append(cond)
     if cond > CHOLQR2_COND_LIMIT:
