@@ -10,6 +10,7 @@
 #include <string>
 #include <unordered_map>
 #include <vector>
+#include <algorithm>
 
 #include "../../include/fdmd.h"
 #include "fdmd_kernels.cuh"
@@ -285,6 +286,150 @@ int launch_gram_sw(const fdmd::TallGramArgs& a, int tiles, int splits, cudaStrea
   }
 }
 
+// ---- panel Gram (fdmd_gram_panel.cuh): whole output per CTA partition -----
+struct PanelPlan {
+  bool ok = false;
+  bool transposed = false;   // run as B^T A (better tiling), reduce transposes back
+  int cost = 0;              // sum over partitions of the busiest sub-partition (8x8 blocks)
+  int WR = 5, WC = 7, P = 0, splits = 0, K1p = 0, K2p = 0, nba = 0, nbb = 0;
+  int64_t rows_per_split = 0;
+  size_t smem = 0;
+  fdmd::PanelTile tile[fdmd::tgp::MAXP * 8];
+};
+
+bool panel_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FDMD_GRAM_IMPL");
+    return !(e && strcmp(e, "tile") == 0);
+  }();
+  return on;
+}
+
+// Warp tiles of WR x WC 8x8 blocks cover the (upper, if symmetric) block grid;
+// they are packed into partitions of 8 consumer warps so that the DMMA count
+// per SM sub-partition (warps w, w+4) is balanced (greedy, heaviest first).
+PanelPlan panel_plan(int64_t n, int K1, int K2, int symmetric, size_t ea, size_t eb) {
+  PanelPlan p;
+  if (symmetric) { p.WR = 5; p.WC = 5; }
+  const int MB = (K1 + 7) / 8, NB = (K2 + 7) / 8;
+  const int TI = (MB + p.WR - 1) / p.WR, TJ = (NB + p.WC - 1) / p.WC;
+  struct T { short i0, j0, kind; int w; };
+  std::vector<T> ts;
+  for (int I = 0; I < TI; ++I)
+    for (int J = 0; J < TJ; ++J) {
+      if (symmetric && J < I) continue;
+      const bool diag = symmetric && I == J;
+      ts.push_back({(short)(I * p.WR), (short)(J * p.WC), (short)(diag ? 2 : 1),
+                    diag ? p.WR * (p.WR + 1) / 2 : p.WR * p.WC});
+    }
+  const int ntile = (int)ts.size();
+  p.P = (ntile + 7) / 8;
+  if (p.P > fdmd::tgp::MAXP) return p;
+  p.K1p = TI * p.WR * 8;
+  p.K2p = TJ * p.WC * 8;
+  p.nba = (int)((p.K1p * ea + 127) / 128);
+  p.nbb = symmetric ? 0 : (int)((p.K2p * eb + 127) / 128);
+  p.smem = (size_t)fdmd::tgp::STAGES * (p.nba + p.nbb) * fdmd::tgp::BOX_BYTES + 2 * fdmd::tgp::STAGES * 8 + 1024;
+  if (p.smem > 227 * 1024) return p;
+  std::stable_sort(ts.begin(), ts.end(), [](const T& x, const T& y) { return x.w > y.w; });
+  const int nbins = p.P * 4;                       // (partition, sub-partition)
+  std::vector<int> load(nbins, 0);
+  std::vector<std::vector<const T*>> bin(nbins);
+  for (const T& x : ts) {
+    int best = -1;
+    for (int b = 0; b < nbins; ++b)
+      if (bin[b].size() < 2 && (best < 0 || load[b] < load[best])) best = b;
+    bin[best].push_back(&x);
+    load[best] += x.w;
+  }
+  for (int part = 0; part < p.P; ++part) {
+    int mx = 0;
+    for (int sub = 0; sub < 4; ++sub) mx = std::max(mx, load[part * 4 + sub]);
+    p.cost += mx;
+  }
+  // warp 0 also feeds the ring (it waits for the slowest warp every chunk):
+  // give it the lightest sub-partition of its CTA, and the idle slot if any
+  for (auto& e : p.tile) e = fdmd::PanelTile{0, 0, 0, 0};
+  for (int part = 0; part < p.P; ++part) {
+    int order[4] = {0, 1, 2, 3};
+    std::stable_sort(order, order + 4, [&](int x, int y) { return load[part * 4 + x] < load[part * 4 + y]; });
+    for (int sub = 0; sub < 4; ++sub) {
+      auto& bl = bin[part * 4 + order[sub]];
+      std::stable_sort(bl.begin(), bl.end(), [](const T* x, const T* y) { return x->w < y->w; });
+      const int off = (int)(2 - bl.size());       // idle first (warp sub), then lightest
+      for (size_t q = 0; q < bl.size(); ++q) {
+        const int warp = sub + 4 * (off + (int)q);
+        p.tile[part * 8 + warp] = fdmd::PanelTile{bl[q]->i0, bl[q]->j0, bl[q]->kind, 0};
+      }
+    }
+  }
+  // row splits: ~2 waves of one CTA per SM, chunk-aligned (16 rows)
+  const int64_t max_splits = std::max<int64_t>(1, (n + 15) / 16);
+  int64_t splits = std::max<int64_t>(1, ((int64_t)sm_count_cached() * 2 + p.P - 1) / p.P);
+  splits = std::min(splits, max_splits);
+  p.rows_per_split = ((n + splits - 1) / splits + 15) / 16 * 16;
+  if (p.rows_per_split == 0) p.rows_per_split = 16;
+  p.splits = (int)std::max<int64_t>(1, (n + p.rows_per_split - 1) / p.rows_per_split);
+  p.ok = true;
+  return p;
+}
+
+// orientation with the cheaper busiest-sub-partition schedule (A^T B or (B^T A)^T)
+PanelPlan panel_plan_best(int64_t n, int K1, int K2, int symmetric, size_t ea, size_t eb) {
+  PanelPlan p = panel_plan(n, K1, K2, symmetric, ea, eb);
+  if (symmetric) return p;
+  PanelPlan q = panel_plan(n, K2, K1, 0, eb, ea);
+  if (q.ok && (!p.ok || q.cost < p.cost)) {
+    q.transposed = true;
+    return q;
+  }
+  return p;
+}
+
+template <typename TA, typename TB, int WR, int WC, bool SYM>
+int launch_gram_panel(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaStream_t s) {
+  auto kt = fdmd::tall_gram_panel_kernel<TA, TB, WR, WC, SYM>;
+  CUtensorMap maps[2];
+  const void* ptr[2] = {a.A, a.B};
+  const int64_t ld[2] = {a.lda, a.ldb};
+  const int kdim[2] = {a.K1, a.K2};
+  const size_t elt[2] = {sizeof(TA), sizeof(TB)};
+  for (int i = 0; i < (SYM ? 1 : 2); ++i) {
+    cuuint64_t dims[2] = {(cuuint64_t)kdim[i], (cuuint64_t)a.n};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld[i] * elt[i])};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / elt[i]), (cuuint32_t)fdmd::tgp::BR};
+    cuuint32_t estr[2] = {1, 1};
+    if (tensor_map_encoder()(&maps[i], elt[i] == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                             2, const_cast<void*>(ptr[i]), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(FDMD_ERR_CUDA, "tall_gram: tensor map encode failed");
+  }
+  if (SYM) maps[1] = maps[0];
+  fdmd::TallGramPanelArgs pa{};
+  pa.g = a;
+  pa.g.K1p = pl.K1p;
+  pa.g.K2p = pl.K2p;
+  pa.g.rows_per_split = pl.rows_per_split;
+  pa.nba = pl.nba;
+  pa.nbb = pl.nbb;
+  pa.lda_boxes = std::min(pl.nba, (int)((a.K1 * sizeof(TA) + 127) / 128));
+  pa.ldb_boxes = SYM ? 0 : std::min(pl.nbb, (int)((a.K2 * sizeof(TB) + 127) / 128));
+  for (int i = 0; i < fdmd::tgp::MAXP * 8; ++i) pa.tile[i] = pl.tile[i];
+  static thread_local int conf_t = -1;
+  static thread_local size_t conf_smem = 0;
+  int dv = 0;
+  cudaGetDevice(&dv);
+  if (conf_t != dv || conf_smem < pl.smem) {
+    CUDA_TRY(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    conf_t = dv;
+    conf_smem = 227 * 1024;
+  }
+  kt<<<dim3(pl.P, pl.splits), fdmd::tgp::THREADS, pl.smem, s>>>(maps[0], maps[1], pa);
+  LAUNCH_CHECK("tall_gram_panel");
+  return FDMD_OK;
+}
+
 template <typename TA, int LA, typename TB, int LB>
 int launch_gram(const fdmd::TallGramArgs& a, int tiles, int splits, cudaStream_t s) {
   auto kern = fdmd::tall_gram_kernel<TA, LA, TB, LB>;
@@ -401,13 +546,19 @@ int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda, const 
 size_t fdmd_tall_gram_workspace(int64_t n, int K1, int K2) {
   // large enough for either plan (a symmetric Gram has fewer tiles -> more splits)
   size_t need = 0;
-  for (int sym = 0; sym < 2; ++sym)
+  for (int sym = 0; sym < 2; ++sym) {
     for (int v = 0; v < 3; ++v) {
       const bool sw = v > 0;
       const int TN = v == 2 ? 224 : 64;
       GramPlan q = gram_plan(n, K1, K2, sym, sw, TN);
       need = std::max(need, (size_t)q.splits * q.K1p * q.K2p * sizeof(double));
     }
+    for (int ea = 4; ea <= 8; ea += 4)
+      for (int eb = 4; eb <= 8; eb += 4) {
+        PanelPlan q = panel_plan_best(n, K1, K2, sym, ea, eb);
+        if (q.ok) need = std::max(need, (size_t)q.splits * q.K1p * q.K2p * sizeof(double));
+      }
+  }
   return need + 256;
 }
 
@@ -424,6 +575,36 @@ int fdmd_tall_gram(const void* A, int a_dtype, int a_layout, int64_t lda, const 
     return fail(FDMD_ERR_INVALID, "bad ldb");
   cudaStream_t s = (cudaStream_t)stream;
   const bool sw = gram_sw_eligible(A, a_dtype, a_layout, lda, B, b_dtype, b_layout, ldb, n);
+  if (sw && panel_enabled() && n > 0) {
+    PanelPlan pl = panel_plan_best(n, K1, K2, symmetric, dsize(a_dtype), dsize(b_dtype));
+    if (pl.ok && !(symmetric && a_dtype != b_dtype)) {
+      const size_t need = (size_t)pl.splits * pl.K1p * pl.K2p * sizeof(double);
+      if (!workspace || workspace_bytes < need)
+        return fail(FDMD_ERR_WORKSPACE, "tall_gram workspace %zu < %zu", workspace_bytes, need);
+      fdmd::TallGramArgs a{};
+      const bool tr = pl.transposed;
+      a.A = tr ? B : A; a.lda = tr ? ldb : lda; a.B = tr ? A : B; a.ldb = tr ? lda : ldb;
+      a.W = static_cast<double*>(workspace);
+      a.n = n; a.K1 = tr ? K2 : K1; a.K2 = tr ? K1 : K2; a.symmetric = symmetric;
+      const int da = tr ? b_dtype : a_dtype, db = tr ? a_dtype : b_dtype;
+      int rc;
+      if (symmetric)
+        rc = da == FDMD_F32 ? launch_gram_panel<float, float, 5, 5, true>(a, pl, s)
+                            : launch_gram_panel<double, double, 5, 5, true>(a, pl, s);
+      else if (da == FDMD_F32)
+        rc = db == FDMD_F32 ? launch_gram_panel<float, float, 5, 7, false>(a, pl, s)
+                            : launch_gram_panel<float, double, 5, 7, false>(a, pl, s);
+      else
+        rc = db == FDMD_F32 ? launch_gram_panel<double, float, 5, 7, false>(a, pl, s)
+                            : launch_gram_panel<double, double, 5, 7, false>(a, pl, s);
+      if (rc != FDMD_OK) return rc;
+      dim3 grid((K2 + 127) / 128, K1);
+      fdmd::gram_reduce_kernel<<<grid, 128, 0, s>>>(a.W, pl.splits, K1, K2, pl.K1p, pl.K2p, symmetric, C, ldc, beta,
+                                                    tr ? 1 : 0);
+      LAUNCH_CHECK("gram_reduce");
+      return FDMD_OK;
+    }
+  }
   // wide tiles for general products; 64x64 for symmetric Grams (a 64 x 224 stripe
   // of a triangle leaves the lower stripes nearly idle: measured 9.8 vs 16 TF/s)
   const int nfb = (K2 > 64 && !symmetric) ? 7 : 2;

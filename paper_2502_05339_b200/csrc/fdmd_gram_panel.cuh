@@ -1,0 +1,203 @@
+// Panel tall_gram: partial[split] = A[rows]^T B[rows] where ONE CTA covers the
+// whole K1 x K2 output (or a 1/P share of it) for its row range, so every
+// reduction row is streamed into shared memory once per CTA partition and no
+// DMMA is spent on tile padding.
+//
+// Why (ncu, r01): with 64 x 64 / 64 x 224 CTA tiles the 200 x 200 Grams of the
+// fit executed 1.4x (general) and 2x (symmetric: the 10 upper tiles of a 4 x 4
+// grid are 64-row squares) the algorithmic DMMA work. Here the output is cut
+// into warp tiles of WR x WC 8x8 blocks (5 x 7 general, 5 x 5 symmetric, where
+// the diagonal tiles skip their lower blocks at compile time); the host packs
+// warp tiles into partitions of 8 consumer warps, balancing the DMMA count per
+// SM sub-partition (warps w and w+4 share one: w & 3).
+//
+// Data movement is the SW128 scheme of fdmd_gram_tma.cuh: 16-row chunks of
+// both operands arrive as 128-byte-row TMA boxes; k-step ks reads the permuted
+// rows {b, b+2, b+4, b+6} (b = 8*(ks/2) + ks%2) so the fragment loads are
+// bank-conflict free. A symmetric Gram loads one operand. There is no
+// dedicated producer warp: a 9th warp would put 3 warps on one sub-partition
+// and cap registers at 168 (spills with a 5 x 7 accumulator tile). Lane 0 of
+// warp 0 — placed on the most lightly loaded sub-partition by the host —
+// refills each stage after all 8 warps released it.
+#pragma once
+#include <cuda.h>
+
+#include "fdmd_gram_tma.cuh"
+
+namespace fdmd {
+
+namespace tgp {
+constexpr int BR = 16;
+constexpr int STAGES = 4;
+constexpr int THREADS = 256;            // 8 warps = 2 per SM sub-partition -> up to 255 regs
+constexpr int MAXP = 8;                 // partitions (x 8 warp tiles) per launch
+constexpr int BOX_BYTES = BR * 128;
+}  // namespace tgp
+
+struct PanelTile {
+  short i0, j0;   // first 8x8 block row / column of the warp tile
+  short kind;     // 0 idle, 1 full, 2 diagonal (symmetric: blocks ii <= jj only)
+  short pad;
+};
+
+struct TallGramPanelArgs {
+  TallGramArgs g;
+  int nba, nbb;                               // 128-B boxes per chunk row (A, B; nbb = 0 when symmetric)
+  int lda_boxes, ldb_boxes;                   // boxes actually loaded (those holding columns < K)
+  PanelTile tile[tgp::MAXP * 8];
+};
+
+template <typename TX> __device__ __forceinline__ int panel_offset(int row, int col) {
+  constexpr int W = 128 / sizeof(TX);
+  const int box = col / W;
+  const int cb = (col % W) * (int)sizeof(TX);
+  return box * tgp::BOX_BYTES + row * 128 + ((((cb >> 4) ^ (row & 7))) << 4) + (cb & 15);
+}
+
+struct PanelFeed {
+  const CUtensorMap* amap;
+  const CUtensorMap* bmap;
+  unsigned char* a_sm;
+  unsigned char* b_sm;
+  int a_stage, b_stage, la, lb, wa, wb;
+  unsigned bytes;
+  int64_t rbeg, nchunks;
+  __device__ __forceinline__ void issue(int64_t c, int s, uint64_t* full) const {
+    mbar_expect_tx(&full[s], bytes);
+    const int r0 = (int)(rbeg + c * tgp::BR);
+    for (int j = 0; j < la; ++j) tma_load_2d(a_sm + s * a_stage + j * tgp::BOX_BYTES, amap, j * wa, r0, &full[s]);
+    for (int j = 0; j < lb; ++j) tma_load_2d(b_sm + s * b_stage + j * tgp::BOX_BYTES, bmap, j * wb, r0, &full[s]);
+  }
+};
+
+// Release stage s of chunk c; the feeding lane then waits for all 8 warps to
+// release it and loads chunk c + STAGES into it.
+__device__ __forceinline__ void panel_release(const PanelFeed& fd, bool feeder, int lane, int64_t c, int s,
+                                              unsigned ph, uint64_t* full, uint64_t* empty) {
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&empty[s]);
+  if (feeder && lane == 0 && c + tgp::STAGES < fd.nchunks) {
+    mbar_wait(&empty[s], ph);
+    fd.issue(c + tgp::STAGES, s, full);
+  }
+}
+
+template <typename TA, typename TB, int WR, int WC, bool DIAG>
+__device__ __forceinline__ void panel_consume(const PanelFeed& fd, bool feeder, const unsigned char* b_base,
+                                              int b_stage_bytes, uint64_t* full, uint64_t* empty, int i0, int j0,
+                                              int lane, double* __restrict__ W, int K2p) {
+  const int g = lane >> 2, t = lane & 3;
+  // byte offsets of this lane's fragments for the two row parities of a k-step
+  int offa[WR][2], offb[WC][2];
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int row = p + 2 * t;
+#pragma unroll
+    for (int ii = 0; ii < WR; ++ii) offa[ii][p] = panel_offset<TA>(row, 8 * (i0 + ii) + g);
+#pragma unroll
+    for (int jj = 0; jj < WC; ++jj) offb[jj][p] = panel_offset<TB>(row, 8 * (j0 + jj) + g);
+  }
+  double acc[WR][WC][2];
+#pragma unroll
+  for (int ii = 0; ii < WR; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < WC; ++jj) acc[ii][jj][0] = acc[ii][jj][1] = 0.0;
+
+  int s = 0;
+  unsigned ph = 0;
+  for (int64_t c = 0; c < fd.nchunks; ++c) {
+    mbar_wait(&full[s], ph);
+    const unsigned char* pa = fd.a_sm + s * fd.a_stage;
+    const unsigned char* pb = b_base + s * b_stage_bytes;
+#pragma unroll
+    for (int ks = 0; ks < tgp::BR / 4; ++ks) {
+      const int p = ks & 1, hi = (ks >> 1) * 1024;   // rows +8 -> +1024 B, same swizzle key
+      double a[WR], b[WC];
+#pragma unroll
+      for (int ii = 0; ii < WR; ++ii) a[ii] = (double)*reinterpret_cast<const TA*>(pa + offa[ii][p] + hi);
+#pragma unroll
+      for (int jj = 0; jj < WC; ++jj) b[jj] = (double)*reinterpret_cast<const TB*>(pb + offb[jj][p] + hi);
+#pragma unroll
+      for (int ii = 0; ii < WR; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < WC; ++jj)
+          if (!DIAG || ii <= jj) dmma884(acc[ii][jj], a[ii], b[jj]);
+    }
+    panel_release(fd, feeder, lane, c, s, ph, full, empty);
+    if (++s == tgp::STAGES) { s = 0; ph ^= 1; }
+  }
+#pragma unroll
+  for (int ii = 0; ii < WR; ++ii) {
+    const int i = 8 * (i0 + ii) + g;
+#pragma unroll
+    for (int jj = 0; jj < WC; ++jj) {
+      if (DIAG && ii > jj) continue;
+      const int j = 8 * (j0 + jj) + 2 * t;
+      *reinterpret_cast<double2*>(W + (int64_t)i * K2p + j) = make_double2(acc[ii][jj][0], acc[ii][jj][1]);
+    }
+  }
+}
+
+template <typename TA, typename TB, int WR, int WC, bool SYM>
+__global__ void __launch_bounds__(tgp::THREADS, 1)
+tall_gram_panel_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                       const __grid_constant__ TallGramPanelArgs pa) {
+  const TallGramArgs& args = pa.g;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  PanelFeed fd;
+  fd.amap = &amap;
+  fd.bmap = &bmap;
+  fd.a_stage = pa.nba * tgp::BOX_BYTES;
+  fd.b_stage = pa.nbb * tgp::BOX_BYTES;
+  fd.a_sm = base;
+  fd.b_sm = base + tgp::STAGES * fd.a_stage;
+  fd.la = pa.lda_boxes;
+  fd.lb = pa.ldb_boxes;
+  fd.wa = 128 / sizeof(TA);
+  fd.wb = 128 / sizeof(TB);
+  // boxes wholly past K are never loaded: their smem only feeds padding outputs
+  fd.bytes = (unsigned)((pa.lda_boxes + pa.ldb_boxes) * tgp::BOX_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(fd.b_sm + tgp::STAGES * fd.b_stage);
+  uint64_t* empty = full + tgp::STAGES;
+
+  const int part = blockIdx.x;
+  fd.rbeg = (int64_t)blockIdx.y * args.rows_per_split;
+  const int64_t rend = min(args.n, fd.rbeg + args.rows_per_split);
+  fd.nchunks = rend > fd.rbeg ? (rend - fd.rbeg + tgp::BR - 1) / tgp::BR : 0;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const bool feeder = warp == 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < tgp::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], tgp::THREADS / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < tgp::STAGES && s < fd.nchunks; ++s) fd.issue(s, s, full);
+
+  const PanelTile tl = pa.tile[part * 8 + warp];
+  double* W = args.W + (int64_t)blockIdx.y * args.K1p * args.K2p;
+  const unsigned char* bb = SYM ? fd.a_sm : fd.b_sm;
+  const int bst = SYM ? fd.a_stage : fd.b_stage;
+  if (tl.kind == 1) {
+    panel_consume<TA, TB, WR, WC, false>(fd, feeder, bb, bst, full, empty, tl.i0, tl.j0, lane, W, args.K2p);
+  } else if (SYM && tl.kind == 2) {
+    panel_consume<TA, TB, WR, WC, true>(fd, feeder, bb, bst, full, empty, tl.i0, tl.j0, lane, W, args.K2p);
+  } else {   // idle slot: keep the ring moving
+    int s = 0;
+    unsigned ph = 0;
+    for (int64_t c = 0; c < fd.nchunks; ++c) {
+      mbar_wait(&full[s], ph);
+      panel_release(fd, feeder, lane, c, s, ph, full, empty);
+      if (++s == tgp::STAGES) { s = 0; ph ^= 1; }
+    }
+  }
+}
+
+}  // namespace fdmd

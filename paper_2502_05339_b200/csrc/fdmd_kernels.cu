@@ -10,5 +10,6 @@
 #include "fdmd_tall.cuh"
 #include "fdmd_tall_tma.cuh"
 #include "fdmd_gram_tma.cuh"
+#include "fdmd_gram_panel.cuh"
 #include "fdmd_tc_decode.cuh"
 #include "fdmd_stream.cuh"

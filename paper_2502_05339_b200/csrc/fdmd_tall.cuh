@@ -457,14 +457,16 @@ __global__ void __launch_bounds__(gr::THREADS, 2) tall_gram_kernel(TallGramArgs 
 
 // out[i][j] = beta*out[i][j] + sum_s W[s][i][j] (fixed order). Symmetric Grams
 // compute 8x8 blocks on/above the diagonal only; the rest is mirrored.
+// transposed: the partials hold (B^T A) (W[s][j][i], row length K2p).
 __global__ void gram_reduce_kernel(const double* __restrict__ W, int splits, int K1, int K2, int K1p,
                                    int K2p, int symmetric, double* __restrict__ out, int64_t ldo,
-                                   double beta) {
+                                   double beta, int transposed = 0) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   if (i >= K1 || j >= K2) return;
   int si = i, sj = j;
   if (symmetric && (i >> 3) > (j >> 3)) { si = j; sj = i; }
+  if (transposed) { const int x = si; si = sj; sj = x; }
   double s = 0.0;
   for (int p = 0; p < splits; ++p) s += W[((int64_t)p * K1p + si) * K2p + sj];
   double* o = out + (int64_t)i * ldo + j;

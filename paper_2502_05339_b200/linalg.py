@@ -284,7 +284,7 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
         _, fix = cholqr2_deferred(Q, shard, stats)
     for _ in range(q):
         with stage("power.Z=XtQ"):
-            Z = allreduce(shard, ops.tall_gram(S, Q, alg_flops=2 * nl * T * l))   # m x l
+            Z = allreduce(shard, ops.tall_gram(S, Q, K1=T, alg_flops=2 * nl * T * l))   # T x l (X^T Q)
             if fix is not None:
                 Z = Z @ fix
         with stage("power.qr(Z)"):

@@ -139,6 +139,69 @@ def test_tall_gram(dv, la, lb, da, db, shape):
     assert np.abs(G - want).max() <= 1e-12 * np.abs(want).max() * max(1, np.sqrt(n) / 100)
 
 
+@pytest.mark.parametrize("K1,K2,sym", [(200, 200, True), (256, 256, True), (400, 400, True), (150, 150, True),
+                                       (8, 8, True), (1, 1, True), (200, 201, False), (201, 200, False),
+                                       (40, 300, False), (400, 401, False), (3, 5, False)])
+@pytest.mark.parametrize("n", [1, 16, 17, 40001])
+@pytest.mark.parametrize("da,db", [("f64", "f64"), ("f32", "f64"), ("f64", "f32")])
+def test_tall_gram_panel_shapes(dv, K1, K2, sym, n, da, db):
+    """Row-major operands take the panel kernel (whole output per CTA
+    partition); K past 8 partitions falls back to the tiled kernel."""
+    if sym and da != db:
+        pytest.skip("symmetric Gram has one operand")
+    rng = np.random.default_rng(K1 * 1000 + K2 + n)
+    tA = torch.float32 if da == "f32" else torch.float64
+    tB = torch.float32 if db == "f32" else torch.float64
+    A = rng.standard_normal((n, K1))
+    if da == "f32":
+        A = A.astype(np.float32).astype(np.float64)
+    At = _tall_from(dv, A, "row", tA)
+    if sym:
+        G = dv.get_ops().tall_gram(At, At, symmetric=True).cpu().numpy()
+        want = A.T @ A
+        assert np.array_equal(G, G.T)
+    else:
+        B = rng.standard_normal((n, K2))
+        if db == "f32":
+            B = B.astype(np.float32).astype(np.float64)
+        Bt = _tall_from(dv, B, "row", tB)
+        G = dv.get_ops().tall_gram(At, Bt).cpu().numpy()
+        want = A.T @ B
+    assert np.abs(G - want).max() <= 1e-12 * max(np.abs(want).max(), 1e-300) * max(1, np.sqrt(n) / 100)
+
+
+def test_tall_gram_panel_matches_tiled_kernel(tmp_path):
+    """The panel and the 64 x TN tiled Gram agree (FDMD_GRAM_IMPL=tile)."""
+    code = (
+        "import numpy as np, torch, sys\n"
+        "sys.path.insert(0, '.')\n"
+        "from paper_2502_05339_b200 import device as dv\n"
+        "rng = np.random.default_rng(3)\n"
+        "out = {}\n"
+        "Y = torch.as_tensor(rng.standard_normal((300001, 200)), device='cuda')\n"
+        "S = torch.as_tensor(rng.standard_normal((300001, 201)), device='cuda', dtype=torch.float32)\n"
+        "from paper_2502_05339_b200.linalg import as_tall\n"
+        "Yt, St = as_tall(Y), as_tall(S)\n"
+        "ops = dv.get_ops()\n"
+        "out['sym'] = ops.tall_gram(Yt, Yt, symmetric=True).cpu().numpy()\n"
+        "out['qts'] = ops.tall_gram(Yt, St).cpu().numpy()\n"
+        "out['stq'] = ops.tall_gram(St, Yt).cpu().numpy()\n"
+        f"np.savez(sys.argv[1], **out)\n")
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for impl in ("panel", "tile"):
+        f = tmp_path / f"{impl}.npz"
+        env = dict(os.environ, FDMD_GRAM_IMPL=impl)
+        subprocess.run([sys.executable, "-c", code, str(f)], cwd=root, env=env, check=True, timeout=300)
+        res[impl] = np.load(f)
+    for k in ("sym", "qts", "stq"):
+        a, b = res["panel"][k], res["tile"][k]
+        assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max(), k
+
+
 def test_tall_gram_symmetric_deterministic(dv):
     rng = np.random.default_rng(5)
     Y = rng.standard_normal((200000, 210))

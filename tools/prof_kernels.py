@@ -43,10 +43,14 @@ def main():
         if a.which in ("all", "gram"):
             ev[0].record(); ops.tall_gram(S, Q); ev[1].record(); torch.cuda.synchronize()
             res["gram StQ"] = (ev[0].elapsed_time(ev[1]), 2.0 * n * m * l)
+            ev[0].record(); ops.tall_gram(Q, S); ev[1].record(); torch.cuda.synchronize()
+            res["gram QtS"] = (ev[0].elapsed_time(ev[1]), 2.0 * n * m * l)
         if a.which in ("all", "trsm"):
             R = torch.triu(torch.randn(l, l, dtype=torch.float64, device="cuda"))
             ev[0].record(); ops.tall_gemm(Q, R, Q); ev[1].record(); torch.cuda.synchronize()
             res["gemm QR inplace"] = (ev[0].elapsed_time(ev[1]), 2.0 * n * l * l)
+            ev[0].record(); ops.tall_gemm(Q, R, Q, upper=True); ev[1].record(); torch.cuda.synchronize()
+            res["trsm QR upper"] = (ev[0].elapsed_time(ev[1]), 1.0 * n * l * l)
         if a.which in ("all", "decode"):
             out = torch.empty((32, n), dtype=torch.float32, device="cuda")
             ev[0].record(); ops.decode(U, coef, out=out); ev[1].record(); torch.cuda.synchronize()
