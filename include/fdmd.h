@@ -51,6 +51,7 @@ const char* fdmd_last_error(void);
 int fdmd_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
 
 #define FDMD_B_UPPER 1 /* tall_gemm flag: B is upper triangular (CholeskyQR's R^-1) */
+#define FDMD_SHARE_SMS 2 /* tall_gemm flag: leave 8 SMs free for small work on another stream */
 
 /* C[n x N] = A[n x K] * B[K x N]. A: f32/f64, ROW/COL. B: f64 row-major (ld ldb).
  * C: f32/f64 ROW/COL, may be NULL (statistics only). FP64 DMMA accumulation.

@@ -155,7 +155,7 @@ int launch_tg_tma(const fdmd::TallGemmArgs& a, cudaStream_t s, int& grid_x, bool
     configured = dev;
   }
   const int64_t ntiles = (a.n + fdmd::tt::BM - 1) / fdmd::tt::BM;
-  grid_x = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, sm_count_cached()));
+  grid_x = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, std::max(1, sm_count_cached() - a.reserve_sms)));
   dim3 grid(grid_x, gy);
   kern<<<grid, fdmd::tt::THREADS, smem, s>>>(map, ta);
   LAUNCH_CHECK("tall_gemm_tma");
@@ -517,6 +517,7 @@ int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda, const 
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.C = C; a.ldc = ldc;
   a.n = n; a.K = K; a.N = N; a.row_offset = row_offset;
   a.b_upper = (flags & FDMD_B_UPPER) ? 1 : 0;
+  a.reserve_sms = (flags & FDMD_SHARE_SMS) ? 8 : 0;
   static const int dbg = [] { const char* e = getenv("FDMD_TG_DEBUG"); return e ? atoi(e) : 0; }();
   a.debug = dbg;
   const bool stats = pair_stats != nullptr;

@@ -39,6 +39,7 @@ struct TallGemmArgs {
   void* C; int64_t ldc;         // C: n x N (ROW: C[i*ldc+j]; COL: C[j*ldc+i])
   int64_t n; int K; int N;
   int b_upper;         // B upper triangular (B[k][c] = 0 for k > c): skip zero blocks
+  int reserve_sms;     // persistent grid leaves this many SMs free
   int debug;           // tuning experiments: bit0 no loads, bit1 no stores, bit2 no DMMA
   // epilogue statistics over column pairs (2u, 2u+1) = (Re, Im) of unit u:
   // per CTA: sum_i |c|^2 and (max_i |c|^2, first argmax i)

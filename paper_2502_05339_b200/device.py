@@ -141,7 +141,7 @@ class CudaOps:
     # -- C[n x N] = A * B (B small fp64, K x N) ---------------------------
     def tall_gemm(self, A: Tall, B: torch.Tensor, C: Optional[Tall], stats: bool = False,
                   row_offset: int = 0, alg_flops: Optional[float] = None,
-                  upper: bool = False) -> Optional[torch.Tensor]:
+                  upper: bool = False, share_sms: bool = False) -> Optional[torch.Tensor]:
         L = _lib.lib()
         K, N = int(B.shape[0]), int(B.shape[1])
         assert K <= A.k or K <= (A.ld if A.layout == "row" else K), (K, A.k)
@@ -159,7 +159,8 @@ class CudaOps:
         c_ld = C.ld if C is not None else A.n
         e0 = self._ev()
         _lib.check(L.fdmd_tall_gemm(_ptr(A.buf), _DT[A.dtype], A.code, A.ld, _ptr(B), B.shape[1],
-                                     _ptr(c_buf), c_dt, c_lay, c_ld, A.n, K, N, 1 if upper else 0,
+                                     _ptr(c_buf), c_dt, c_lay, c_ld, A.n, K, N,
+                                     (1 if upper else 0) | (2 if share_sms else 0),
                                      _ptr(st), row_offset, _ptr(ws), wsb, _stream()), "tall_gemm")
         self._done("tall_gemm", 2.0 * A.n * K * N if alg_flops is None else alg_flops, e0)
         self.launches += 2 if stats else 1

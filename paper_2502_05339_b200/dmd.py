@@ -12,6 +12,7 @@ the diagnostic, ``table_dtype`` for the decode table, ``timings`` dict.
 
 from __future__ import annotations
 
+import contextlib
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -457,6 +458,17 @@ def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, po
     return basis
 
 
+_SIDE = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    """Per-device stream for r x r work that overlaps a tall kernel."""
+    key = str(dev)
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=dev)
+    return _SIDE[key]
+
+
 def _eig_device(Khat: torch.Tensor):
     """eig_small (linalg.py:107-133) on the device: cuSOLVER Xgeev + residual check."""
     w, V = dv.get_ops().geev(Khat)
@@ -651,55 +663,71 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
     Sv = basis.S.cpu().numpy()
     _check_sigma(Sv)
     t0 = time.perf_counter()
-    Dm = (basis.V.conj() * basis.S[None, :]).to(torch.complex128)      # dmd.py:384
-    if init is None:
-        # alpha0 = exact_dmd(data, r, svd_mode, seed).lam (dmd.py:387): the same
-        # seed reproduces the same SVD, so the eigenvalues come from it directly.
-        # eigenvalues only: the init needs lam, not the residual-checked vectors
-        # of eig_small (linalg.py:107-133) that exact_dmd would also build
-        with stage("small.eig(Khat)"):
-            VS = basis.V / basis.S[None, :]
-            Khat = basis.UtS[:, 1:] @ VS
-            with stage("small.geev"):
-                lam_raw, _ = dv.get_ops().geev(Khat, vectors=False)
-            alpha0 = pair_plan(lam_raw).lam
-    else:
-        alpha0 = np.asarray(init, dtype=np.complex128)
-        if alpha0.size != r:
-            raise ValueError(f"init has {alpha0.size} eigenvalues, expected {r}")
-    try:
-        with stage("small.varpro_lm"):
-            alpha, B, history, converged = _varpro_lm_device(Dm, alpha0, cfg)
-    except _AlphaCollapse:
-        rng = np.random.default_rng(0 if seed is None else seed)
-        jitter = 1e-10 * (1.0 + np.abs(alpha0)) * np.exp(2j * np.pi * rng.random(alpha0.size))
-        try:
-            alpha, B, history, converged = _varpro_lm_device(Dm, alpha0 + jitter, cfg)
-        except _AlphaCollapse:
-            raise ConvergenceError("eigenvalue iterates collapsed below separation tolerance twice") from None
-    alpha_h = alpha.cpu().numpy()
-    B_h = B.cpu().numpy()
-    a_s, B_s = _symmetrize(alpha_h, B_h)
-    Dh = Dm.cpu().numpy()
-    f_sym = float(np.linalg.norm(Dh - vandermonde(a_s, T) @ B_s))
-    if f_sym <= history[-1] * (1 + 1e-9) and f_sym <= history[0] * (1 + 1e-12):
-        alpha_h, B_h = a_s, B_s
-    if timings is not None:
-        timings["lm_s"] = time.perf_counter() - t0
-    plan = pair_plan(alpha_h)
+    tdt = table_dtype or _default_table_dtype(data)
+    dev = basis.V.device
+    on_cuda = dev.type == "cuda"
+    ready = torch.cuda.Event() if on_cuda else None
+    if ready is not None:
+        ready.record()
     # phi = U @ B.T (dmd.py:414). The POD basis U = Q Ub_r is lifted once into
     # a column-major table (the north_star reconstruction basis), Q is released,
     # and the modes are formed from U — peak HBM stays S + Q + U at config 3.
-    Bt = torch.as_tensor(B_h.T.copy(), device=basis.V.device)                # r x r
-    tdt = table_dtype or _default_table_dtype(data)
+    # The lift does not depend on the eigenvalues: it is launched first, on all
+    # but 8 SMs, and the r x r work below (eig, variable projection) runs on a
+    # side stream in its shadow.
     if basis.Umap is None:
         U = basis.A
     else:
         with stage("lift.U=QUb"):
             U = alloc_tall(basis.A.n, r, tdt, "col", device=basis.A.buf.device)
             nl = float(basis.A.n)
-            dv.get_ops().tall_gemm(basis.A, basis.Umap, U, alg_flops=2 * nl * basis.A.k * r)   # linalg.py:88
-            basis.A = None                                                   # release Q
+            dv.get_ops().tall_gemm(basis.A, basis.Umap, U, alg_flops=2 * nl * basis.A.k * r,   # linalg.py:88
+                                   share_sms=True)
+    side = _side_stream(dev) if on_cuda else None
+    if side is not None:
+        side.wait_event(ready)
+    with (torch.cuda.stream(side) if side is not None else contextlib.nullcontext()):
+        Dm = (basis.V.conj() * basis.S[None, :]).to(torch.complex128)      # dmd.py:384
+        if init is None:
+            # alpha0 = exact_dmd(data, r, svd_mode, seed).lam (dmd.py:387): the same
+            # seed reproduces the same SVD, so the eigenvalues come from it directly.
+            # eigenvalues only: the init needs lam, not the residual-checked vectors
+            # of eig_small (linalg.py:107-133) that exact_dmd would also build
+            with stage("small.eig(Khat)"):
+                VS = basis.V / basis.S[None, :]
+                Khat = basis.UtS[:, 1:] @ VS
+                with stage("small.geev"):
+                    lam_raw, _ = dv.get_ops().geev(Khat, vectors=False)
+                alpha0 = pair_plan(lam_raw).lam
+        else:
+            alpha0 = np.asarray(init, dtype=np.complex128)
+            if alpha0.size != r:
+                raise ValueError(f"init has {alpha0.size} eigenvalues, expected {r}")
+        try:
+            with stage("small.varpro_lm"):
+                alpha, B, history, converged = _varpro_lm_device(Dm, alpha0, cfg)
+        except _AlphaCollapse:
+            rng = np.random.default_rng(0 if seed is None else seed)
+            jitter = 1e-10 * (1.0 + np.abs(alpha0)) * np.exp(2j * np.pi * rng.random(alpha0.size))
+            try:
+                alpha, B, history, converged = _varpro_lm_device(Dm, alpha0 + jitter, cfg)
+            except _AlphaCollapse:
+                raise ConvergenceError("eigenvalue iterates collapsed below separation tolerance twice") from None
+        alpha_h = alpha.cpu().numpy()
+        B_h = B.cpu().numpy()
+        Dh = Dm.cpu().numpy()
+    if side is not None:
+        torch.cuda.current_stream().wait_stream(side)
+    a_s, B_s = _symmetrize(alpha_h, B_h)
+    f_sym = float(np.linalg.norm(Dh - vandermonde(a_s, T) @ B_s))
+    if f_sym <= history[-1] * (1 + 1e-9) and f_sym <= history[0] * (1 + 1e-12):
+        alpha_h, B_h = a_s, B_s
+    if timings is not None:
+        timings["lm_s"] = time.perf_counter() - t0
+    plan = pair_plan(alpha_h)
+    Bt = torch.as_tensor(B_h.T.copy(), device=dev)                          # r x r
+    if basis.Umap is not None:
+        basis.A = None                                                       # release Q
     with stage("optdmd.modes_total"):
         modes = _modes_pass(U, Bt, plan, 0, data.shard, tdt, timings, a_orthonormal=True)
     model = ReducedModel(None, plan.lam, Sv, data.dt, grid_meta=data.grid_meta,

@@ -15,7 +15,7 @@ class CpuOps:
     def __init__(self):
         self.launches = 0
 
-    def tall_gemm(self, A, B, C, stats=False, row_offset=0, alg_flops=None, upper=False):
+    def tall_gemm(self, A, B, C, stats=False, row_offset=0, alg_flops=None, upper=False, share_sms=False):
         K = B.shape[0]
         Av = _logical(A).to(torch.float64)
         if Av.shape[1] < K:  # row-major buffers may be multiplied over padded columns
@@ -77,6 +77,6 @@ class CpuOps:
         e = Sv[:, 1:T + 1] - rec
         return torch.tensor([float((e * e).sum()), float((Sv[:, 1:T + 1] ** 2).sum())], dtype=torch.float64)
 
-    def geev(self, K):
+    def geev(self, K, vectors=True):
         w, V = np.linalg.eig(K.to(torch.float64).cpu().numpy())
-        return w, V
+        return (w, V) if vectors else (w, None)
