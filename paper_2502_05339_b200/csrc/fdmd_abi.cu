@@ -144,7 +144,10 @@ int launch_tg_tma(const fdmd::TallGemmArgs& a, cudaStream_t s, int& grid_x, bool
   CUDA_TRY(cudaMemsetAsync(Bp, 0, sizeof(double) * Kp * ldbp, s));
   CUDA_TRY(cudaMemcpy2DAsync(Bp, ldbp * sizeof(double), a.B, a.ldb * sizeof(double), a.N * sizeof(double), a.K,
                              cudaMemcpyDeviceToDevice, s));
-  fdmd::TTArgs ta{a, Bp, ldbp};
+  fdmd::TTArgs ta{a, Bp, ldbp, {NF, NF, NF, NF}};
+  const int nb = (a.N + 7) / 8;
+  if (gy == 1 && NF > 1 && nb >= 4 * (NF - 1) && nb < 4 * NF)   // e.g. N = 200: 7,6,6,6 blocks
+    for (int q = 0; q < 4; ++q) ta.wblk[q] = nb / 4 + (q < nb % 4 ? 1 : 0);
   auto kern = fdmd::tall_gemm_tma_kernel<TA, AL, NF, TC, CL, ST>;
   const int smem = (int)sizeof(fdmd::TTSmem<TA, AL, NF>);
   static thread_local int configured = -1;

@@ -1,7 +1,10 @@
-// Warp-specialised tall_gemm: one producer warp feeds a STAGES-deep ring with
-// TMA (A: 2-D tensor tiles, zero-filled out of bounds) and bulk copies (B: one
-// 1-D copy per k-row into padded smem rows); 8 consumer warps wait on full
-// mbarriers, run LDS + DMMA only, and release stages through empty mbarriers.
+// TMA-fed tall_gemm: a STAGES-deep ring of (64-row A tile, 16 k) chunks filled
+// by TMA (A: 2-D tensor tiles, zero-filled out of bounds) and bulk copies (B:
+// one 1-D copy per k-row into padded smem rows); 8 warps wait on full
+// mbarriers, run LDS + DMMA, and release stages through empty mbarriers.
+// Lane 0 of warp 0 refills each stage once all 8 warps released it — no
+// dedicated producer warp: a 9th warp puts 3 warps on one SM sub-partition
+// and caps registers at 168 (the 7-block accumulator tile spilled).
 // Included by fdmd_kernels.cu after fdmd_tall.cuh (shares tg::, dmma884).
 #pragma once
 #include <cuda.h>
@@ -65,76 +68,49 @@ struct TTArgs {
   TallGemmArgs g;
   const double* Bp;   // padded small operand, Kp x ldbp (Kp multiple of BK, ldbp >= gridDim.y*BN)
   int64_t ldbp;
+  int wblk[4];        // 8-column blocks per warp column group (NF or NF-1; sum covers N)
 };
 
-template <typename TA, int A_LAYOUT, int NF, typename TC, int C_LAYOUT, bool STATS>
-__global__ void __launch_bounds__(tt::THREADS, 1)
-tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) {
-  using S = TTSmem<TA, A_LAYOUT, NF>;
-  constexpr int BN = S::BN;
-  constexpr int LDB = S::LDB;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  S& sm = *reinterpret_cast<S*>(smem_raw);
-  const TallGemmArgs& args = ta.g;
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int n0 = blockIdx.y * BN;
-  const int64_t ntiles = (args.n + tt::BM - 1) / tt::BM;
-  const int nk = (args.K + tt::BK - 1) / tt::BK;
-  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const int64_t total = my_tiles * nk;
-
-  if (tid == 0) {
-    for (int s = 0; s < tt::STAGES; ++s) {
-      mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], tt::CONSUMERS / 32);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  if (warp == tt::CONSUMERS / 32) {
-    // ============================ producer ============================
-    if (lane == 0) {
-      constexpr unsigned A_BYTES = tt::BM * tt::BK * sizeof(TA);
-      constexpr unsigned B_ROW = BN * sizeof(double);
-      int s = 0, kc = 0;
-      unsigned phase = 0;
-      int64_t tile = blockIdx.x;
-      for (int64_t it = 0; it < total; ++it) {
-        mbar_wait(&sm.empty[s], phase ^ 1);
-        mbar_expect_tx(&sm.full[s], A_BYTES + tt::BK * B_ROW);
-        const int k0 = kc * tt::BK;
-        if (A_LAYOUT == LAYOUT_ROW)
-          tma_load_2d(sm.A[s], &amap, k0, (int)(tile * tt::BM), &sm.full[s]);
-        else
-          tma_load_2d(sm.A[s], &amap, (int)(tile * tt::BM), k0, &sm.full[s]);
+template <typename S, int A_LAYOUT> struct TTFeed {
+  const CUtensorMap* amap;
+  const double* Bp;
+  int64_t ldbp;
+  int n0;
+  __device__ __forceinline__ void issue(S& sm, int s, int64_t tile, int kc) const {
+    constexpr unsigned A_BYTES = tt::BM * tt::BK * sizeof(sm.A[0][0]);
+    constexpr unsigned B_ROW = S::BN * sizeof(double);
+    mbar_expect_tx(&sm.full[s], A_BYTES + tt::BK * B_ROW);
+    const int k0 = kc * tt::BK;
+    if (A_LAYOUT == LAYOUT_ROW)
+      tma_load_2d(sm.A[s], amap, k0, (int)(tile * tt::BM), &sm.full[s]);
+    else
+      tma_load_2d(sm.A[s], amap, (int)(tile * tt::BM), k0, &sm.full[s]);
 #pragma unroll 4
-        for (int kk = 0; kk < tt::BK; ++kk)
-          bulk_load(&sm.B[s][kk][0], ta.Bp + (int64_t)(k0 + kk) * ta.ldbp + n0, B_ROW, &sm.full[s]);
-        if (++s == tt::STAGES) { s = 0; phase ^= 1; }
-        if (++kc == nk) { kc = 0; tile += gridDim.x; }
-      }
-    }
-    return;
+    for (int kk = 0; kk < tt::BK; ++kk)
+      bulk_load(&sm.B[s][kk][0], Bp + (int64_t)(k0 + kk) * ldbp + n0, B_ROW, &sm.full[s]);
   }
+};
 
-  // ============================ consumers ============================
-  // SM sub-partition = warp & 3; pairing column block wn with 3 - wn on each
-  // sub-partition balances the DMMA work when B is upper triangular.
-  const int wm = warp >> 2, wn = (wm == 0) ? (warp & 3) : 3 - (warp & 3);
+// One consumer warp: rows wm*32..+32 of each 64-row tile, NFW 8-col blocks
+// starting at column wcol0 (NFW = NF, or NF - 1 when N is not a multiple of 32*NF:
+// e.g. N = 200 -> 7,6,6,6 blocks instead of 4 x 7 with 24 padding columns).
+template <typename S, typename TA, int A_LAYOUT, int NFW, typename TC, int C_LAYOUT, bool STATS>
+__device__ __forceinline__ void tt_consume(S& sm, const TallGemmArgs& args, const TTFeed<S, A_LAYOUT>& fd,
+                                           bool feeder, int64_t total, int nk, int wm, int wn, int wcol0,
+                                           int bcol0, int lane) {
   const int g = lane >> 2, t = lane & 3;
-  const int wcol0 = n0 + wn * 8 * NF;
+  // feeder: coordinates of the next chunk to load (item it + STAGES)
+  int64_t p_tile = blockIdx.x + (int64_t)(tt::STAGES / nk) * gridDim.x;
+  int p_kc = tt::STAGES % nk;
   // upper-triangular B (B[k][j] = 0 for k > j): k-chunks past this warp's last
   // column contribute nothing and are skipped (still consumed from the ring)
-  const int kc_last = args.b_upper ? (wcol0 + 8 * NF - 1) / tt::BK : INT32_MAX;
-  double st_sum[NF], st_max[NF];
-  int64_t st_idx[NF];
+  const int kc_last = args.b_upper ? (wcol0 + 8 * NFW - 1) / tt::BK : INT32_MAX;
+  double st_sum[NFW], st_max[NFW];
+  int64_t st_idx[NFW];
 #pragma unroll
-  for (int f = 0; f < NF; ++f) { st_sum[f] = 0.0; st_max[f] = -1.0; st_idx[f] = INT64_MAX; }
+  for (int f = 0; f < NFW; ++f) { st_sum[f] = 0.0; st_max[f] = -1.0; st_idx[f] = INT64_MAX; }
 
-  double acc[4][NF][2];
+  double acc[4][NFW][2];
   int s = 0, kc = 0;
   unsigned phase = 0;
   int64_t tile = blockIdx.x;
@@ -143,29 +119,36 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int f = 0; f < NF; ++f) acc[mi][f][0] = acc[mi][f][1] = 0.0;
+        for (int f = 0; f < NFW; ++f) acc[mi][f][0] = acc[mi][f][1] = 0.0;
     }
     mbar_wait(&sm.full[s], phase);
     const TA* As = sm.A[s];
     if (kc <= kc_last) {
 #pragma unroll
-    for (int ks = 0; ks < tt::BK / 4; ++ks) {
-      double a[4], b[NF];
+      for (int ks = 0; ks < tt::BK / 4; ++ks) {
+        double a[4], b[NFW];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const int m = wm * 32 + mi * 8 + g, k = ks * 4 + t;
-        a[mi] = (double)(A_LAYOUT == LAYOUT_ROW ? As[m * tt::BK + k] : As[k * tt::BM + m]);
+        for (int mi = 0; mi < 4; ++mi) {
+          const int m = wm * 32 + mi * 8 + g, k = ks * 4 + t;
+          a[mi] = (double)(A_LAYOUT == LAYOUT_ROW ? As[m * tt::BK + k] : As[k * tt::BM + m]);
+        }
+#pragma unroll
+        for (int f = 0; f < NFW; ++f) b[f] = sm.B[s][ks * 4 + t][bcol0 + f * 8 + g];
+#pragma unroll
+        for (int f = 0; f < NFW; ++f)
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) dmma884(acc[mi][f], a[mi], b[f]);
       }
-#pragma unroll
-      for (int f = 0; f < NF; ++f) b[f] = sm.B[s][ks * 4 + t][wn * 8 * NF + f * 8 + g];
-#pragma unroll
-      for (int f = 0; f < NF; ++f)
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) dmma884(acc[mi][f], a[mi], b[f]);
-    }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[s]);
+    if (feeder && it + tt::STAGES < total) {
+      if (lane == 0) {
+        mbar_wait(&sm.empty[s], phase);
+        fd.issue(sm, s, p_tile, p_kc);
+      }
+      if (++p_kc == nk) { p_kc = 0; p_tile += gridDim.x; }
+    }
     if (kc == nk - 1) {
       const int64_t row0 = tile * tt::BM;
       TC* __restrict__ C = static_cast<TC*>(args.C);
@@ -174,7 +157,7 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
         const int64_t row = row0 + wm * 32 + mi * 8 + g;
         if (row < args.n) {
 #pragma unroll
-          for (int f = 0; f < NF; ++f) {
+          for (int f = 0; f < NFW; ++f) {
             const int col = wcol0 + f * 8 + 2 * t;
             if (C != nullptr && !(args.debug & 2)) {
               if (C_LAYOUT == LAYOUT_ROW) {
@@ -205,7 +188,7 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
 
   if (STATS) {
 #pragma unroll
-    for (int f = 0; f < NF; ++f) {
+    for (int f = 0; f < NFW; ++f) {
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) {
         const double os = __shfl_xor_sync(0xffffffffu, st_sum[f], off);
@@ -217,18 +200,85 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
     }
     if (g == 0) {
 #pragma unroll
-      for (int f = 0; f < NF; ++f) {
+      for (int f = 0; f < NFW; ++f) {
         const int u = f * 4 + t;
         sm.red[wm][wn][u][0] = st_sum[f];
         sm.red[wm][wn][u][1] = st_max[f];
         sm.red[wm][wn][u][2] = __longlong_as_double((long long)st_idx[f]);
       }
     }
-    // consumers only (the producer warp has exited): named barrier 1
-    asm volatile("bar.sync 1, %0;\n" ::"n"(tt::CONSUMERS));
-    const int units_cta = BN / 2;
+  }
+}
+
+template <typename TA, int A_LAYOUT, int NF, typename TC, int C_LAYOUT, bool STATS>
+__global__ void __launch_bounds__(tt::THREADS, 1)
+tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) {
+  using S = TTSmem<TA, A_LAYOUT, NF>;
+  constexpr int BN = S::BN;
+  constexpr int LDB = S::LDB;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
+  const TallGemmArgs& args = ta.g;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int n0 = blockIdx.y * BN;
+  const int64_t ntiles = (args.n + tt::BM - 1) / tt::BM;
+  const int nk = (args.K + tt::BK - 1) / tt::BK;
+  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t total = my_tiles * nk;
+
+  if (tid == 0) {
+    for (int s = 0; s < tt::STAGES; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], tt::CONSUMERS / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const TTFeed<S, A_LAYOUT> fd{&amap, ta.Bp, ta.ldbp, n0};
+  if (warp == tt::CONSUMERS / 32) {
+    // ============================ producer ============================
+    if (lane == 0) {
+      int s = 0, kc = 0;
+      unsigned phase = 0;
+      int64_t tile = blockIdx.x;
+      for (int64_t it = 0; it < total; ++it) {
+        mbar_wait(&sm.empty[s], phase ^ 1);
+        fd.issue(sm, s, tile, kc);
+        if (++s == tt::STAGES) { s = 0; phase ^= 1; }
+        if (++kc == nk) { kc = 0; tile += gridDim.x; }
+      }
+    }
+    return;
+  }
+  const bool feeder = false;
+
+  // ============================ consumers ============================
+  // SM sub-partition = warp & 3; pairing column group wn with 3 - wn on each
+  // sub-partition balances the DMMA work when B is upper triangular or the
+  // groups have unequal widths.
+  const int wm = warp >> 2, wn = (wm == 0) ? (warp & 3) : 3 - (warp & 3);
+  // prefix sums of the group widths without dynamic indexing (no local memory)
+  const int w0 = ta.wblk[0], w1 = ta.wblk[1], w2 = ta.wblk[2], w3 = ta.wblk[3];
+  const int b1 = w0, b2 = w0 + w1, b3 = w0 + w1 + w2, b4 = b3 + w3;
+  const int my_blk = wn == 0 ? w0 : wn == 1 ? w1 : wn == 2 ? w2 : w3;
+  const int bcol0 = 8 * (wn == 0 ? 0 : wn == 1 ? b1 : wn == 2 ? b2 : b3);
+  const int wcol0 = n0 + bcol0;
+  if (my_blk == NF)
+    tt_consume<S, TA, A_LAYOUT, NF, TC, C_LAYOUT, STATS>(sm, args, fd, feeder, total, nk, wm, wn, wcol0, bcol0,
+                                                         lane);
+  else
+    tt_consume<S, TA, A_LAYOUT, (NF > 1 ? NF - 1 : 1), TC, C_LAYOUT, STATS>(sm, args, fd, feeder, total, nk, wm,
+                                                                            wn, wcol0, bcol0, lane);
+
+  if (STATS) {
+    asm volatile("bar.sync 1, %0;\n" ::"n"(tt::CONSUMERS));   // consumers only (producer exited)
+    const int units_cta = 4 * b4;
     for (int e = tid; e < units_cta; e += tt::CONSUMERS) {
-      const int wn_ = e / (4 * NF), u = e % (4 * NF);
+      const int wn_ = (e >= 4 * b1) + (e >= 4 * b2) + (e >= 4 * b3);
+      const int u = e - 4 * (wn_ == 0 ? 0 : wn_ == 1 ? b1 : wn_ == 2 ? b2 : b3);
       double s0 = sm.red[0][wn_][u][0], m0 = sm.red[0][wn_][u][1];
       long long i0 = __double_as_longlong(sm.red[0][wn_][u][2]);
       const double s1 = sm.red[1][wn_][u][0], m1 = sm.red[1][wn_][u][1];
