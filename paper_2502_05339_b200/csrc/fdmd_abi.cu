@@ -124,16 +124,19 @@ int launch_tg_tma(const fdmd::TallGemmArgs& a, cudaStream_t s, int& grid_x, bool
   CUtensorMap map;
   cuuint64_t dims[2], strides[1];
   cuuint32_t box[2], estr[2] = {1, 1};
+  // swizzled boxes (layout in fdmd_tall_tma.cuh: TTSmem / tt_a_offset)
+  CUtensorMapSwizzle swz;
   if (AL == fdmd::LAYOUT_ROW) {
     dims[0] = (cuuint64_t)a.K; dims[1] = (cuuint64_t)a.n; box[0] = fdmd::tt::BK; box[1] = fdmd::tt::BM;
+    swz = elt == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   } else {
-    dims[0] = (cuuint64_t)a.n; dims[1] = (cuuint64_t)a.K; box[0] = fdmd::tt::BM; box[1] = fdmd::tt::BK;
+    dims[0] = (cuuint64_t)a.n; dims[1] = (cuuint64_t)a.K; box[0] = (cuuint32_t)(128 / elt); box[1] = fdmd::tt::BK;
+    swz = CU_TENSOR_MAP_SWIZZLE_128B;
   }
   strides[0] = (cuuint64_t)(a.lda * elt);
   CUresult r = encode(&map, elt == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
                       const_cast<void*>(a.A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return FDMD_OK;  // unsupported shape: ring kernel
   constexpr int BN = 32 * NF;
   const int gy = (a.N + BN - 1) / BN;
@@ -149,7 +152,7 @@ int launch_tg_tma(const fdmd::TallGemmArgs& a, cudaStream_t s, int& grid_x, bool
   if (gy == 1 && NF > 1 && nb >= 4 * (NF - 1) && nb < 4 * NF)   // e.g. N = 200: 7,6,6,6 blocks
     for (int q = 0; q < 4; ++q) ta.wblk[q] = nb / 4 + (q < nb % 4 ? 1 : 0);
   auto kern = fdmd::tall_gemm_tma_kernel<TA, AL, NF, TC, CL, ST>;
-  const int smem = (int)sizeof(fdmd::TTSmem<TA, AL, NF>);
+  const int smem = (int)sizeof(fdmd::TTSmem<TA, AL, NF>) + 1024;   // + alignment slack
   static thread_local int configured = -1;
   int dev = 0;
   cudaGetDevice(&dev);

@@ -17,8 +17,11 @@ namespace tt {
 constexpr int BM = 64;
 constexpr int BK = 16;
 constexpr int STAGES = 4;
-constexpr int CONSUMERS = 256;          // 8 warps, 2 (M) x 4 (N)
-constexpr int THREADS = CONSUMERS + 32;  // + producer warp
+constexpr int CONSUMERS = 256;          // 8 warps (2 warpgroups), 2 (M) x 4 (N)
+constexpr int THREADS = CONSUMERS + 128; // + producer warpgroup (one lane issues; setmaxnreg moves its
+                                         //   registers to the consumers: 232 each instead of 168)
+constexpr int REG_CONSUMER = 232;   // 2 x 232 + 40 = 3 x 168 (the launch allocation)
+constexpr int REG_PRODUCER = 40;
 }  // namespace tt
 
 // ---------------------------------------------------------------- mbarrier --
@@ -55,14 +58,28 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
 
 template <typename TA, int AL, int NF> struct TTSmem {
   static constexpr int BN = 32 * NF;
-  static constexpr int LDB = BN + 4;                     // padded B rows (4 mod 16 doubles)
-  // A as written by TMA (dense box): ROW -> a[m][k] (BM x BK), COL -> a[k][m] (BK x BM)
-  TA A[tt::STAGES][tt::BM * tt::BK];
+  // B rows padded to 8 mod 16 doubles: k-rows t and t+1 land in opposite bank
+  // halves, so a b-fragment (4 rows x 8 columns) is 2 wavefronts (no conflict)
+  static constexpr int LDB = BN + 8;
+  // A as written by TMA with a swizzle (tt_a_offset): ROW -> [m][k] rows of
+  // BK elements (64-B / 128-B swizzle for f32 / f64); COL -> 128-B boxes of
+  // m, one 128-B row per k, 128-B swizzle. Both read conflict-free (f32 COL: 2-way).
+  alignas(1024) TA A[tt::STAGES][tt::BM * tt::BK];
   double B[tt::STAGES][tt::BK][LDB];
   double red[2][4][8 * NF / 2][3];
   uint64_t full[tt::STAGES];
   uint64_t empty[tt::STAGES];
 };
+
+// byte offset of A(m, k) inside a stage (see TTSmem)
+template <typename TA, int AL> __device__ __forceinline__ int tt_a_offset(int m, int k) {
+  if (AL == LAYOUT_ROW) {
+    if (sizeof(TA) == 8) return m * 128 + (((k >> 1) ^ (m & 7)) << 4) + (k & 1) * 8;
+    return m * 64 + (((k >> 2) ^ ((m >> 1) & 3)) << 4) + (k & 3) * 4;
+  }
+  if (sizeof(TA) == 8) return (m >> 4) * (tt::BK * 128) + k * 128 + ((((m & 15) >> 1) ^ (k & 7)) << 4) + (m & 1) * 8;
+  return (m >> 5) * (tt::BK * 128) + k * 128 + ((((m & 31) >> 2) ^ (k & 7)) << 4) + (m & 3) * 4;
+}
 
 struct TTArgs {
   TallGemmArgs g;
@@ -81,10 +98,15 @@ template <typename S, int A_LAYOUT> struct TTFeed {
     constexpr unsigned B_ROW = S::BN * sizeof(double);
     mbar_expect_tx(&sm.full[s], A_BYTES + tt::BK * B_ROW);
     const int k0 = kc * tt::BK;
-    if (A_LAYOUT == LAYOUT_ROW)
+    if (A_LAYOUT == LAYOUT_ROW) {
       tma_load_2d(sm.A[s], amap, k0, (int)(tile * tt::BM), &sm.full[s]);
-    else
-      tma_load_2d(sm.A[s], amap, (int)(tile * tt::BM), k0, &sm.full[s]);
+    } else {
+      constexpr int MB = 128 / (int)sizeof(sm.A[0][0]);        // m per 128-B box row
+#pragma unroll
+      for (int j = 0; j < tt::BM / MB; ++j)
+        tma_load_2d(reinterpret_cast<unsigned char*>(sm.A[s]) + j * tt::BK * 128, amap,
+                    (int)(tile * tt::BM) + j * MB, k0, &sm.full[s]);
+    }
 #pragma unroll 4
     for (int kk = 0; kk < tt::BK; ++kk)
       bulk_load(&sm.B[s][kk][0], Bp + (int64_t)(k0 + kk) * ldbp + n0, B_ROW, &sm.full[s]);
@@ -122,7 +144,7 @@ __device__ __forceinline__ void tt_consume(S& sm, const TallGemmArgs& args, cons
         for (int f = 0; f < NFW; ++f) acc[mi][f][0] = acc[mi][f][1] = 0.0;
     }
     mbar_wait(&sm.full[s], phase);
-    const TA* As = sm.A[s];
+    const unsigned char* As = reinterpret_cast<const unsigned char*>(sm.A[s]);
     if (kc <= kc_last) {
 #pragma unroll
       for (int ks = 0; ks < tt::BK / 4; ++ks) {
@@ -130,7 +152,7 @@ __device__ __forceinline__ void tt_consume(S& sm, const TallGemmArgs& args, cons
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
           const int m = wm * 32 + mi * 8 + g, k = ks * 4 + t;
-          a[mi] = (double)(A_LAYOUT == LAYOUT_ROW ? As[m * tt::BK + k] : As[k * tt::BM + m]);
+          a[mi] = (double)*reinterpret_cast<const TA*>(As + tt_a_offset<TA, A_LAYOUT>(m, k));
         }
 #pragma unroll
         for (int f = 0; f < NFW; ++f) b[f] = sm.B[s][ks * 4 + t][bcol0 + f * 8 + g];
@@ -217,7 +239,7 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
   constexpr int BN = S::BN;
   constexpr int LDB = S::LDB;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  S& sm = *reinterpret_cast<S*>(smem_raw);
+  S& sm = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const TallGemmArgs& args = ta.g;
 
   const int tid = threadIdx.x;
@@ -238,9 +260,10 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
   __syncthreads();
 
   const TTFeed<S, A_LAYOUT> fd{&amap, ta.Bp, ta.ldbp, n0};
-  if (warp == tt::CONSUMERS / 32) {
+  if (warp >= tt::CONSUMERS / 32) {
     // ============================ producer ============================
-    if (lane == 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(tt::REG_PRODUCER));
+    if (warp == tt::CONSUMERS / 32 && lane == 0) {
       int s = 0, kc = 0;
       unsigned phase = 0;
       int64_t tile = blockIdx.x;
@@ -254,6 +277,7 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
     return;
   }
   const bool feeder = false;
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(tt::REG_CONSUMER));
 
   // ============================ consumers ============================
   // SM sub-partition = warp & 3; pairing column group wn with 3 - wn on each
