@@ -134,9 +134,10 @@ class CudaOps:
         e.record()
         return e
 
-    def _done(self, name, flops, e0):
+    def _done(self, name, flops, e0, nbytes=0.0):
+        """Record (name, algorithmic flops, ev0, ev1, algorithmic HBM bytes)."""
         if e0 is not None:
-            self.profile.append((name, float(flops), e0, self._ev()))
+            self.profile.append((name, float(flops), e0, self._ev(), float(nbytes)))
 
     # -- C[n x N] = A * B (B small fp64, K x N) ---------------------------
     def tall_gemm(self, A: Tall, B: torch.Tensor, C: Optional[Tall], stats: bool = False,
@@ -162,7 +163,9 @@ class CudaOps:
                                      _ptr(c_buf), c_dt, c_lay, c_ld, A.n, K, N,
                                      (1 if upper else 0) | (2 if share_sms else 0),
                                      _ptr(st), row_offset, _ptr(ws), wsb, _stream()), "tall_gemm")
-        self._done("tall_gemm", 2.0 * A.n * K * N if alg_flops is None else alg_flops, e0)
+        # algorithmic bytes: A read once, C written once (in place: read + write)
+        nb = A.n * K * A.buf.element_size() + (A.n * N * C.buf.element_size() if C is not None else 0)
+        self._done("tall_gemm", 2.0 * A.n * K * N if alg_flops is None else alg_flops, e0, nb)
         self.launches += 2 if stats else 1
         return st
 
@@ -183,7 +186,8 @@ class CudaOps:
                                      1 if symmetric else 0, _ptr(ws), wsb, _stream()), "tall_gram")
         if alg_flops is None:
             alg_flops = (1.0 if symmetric else 2.0) * A.n * K1 * K2
-        self._done("tall_gram", alg_flops, e0)
+        nb = A.n * (K1 * A.buf.element_size() + (0 if symmetric else K2 * B.buf.element_size()))
+        self._done("tall_gram", alg_flops, e0, nb)
         self.launches += 2
         return out
 
