@@ -144,8 +144,9 @@ tall_gram_panel_kernel(const __grid_constant__ CUtensorMap amap, const __grid_co
                        const __grid_constant__ TallGramPanelArgs pa) {
   const TallGramArgs& args = pa.g;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* base =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting the __shared__ array itself (keeps the shared window:
+  // LDS, not generic LD, for every fragment load)
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   PanelFeed fd;
   fd.amap = &amap;
   fd.bmap = &bmap;

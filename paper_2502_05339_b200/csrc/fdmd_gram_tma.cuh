@@ -61,7 +61,7 @@ tall_gram_sw_kernel(const __grid_constant__ CUtensorMap amap, const __grid_const
   using SB = SwOperand<TB, TN>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TGSSmem<TA, TB, NFB>& sm =
-      *reinterpret_cast<TGSSmem<TA, TB, NFB>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+      *reinterpret_cast<TGSSmem<TA, TB, NFB>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
 
   int ti, tj;
   if (args.symmetric && TN == tgs::TM) {   // square tiles: enumerate the upper triangle only

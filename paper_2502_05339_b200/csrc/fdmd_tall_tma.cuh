@@ -58,9 +58,10 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
 
 template <typename TA, int AL, int NF> struct TTSmem {
   static constexpr int BN = 32 * NF;
-  // B rows padded to 8 mod 16 doubles: k-rows t and t+1 land in opposite bank
-  // halves, so a b-fragment (4 rows x 8 columns) is 2 wavefronts (no conflict)
-  static constexpr int LDB = BN + 8;
+  // B rows padded to 4 mod 16 doubles: 64-bit loads are served per half-warp
+  // (lanes g = 0..3 or 4..7, t = 0..3); rows t then start 8 banks apart and a
+  // half-warp's 16 doubles cover all 32 banks once (no conflict)
+  static constexpr int LDB = BN + 4;
   // A as written by TMA with a swizzle (tt_a_offset): ROW -> [m][k] rows of
   // BK elements (64-B / 128-B swizzle for f32 / f64); COL -> 128-B boxes of
   // m, one 128-B row per k, 128-B swizzle. Both read conflict-free (f32 COL: 2-way).
@@ -239,7 +240,8 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
   constexpr int BN = S::BN;
   constexpr int LDB = S::LDB;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  S& sm = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting the __shared__ array (keeps LDS addressing)
+  S& sm = *reinterpret_cast<S*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const TallGemmArgs& args = ta.g;
 
   const int tid = threadIdx.x;

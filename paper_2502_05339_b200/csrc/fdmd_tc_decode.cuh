@@ -98,7 +98,7 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
                  const TCArgs args) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // align the SW128 atoms to 1024 B
-  TCSmem& sm = *reinterpret_cast<TCSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  TCSmem& sm = *reinterpret_cast<TCSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkc = (args.r + tc::BKC - 1) / tc::BKC;
   const int ksteps_last = ((args.r - (nkc - 1) * tc::BKC) + 15) / 16;   // valid 16-wide steps in last chunk
