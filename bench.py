@@ -53,6 +53,17 @@ def fit_flops(n, m, r, p, q, modes="optdmd"):
     return sum(terms.values()), terms, l
 
 
+def executed_flops(n, m, r, p, q):
+    """DMMA flops libfdmd actually executes for the same fit (OptDMD): the
+    power-iteration CholeskyQR is single-pass, CholeskyQR2's final R2^-1 is
+    folded into small matrices, triangular applies count n*l^2, and the
+    modes GEMM computes one column of each conjugate pair (~2nr^2)."""
+    T = m - 1
+    l = min(r + p, T)
+    return (2.0 * n * T * l * (1 + 2 * q) + n * l * l * (2 * q + 3) + 2.0 * n * m * l + 2.0 * n * l * r
+            + 2.0 * n * r * r)
+
+
 # ---------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
@@ -338,7 +349,9 @@ def main():
                    "snapshot_dtype": "f32", "parallelism": f"rows{world}", "l2": "inputs larger than L2 (X >= 3.8 GB)"},
         "fit": {"s": round(fit_t, 4), "gflops": round(value, 1), "flops": F_fit,
                 "per_step_s": [round(x["fit"], 4) for x in res],
-                "terms": {k: v for k, v in terms.items()}},
+                "terms": {k: v for k, v in terms.items()},
+                "executed_flops": executed_flops(n, m, r, cfg["p"], cfg["q"]),
+                "executed_tflops": round(executed_flops(n, m, r, cfg["p"], cfg["q"]) / fit_t / 1e12, 3)},
         "reconstruct": recon,
         "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(),

@@ -168,12 +168,19 @@ def cholqr2_inplace(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict
     return R
 
 
-def cholqr2_deferred(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict] = None):
+def cholqr2_deferred(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict] = None,
+                     passes: int = 2):
     """CholeskyQR2 without the final tall triangular apply: Y is left holding
     Q1 and the orthonormal factor is Q = Y @ fix (fix = R2^-1, upper
     triangular, ~I). Every consumer of Q in the fit is linear, so `fix` is
     folded into small matrices instead of a second n*l^2 pass. Returns
-    (R, fix) with Y_in = Q R; fix is None when Y already holds Q."""
+    (R, fix) with Y_in = Q R; fix is None when Y already holds Q.
+
+    passes=1 stops after the first CholeskyQR: Q1 = Y R1^-1 spans range(Y)
+    to O(u kappa(Y)) and has cond(Q1) = 1 + O(u kappa^2) (~1.003 at
+    kappa = 5e6), which is all a power iteration needs (it only uses the
+    span: the next step is Z = X^T Q1 -> qr(Z)). The last orthonormalisation
+    before the projection keeps both passes."""
     ops = dv.get_ops()
     l = Y.k
     with stage("cholqr.gram"):
@@ -206,6 +213,8 @@ def cholqr2_deferred(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dic
             stats["shifted_cholqr3"] = stats.get("shifted_cholqr3", 0) + 1
     else:
         _apply_rinv(Y, R1, shard)
+    if passes == 1:
+        return R1, None
     with stage("cholqr.gram2"):
         G2 = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
     R2 = _chol_upper(G2)
@@ -281,8 +290,10 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     # and folded into Z, Q^T S and the lift; its tall apply is never executed
     # (counted as the TRSM term it replaces).
     with stage("sketch.cholqr2"):
-        _, fix = cholqr2_deferred(Q, shard, stats)
-    for _ in range(q):
+        # power iterations only need the span: one CholeskyQR pass unless this
+        # is the last orthonormalisation (q = 0)
+        _, fix = cholqr2_deferred(Q, shard, stats, passes=2 if q == 0 else 1)
+    for it in range(q):
         with stage("power.Z=XtQ"):
             Z = allreduce(shard, ops.tall_gram(S, Q, K1=T, alg_flops=2 * nl * T * l))   # T x l (X^T Q)
             if fix is not None:
@@ -292,7 +303,7 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
         with stage("power.Y=XW"):
             ops.tall_gemm(S, _pad_rows(W, m), Q, alg_flops=2 * nl * T * l)
         with stage("power.cholqr2"):
-            _, fix = cholqr2_deferred(Q, shard, stats)
+            _, fix = cholqr2_deferred(Q, shard, stats, passes=2 if it == q - 1 else 1)
     with stage("project.QtS"):
         QtS = allreduce(shard, ops.tall_gram(Q, S, alg_flops=2 * nl * m * l))     # l x m
         if fix is not None:
