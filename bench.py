@@ -55,12 +55,14 @@ def fit_flops(n, m, r, p, q, modes="optdmd"):
 
 def executed_flops(n, m, r, p, q):
     """DMMA flops libfdmd actually executes for the same fit (OptDMD): the
-    power-iteration CholeskyQR is single-pass, CholeskyQR2's final R2^-1 is
-    folded into small matrices, triangular applies count n*l^2, and the
-    modes GEMM computes one column of each conjugate pair (~2nr^2)."""
+    power-iteration CholeskyQR is one SYRK with R1^-1 folded into Z,
+    CholeskyQR2's final R2^-1 is folded into small matrices, triangular
+    applies count n*l^2, and the modes GEMM computes one column of each
+    conjugate pair (~2nr^2)."""
     T = m - 1
     l = min(r + p, T)
-    return (2.0 * n * T * l * (1 + 2 * q) + n * l * l * (2 * q + 3) + 2.0 * n * m * l + 2.0 * n * l * r
+    # power stages: one SYRK (n l^2) each, R1^-1 folded into Z; final: SYRK + TRSM + SYRK
+    return (2.0 * n * T * l * (1 + 2 * q) + n * l * l * (q + 3) + 2.0 * n * m * l + 2.0 * n * l * r
             + 2.0 * n * r * r)
 
 

@@ -179,7 +179,8 @@ def cholqr2_deferred(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dic
     passes=1 stops after the first CholeskyQR: Q1 = Y R1^-1 spans range(Y)
     to O(u kappa(Y)) and has cond(Q1) = 1 + O(u kappa^2) (~1.003 at
     kappa = 5e6), which is all a power iteration needs (it only uses the
-    span: the next step is Z = X^T Q1 -> qr(Z)). The last orthonormalisation
+    span: the next step is Z = X^T Q1 -> qr(Z)); Q1 is not even formed
+    (fix = R1^-1) unless the shifted variant ran. The last orthonormalisation
     before the projection keeps both passes."""
     ops = dv.get_ops()
     l = Y.k
@@ -211,6 +212,12 @@ def cholqr2_deferred(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dic
         R1 = R1b @ R0
         if stats is not None:
             stats["shifted_cholqr3"] = stats.get("shifted_cholqr3", 0) + 1
+    elif passes == 1:
+        # single pass, nothing applied to the tall buffer: Q1 = Y @ R1^-1 is
+        # left implicit (fix = R1^-1); X^T Q1 = (X^T Y) R1^-1 has the same
+        # O(u kappa(Y)) error as a product with an explicitly formed Q1
+        eye = torch.eye(l, dtype=torch.float64, device=R1.device)
+        return R1, torch.linalg.solve_triangular(R1, eye, upper=True)
     else:
         _apply_rinv(Y, R1, shard)
     if passes == 1:
