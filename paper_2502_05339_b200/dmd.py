@@ -255,11 +255,12 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
         raw = alloc_tall(n_loc, 2 * U, table_dtype, "col", device=dev)
     row0 = 0 if shard is None else shard.row0
     t0 = time.perf_counter()
-    # algorithmic count: real n x K times complex K x r (SURVEY §8d F_modes = 4 n K r);
-    # only one column of each conjugate pair is executed
+    # SURVEY §8d counts F_modes = 4 n K r (real n x K times complex K x r); only
+    # one column of each conjugate pair is executed, so the kernel is credited
+    # with its executed 2 n K (2U) flops (the fit-level metric keeps the formula)
     with stage("modes.raw+stats"):
         st = ops.tall_gemm(A, Bm, raw, stats=True, row_offset=row0,
-                           alg_flops=4.0 * n_loc * K * plan.lam.size)  # (U, 3)
+                           alg_flops=2.0 * n_loc * K * 2 * U)  # (U, 3)
     post = stage("modes.post")
     post.__enter__()
     st = la._reduce_pair_stats(st, shard)
