@@ -172,7 +172,8 @@ class CudaOps:
     # -- C[K1 x K2] = A^T B over n ----------------------------------------
     def tall_gram(self, A: Tall, B: Tall, K1: Optional[int] = None, K2: Optional[int] = None,
                   symmetric: bool = False, out: Optional[torch.Tensor] = None,
-                  alg_flops: Optional[float] = None) -> torch.Tensor:
+                  alg_flops: Optional[float] = None, beta: float = 0.0) -> torch.Tensor:
+        """out[K1 x K2] = beta * out + A^T B (fixed-order, deterministic)."""
         L = _lib.lib()
         K1 = A.k if K1 is None else K1
         K2 = B.k if K2 is None else K2
@@ -182,7 +183,7 @@ class CudaOps:
         ws = self.ws.get(wsb, A.buf.device)
         e0 = self._ev()
         _lib.check(L.fdmd_tall_gram(_ptr(A.buf), _DT[A.dtype], A.code, A.ld, _ptr(B.buf), _DT[B.dtype],
-                                     B.code, B.ld, _ptr(out), out.stride(0), 0.0, A.n, K1, K2,
+                                     B.code, B.ld, _ptr(out), out.stride(0), float(beta), A.n, K1, K2,
                                      1 if symmetric else 0, _ptr(ws), wsb, _stream()), "tall_gram")
         if alg_flops is None:
             alg_flops = (1.0 if symmetric else 2.0) * A.n * K1 * K2

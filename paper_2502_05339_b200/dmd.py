@@ -47,10 +47,17 @@ class SnapshotMatrix:
     HBM and is upcast exactly in-kernel, other dtypes become float64), a
     CUDA tensor, or an existing row-major ``Tall``. ``shard`` marks a row
     block of a row-sharded matrix (multi-GPU).
+
+    ``stream=True`` (host torch tensor, ideally pinned): the upload is
+    deferred and streamed in chunks by the first consumer — a randomized fit
+    overlaps it with its first sketch stage (linalg.PendingUpload); any other
+    access to ``S`` completes it first. The non-finite check then runs on
+    the device per chunk and raises ValueError from the consumer.
     """
 
     def __init__(self, states, dt, grid_meta=None, meta=None, *, shard: Optional[Shard] = None,
-                 device=None, check_finite=True):
+                 device=None, check_finite=True, stream=False):
+        self.pending = None
         if isinstance(states, Tall):
             S = states
         else:
@@ -60,14 +67,22 @@ class SnapshotMatrix:
                 shape = states.shape
             if len(shape) != 2 or shape[1] < 2:
                 raise ValueError("snapshot matrix needs at least 2 columns")
-            S = la.as_tall(states, device)
+            if stream and isinstance(states, torch.Tensor) and states.device.type == "cpu" and shape[0] > 0:
+                host = states if states.dtype in (torch.float32, torch.float64) else states.double()
+                S = alloc_tall(int(shape[0]), int(shape[1]), host.dtype, "row", device=device or dv.default_device())
+                if S.ld > S.k:
+                    S.buf[:, S.k:].zero_()
+                self.pending = la.PendingUpload(host, S)
+            else:
+                S = la.as_tall(states, device)
         if S.k < 2:
             raise ValueError("snapshot matrix needs at least 2 columns")
-        if check_finite and S.n > 0 and not bool(torch.isfinite(S.view()).all().item()):
+        if (self.pending is None and check_finite and S.n > 0
+                and not bool(torch.isfinite(S.view()).all().item())):
             raise ValueError("snapshot matrix contains non-finite entries")
         if not dt > 0:
             raise ValueError("dt must be positive")
-        self.S = S
+        self._S = S
         self.dt = float(dt)
         self.grid_meta = grid_meta
         self.meta = dict(meta or {})
@@ -75,12 +90,30 @@ class SnapshotMatrix:
         self._host = None
 
     @property
+    def S(self) -> Tall:
+        """The device matrix; completes a streamed upload first."""
+        if self.pending is not None:
+            p, self.pending = self.pending, None
+            p.run()
+        return self._S
+
+    @S.setter
+    def S(self, value: Tall):
+        self._S = value
+        self.pending = None
+
+    def take_pending(self):
+        """(device Tall, PendingUpload or None) for a consumer that streams."""
+        p, self.pending = self.pending, None
+        return self._S, p
+
+    @property
     def n(self):
-        return self.S.n if self.shard is None else self.shard.n_global
+        return self._S.n if self.shard is None else self.shard.n_global
 
     @property
     def n_transitions(self):
-        return self.S.k - 1
+        return self._S.k - 1
 
     @property
     def states(self):
@@ -425,7 +458,7 @@ class _Basis:
 
 def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, power_iters,
                timings: Optional[dict]) -> _Basis:
-    S = data.S
+    S, pending = data.take_pending() if svd_mode == "randomized" else (data.S, None)
     T = S.k - 1
     n_tot = data.n
     t0 = time.perf_counter()
@@ -438,7 +471,11 @@ def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, po
         if not 1 <= r <= min(n_tot, T):
             raise ValueError(f"rank {r} out of range [1, {min(n_tot, T)}]")
         omega = la.draw_omega(T, l, seed)
-        f = la.sketch_factors(S, T, l, q, omega, data.shard)
+        try:
+            f = la.sketch_factors(S, T, l, q, omega, data.shard, pending=pending)
+        except BaseException:
+            data.pending = pending      # a streamed upload that failed is redone by the next consumer
+            raise
         Ub_r = f.Ub[:, :r].contiguous()
         UtS = Ub_r.t() @ f.QtS
         basis = _Basis(f.Q, f.right(Ub_r).contiguous(), f.s[:r].contiguous(), f.Vh[:r].t().contiguous(),
@@ -493,7 +530,7 @@ def _residual_diag(data: SnapshotMatrix, modes: DeviceModes, lam: np.ndarray):
 
 
 def _default_table_dtype(data: SnapshotMatrix):
-    return data.S.dtype
+    return data._S.dtype
 
 
 # ---------------------------------------------------------------------------

@@ -94,6 +94,56 @@ def as_tall(M, device=None) -> Tall:
     return T
 
 
+class PendingUpload:
+    """A host snapshot matrix being streamed into a row-major device Tall.
+
+    The copy runs in ~512 MB row chunks on a copy stream (pinned host memory
+    -> contiguous staging buffer, double-buffered), each chunk re-pitched into
+    S on the compute stream; `run(on_chunk)` calls on_chunk(r0, rows) in
+    compute-stream order as soon as a chunk has landed, so row-separable work
+    (the first sketch stage) overlaps the rest of the transfer. Every chunk
+    is also checked for non-finite entries (SnapshotMatrix validation,
+    dmd.py:26-50): `run` raises ValueError once the upload completes."""
+
+    def __init__(self, host: torch.Tensor, S: Tall, chunk_bytes: int = 512 << 20):
+        self.host = host
+        self.S = S
+        self.k = int(host.shape[1])
+        self.chunk = max(1, chunk_bytes // (self.k * host.element_size()))
+
+    def run(self, on_chunk=None):
+        S, k, host = self.S, self.k, self.host
+        dev = S.buf.device
+        comp = torch.cuda.current_stream(dev)
+        copy = torch.cuda.Stream(device=dev)
+        rows = S.n
+        nst = min(self.chunk, rows)
+        staging = [torch.empty(nst * k, dtype=S.dtype, device=dev) for _ in range(2)]
+        freed = [None, None]
+        ok = torch.ones((), dtype=torch.bool, device=dev)
+        for i, r0 in enumerate(range(0, rows, self.chunk)):
+            rr = min(self.chunk, rows - r0)
+            b = i & 1
+            with torch.cuda.stream(copy):
+                if freed[b] is not None:
+                    copy.wait_event(freed[b])
+                staging[b][: rr * k].copy_(host[r0:r0 + rr].reshape(-1), non_blocking=True)
+                landed = torch.cuda.Event()
+                landed.record(copy)
+            comp.wait_event(landed)
+            dst = S.buf[r0:r0 + rr, :k]
+            dst.copy_(staging[b][: rr * k].view(rr, k))
+            ok &= torch.isfinite(dst).all()
+            freed[b] = torch.cuda.Event()
+            freed[b].record(comp)
+            if on_chunk is not None:
+                on_chunk(r0, rr)
+        for st in staging:
+            st.record_stream(comp)
+        if not bool(ok.item()):
+            raise ValueError("snapshot matrix contains non-finite entries")
+
+
 def copy_rows_h2d(T: Tall, t: torch.Tensor, row0: int = 0):
     """Copy a (rows x k) host/device tensor into rows [row0, row0+rows) of a
     row-major Tall with a pitched 2-D copy (no staging buffer)."""
@@ -169,7 +219,7 @@ def cholqr2_inplace(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict
 
 
 def cholqr2_deferred(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dict] = None,
-                     passes: int = 2):
+                     passes: int = 2, G: Optional[torch.Tensor] = None):
     """CholeskyQR2 without the final tall triangular apply: Y is left holding
     Q1 and the orthonormal factor is Q = Y @ fix (fix = R2^-1, upper
     triangular, ~I). Every consumer of Q in the fit is linear, so `fix` is
@@ -184,8 +234,9 @@ def cholqr2_deferred(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dic
     before the projection keeps both passes."""
     ops = dv.get_ops()
     l = Y.k
-    with stage("cholqr.gram"):
-        G = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
+    if G is None:   # (a streamed first stage hands in Y^T Y, already all-reduced)
+        with stage("cholqr.gram"):
+            G = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
     with stage("cholqr.chol+cond"):
         R1 = _chol_upper(G)
         if R1 is None:
@@ -274,13 +325,21 @@ def _pad_rows(Bsmall: torch.Tensor, rows: int) -> torch.Tensor:
     return out
 
 
+def _rows(T: Tall, r0: int, rr: int) -> Tall:
+    return Tall(T.buf[r0:r0 + rr], "row", rr, T.k)
+
+
 def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Optional[Shard] = None,
-                   Q: Optional[Tall] = None) -> SketchFactors:
+                   Q: Optional[Tall] = None, pending: Optional[PendingUpload] = None) -> SketchFactors:
     """Range finder + power passes + projection for X = S[:, :T].
 
     Kernel sequence (DESIGN.md §Fit pipeline): Y = S[Omega;0] -> CholQR2 ->
     q x {Z = S^T Q (allreduce) -> W = qr(Z[:T]) -> Y = S[W;0] -> CholQR2} ->
     Q^T S (allreduce) -> svd(Q^T X) on device.
+
+    With `pending` (S still streaming in from the host), the first stage —
+    Y = S[Omega;0], Y^T Y and X^T Y, all row-separable — runs chunk by chunk
+    as rows land, in the shadow of the host->device transfer.
     """
     ops = dv.get_ops()
     dev = S.buf.device
@@ -290,21 +349,43 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
         with stage("sketch.alloc_Q"):
             Q = alloc_tall(S.n, l, torch.float64, "row", device=dev)
     Om = torch.as_tensor(np.asarray(omega, dtype=np.float64), device=dev)
+    Omp = _pad_rows(Om, m)
     nl = float(S.n)
-    with stage("sketch.Y=XOmega"):
-        ops.tall_gemm(S, _pad_rows(Om, m), Q, alg_flops=2 * nl * T * l)
+    G0 = Zp = None
+    if pending is None:
+        with stage("sketch.Y=XOmega"):
+            ops.tall_gemm(S, Omp, Q, alg_flops=2 * nl * T * l)
+    else:
+        G0 = torch.zeros((l, l), dtype=torch.float64, device=dev)
+        Zp = torch.zeros((T, l), dtype=torch.float64, device=dev) if q > 0 else None
+
+        def first_stage(r0, rr):
+            Sc, Yc = _rows(S, r0, rr), _rows(Q, r0, rr)
+            ops.tall_gemm(Sc, Omp, Yc, alg_flops=2.0 * rr * T * l)
+            ops.tall_gram(Yc, Yc, symmetric=True, out=G0, beta=1.0)
+            if Zp is not None:
+                ops.tall_gram(Sc, Yc, K1=T, out=Zp, beta=1.0, alg_flops=2.0 * rr * T * l)
+
+        with stage("sketch.stream_upload+Y+G+XtY"):
+            pending.run(first_stage)
+        G0 = allreduce(shard, G0)
+        if Zp is not None:
+            Zp = allreduce(shard, Zp)
     # CholeskyQR2's final R2^-1 is kept as the small `fix` (Q = buffer @ fix)
     # and folded into Z, Q^T S and the lift; its tall apply is never executed
     # (counted as the TRSM term it replaces).
     with stage("sketch.cholqr2"):
         # power iterations only need the span: one CholeskyQR pass unless this
         # is the last orthonormalisation (q = 0)
-        _, fix = cholqr2_deferred(Q, shard, stats, passes=2 if q == 0 else 1)
+        _, fix = cholqr2_deferred(Q, shard, stats, passes=2 if q == 0 else 1, G=G0)
     for it in range(q):
         with stage("power.Z=XtQ"):
-            Z = allreduce(shard, ops.tall_gram(S, Q, K1=T, alg_flops=2 * nl * T * l))   # T x l (X^T Q)
-            if fix is not None:
-                Z = Z @ fix
+            if it == 0 and Zp is not None and fix is not None:
+                Z = Zp @ fix            # streamed X^T Y, buffer untouched (R1^-1 folded)
+            else:
+                Z = allreduce(shard, ops.tall_gram(S, Q, K1=T, alg_flops=2 * nl * T * l))   # T x l (X^T Q)
+                if fix is not None:
+                    Z = Z @ fix
         with stage("power.qr(Z)"):
             W, _ = torch.linalg.qr(Z[:T], mode="reduced")    # T x l (Householder, device)
         with stage("power.Y=XW"):

@@ -31,7 +31,7 @@ class CpuOps:
             _logical(C).copy_(P.to(C.dtype))
         return st
 
-    def tall_gram(self, A, B, K1=None, K2=None, symmetric=False, out=None, alg_flops=None):
+    def tall_gram(self, A, B, K1=None, K2=None, symmetric=False, out=None, alg_flops=None, beta=0.0):
         Av = _logical(A).to(torch.float64)
         Bv = _logical(B).to(torch.float64)
         K1 = A.k if K1 is None else K1
@@ -40,7 +40,7 @@ class CpuOps:
             Av = A.buf[:K1, : A.n].t().to(torch.float64)
         G = Av[:, :K1].t() @ Bv[:, :K2]
         if out is not None:
-            out.copy_(G)
+            out.copy_(G if beta == 0.0 else beta * out + G)
             return out
         return G.contiguous()
 

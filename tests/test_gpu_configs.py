@@ -109,3 +109,45 @@ def test_dmdc_against_oracle_and_truth(fd, noise):
                                    atol=1e-8)
         np.testing.assert_allclose(np.linalg.norm(model.provenance["B_tilde"], axis=0),
                                    np.linalg.norm(ref["B"], axis=0), rtol=1e-8)
+
+
+@pytest.mark.parametrize("q", [0, 1, 2])
+def test_streamed_upload_fit_matches_resident(fd, q):
+    """SnapshotMatrix(stream=True): the host->device transfer overlaps the
+    first sketch stage (Y, Y^T Y, X^T Y per chunk); results equal the
+    resident fit, and non-finite input raises ValueError from the fit."""
+    from paper_2502_05339_b200 import linalg as la
+    rng = np.random.default_rng(q)
+    n, m = 300_001, 41
+    X = (rng.standard_normal((n, 8)) @ rng.standard_normal((8, m))
+         + 1e-3 * rng.standard_normal((n, m))).astype(np.float32)
+    host = torch.from_numpy(X).pin_memory()
+    old = la.PendingUpload.__init__
+
+    def small_chunks(self, h, S, chunk_bytes=512 << 20):
+        old(self, h, S, chunk_bytes=3 << 20)     # many chunks at test size
+    la.PendingUpload.__init__ = small_chunks
+    try:
+        ds = fd.SnapshotMatrix(host, 0.1, stream=True)
+        assert ds.pending is not None
+        a = fd.exact_dmd(ds, 8, svd_mode="randomized", seed=2, oversample=10, power_iters=q, residual=False)
+        assert ds.pending is None
+        b = fd.exact_dmd(fd.SnapshotMatrix(X, 0.1), 8, svd_mode="randomized", seed=2, oversample=10,
+                         power_iters=q, residual=False)
+        assert match_eigs(a.lam, b.lam) <= 1e-10
+        np.testing.assert_allclose(a.sigma, b.sigma, rtol=1e-11)
+        o1 = fd.optdmd(fd.SnapshotMatrix(host, 0.1, stream=True), 8, svd_mode="randomized", seed=2,
+                       oversample=10, power_iters=q, lm_config=fd.LMConfig(max_iters=5))
+        o2 = fd.optdmd(fd.SnapshotMatrix(X, 0.1), 8, svd_mode="randomized", seed=2, oversample=10,
+                       power_iters=q, lm_config=fd.LMConfig(max_iters=5))
+        assert match_eigs(o1.lam, o2.lam) <= 1e-9
+        # S access completes a pending upload
+        d3 = fd.SnapshotMatrix(host, 0.1, stream=True)
+        np.testing.assert_array_equal(d3.S.view().cpu().numpy(), X)
+        Xb = X.copy()
+        Xb[123_456, 7] = np.nan
+        bad = fd.SnapshotMatrix(torch.from_numpy(Xb).pin_memory(), 0.1, stream=True)
+        with pytest.raises(ValueError, match="non-finite"):
+            fd.exact_dmd(bad, 8, svd_mode="randomized", seed=2, oversample=10, power_iters=q)
+    finally:
+        la.PendingUpload.__init__ = old
