@@ -106,7 +106,8 @@ int fdmd_residual(const void* S, int s_dtype, int64_t lds, const void* D, int d_
 /* Real nonsymmetric eigendecomposition (cuSOLVER Xgeev). A: n x n column-major
  * f64 (overwritten). Outputs: w_host (2n doubles: re, im interleaved),
  * vr_host (n x n column-major, LAPACK packing: a complex pair occupies columns
- * j (real part) and j+1 (imaginary part)). Synchronous. */
+ * j (real part) and j+1 (imaginary part)); vr_host = NULL computes the
+ * eigenvalues only (the OptDMD initial guess, dmd.py:387). Synchronous. */
 int fdmd_geev(int n, double* A, double* w_host, double* vr_host, void* stream);
 
 /* tcgen05 batched reconstruction (FP32-accurate 2-way FP16 split, see
