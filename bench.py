@@ -147,8 +147,8 @@ def run_reference(args, cfg):
         "warmup": args.warmup, "ms_per_step": round(tmed * 1e3, 1), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"config{cfg['cfg']} fit, row sample", "rows": res["rows"], "m": 201, "r": cfg["r"],
-                   "p": cfg["p"], "q": cfg["q"], "lm_iters": cfg["lm_iters"]},
+        "config": dict(arm_config(cfg, res["n"], res["m"], cfg["r"], res["l"], f"cpu{os.cpu_count()}threads"),
+                       sample_rows=res["rows"]),
         "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
                          "sample": res["sample"]},
         "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -156,15 +156,24 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def arm_config(cfg, n, m, r, l, parallelism):
+    """The workload both bench arms report (the reference arm adds sample_rows)."""
+    return {"workload": f"config{cfg['cfg']} fit (OptDMD, {cfg['lm_iters']} LM iters) + config4 reconstruct",
+            "n": n, "m": m, "r": r, "l": l, "p": cfg["p"], "q": cfg["q"], "grid": f"{cfg['grid']}^3x3",
+            "snapshot_dtype": "f32", "parallelism": parallelism, "l2": "inputs larger than L2 (X >= 3.8 GB)"}
+
+
 def cpu_sample(orc, synth, cfg, rows):
     p = synth.config_params(cfg["cfg"], seed=cfg["seed"], grid=cfg["grid"])
+    n_full = p.n
     rows = min(rows, p.n)
     X = synth.generate_host(p, 0, rows).astype(np.float64)
     flops, _, _ = fit_flops(rows, p.m, cfg["r"], cfg["p"], cfg["q"])
     sample = (f"config{cfg['cfg']} rows [0,{rows}) x {p.m} snapshots; oracle optdmd r={cfg['r']} "
               f"p={cfg['p']} q={cfg['q']} {cfg['lm_iters']} LM iters, numpy/OpenBLAS fp64; "
               f"GFLOP/s from the SURVEY §8d formula at n={rows}")
-    return {"X": X, "rows": rows, "flops": flops, "sample": sample}
+    _, _, l = fit_flops(n_full, p.m, cfg["r"], cfg["p"], cfg["q"])
+    return {"X": X, "rows": rows, "flops": flops, "sample": sample, "n": n_full, "m": p.m, "l": l}
 
 
 def cpu_fit(orc, X, cfg):
@@ -347,9 +356,7 @@ def main():
         "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 1), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config{cfg['cfg']} fit (OptDMD, {cfg['lm_iters']} LM iters) + config4 reconstruct",
-                   "n": n, "m": m, "r": r, "l": l, "p": cfg["p"], "q": cfg["q"], "grid": f"{cfg['grid']}^3x3",
-                   "snapshot_dtype": "f32", "parallelism": f"rows{world}", "l2": "inputs larger than L2 (X >= 3.8 GB)"},
+        "config": arm_config(cfg, n, m, r, l, f"rows{world}"),
         "fit": {"s": round(fit_t, 4), "gflops": round(value, 1), "flops": F_fit,
                 "per_step_s": [round(x["fit"], 4) for x in res],
                 "terms": {k: v for k, v in terms.items()},
