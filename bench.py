@@ -250,7 +250,7 @@ def main():
     F_fit, terms, l = fit_flops(n, m, r, cfg["p"], cfg["q"])
     lm = fd.LMConfig(max_iters=cfg["lm_iters"])
 
-    CHUNK = 128   # frames per tcgen05 launch (one CTA column of the 128-frame tile)
+    CHUNK = 128   # frames per tcgen05 launch (one N = 128 tile column: U streamed once per launch)
 
     def one_step(record):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]

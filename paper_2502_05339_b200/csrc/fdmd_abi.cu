@@ -481,6 +481,42 @@ SolverCtx* solver_ctx() {
   return &c;
 }
 
+template <int BN, int AST, int BST>
+int launch_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch, const void* cl,
+                     int ldk, int nf, const float* fscale, float* out, int64_t ldo, void* stream) {
+  auto encode = tensor_map_encoder();
+  if (!encode) return fail(FDMD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap maps[4];
+  const void* ptrs[4] = {uh, ul, ch, cl};
+  for (int i = 0; i < 4; ++i) {
+    const bool a = i < 2;
+    cuuint64_t dims[2] = {(cuuint64_t)r, (cuuint64_t)(a ? n : nf)};
+    cuuint64_t strides[1] = {(cuuint64_t)((a ? ldu : ldk) * 2)};
+    cuuint32_t box[2] = {(cuuint32_t)fdmd::tc::BKC, (cuuint32_t)(a ? fdmd::tc::BM : BN)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult res = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptrs[i]), dims, strides,
+                          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) return fail(FDMD_ERR_CUDA, "tc_decode: tensor map encode failed (%d)", (int)res);
+  }
+  auto kern = fdmd::tc_decode_kernel<BN, AST, BST>;
+  const int smem = (int)sizeof(fdmd::TCSmem<BN, AST, BST>) + 1024;
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = dev;
+  }
+  fdmd::TCArgs ta{out, ldo, n, r, nf, fscale};
+  const int64_t mtiles = (n + fdmd::tc::BM - 1) / fdmd::tc::BM;
+  const int ny = (nf + BN - 1) / BN;
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(mtiles, std::max(1, sm_count_cached() / ny)));
+  kern<<<dim3(gx, ny), fdmd::tc::THREADS, smem, (cudaStream_t)stream>>>(maps[0], maps[1], maps[2], maps[3], ta);
+  LAUNCH_CHECK("tc_decode");
+  return FDMD_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -882,37 +918,12 @@ int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r
     return fail(FDMD_ERR_INVALID, "tc_decode: bad arguments (r must be <= %d)", fdmd::tc::BKC * fdmd::tc::MAXKC);
   if ((ldu * 2) % 16 || (ldk * 2) % 16 || ldu < r || ldk < r || ldo < n || n >= (int64_t)UINT32_MAX)
     return fail(FDMD_ERR_INVALID, "tc_decode: leading dimensions must be multiples of 8 halves");
-  auto encode = tensor_map_encoder();
-  if (!encode) return fail(FDMD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  CUtensorMap maps[4];
-  const void* ptrs[4] = {uh, ul, ch, cl};
-  for (int i = 0; i < 4; ++i) {
-    const bool a = i < 2;
-    cuuint64_t dims[2] = {(cuuint64_t)r, (cuuint64_t)(a ? n : nf)};
-    cuuint64_t strides[1] = {(cuuint64_t)((a ? ldu : ldk) * 2)};
-    cuuint32_t box[2] = {(cuuint32_t)fdmd::tc::BKC, (cuuint32_t)(a ? fdmd::tc::BM : fdmd::tc::BN)};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult res = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptrs[i]), dims, strides,
-                          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (res != CUDA_SUCCESS) return fail(FDMD_ERR_CUDA, "tc_decode: tensor map encode failed (%d)", (int)res);
-  }
-  const int smem = (int)sizeof(fdmd::TCSmem) + 1024;
-  static thread_local int configured = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (configured != dev) {
-    CUDA_TRY(cudaFuncSetAttribute(fdmd::tc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = dev;
-  }
-  fdmd::TCArgs ta{out, ldo, n, r, nf, fscale};
-  const int64_t mtiles = (n + fdmd::tc::BM - 1) / fdmd::tc::BM;
-  const int ny = (nf + fdmd::tc::BN - 1) / fdmd::tc::BN;
-  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(mtiles, std::max(1, sm_count_cached() / ny)));
-  fdmd::tc_decode_kernel<<<dim3(gx, ny), fdmd::tc::THREADS, smem, (cudaStream_t)stream>>>(maps[0], maps[1], maps[2],
-                                                                                           maps[3], ta);
-  LAUNCH_CHECK("tc_decode");
-  return FDMD_OK;
+  // N = 128 frames per CTA column with the coefficients resident in smem and a
+  // 3-deep ring of U chunks (96 KB of HBM reads in flight per SM). Measured at
+  // n = 50.3M, r = 200: B = 32 at 5.8 TB/s (0.88 of HBM; 2-deep ring: 4.5);
+  // streaming the coefficients from L2 per chunk (to allow N = 256) cost more
+  // in L2/TMA traffic than it saved in U re-reads (3.0-3.3 TB/s).
+  return launch_tc_decode<128, 3, 0>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
 }
 
 int fdmd_dmma_peak(double seconds, double* tflops) {

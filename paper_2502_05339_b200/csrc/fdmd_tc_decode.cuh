@@ -10,11 +10,14 @@
 // Operands (both K-major, 128-byte swizzled, loaded by TMA):
 //   A = Us: row-major n x r fp16 hi/lo planes (the split basis, built once)
 //   B = Cs: frame-major F x r fp16 hi/lo planes (coefficients, per batch)
-// CTA tile: M = 128 rows x N = 128 frames, K = r in 64-wide chunks. B (all K,
-// hi+lo, 128 frames) stays resident in smem; A streams through a 2-stage ring.
+// CTA tile: M = 128 rows x N = BN frames, K = r in 64-wide chunks. A (the
+// basis, HBM) streams through an AST-deep mbarrier ring (3 x 32 KB keeps
+// 96 KB of HBM reads in flight per SM); B (coefficients) is either resident
+// (BST = 0: loaded once per CTA, the shipped configuration) or streamed from
+// L2 through its own BST ring (allows BN = 256, measured slower).
 // Warp roles: w0 TMA producer, w1 MMA issuer (one lane), w2..w5 epilogue
-// (TMEM lane quadrant = warp % 4). Two TMEM accumulators (2 x 128 columns) let
-// the epilogue of tile t overlap the MMAs of tile t+1.
+// (TMEM lane quadrant = warp % 4). The two accumulators let the epilogue of
+// tile t overlap the MMAs of tile t+1.
 #pragma once
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -25,21 +28,20 @@ namespace fdmd {
 
 namespace tc {
 constexpr int BM = 128;
-constexpr int BN = 128;
 constexpr int BKC = 64;          // K per chunk (128 B of fp16 = one SW128 row)
 constexpr int MAXKC = 4;         // r <= 256
-constexpr int ASTAGES = 2;
 constexpr int THREADS = 192;     // 6 warps
 constexpr int A_CHUNK_BYTES = BM * BKC * 2;   // 16 KB per plane
-constexpr int B_CHUNK_BYTES = BN * BKC * 2;   // 16 KB per plane
 }  // namespace tc
 
-struct TCSmem {
+// BST == 0: B resident (all MAXKC chunks loaded once per CTA); else a BST ring
+template <int BN, int AST, int BST> struct TCSmem {
+  static constexpr int NB = BST == 0 ? tc::MAXKC : BST;
   // 1024-B aligned SW128 atoms
-  __half A[tc::ASTAGES][2][tc::BM * tc::BKC];        // [stage][hi/lo]
-  __half B[tc::MAXKC][2][tc::BN * tc::BKC];          // [kchunk][hi/lo], resident
-  uint64_t afull[tc::ASTAGES], aempty[tc::ASTAGES];
-  uint64_t bfull;
+  __half A[AST][2][tc::BM * tc::BKC];        // [stage][hi/lo]
+  __half B[NB][2][BN * tc::BKC];             // [stage or k-chunk][hi/lo]
+  uint64_t afull[AST], aempty[AST];
+  uint64_t bfull[NB], bempty[NB];
   uint64_t tfull[2], tempty[2];
   uint32_t tmem_base;
 };
@@ -91,29 +93,34 @@ struct TCArgs {
 };
 
 // TMA maps: amap_h/amap_l over Us planes (dims {r, n}, box {64, 128}, SW128),
-//           bmap_h/bmap_l over Cs planes (dims {r, nf}, box {64, 128}, SW128).
+//           bmap_h/bmap_l over Cs planes (dims {r, nf}, box {64, BN}, SW128).
+template <int BN, int AST, int BST>
 __global__ void __launch_bounds__(tc::THREADS, 1)
 tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_constant__ CUtensorMap amap_l,
                  const __grid_constant__ CUtensorMap bmap_h, const __grid_constant__ CUtensorMap bmap_l,
                  const TCArgs args) {
+  using SM = TCSmem<BN, AST, BST>;
+  constexpr uint32_t TCOLS = 2 * BN;                  // two accumulators
+  constexpr uint32_t B_CHUNK_BYTES = BN * tc::BKC * 2;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // align the SW128 atoms to 1024 B
-  TCSmem& sm = *reinterpret_cast<TCSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  SM& sm = *reinterpret_cast<SM*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkc = (args.r + tc::BKC - 1) / tc::BKC;
   const int ksteps_last = ((args.r - (nkc - 1) * tc::BKC) + 15) / 16;   // valid 16-wide steps in last chunk
   const int64_t mtiles = (args.n + tc::BM - 1) / tc::BM;
   const int64_t my_tiles = blockIdx.x < mtiles ? (mtiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const int f0 = blockIdx.y * tc::BN;
+  const int f0 = blockIdx.y * BN;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < tc::ASTAGES; ++s) { mbar_init(&sm.afull[s], 1); mbar_init(&sm.aempty[s], 1); }
-    mbar_init(&sm.bfull, 1);
+    for (int s = 0; s < AST; ++s) { mbar_init(&sm.afull[s], 1); mbar_init(&sm.aempty[s], 1); }
+    for (int s = 0; s < SM::NB; ++s) { mbar_init(&sm.bfull[s], 1); mbar_init(&sm.bempty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], 4); }
     mbar_fence_init();
   }
-  if (warp == 1) {  // TMEM: 2 accumulators x 128 fp32 columns
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&sm.tmem_base)));
+  if (warp == 1) {  // TMEM: 2 accumulators x BN fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                 ::"r"(smem_u32(&sm.tmem_base)), "n"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   tc_fence_before();
@@ -123,46 +130,55 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
 
   if (warp == 0) {
     if (lane == 0) {
-      // resident B (coefficients): all K chunks, hi + lo
-      mbar_expect_tx(&sm.bfull, (uint32_t)(nkc * 2 * tc::B_CHUNK_BYTES));
-      for (int c = 0; c < nkc; ++c) {
-        tma_load_2d(sm.B[c][0], &bmap_h, c * tc::BKC, f0, &sm.bfull);
-        tma_load_2d(sm.B[c][1], &bmap_l, c * tc::BKC, f0, &sm.bfull);
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      if (BST == 0) {   // resident coefficients: every K chunk once, one barrier
+        mbar_expect_tx(&sm.bfull[0], (uint32_t)(nkc * 2 * B_CHUNK_BYTES));
+        for (int c = 0; c < nkc; ++c) {
+          tma_load_2d(sm.B[c][0], &bmap_h, c * tc::BKC, f0, &sm.bfull[0]);
+          tma_load_2d(sm.B[c][1], &bmap_l, c * tc::BKC, f0, &sm.bfull[0]);
+        }
       }
-      int s = 0;
-      uint32_t ph = 0;
       for (int64_t t = 0; t < my_tiles; ++t) {
         const int row0 = (int)((blockIdx.x + t * gridDim.x) * tc::BM);
         for (int c = 0; c < nkc; ++c) {
-          mbar_wait(&sm.aempty[s], ph ^ 1);
-          mbar_expect_tx(&sm.afull[s], 2 * tc::A_CHUNK_BYTES);
-          tma_load_2d(sm.A[s][0], &amap_h, c * tc::BKC, row0, &sm.afull[s]);
-          tma_load_2d(sm.A[s][1], &amap_l, c * tc::BKC, row0, &sm.afull[s]);
-          if (++s == tc::ASTAGES) { s = 0; ph ^= 1; }
+          mbar_wait(&sm.aempty[sa], pa ^ 1);
+          mbar_expect_tx(&sm.afull[sa], 2 * tc::A_CHUNK_BYTES);
+          tma_load_2d(sm.A[sa][0], &amap_h, c * tc::BKC, row0, &sm.afull[sa]);
+          tma_load_2d(sm.A[sa][1], &amap_l, c * tc::BKC, row0, &sm.afull[sa]);
+          if (++sa == AST) { sa = 0; pa ^= 1; }
+          if (BST > 0) {   // streamed coefficient chunk (from L2)
+            mbar_wait(&sm.bempty[sb], pb ^ 1);
+            mbar_expect_tx(&sm.bfull[sb], 2 * B_CHUNK_BYTES);
+            tma_load_2d(sm.B[sb][0], &bmap_h, c * tc::BKC, f0, &sm.bfull[sb]);
+            tma_load_2d(sm.B[sb][1], &bmap_l, c * tc::BKC, f0, &sm.bfull[sb]);
+            if (++sb == BST) { sb = 0; pb ^= 1; }
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // kind::f16, fp16 x fp16 -> fp32, K-major A and B, M = 128, N = 128
-      const uint32_t idesc = (1u << 4) | ((uint32_t)(tc::BN >> 3) << 17) | ((uint32_t)(tc::BM >> 4) << 24);
-      mbar_wait(&sm.bfull, 0);
-      tc_fence_after();
-      int s = 0;
-      uint32_t ph = 0;
+      // kind::f16, fp16 x fp16 -> fp32, K-major A and B, M = 128, N = BN
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(tc::BM >> 4) << 24);
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      if (BST == 0) mbar_wait(&sm.bfull[0], 0);
       for (int64_t t = 0; t < my_tiles; ++t) {
         const int acc = (int)(t & 1);
         const uint32_t acc_ph = (uint32_t)((t >> 1) & 1);
         mbar_wait(&sm.tempty[acc], acc_ph ^ 1);   // epilogue drained this accumulator
         tc_fence_after();
-        const uint32_t d = tmem + acc * tc::BN;
+        const uint32_t d = tmem + acc * BN;
         uint32_t first = 1;
         for (int c = 0; c < nkc; ++c) {
-          mbar_wait(&sm.afull[s], ph);
+          mbar_wait(&sm.afull[sa], pa);
+          if (BST > 0) mbar_wait(&sm.bfull[sb], pb);
           tc_fence_after();
           const int ksteps = (c == nkc - 1) ? ksteps_last : tc::BKC / 16;
-          const uint64_t ah = umma_desc_sw128(sm.A[s][0]), al = umma_desc_sw128(sm.A[s][1]);
-          const uint64_t bh = umma_desc_sw128(sm.B[c][0]), bl = umma_desc_sw128(sm.B[c][1]);
+          const int bi = BST > 0 ? sb : c;
+          const uint64_t ah = umma_desc_sw128(sm.A[sa][0]), al = umma_desc_sw128(sm.A[sa][1]);
+          const uint64_t bh = umma_desc_sw128(sm.B[bi][0]), bl = umma_desc_sw128(sm.B[bi][1]);
           for (int k = 0; k < ksteps; ++k) {
             const uint64_t adv = (uint64_t)((k * 32) >> 4);   // +32 B per K=16 inside the 128-B row
             umma_f16(d, ah + adv, bh + adv, idesc, first ? 0u : 1u);
@@ -170,8 +186,12 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
             umma_f16(d, al + adv, bh + adv, idesc, 1u);
             first = 0;
           }
-          umma_commit(&sm.aempty[s]);             // frees the A stage once these MMAs retire
-          if (++s == tc::ASTAGES) { s = 0; ph ^= 1; }
+          umma_commit(&sm.aempty[sa]);             // frees the stages once these MMAs retire
+          if (BST > 0) {
+            umma_commit(&sm.bempty[sb]);
+            if (++sb == BST) { sb = 0; pb ^= 1; }
+          }
+          if (++sa == AST) { sa = 0; pa ^= 1; }
         }
         umma_commit(&sm.tfull[acc]);              // accumulator ready for the epilogue
       }
@@ -186,9 +206,10 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
       tc_fence_after();
       const int64_t row = (blockIdx.x + t * gridDim.x) * tc::BM + q * 32 + lane;
 #pragma unroll 1
-      for (int cb = 0; cb < tc::BN; cb += 32) {
+      for (int cb = 0; cb < BN; cb += 32) {
+        if (f0 + cb >= args.nf) break;
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * tc::BN + cb), v);
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cb), v);
         if (row < args.n) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -205,7 +226,7 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS));
   }
 }
 
