@@ -395,23 +395,47 @@ PanelPlan panel_plan_best(int64_t n, int K1, int K2, int symmetric, size_t ea, s
 template <typename TA, typename TB, int WR, int WC, bool SYM>
 int launch_gram_panel(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaStream_t s) {
   auto kt = fdmd::tall_gram_panel_kernel<TA, TB, WR, WC, SYM>;
-  CUtensorMap maps[2];
+  CUtensorMap maps[2], tmaps[2];
   const void* ptr[2] = {a.A, a.B};
   const int64_t ld[2] = {a.lda, a.ldb};
   const int kdim[2] = {a.K1, a.K2};
   const size_t elt[2] = {sizeof(TA), sizeof(TB)};
+  int nfull[2] = {0, 0}, tail[2] = {0, 0};
+  // Full 128-B column blocks of a row-major n x K operand are one 3-D box
+  // ({W elements, 16 rows, full blocks} over dims {W, n, K / W} with strides
+  // {ld, W}): they land as consecutive 16-row x 128-B SW128 boxes, the layout
+  // panel_offset reads. A ragged last block (K % W != 0) is a 2-D box with
+  // zero fill past K (a 3-D box would read the next row's columns, and past
+  // the allocation on the last row).
   for (int i = 0; i < (SYM ? 1 : 2); ++i) {
-    cuuint64_t dims[2] = {(cuuint64_t)kdim[i], (cuuint64_t)a.n};
-    cuuint64_t strides[1] = {(cuuint64_t)(ld[i] * elt[i])};
-    cuuint32_t box[2] = {(cuuint32_t)(128 / elt[i]), (cuuint32_t)fdmd::tgp::BR};
-    cuuint32_t estr[2] = {1, 1};
-    if (tensor_map_encoder()(&maps[i], elt[i] == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
-                             2, const_cast<void*>(ptr[i]), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return fail(FDMD_ERR_CUDA, "tall_gram: tensor map encode failed");
+    const int W = 128 / (int)elt[i];
+    const int loaded = i == 0 ? std::min(pl.nba, (kdim[0] + W - 1) / W) : std::min(pl.nbb, (kdim[1] + W - 1) / W);
+    const int full = std::min(loaded, kdim[i] / W);
+    nfull[i] = full;
+    tail[i] = loaded > full ? 1 : 0;
+    const auto dt = elt[i] == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+    if (full > 0) {
+      cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)a.n, (cuuint64_t)(kdim[i] / W)};
+      cuuint64_t strides[2] = {(cuuint64_t)(ld[i] * elt[i]), (cuuint64_t)(W * elt[i])};
+      cuuint32_t box[3] = {(cuuint32_t)W, (cuuint32_t)fdmd::tgp::BR, (cuuint32_t)full};
+      cuuint32_t estr[3] = {1, 1, 1};
+      if (tensor_map_encoder()(&maps[i], dt, 3, const_cast<void*>(ptr[i]), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return fail(FDMD_ERR_CUDA, "tall_gram: tensor map encode failed");
+    }
+    if (tail[i]) {
+      cuuint64_t dims[2] = {(cuuint64_t)kdim[i], (cuuint64_t)a.n};
+      cuuint64_t strides[1] = {(cuuint64_t)(ld[i] * elt[i])};
+      cuuint32_t box[2] = {(cuuint32_t)W, (cuuint32_t)fdmd::tgp::BR};
+      cuuint32_t estr[2] = {1, 1};
+      if (tensor_map_encoder()(&tmaps[i], dt, 2, const_cast<void*>(ptr[i]), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return fail(FDMD_ERR_CUDA, "tall_gram: tensor map encode failed");
+    }
   }
-  if (SYM) maps[1] = maps[0];
+  if (SYM) { maps[1] = maps[0]; tmaps[1] = tmaps[0]; }
   fdmd::TallGramPanelArgs pa{};
   pa.g = a;
   pa.g.K1p = pl.K1p;
@@ -419,8 +443,12 @@ int launch_gram_panel(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaStre
   pa.g.rows_per_split = pl.rows_per_split;
   pa.nba = pl.nba;
   pa.nbb = pl.nbb;
-  pa.lda_boxes = std::min(pl.nba, (int)((a.K1 * sizeof(TA) + 127) / 128));
-  pa.ldb_boxes = SYM ? 0 : std::min(pl.nbb, (int)((a.K2 * sizeof(TB) + 127) / 128));
+  pa.lda_boxes = nfull[0] + tail[0];
+  pa.ldb_boxes = SYM ? 0 : nfull[1] + tail[1];
+  pa.a_full = nfull[0];
+  pa.b_full = SYM ? 0 : nfull[1];
+  pa.a_tail = tail[0];
+  pa.b_tail = SYM ? 0 : tail[1];
   for (int i = 0; i < fdmd::tgp::MAXP * 8; ++i) pa.tile[i] = pl.tile[i];
   static thread_local int conf_t = -1;
   static thread_local size_t conf_smem = 0;
@@ -431,7 +459,7 @@ int launch_gram_panel(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaStre
     conf_t = dv;
     conf_smem = 227 * 1024;
   }
-  kt<<<dim3(pl.P, pl.splits), fdmd::tgp::THREADS, pl.smem, s>>>(maps[0], maps[1], pa);
+  kt<<<dim3(pl.P, pl.splits), fdmd::tgp::THREADS, pl.smem, s>>>(maps[0], maps[1], tmaps[0], tmaps[1], pa);
   LAUNCH_CHECK("tall_gram_panel");
   return FDMD_OK;
 }

@@ -44,6 +44,7 @@ struct TallGramPanelArgs {
   TallGramArgs g;
   int nba, nbb;                               // 128-B boxes per chunk row (A, B; nbb = 0 when symmetric)
   int lda_boxes, ldb_boxes;                   // boxes actually loaded (those holding columns < K)
+  int a_full, b_full, a_tail, b_tail;         // full 128-B blocks (one 3-D TMA) + ragged block (2-D TMA)
   PanelTile tile[tgp::MAXP * 8];
 };
 
@@ -57,6 +58,9 @@ template <typename TX> __device__ __forceinline__ int panel_offset(int row, int 
 struct PanelFeed {
   const CUtensorMap* amap;
   const CUtensorMap* bmap;
+  const CUtensorMap* atmap;
+  const CUtensorMap* btmap;
+  int afull, bfull, atail, btail;
   unsigned char* a_sm;
   unsigned char* b_sm;
   int a_stage, b_stage, la, lb, wa, wb;
@@ -65,8 +69,13 @@ struct PanelFeed {
   __device__ __forceinline__ void issue(int64_t c, int s, uint64_t* full) const {
     mbar_expect_tx(&full[s], bytes);
     const int r0 = (int)(rbeg + c * tgp::BR);
-    for (int j = 0; j < la; ++j) tma_load_2d(a_sm + s * a_stage + j * tgp::BOX_BYTES, amap, j * wa, r0, &full[s]);
-    for (int j = 0; j < lb; ++j) tma_load_2d(b_sm + s * b_stage + j * tgp::BOX_BYTES, bmap, j * wb, r0, &full[s]);
+    // one 3-D TMA per operand for its full 128-B column blocks (they land as
+    // consecutive 16-row x 128-B SW128 boxes, the layout panel_offset reads)
+    // + one 2-D TMA for a ragged last block (zero-filled past K)
+    if (afull > 0) tma_load_3d(a_sm + s * a_stage, amap, 0, r0, 0, &full[s]);
+    if (atail) tma_load_2d(a_sm + s * a_stage + afull * tgp::BOX_BYTES, atmap, afull * wa, r0, &full[s]);
+    if (bfull > 0) tma_load_3d(b_sm + s * b_stage, bmap, 0, r0, 0, &full[s]);
+    if (btail) tma_load_2d(b_sm + s * b_stage + bfull * tgp::BOX_BYTES, btmap, bfull * wb, r0, &full[s]);
   }
 };
 
@@ -141,6 +150,7 @@ __device__ __forceinline__ void panel_consume(const PanelFeed& fd, bool feeder, 
 template <typename TA, typename TB, int WR, int WC, bool SYM>
 __global__ void __launch_bounds__(tgp::THREADS, 1)
 tall_gram_panel_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                       const __grid_constant__ CUtensorMap atmap, const __grid_constant__ CUtensorMap btmap,
                        const __grid_constant__ TallGramPanelArgs pa) {
   const TallGramArgs& args = pa.g;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -150,6 +160,12 @@ tall_gram_panel_kernel(const __grid_constant__ CUtensorMap amap, const __grid_co
   PanelFeed fd;
   fd.amap = &amap;
   fd.bmap = &bmap;
+  fd.atmap = &atmap;
+  fd.btmap = &btmap;
+  fd.afull = pa.a_full;
+  fd.bfull = pa.b_full;
+  fd.atail = pa.a_tail;
+  fd.btail = pa.b_tail;
   fd.a_stage = pa.nba * tgp::BOX_BYTES;
   fd.b_stage = pa.nbb * tgp::BOX_BYTES;
   fd.a_sm = base;
