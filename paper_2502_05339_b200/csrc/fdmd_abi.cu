@@ -147,6 +147,21 @@ int launch_tg_tma(const fdmd::TallGemmArgs& a, cudaStream_t s, int& grid_x, bool
   CUDA_TRY(cudaMemsetAsync(Bp, 0, sizeof(double) * Kp * ldbp, s));
   CUDA_TRY(cudaMemcpy2DAsync(Bp, ldbp * sizeof(double), a.B, a.ldb * sizeof(double), a.N * sizeof(double), a.K,
                              cudaMemcpyDeviceToDevice, s));
+  // B as one TMA box per chunk: {BN + 4 columns (the smem row padding), 16 k}
+  CUtensorMap bmap;
+  {
+    constexpr int LDB = fdmd::TTSmem<TA, AL, NF>::LDB;
+    cuuint64_t bd[2] = {(cuuint64_t)ldbp, (cuuint64_t)Kp};
+    cuuint64_t bs[1] = {(cuuint64_t)(ldbp * sizeof(double))};
+    cuuint32_t bb[2] = {(cuuint32_t)LDB, (cuuint32_t)fdmd::tt::BK};
+    cuuint32_t be[2] = {1, 1};
+    if (encode(&bmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, Bp, bd, bs, bb, be, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      cudaFreeAsync(Bp, s);
+      return FDMD_OK;   // fall back to the ring kernel (used stays false)
+    }
+  }
   fdmd::TTArgs ta{a, Bp, ldbp, {NF, NF, NF, NF}};
   const int nb = (a.N + 7) / 8;
   if (gy == 1 && NF > 1 && nb >= 4 * (NF - 1) && nb < 4 * NF)   // e.g. N = 200: 7,6,6,6 blocks
@@ -163,7 +178,7 @@ int launch_tg_tma(const fdmd::TallGemmArgs& a, cudaStream_t s, int& grid_x, bool
   const int64_t ntiles = (a.n + fdmd::tt::BM - 1) / fdmd::tt::BM;
   grid_x = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, std::max(1, sm_count_cached() - a.reserve_sms)));
   dim3 grid(grid_x, gy);
-  kern<<<grid, fdmd::tt::THREADS, smem, s>>>(map, ta);
+  kern<<<grid, fdmd::tt::THREADS, smem, s>>>(map, bmap, ta);
   LAUNCH_CHECK("tall_gemm_tma");
   CUDA_TRY(cudaFreeAsync(Bp, s));
   used = true;

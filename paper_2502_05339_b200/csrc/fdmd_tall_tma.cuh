@@ -96,12 +96,13 @@ struct TTArgs {
 
 template <typename S, int A_LAYOUT> struct TTFeed {
   const CUtensorMap* amap;
+  const CUtensorMap* bmap;   // padded B: one {LDB, 16} box per chunk lands as the padded smem rows
   const double* Bp;
   int64_t ldbp;
   int n0;
   __device__ __forceinline__ void issue(S& sm, int s, int64_t tile, int kc) const {
     constexpr unsigned A_BYTES = tt::BM * tt::BK * sizeof(sm.A[0][0]);
-    constexpr unsigned B_ROW = S::BN * sizeof(double);
+    constexpr unsigned B_ROW = S::LDB * sizeof(double);
     mbar_expect_tx(&sm.full[s], A_BYTES + tt::BK * B_ROW);
     const int k0 = kc * tt::BK;
     if (A_LAYOUT == LAYOUT_ROW) {
@@ -113,9 +114,7 @@ template <typename S, int A_LAYOUT> struct TTFeed {
         tma_load_2d(reinterpret_cast<unsigned char*>(sm.A[s]) + j * tt::BK * 128, amap,
                     (int)(tile * tt::BM) + j * MB, k0, &sm.full[s]);
     }
-#pragma unroll 4
-    for (int kk = 0; kk < tt::BK; ++kk)
-      bulk_load(&sm.B[s][kk][0], Bp + (int64_t)(k0 + kk) * ldbp + n0, B_ROW, &sm.full[s]);
+    tma_load_2d(&sm.B[s][0][0], bmap, n0, k0, &sm.full[s]);
   }
 };
 
@@ -240,7 +239,8 @@ __device__ __forceinline__ void tt_consume(S& sm, const TallGemmArgs& args, cons
 
 template <typename TA, int A_LAYOUT, int NF, typename TC, int C_LAYOUT, bool STATS>
 __global__ void __launch_bounds__(tt::THREADS, 1)
-tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) {
+tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                     const TTArgs ta) {
   using S = TTSmem<TA, A_LAYOUT, NF>;
   constexpr int BN = S::BN;
   constexpr int LDB = S::LDB;
@@ -266,7 +266,7 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const TTArgs ta) 
   }
   __syncthreads();
 
-  const TTFeed<S, A_LAYOUT> fd{&amap, ta.Bp, ta.ldbp, n0};
+  const TTFeed<S, A_LAYOUT> fd{&amap, &bmap, ta.Bp, ta.ldbp, n0};
   if (warp >= tt::CONSUMERS / 32) {
     // ============================ producer ============================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(tt::REG_PRODUCER));
