@@ -414,17 +414,15 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
             for c in (c1, c2):
                 g_src.append(c[0]); g_al.append(c[1]); g_be.append(c[2])
         ops.table_apply(raw, g_src, g_al, g_be, general, 2 * r)
-    # the decode table overwrites the raw buffer in place (no second n x r allocation)
-    with stage("modes.table_apply"):
-        if lay.ncol <= raw.k:
-            table = ops.table_apply_inplace(raw, t_src, t_al, t_be, lay.ncol)
-        else:   # many complex self-paired modes (extra Im columns): out of place
-            table = alloc_tall(n_loc, lay.ncol, table_dtype, "col", device=dev)
-            ops.table_apply(raw, t_src, t_al, t_be, table, lay.ncol)
-    del raw
+    # the decode table stays implicit: table = raw @ mix (nraw x ncol, host);
+    # no n x r rewrite (DeviceModes folds mix into every small-matrix product)
+    mix = np.zeros((raw.k, lay.ncol), dtype=np.float64)
+    for k, (u, al, be) in enumerate(zip(t_src, t_al, t_be)):
+        mix[2 * u, k] = al
+        mix[2 * u + 1, k] = be
     if timings is not None:
         timings["modes_s"] = time.perf_counter() - t0
-    return DeviceModes(table, lay, shard, general)
+    return DeviceModes(raw, lay, shard, general, mix=mix)
 
 
 # ---------------------------------------------------------------------------

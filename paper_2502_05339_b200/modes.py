@@ -109,15 +109,22 @@ class TableLayout:
 
 
 class DeviceModes:
-    """Decode table in HBM (+ optional general basis) and its cached Gram."""
+    """Decode table in HBM (+ optional general basis) and its cached Gram.
+
+    ``mix`` (nraw x ncol, host float64): the table is implicit, table =
+    table_buf @ mix — the fit keeps the raw [Re, Im] mode columns and folds
+    the reference's normalisation / phase canonicalisation / pair locking
+    (dmd.py:189-213) into this small matrix instead of rewriting n x r
+    values (every consumer multiplies the table by a small matrix)."""
 
     def __init__(self, table: Tall, layout: TableLayout, shard: Optional[Shard] = None,
-                 general: Optional[Tall] = None):
+                 general: Optional[Tall] = None, mix: Optional[np.ndarray] = None):
         assert table.layout == "col"
         self.table = table
         self.layout = layout
         self.shard = shard
         self.general = general
+        self.mix = None if mix is None else np.asarray(mix, dtype=np.float64)
         self._pinv_small = None
 
     @property
@@ -137,6 +144,8 @@ class DeviceModes:
                 E[2 * a, a] = 1.0
                 E[2 * a + 1, a] = 1.0j
             return self.general, E
+        if self.mix is not None:
+            return self.table, self.mix @ self.layout.E()
         return self.table, self.layout.E()
 
     def pinv_small(self) -> np.ndarray:
@@ -169,14 +178,24 @@ class DeviceModes:
         return self.pinv_small() @ (E.conj().T @ y)
 
     # -- decode ------------------------------------------------------------
-    def decode_coeff(self, C: torch.Tensor, out: Optional[torch.Tensor] = None, general=False) -> torch.Tensor:
-        """frames (B x n_local) = D[:, :ncol] @ C (ncol x B)."""
-        D = self.general if (general and self.general is not None) else self.table
-        ncol = int(C.shape[0])
-        return dv.get_ops().decode(D, C, out=out, ncols=ncol)
+    def decode_coeff(self, C: torch.Tensor, out: Optional[torch.Tensor] = None, general=False,
+                     basis_coords=False) -> torch.Tensor:
+        """frames (B x n_local) = table[:, :ncol] @ C (ncol x B) — or, with
+        basis_coords, D @ C for C in the coordinates of basis()'s D."""
+        if general and self.general is not None:
+            return dv.get_ops().decode(self.general, C, out=out, ncols=int(C.shape[0]))
+        if self.mix is not None and not basis_coords:
+            M = torch.as_tensor(self.mix[:, : int(C.shape[0])], device=C.device)
+            C = M @ C.to(torch.float64)
+        return dv.get_ops().decode(self.table, C, out=out, ncols=int(C.shape[0]))
 
     def host_table(self) -> np.ndarray:
         """n x ncol_table float64 (the reference's decode_table cols)."""
+        if self.mix is not None:
+            nraw = self.mix.shape[0]
+            v = self.table.buf[:nraw, : self.table.n].t().to(torch.float64)
+            M = torch.as_tensor(self.mix[:, : self.layout.ncol_table], device=v.device)
+            return (v @ M).cpu().numpy()
         v = self.table.buf[: self.layout.ncol_table, : self.table.n]
         return v.t().to(torch.float64).cpu().numpy().copy()
 

@@ -115,7 +115,8 @@ def decode(model, z, *, out: Optional[torch.Tensor] = None, to_host: bool = True
         D, E = modes.basis()
         ez = E @ z
         C = np.stack([ez.real, ez.imag], axis=1)
-        frames = modes.decode_coeff(torch.as_tensor(C, device=dev), general=modes.general is not None)
+        frames = modes.decode_coeff(torch.as_tensor(C, device=dev), general=modes.general is not None,
+                                    basis_coords=True)
         yr, yi = frames[0], frames[1]
         y2 = float(torch.sum(yr.double() ** 2).item()) + float(torch.sum(yi.double() ** 2).item())
         yi2 = float(torch.sum(yi.double() ** 2).item())
