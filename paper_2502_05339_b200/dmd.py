@@ -919,6 +919,6 @@ def _sketch_shifted(S: Tall, c0: int, T: int, l: int, q: int, omega: np.ndarray)
         la.cholqr2_inplace(Q)
     QtS = ops.tall_gram(Q, S)
     B = QtS[:, c0:c0 + T]
-    Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvd" if B.is_cuda else None)
+    Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvdj" if B.is_cuda else None)
     # QtS re-indexed so that column 1.. of the returned block is Q^T X'_{shifted}
     return la.SketchFactors(Q, Ub, s, Vh, QtS, {})

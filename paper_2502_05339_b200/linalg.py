@@ -398,7 +398,7 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
             QtS = fix.t() @ QtS
     with stage("small.svd(B)"):
         B = QtS[:, :T]
-        Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvd" if B.is_cuda else None)
+        Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvdj" if B.is_cuda else None)
     return SketchFactors(Q, Ub, s, Vh, QtS, stats, fix)
 
 
@@ -488,7 +488,7 @@ def truncated_svd(M, r, *, shard: Optional[Shard] = None, keep_device=False) -> 
     X = A.view().to(torch.float64)
     if rows >= cols:
         Qf, Rf = torch.linalg.qr(X, mode="reduced")
-        Ur, s, Vh = torch.linalg.svd(Rf, full_matrices=False, driver="gesvd" if Rf.is_cuda else None)
+        Ur, s, Vh = torch.linalg.svd(Rf, full_matrices=False, driver="gesvdj" if Rf.is_cuda else None)
         Ufull = Qf @ Ur
     else:
         Ufull, s, Vh = torch.linalg.svd(X, full_matrices=False, driver="gesvd" if X.is_cuda else None)

@@ -42,6 +42,9 @@ def main():
         "torch_eig_ms": timed(lambda: torch.linalg.eig(K)),
         "svd_B_ms": timed(lambda: torch.linalg.svd(B, full_matrices=False)),
         "svdvals_B_ms": timed(lambda: torch.linalg.svdvals(B)),
+        "svd_gesvdj_ms": timed(lambda: torch.linalg.svd(B[:r, :r], full_matrices=False, driver="gesvdj")),
+        "svd_gesvda_ms": timed(lambda: torch.linalg.svd(B[:r, :r], full_matrices=False, driver="gesvda")),
+        "svd_gesvd_sq_ms": timed(lambda: torch.linalg.svd(B[:r, :r], full_matrices=False, driver="gesvd")),
         "eigh_G_ms": timed(lambda: torch.linalg.eigh(G)),
         "cholesky_G_ms": timed(lambda: torch.linalg.cholesky(G)),
         "cholesky_ex_G_ms": timed(lambda: torch.linalg.cholesky_ex(G)),
@@ -56,6 +59,11 @@ def main():
     }
     for k, v in out.items():
         print(f"{k:24s} {v:9.2f}")
+    Bs = B[:r, :r]
+    U1, s1, V1 = torch.linalg.svd(Bs, full_matrices=False, driver="gesvd")
+    U2, s2, V2 = torch.linalg.svd(Bs, full_matrices=False, driver="gesvdj")
+    print("gesvdj vs gesvd: sigma rel", float(((s2 - s1) / s1).abs().max()),
+          " |U^T U2| diag min", float((U1.T @ U2).diagonal().abs().min()))
 
 
 if __name__ == "__main__":
