@@ -15,8 +15,8 @@
 // 96 KB of HBM reads in flight per SM); B (coefficients) is either resident
 // (BST = 0: loaded once per CTA, the shipped configuration) or streamed from
 // L2 through its own BST ring (allows BN = 256, measured slower).
-// Warp roles: w0 TMA producer, w1 MMA issuer (one lane), w2..w5 epilogue
-// (TMEM lane quadrant = warp % 4). The two accumulators let the epilogue of
+// Warp roles: w0 TMA producer, w1 MMA issuer (one lane), w2..w9 epilogue
+// (TMEM lane quadrant = warp % 4, two warps per quadrant on column halves). The two accumulators let the epilogue of
 // tile t overlap the MMAs of tile t+1.
 #pragma once
 #include <cuda.h>
@@ -30,7 +30,8 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BKC = 64;          // K per chunk (128 B of fp16 = one SW128 row)
 constexpr int MAXKC = 4;         // r <= 256
-constexpr int THREADS = 192;     // 6 warps
+constexpr int EPI = 8;           // epilogue warps (2 per TMEM lane quadrant, half the columns each; 4: 14.4 ms, 8: 11.8, 16: 12.3 at B = 128)
+constexpr int THREADS = 64 + 32 * EPI;
 constexpr int A_CHUNK_BYTES = BM * BKC * 2;   // 16 KB per plane
 }  // namespace tc
 
@@ -115,7 +116,7 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
   if (threadIdx.x == 0) {
     for (int s = 0; s < AST; ++s) { mbar_init(&sm.afull[s], 1); mbar_init(&sm.aempty[s], 1); }
     for (int s = 0; s < SM::NB; ++s) { mbar_init(&sm.bfull[s], 1); mbar_init(&sm.bempty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], 4); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], tc::EPI); }
     mbar_fence_init();
   }
   if (warp == 1) {  // TMEM: 2 accumulators x BN fp32 columns
@@ -197,8 +198,12 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
       }
     }
   } else {
-    // epilogue warps 2..5 -> TMEM lane quadrant q = warp % 4
+    // epilogue warps 2.. -> TMEM lane quadrant q = warp % 4; the EPI / 4 warps
+    // of a quadrant split the BN columns
     const int q = warp & 3;
+    constexpr int SPLIT = tc::EPI / 4;
+    const int part = (warp - 2) / 4;
+    const int c_lo = part * (BN / SPLIT), c_hi = c_lo + BN / SPLIT;
     for (int64_t t = 0; t < my_tiles; ++t) {
       const int acc = (int)(t & 1);
       const uint32_t acc_ph = (uint32_t)((t >> 1) & 1);
@@ -206,7 +211,7 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
       tc_fence_after();
       const int64_t row = (blockIdx.x + t * gridDim.x) * tc::BM + q * 32 + lane;
 #pragma unroll 1
-      for (int cb = 0; cb < BN; cb += 32) {
+      for (int cb = c_lo; cb < c_hi; cb += 32) {
         if (f0 + cb >= args.nf) break;
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cb), v);
