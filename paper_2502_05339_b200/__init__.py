@@ -16,7 +16,18 @@ from .dmd import (
     optdmd,
     vandermonde,
 )
-from .errors import ConvergenceError, EigenvalueFloorError, FlowDmdError, RolloutOverflowError
+from . import model_io
+from .errors import (
+    BadMagicError,
+    BadVersionError,
+    ChecksumError,
+    ConvergenceError,
+    EigenvalueFloorError,
+    FlowDmdError,
+    FormatError,
+    RolloutOverflowError,
+    SizeMismatchError,
+)
 from .linalg import SvdResult, eig_small, lstsq, pinv, randomized_svd, truncated_svd
 from .runtime import (
     ImaginaryResidueWarning,
