@@ -60,6 +60,34 @@ def main():
              frame5=decode(loaded, step_k(loaded, z0, 5)), z0=z0.z,
              hb_phi=phi, hb_lam=lam, density=density,
              manifest=open(os.path.join(OUT, "dataset", "manifest")).read())
+    # the reference CLI on the golden dataset (cli.py:126-270)
+    import contextlib
+    import io as _io
+    from flowdmd.cli import cli_main
+    cli = os.path.join(OUT, "cli")
+    os.makedirs(cli)
+    ds = os.path.join(OUT, "dataset")
+    runs = {
+        "train": ["train", ds, "-o", os.path.join(cli, "trained.kdmd"), "--rank", "6"],
+        "train_opt": ["train", ds, "-o", os.path.join(cli, "trained_opt.kdmd"), "--rank", "6",
+                      "--method", "optdmd", "--svd", "randomized", "--seed", "3"],
+        "rollout": ["rollout", "--model", os.path.join(OUT, "model.kdmd"), "--dataset", ds, "--start-frame", "2",
+                    "--k", "2", "--frames", "5", "--out", os.path.join(cli, "rollout")],
+        "reverse": ["reverse", "--model", os.path.join(OUT, "model.kdmd"), "--dataset", ds, "--start-frame", "30",
+                    "--frames", "3", "--out", os.path.join(cli, "reverse")],
+        "eval": ["eval", "--model", os.path.join(OUT, "model.kdmd"), "--dataset", ds, "--stride", "3"],
+        "bad_start": ["rollout", "--model", os.path.join(OUT, "model.kdmd"), "--dataset", ds, "--start-frame",
+                      "99", "--out", os.path.join(cli, "nope")],
+    }
+    outs = {}
+    for name, argv in runs.items():
+        so, se = _io.StringIO(), _io.StringIO()
+        with contextlib.redirect_stdout(so), contextlib.redirect_stderr(se):
+            rc = cli_main(argv)
+        outs[name] = (rc, so.getvalue(), se.getvalue())
+    with open(os.path.join(cli, "outputs.txt"), "w") as fh:
+        for name, (rc, so, se) in outs.items():
+            fh.write(f"## {name} rc={rc}\n{so}--stderr--\n{se}")
     for root, _, files in os.walk(OUT):
         for f in files:
             print(os.path.relpath(os.path.join(root, f), ROOT), os.path.getsize(os.path.join(root, f)))
