@@ -181,6 +181,65 @@ def _pinned(shape, dtype):
     return torch.empty(shape, dtype=dtype, pin_memory=torch.cuda.is_available())
 
 
+def _stream_out(fh, crc: int, blocks, rows_max: int, n: int, dtype) -> int:
+    """Write device blocks (rows x n) to `fh` in order with a running CRC32.
+    Double-buffered pinned staging: a writer thread (zlib.crc32 and the file
+    write release the GIL) drains block i while the caller forms block i+1
+    on the device and copies it down."""
+    from concurrent.futures import ThreadPoolExecutor
+    bufs = [_pinned((rows_max, n), dtype) for _ in range(2)]
+    state = {"crc": crc}
+
+    def sink(mv):
+        state["crc"] = zlib.crc32(mv, state["crc"])
+        fh.write(mv)
+
+    pend = [None, None]
+    with ThreadPoolExecutor(1) as ex:
+        for i, blk in enumerate(blocks):
+            b = i & 1
+            if pend[b] is not None:
+                pend[b].result()
+            hv = bufs[b][: blk.shape[0]]
+            hv.copy_(blk, non_blocking=True)
+            if blk.is_cuda:
+                torch.cuda.current_stream(blk.device).synchronize()
+            pend[b] = ex.submit(sink, memoryview(hv.numpy()).cast("B"))
+        for f in pend:
+            if f is not None:
+                f.result()
+    return state["crc"]
+
+
+def _stream_in(fh, crc: int, rows: list, n: int, dtype, consume):
+    """Read consecutive blocks (rows[i] x n) from `fh` with a running CRC32:
+    a reader thread fills the other pinned buffer while `consume(i, host)`
+    uploads the current one. Stops early when consume returns False.
+    Returns (crc, completed)."""
+    from concurrent.futures import ThreadPoolExecutor
+    bufs = [_pinned((max(rows), n), dtype) for _ in range(2)]
+    state = {"crc": crc}
+
+    def fill(b, k):
+        hv = bufs[b][:k]
+        mv = memoryview(hv.numpy()).cast("B")
+        fh.readinto(mv)
+        state["crc"] = zlib.crc32(mv, state["crc"])
+        return hv
+
+    with ThreadPoolExecutor(1) as ex:
+        fut = ex.submit(fill, 0, rows[0])
+        for i, k in enumerate(rows):
+            hv = fut.result()
+            if i + 1 < len(rows):
+                fut = ex.submit(fill, (i + 1) & 1, rows[i + 1])
+            if consume(i, hv) is False:
+                if i + 1 < len(rows):
+                    fut.result()
+                return state["crc"], False
+    return state["crc"], True
+
+
 def _phi_block(model, a0: int, a1: int) -> torch.Tensor:
     """phi[:, a0:a1] transposed (b x n complex128, device), from the table."""
     modes = model.modes
@@ -209,17 +268,8 @@ def save_model(path, model):
         w.write(_u32(len(grid_block)) + grid_block)
         w.write(np.ascontiguousarray(model.sigma, dtype=_F64).tobytes())
         w.write(np.ascontiguousarray(model.lam, dtype=_C128).tobytes())
-        host = None
-        for a0 in range(0, r, BLOCK_MODES):
-            a1 = min(r, a0 + BLOCK_MODES)
-            blk = _phi_block(model, a0, a1)                                 # (b, n) c128, column a at row a-a0
-            if host is None or host.shape[0] < blk.shape[0]:
-                host = _pinned((BLOCK_MODES, n), torch.complex128)
-            hv = host[: blk.shape[0]]
-            hv.copy_(blk, non_blocking=True)
-            if blk.is_cuda:
-                torch.cuda.current_stream(blk.device).synchronize()
-            w.write(memoryview(hv.numpy()).cast("B"))
+        blocks = (_phi_block(model, a0, min(r, a0 + BLOCK_MODES)) for a0 in range(0, r, BLOCK_MODES))
+        w.crc = _stream_out(fh, w.crc, blocks, BLOCK_MODES, n, torch.complex128)   # (b, n) c128 = phi columns
         w.write(_u32(len(prov_block)) + prov_block)
         fh.write(_u32(w.crc))
     os.replace(tmp, path)
@@ -295,16 +345,11 @@ def load_model(path, device=None, table_dtype=torch.float64):
         builder = _TableBuilder(n, lam, partner, table_dtype, dev) if adjacent else None
         host_phi = None
         if builder is not None:
-            host = _pinned((BLOCK_MODES, n), torch.complex128)
-            for a0 in range(0, r, BLOCK_MODES):
-                a1 = min(r, a0 + BLOCK_MODES)
-                hv = host[: a1 - a0]
-                mv = memoryview(hv.numpy()).cast("B")
-                fh.readinto(mv)
-                crc = zlib.crc32(mv, crc)
-                if not builder.add(a0, hv):
-                    builder = None          # partner columns are not exact conjugates
-                    break
+            rows = [min(BLOCK_MODES, r - a0) for a0 in range(0, r, BLOCK_MODES)]
+            crc, done = _stream_in(fh, crc, rows, n, torch.complex128,
+                                   lambda i, hv: builder.add(i * BLOCK_MODES, hv))
+            if not done:
+                builder = None              # partner columns are not exact conjugates
         if builder is None:
             # hand-built model (non-conjugate partners): phi goes through the host
             # ReducedModel(phi, ...) constructor path instead
@@ -392,21 +437,10 @@ def save_dataset(path, snapshots, density=None):
     S = snapshots.S
     n, frames = S.n, S.k
     os.makedirs(path, exist_ok=True)
-    crc = 0
     with open(os.path.join(path, SNAPSHOTS_NAME), "wb") as fh:
-        host = None
-        for j0 in range(0, frames, BLOCK_COLS):
-            j1 = min(frames, j0 + BLOCK_COLS)
-            blk = S.buf[:n, j0:j1].t().to(torch.float64).contiguous()       # (cols, n): file order
-            if host is None:
-                host = _pinned((BLOCK_COLS, n), torch.float64)
-            hv = host[: j1 - j0]
-            hv.copy_(blk, non_blocking=True)
-            if blk.is_cuda:
-                torch.cuda.current_stream(blk.device).synchronize()
-            mv = memoryview(hv.numpy()).cast("B")
-            crc = zlib.crc32(mv, crc)
-            fh.write(mv)
+        blocks = (S.buf[:n, j0:min(frames, j0 + BLOCK_COLS)].t().to(torch.float64).contiguous()
+                  for j0 in range(0, frames, BLOCK_COLS))                  # (cols, n): file order
+        crc = _stream_out(fh, 0, blocks, BLOCK_COLS, n, torch.float64)
     grid_kv = grid_to_kv(snapshots.grid_meta)
     manifest = {"kind": "dataset", "grid_kind": grid_kv["kind"]}
     for key, value in grid_kv.items():
@@ -465,17 +499,13 @@ def load_dataset(path, device=None, dtype=torch.float64):
     S = alloc_tall(n, frames, dtype, "row", device=dev)
     if S.ld > frames:
         S.buf[:, frames:].zero_()
-    crc = 0
+    def put(i, hv):                                                      # (cols, n) host block
+        j0 = i * BLOCK_COLS
+        S.buf[:n, j0:j0 + hv.shape[0]] = hv.to(dev, non_blocking=False).t().to(dtype)   # device transpose
+
     with open(snap, "rb") as fh:
-        host = _pinned((BLOCK_COLS, n), torch.float64)
-        for j0 in range(0, frames, BLOCK_COLS):
-            j1 = min(frames, j0 + BLOCK_COLS)
-            hv = host[: j1 - j0]
-            mv = memoryview(hv.numpy()).cast("B")
-            fh.readinto(mv)
-            crc = zlib.crc32(mv, crc)
-            blk = hv.to(dev, non_blocking=False)                       # (cols, n)
-            S.buf[:n, j0:j1] = blk.t().to(dtype)                        # device transpose into row-major
+        rows = [min(BLOCK_COLS, frames - j0) for j0 in range(0, frames, BLOCK_COLS)]
+        crc, _ = _stream_in(fh, 0, rows, n, torch.float64, put)
     if "snapshots_crc32" in kv and crc != int(kv["snapshots_crc32"]):
         raise ChecksumError(f"{path}: snapshots.bin checksum mismatch")
     grid_kv = {"kind": kv.get("grid_kind", "none")}
