@@ -524,9 +524,10 @@ SolverCtx* solver_ctx() {
   return &c;
 }
 
-template <int BN, int AST, int BST>
-int launch_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch, const void* cl,
-                     int ldk, int nf, const float* fscale, float* out, int64_t ldo, void* stream) {
+template <int BN, int AST, int BST, int MC>
+int launch_tc_decode_mc(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch,
+                        const void* cl, int ldk, int nf, const float* fscale, float* out, int64_t ldo,
+                        void* stream) {
   auto encode = tensor_map_encoder();
   if (!encode) return fail(FDMD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap maps[4];
@@ -535,14 +536,15 @@ int launch_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int
     const bool a = i < 2;
     cuuint64_t dims[2] = {(cuuint64_t)r, (cuuint64_t)(a ? n : nf)};
     cuuint64_t strides[1] = {(cuuint64_t)((a ? ldu : ldk) * 2)};
-    cuuint32_t box[2] = {(cuuint32_t)fdmd::tc::BKC, (cuuint32_t)(a ? fdmd::tc::BM : BN)};
+    // A: each cluster CTA loads a 128/MC-row slice and multicasts it
+    cuuint32_t box[2] = {(cuuint32_t)fdmd::tc::BKC, (cuuint32_t)(a ? fdmd::tc::BM / MC : BN)};
     cuuint32_t estr[2] = {1, 1};
     CUresult res = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptrs[i]), dims, strides,
                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res != CUDA_SUCCESS) return fail(FDMD_ERR_CUDA, "tc_decode: tensor map encode failed (%d)", (int)res);
   }
-  auto kern = fdmd::tc_decode_kernel<BN, AST, BST>;
+  auto kern = fdmd::tc_decode_kernel<BN, AST, BST, MC>;
   const int smem = (int)sizeof(fdmd::TCSmem<BN, AST, BST>) + 1024;
   static thread_local int configured = -1;
   int dev = 0;
@@ -554,8 +556,37 @@ int launch_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int
   fdmd::TCArgs ta{out, ldo, n, r, nf, fscale};
   const int64_t mtiles = (n + fdmd::tc::BM - 1) / fdmd::tc::BM;
   const int ny = (nf + BN - 1) / BN;
-  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(mtiles, std::max(1, sm_count_cached() / ny)));
-  kern<<<dim3(gx, ny), fdmd::tc::THREADS, smem, (cudaStream_t)stream>>>(maps[0], maps[1], maps[2], maps[3], ta);
+  const int gy = (ny + MC - 1) / MC * MC;          // whole clusters (tail CTAs of a cluster only compute)
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.blockDim = dim3(fdmd::tc::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  int gx;
+  if (MC == 1) {
+    gx = (int)std::max<int64_t>(1, std::min<int64_t>(mtiles, std::max(1, sm_count_cached() / ny)));
+    cfg.numAttrs = 0;
+  } else {
+    // persistent: every cluster co-resident (clusters are packed per GPC, so
+    // fewer than sm_count / MC may fit)
+    static thread_local int max_clusters[9] = {0};
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = MC;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (max_clusters[MC] <= 0) {
+      cfg.gridDim = dim3(1, MC);
+      int nc = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveClusters(&nc, (void*)kern, &cfg));
+      max_clusters[MC] = std::max(1, nc);
+    }
+    const int rows_of_clusters = gy / MC;
+    gx = (int)std::max<int64_t>(1, std::min<int64_t>(mtiles, std::max(1, max_clusters[MC] / rows_of_clusters)));
+  }
+  cfg.gridDim = dim3(gx, MC == 1 ? ny : gy);
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], ta));
   LAUNCH_CHECK("tc_decode");
   return FDMD_OK;
 }
@@ -966,7 +997,18 @@ int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r
   // n = 50.3M, r = 200: B = 32 at 5.8 TB/s (0.88 of HBM; 2-deep ring: 4.5);
   // streaming the coefficients from L2 per chunk (to allow N = 256) cost more
   // in L2/TMA traffic than it saved in U re-reads (3.0-3.3 TB/s).
-  return launch_tc_decode<128, 3, 0>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
+  // Batches over 128 frames run as clusters of MC CTAs along the frame axis
+  // sharing every basis chunk through TMA multicast (basis read once per
+  // MC * 128 frames).
+  const int ny = (nf + 127) / 128;
+  static const int mc_cap = [] { const char* e = getenv("FDMD_TC_MAX_CLUSTER"); return e ? atoi(e) : 8; }();
+  if (ny == 1 || mc_cap <= 1)
+    return launch_tc_decode_mc<128, 3, 0, 1>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
+  if (ny == 2 || mc_cap < 4)
+    return launch_tc_decode_mc<128, 3, 0, 2>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
+  if (ny <= 4 || mc_cap < 8)
+    return launch_tc_decode_mc<128, 3, 0, 4>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
+  return launch_tc_decode_mc<128, 3, 0, 8>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
 }
 
 int fdmd_dmma_peak(double seconds, double* tflops) {

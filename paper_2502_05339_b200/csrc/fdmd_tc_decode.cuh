@@ -18,6 +18,14 @@
 // Warp roles: w0 TMA producer, w1 MMA issuer (one lane), w2..w9 epilogue
 // (TMEM lane quadrant = warp % 4, two warps per quadrant on column halves). The two accumulators let the epilogue of
 // tile t overlap the MMAs of tile t+1.
+//
+// Batches wider than one N tile (MC > 1): a cluster of MC CTAs along y covers
+// MC frame tiles of the SAME row tiles. Each CTA loads 1/MC of every A chunk
+// (128/MC rows) with .multicast::cluster into all MC CTAs' rings, so the basis
+// is read from HBM once per MC*BN frames instead of once per BN (unicast
+// siblings were measured to re-read it: B = 256 took 2x B = 128). A ring
+// stage is refilled only after all MC CTAs' MMAs released it: every MMA warp
+// commits to the aempty barrier of all cluster CTAs (count MC).
 #pragma once
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -65,6 +73,27 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
                ::"r"(smem_u32(bar)) : "memory");
 }
+// aempty of every CTA in the cluster (mask) once the issuing thread's MMAs retire
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+               ::"r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+// 2-D tile into the same smem offset (and mbarrier offset) of every CTA in mask
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 
@@ -93,14 +122,18 @@ struct TCArgs {
   const float* fscale; // per-frame output scale 2^-(su + sc_f)
 };
 
-// TMA maps: amap_h/amap_l over Us planes (dims {r, n}, box {64, 128}, SW128),
+// TMA maps: amap_h/amap_l over Us planes (dims {r, n}, box {64, 128 / MC}, SW128),
 //           bmap_h/bmap_l over Cs planes (dims {r, nf}, box {64, BN}, SW128).
-template <int BN, int AST, int BST>
+template <int BN, int AST, int BST, int MC>
 __global__ void __launch_bounds__(tc::THREADS, 1)
 tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_constant__ CUtensorMap amap_l,
                  const __grid_constant__ CUtensorMap bmap_h, const __grid_constant__ CUtensorMap bmap_l,
                  const TCArgs args) {
+  static_assert(MC == 1 || MC == 2 || MC == 4 || MC == 8, "cluster size");
   using SM = TCSmem<BN, AST, BST>;
+  constexpr int SLICE_ROWS = tc::BM / MC;                       // A rows this CTA loads per chunk
+  constexpr int SLICE_ELEMS = SLICE_ROWS * tc::BKC;            // multiple of one 8-row SW128 atom
+  constexpr uint16_t MC_MASK = (uint16_t)((1u << MC) - 1u);
   constexpr uint32_t TCOLS = 2 * BN;                  // two accumulators
   constexpr uint32_t B_CHUNK_BYTES = BN * tc::BKC * 2;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -114,7 +147,7 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
   const int f0 = blockIdx.y * BN;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < AST; ++s) { mbar_init(&sm.afull[s], 1); mbar_init(&sm.aempty[s], 1); }
+    for (int s = 0; s < AST; ++s) { mbar_init(&sm.afull[s], 1); mbar_init(&sm.aempty[s], MC); }
     for (int s = 0; s < SM::NB; ++s) { mbar_init(&sm.bfull[s], 1); mbar_init(&sm.bempty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], tc::EPI); }
     mbar_fence_init();
@@ -125,9 +158,11 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   tc_fence_before();
-  __syncthreads();
+  if (MC > 1) cluster_sync_all();   // peers' barriers are initialised before any multicast
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  const uint32_t crank = MC > 1 ? cluster_ctarank() : 0u;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -144,9 +179,15 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
         const int row0 = (int)((blockIdx.x + t * gridDim.x) * tc::BM);
         for (int c = 0; c < nkc; ++c) {
           mbar_wait(&sm.aempty[sa], pa ^ 1);
-          mbar_expect_tx(&sm.afull[sa], 2 * tc::A_CHUNK_BYTES);
-          tma_load_2d(sm.A[sa][0], &amap_h, c * tc::BKC, row0, &sm.afull[sa]);
-          tma_load_2d(sm.A[sa][1], &amap_l, c * tc::BKC, row0, &sm.afull[sa]);
+          mbar_expect_tx(&sm.afull[sa], 2 * tc::A_CHUNK_BYTES);   // all MC slices land here
+          if (MC == 1) {
+            tma_load_2d(sm.A[sa][0], &amap_h, c * tc::BKC, row0, &sm.afull[sa]);
+            tma_load_2d(sm.A[sa][1], &amap_l, c * tc::BKC, row0, &sm.afull[sa]);
+          } else {
+            const int rs = (int)crank * SLICE_ROWS;
+            tma_load_2d_mc(sm.A[sa][0] + crank * SLICE_ELEMS, &amap_h, c * tc::BKC, row0 + rs, &sm.afull[sa], MC_MASK);
+            tma_load_2d_mc(sm.A[sa][1] + crank * SLICE_ELEMS, &amap_l, c * tc::BKC, row0 + rs, &sm.afull[sa], MC_MASK);
+          }
           if (++sa == AST) { sa = 0; pa ^= 1; }
           if (BST > 0) {   // streamed coefficient chunk (from L2)
             mbar_wait(&sm.bempty[sb], pb ^ 1);
@@ -157,6 +198,13 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
           }
         }
       }
+      // producer tail (MC > 1): every peer's release of our ring has landed
+      // before this CTA may leave (remote commits target our barriers)
+      if (MC > 1)
+        for (int s = 0; s < AST; ++s) {
+          mbar_wait(&sm.aempty[sa], pa ^ 1);
+          if (++sa == AST) { sa = 0; pa ^= 1; }
+        }
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -187,7 +235,8 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
             umma_f16(d, al + adv, bh + adv, idesc, 1u);
             first = 0;
           }
-          umma_commit(&sm.aempty[sa]);             // frees the stages once these MMAs retire
+          if (MC == 1) umma_commit(&sm.aempty[sa]);   // frees the stage once these MMAs retire
+          else umma_commit_mc(&sm.aempty[sa], MC_MASK);
           if (BST > 0) {
             umma_commit(&sm.bempty[sb]);
             if (++sb == BST) { sb = 0; pb ^= 1; }
@@ -228,7 +277,9 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
       if (lane == 0) mbar_arrive(&sm.tempty[acc]);
     }
   }
-  __syncthreads();
+  __syncwarp();
+  if (MC > 1) cluster_sync_all();   // no CTA leaves while peers may still signal it
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS));

@@ -320,7 +320,7 @@ class ModalBasis:
         self._tc = None
 
     def coefficients(self, times) -> torch.Tensor:
-        t = torch.as_tensor(np.asarray(times, dtype=np.float64), device=self.U.buf.device)
+        t = torch.as_tensor(np.asarray(times, dtype=np.float64), device=self.W.device)
         Lt = torch.exp(self.omega[:, None] * t[None, :].to(torch.complex128)) * self.b[:, None]
         return (self.W @ Lt).real.contiguous()      # r x B
 
@@ -329,8 +329,17 @@ class ModalBasis:
             self._tc = dv.get_ops().tc_basis(self.U)
         return self._tc
 
+    def release_fp32(self):
+        """Drop this object's reference to the fp32 basis once the tcgen05
+        planes exist (same bytes): frees HBM for wider frame batches; every
+        batch size then runs on the tcgen05 kernel."""
+        if not self.use_tc:
+            raise ValueError("release_fp32 needs the tcgen05 path (fp32 CUDA basis)")
+        self.tc_state()
+        self.U = None
+
     def reconstruct(self, times, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         C = self.coefficients(times)
-        if self.use_tc and C.shape[1] >= self.TC_MIN_BATCH:
+        if self.use_tc and (C.shape[1] >= self.TC_MIN_BATCH or self.U is None):
             return dv.get_ops().tc_decode(self.tc_state(), C, out=out)
         return dv.get_ops().decode(self.U, C, out=out)

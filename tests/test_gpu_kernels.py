@@ -232,9 +232,12 @@ def test_decode(dv, dtype, B, n, r):
 
 
 @pytest.mark.parametrize("n,r,B", [(100003, 200, 32), (5000, 150, 128), (70000, 200, 300), (257, 7, 16),
-                                   (100000, 256, 129)])
+                                   (100000, 256, 129), (70001, 200, 512), (30011, 150, 1024), (5000, 64, 640),
+                                   (300, 200, 384), (40000, 200, 2100)])
 def test_tc_decode_fp16_split(dv, n, r, B):
-    """tcgen05 2-way FP16 split reconstruction: FP32-accurate (rel-L2 per frame)."""
+    """tcgen05 2-way FP16 split reconstruction: FP32-accurate (rel-L2 per frame).
+    B > 128 runs as clusters of 2/4/8 CTAs sharing basis chunks by TMA
+    multicast (ragged cluster tails: B = 300, 640, 2100)."""
     rng = np.random.default_rng(n + r + B)
     U = np.linalg.qr(rng.standard_normal((n, r)))[0] if n >= r else rng.standard_normal((n, r))
     U = U.astype(np.float32).astype(np.float64)

@@ -18,6 +18,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=50331648)
     ap.add_argument("--r", type=int, default=200)
+    ap.add_argument("--batches", type=int, nargs="*", default=[32, 128, 256, 384, 512, 640])
     a = ap.parse_args()
     n, r = a.n, a.r
     ops = dv.get_ops()
@@ -27,7 +28,9 @@ def main():
     del U
     torch.cuda.empty_cache()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    for B in (32, 128, 256):
+    free, total = torch.cuda.mem_get_info()
+    print(f"mem free {free/1e9:.1f} GB of {total/1e9:.1f} GB after the split basis")
+    for B in a.batches:
         coef = torch.randn(r, B, dtype=torch.float32, device="cuda")
         out = torch.empty((B, n), dtype=torch.float32, device="cuda")
         ops.tc_decode(tcb, coef, out=out)
@@ -39,6 +42,7 @@ def main():
         gbs = (4.0 * n * r + 4.0 * n * B) / ms / 1e6
         print(f"tc_decode B={B:5d}  {ms:8.3f} ms  {B / ms * 1e3:9.1f} frames/s  {gbs:8.1f} GB/s")
         del out
+        torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":

@@ -1,7 +1,8 @@
 import sys, torch
 sys.path.insert(0, '.')
 from paper_2502_05339_b200 import device as dv
-n, r, B = 12582912, 200, 128
+n, r = 12582912, 200
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 ops = dv.get_ops()
 U = dv.alloc_tall(n, r, torch.float32, "col"); U.buf.normal_()
 tcb = ops.tc_basis(U)
