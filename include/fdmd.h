@@ -17,6 +17,9 @@
  *   fdmd_residual      provenance["residual"] (dmd.py:269-272)
  *   fdmd_geev          np.linalg.eig in eig_small (linalg.py:120) — cuSOLVER Xgeev
  *   fdmd_synth3d       BASELINE.json configs 1-4 snapshot generator (device)
+ *   fdmd_mac_*         2-D serving / guided upscaling: frame planes (server.py:205-214),
+ *                      density transport (solver.py:133-150), injection and the
+ *                      guide projection (upres.py:21-50, 154-169)
  *
  * Conventions: every pointer argument is DEVICE memory unless named *_host;
  * `stream` is a cudaStream_t (NULL = legacy default stream). Calls are
@@ -123,6 +126,37 @@ int fdmd_split_coef(const float* coef, int ldc, int r, int nf, float su_inv, voi
                     float* fscale, void* stream);
 int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch, const void* cl,
                    int ldk, int nf, const float* fscale, float* out, int64_t ldo, void* stream);
+
+/* ---- 2-D MAC-grid serving / guided upscaling ----
+ * State layout (grid.py:1-18): u block ny x (nx+1), then v block (ny+1) x nx. */
+#define FDMD_MAC_VELOCITY 0
+#define FDMD_MAC_SPEED 1
+
+/* Fused decode -> cell-centred planes. Replaces ModelServer.frame_payload's
+ * decode(model, z) + unflatten + centring (+ speed) (server.py:205-214).
+ * D: column-major decode table (ncol x n_state, ld ldd, dtype F32/F64);
+ * coef: ncol f64 table coefficients (device). out: f64, VELOCITY -> 2 planes
+ * [uc; vc] of ny x nx, SPEED -> 1 plane sqrt(uc^2 + vc^2). */
+int fdmd_mac_decode(const void* D, int dtype, int64_t ldd, int ncol, const double* coef, int nx, int ny,
+                    int field, double* out, void* stream);
+
+/* Semi-Lagrangian transport of a cell-centred scalar q (ny x nx f64) for
+ * one step dt through the flat MAC velocity `vel` (dtype F32/F64).
+ * Replaces advect_semi_lagrangian(vel, ScalarField, dt) (solver.py:167-171,
+ * 133-150 with maccormack=False) as used by server.py:232 and runtime.py:259. */
+int fdmd_mac_advect(const void* vel, int dtype, int nx, int ny, double h, double dt, const double* q, double* q_out,
+                    void* stream);
+
+/* Nearest-face prolongation of nv coarse states (ld_low apart) onto the
+ * fine grid (ld_fine apart): build_inject(high, factor) @ L (upres.py:21-50, 121). */
+int fdmd_mac_inject(const double* low, int nx_high, int ny_high, int factor, int nv, int64_t ld_low,
+                    int64_t ld_fine, double* fine, void* stream);
+
+/* Guide-consistency projection x = H + A^T (A A^T)^-1 (L - A H) for the
+ * face-averaging downsample A (grid.py:195-236); A A^T = gram_diag * I.
+ * Replaces build_projector + constrained_project (upres.py:140-169). */
+int fdmd_mac_project(const double* H, const double* L, int nx_high, int ny_high, int factor, double gram_diag,
+                     double* x, void* stream);
 
 /* FP64 tensor-pipe (DMMA.8x8x4) throughput probe on the current device:
  * a register-only mma.sync f64 loop lasting ~`seconds`/4; writes TFLOP/s.

@@ -530,3 +530,134 @@ def controlled_system(n, pairs, ell, m, seed, noise=0.0):
     if noise:
         X = X + noise * rng.standard_normal(X.shape)
     return X, U, np.asarray(eigs), Bf
+
+
+# --------------------------------------------------------------------------
+# §8(f) rows 2-3: MAC grids, serving frames, spectral editing, guided
+# upscaling (grid.py, solver.py, server.py, editing.py, upres.py)
+# --------------------------------------------------------------------------
+
+def mac_sizes(nx, ny):
+    """grid.py:67-82 — (n_u, n_v)."""
+    return (nx + 1) * ny, nx * (ny + 1)
+
+
+def build_downsample(nx, ny, f):
+    """grid.py:195-236 — face-averaging restriction (scipy CSR, entry order t = 0..f-1)."""
+    import scipy.sparse as sp
+    nxl, nyl = nx // f, ny // f
+    n_u, _ = mac_sizes(nx, ny)
+    nl_u, nl_v = mac_sizes(nxl, nyl)
+    rows, cols, vals = [], [], []
+    jl, il = np.meshgrid(np.arange(nyl), np.arange(nxl + 1), indexing="ij")
+    low = (jl * (nxl + 1) + il).ravel()
+    for t in range(f):
+        rows.append(low)
+        cols.append(((jl * f + t) * (nx + 1) + il * f).ravel())
+        vals.append(np.full(low.size, 1.0 / f))
+    jl, il = np.meshgrid(np.arange(nyl + 1), np.arange(nxl), indexing="ij")
+    low = (nl_u + jl * nxl + il).ravel()
+    for t in range(f):
+        rows.append(low)
+        cols.append((n_u + (jl * f) * nx + il * f + t).ravel())
+        vals.append(np.full(low.size, 1.0 / f))
+    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(nl_u + nl_v, sum(mac_sizes(nx, ny))))
+
+
+def build_inject(nx, ny, f):
+    """upres.py:21-50 — nearest-face prolongation (scipy CSR, ones)."""
+    import scipy.sparse as sp
+    nxl, nyl = nx // f, ny // f
+    n_u, _ = mac_sizes(nx, ny)
+    nl_u, nl_v = mac_sizes(nxl, nyl)
+    jh, ih = np.meshgrid(np.arange(ny), np.arange(nx + 1), indexing="ij")
+    r1 = (jh * (nx + 1) + ih).ravel()
+    c1 = ((jh // f) * (nxl + 1) + np.minimum((ih + f // 2) // f, nxl)).ravel()
+    jh, ih = np.meshgrid(np.arange(ny + 1), np.arange(nx), indexing="ij")
+    r2 = (n_u + jh * nx + ih).ravel()
+    c2 = (nl_u + np.minimum((jh + f // 2) // f, nyl) * nxl + ih // f).ravel()
+    rows = np.concatenate([r1, r2])
+    return sp.csr_matrix((np.ones(rows.size), (rows, np.concatenate([c1, c2]))),
+                         shape=(sum(mac_sizes(nx, ny)), nl_u + nl_v))
+
+
+def center_planes(flat, nx, ny, field):
+    """server.py:205-214 — cell-centred velocity planes or speed."""
+    n_u, _ = mac_sizes(nx, ny)
+    u = flat[:n_u].reshape(ny, nx + 1)
+    v = flat[n_u:].reshape(ny + 1, nx)
+    uc = 0.5 * (u[:, :-1] + u[:, 1:])
+    vc = 0.5 * (v[:-1, :] + v[1:, :])
+    if field == "velocity":
+        return np.stack([uc, vc])
+    return np.sqrt(uc * uc + vc * vc)[None, :, :]
+
+
+def encode_planes(planes, fmt):
+    """server.py:288-302 — 12-byte header + f32 / u8 planes."""
+    channels, ny, nx = planes.shape
+    header = np.asarray([nx, ny, channels], dtype="<u4").tobytes()
+    if fmt == "bin":
+        return header + planes.astype("<f4").tobytes()
+    lo, hi = planes.min(), planes.max()
+    span = hi - lo
+    if span <= 0:
+        data = np.zeros(planes.shape, dtype=np.uint8)
+    else:
+        data = np.clip((planes - lo) / span * 255.0, 0, 255).astype(np.uint8)
+    return header + data.tobytes()
+
+
+def bilinear(f, col, row):
+    """solver.py:79-101 (values only)."""
+    nr, nc = f.shape
+    col = np.clip(col, 0.0, nc - 1.0)
+    row = np.clip(row, 0.0, nr - 1.0)
+    i0 = np.minimum(col.astype(np.int64), nc - 2)
+    j0 = np.minimum(row.astype(np.int64), nr - 2)
+    tx = col - i0
+    ty = row - j0
+    return (f[j0, i0] * (1 - tx) * (1 - ty) + f[j0, i0 + 1] * tx * (1 - ty)
+            + f[j0 + 1, i0] * (1 - tx) * ty + f[j0 + 1, i0 + 1] * tx * ty)
+
+
+def advect_density(flat, nx, ny, h, q, dt):
+    """solver.py:133-150 (maccormack=False, cell centres) via 104-108, 111-121."""
+    n_u, _ = mac_sizes(nx, ny)
+    u = flat[:n_u].reshape(ny, nx + 1)
+    v = flat[n_u:].reshape(ny + 1, nx)
+    j, i = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+    X, Y = (i + 0.5) * h, (j + 0.5) * h
+    up = bilinear(u, X / h, Y / h - 0.5)
+    vp = bilinear(v, X / h - 0.5, Y / h)
+    return bilinear(q, (X - dt * up) / h - 0.5, (Y - dt * vp) / h - 0.5)
+
+
+def apply_edit(phi, lam, dt, weights, growth, freq):
+    """editing.py:130-149 — (new phi, new lam)."""
+    part = partner_map(lam)
+    om = np.log(lam) / dt
+    new_lam = np.exp((growth * om.real + 1j * freq * om.imag) * dt)
+    new_phi = phi * weights[None, :]
+    for a in range(lam.size):
+        b = part[a]
+        if b > a:
+            new_lam[b] = np.conj(new_lam[a])
+            new_phi[:, b] = np.conj(new_phi[:, a])
+    return new_phi, new_lam
+
+
+def constrained_project(nx, ny, f, H, L):
+    """upres.py:142-169 — x = H + A^T (A A^T)^-1 (L - A H) with SuperLU."""
+    import scipy.sparse.linalg as spla
+    A = build_downsample(nx, ny, f)
+    lu = spla.splu((A @ A.T).tocsc())
+    return H + A.T @ lu.solve(L - A @ H)
+
+
+def upres_step(phi, lam, z, L, nx, ny, f, split):
+    """upres.py:110-130 — (new z, decoded field); split already effective."""
+    P = encode(phi, build_inject(nx, ny, f) @ L)
+    zn = np.concatenate([P[:split], (lam * z)[split:]])
+    return zn, decode(phi, lam, zn)

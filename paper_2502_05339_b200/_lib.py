@@ -51,6 +51,10 @@ SIGNATURES = {
     "fdmd_split_basis": (_i, [_vp, _i64, _i64, _i, _c.c_float, _vp, _vp, _i64, _vp]),
     "fdmd_split_coef": (_i, [_vp, _i, _i, _i, _c.c_float, _vp, _vp, _i, _vp, _vp]),
     "fdmd_tc_decode": (_i, [_vp, _vp, _i64, _i64, _i, _vp, _vp, _i, _i, _vp, _vp, _i64, _vp]),
+    "fdmd_mac_decode": (_i, [_vp, _i, _i64, _i, _vp, _i, _i, _i, _vp, _vp]),
+    "fdmd_mac_advect": (_i, [_vp, _i, _i, _i, _d, _d, _vp, _vp, _vp]),
+    "fdmd_mac_inject": (_i, [_vp, _i, _i, _i, _i, _i64, _i64, _vp, _vp]),
+    "fdmd_mac_project": (_i, [_vp, _vp, _i, _i, _i, _d, _vp, _vp]),
     "fdmd_synth3d": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _d, _u64, _i64, _i64, _vp, _i, _i64, _vp]),
 }
 

@@ -1011,6 +1011,75 @@ int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r
   return launch_tc_decode_mc<128, 3, 0, 8>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
 }
 
+int fdmd_mac_decode(const void* D, int dtype, int64_t ldd, int ncol, const double* coef, int nx, int ny,
+                    int field, double* out, void* stream) {
+  if (!D || !coef || !out || ncol <= 0 || nx < 2 || ny < 2) return fail(FDMD_ERR_INVALID, "mac_decode: bad arguments");
+  if (field != FDMD_MAC_VELOCITY && field != FDMD_MAC_SPEED) return fail(FDMD_ERR_INVALID, "mac_decode: bad field");
+  const int64_t n = (int64_t)(nx + 1) * ny + (int64_t)nx * (ny + 1);
+  if (ldd < n) return fail(FDMD_ERR_INVALID, "mac_decode: ldd < n_state");
+  // TJ cell rows per CTA: faces staged in <= 48 KB of shared memory
+  const size_t per_row = (size_t)(2 * nx + 1) * sizeof(double);
+  const size_t fixed = (size_t)(((ncol + 1) & ~1) + nx) * sizeof(double);
+  if (fixed + per_row > 200 * 1024) return fail(FDMD_ERR_INVALID, "mac_decode: grid row too wide");
+  int tj = (int)std::max<size_t>(1, std::min<size_t>(8, (48 * 1024 - std::min<size_t>(fixed, 48 * 1024)) / per_row));
+  tj = std::min(tj, ny);
+  const size_t smem = fixed + (size_t)tj * per_row;
+  const int blocks = (ny + tj - 1) / tj;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == FDMD_F32) {
+    auto k = fdmd::mac_decode_kernel<float>;
+    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<blocks, 256, smem, s>>>((const float*)D, ldd, ncol, coef, nx, ny, tj, field, out);
+  } else {
+    auto k = fdmd::mac_decode_kernel<double>;
+    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<blocks, 256, smem, s>>>((const double*)D, ldd, ncol, coef, nx, ny, tj, field, out);
+  }
+  LAUNCH_CHECK("mac_decode");
+  return FDMD_OK;
+}
+
+int fdmd_mac_advect(const void* vel, int dtype, int nx, int ny, double h, double dt, const double* q, double* q_out,
+                    void* stream) {
+  if (!vel || !q || !q_out || nx < 2 || ny < 2 || !(h > 0)) return fail(FDMD_ERR_INVALID, "mac_advect: bad arguments");
+  if (q == q_out) return fail(FDMD_ERR_INVALID, "mac_advect: q_out must not alias q");
+  const int64_t cells = (int64_t)nx * ny;
+  const int blocks = (int)((cells + 255) / 256);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == FDMD_F32)
+    fdmd::mac_advect_kernel<float><<<blocks, 256, 0, s>>>((const float*)vel, nx, ny, h, dt, q, q_out);
+  else
+    fdmd::mac_advect_kernel<double><<<blocks, 256, 0, s>>>((const double*)vel, nx, ny, h, dt, q, q_out);
+  LAUNCH_CHECK("mac_advect");
+  return FDMD_OK;
+}
+
+int fdmd_mac_inject(const double* low, int nx_high, int ny_high, int factor, int nv, int64_t ld_low,
+                    int64_t ld_fine, double* fine, void* stream) {
+  if (!low || !fine || factor < 2 || nx_high % factor || ny_high % factor || nv < 1)
+    return fail(FDMD_ERR_INVALID, "mac_inject: bad arguments");
+  const int64_t nh = (int64_t)(nx_high + 1) * ny_high + (int64_t)nx_high * (ny_high + 1);
+  const int nxl = nx_high / factor, nyl = ny_high / factor;
+  const int64_t nl = (int64_t)(nxl + 1) * nyl + (int64_t)nxl * (nyl + 1);
+  if (ld_low < nl || ld_fine < nh) return fail(FDMD_ERR_INVALID, "mac_inject: bad leading dimension");
+  fdmd::mac_inject_kernel<<<(unsigned)((nh + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      low, nx_high, ny_high, factor, nv, ld_low, ld_fine, fine);
+  LAUNCH_CHECK("mac_inject");
+  return FDMD_OK;
+}
+
+int fdmd_mac_project(const double* H, const double* L, int nx_high, int ny_high, int factor, double gram_diag,
+                     double* x, void* stream) {
+  if (!H || !L || !x || factor < 2 || nx_high % factor || ny_high % factor || !(gram_diag > 0))
+    return fail(FDMD_ERR_INVALID, "mac_project: bad arguments");
+  if (x == H) return fail(FDMD_ERR_INVALID, "mac_project: x must not alias H");
+  const int64_t nh = (int64_t)(nx_high + 1) * ny_high + (int64_t)nx_high * (ny_high + 1);
+  fdmd::mac_project_kernel<<<(unsigned)((nh + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      H, L, nx_high, ny_high, factor, 1.0 / factor, gram_diag, x);
+  LAUNCH_CHECK("mac_project");
+  return FDMD_OK;
+}
+
 int fdmd_dmma_peak(double seconds, double* tflops) {
   if (!tflops || seconds <= 0) return fail(FDMD_ERR_INVALID, "dmma_peak: bad arguments");
   double* d = nullptr;

@@ -267,6 +267,56 @@ class CudaOps:
         self.launches += 2
         return y
 
+    # -- 2-D MAC grids: serving / guided upscaling --------------------------
+    def mac_decode(self, D: Tall, coef: torch.Tensor, nx: int, ny: int, field: str,
+                   ncols: Optional[int] = None) -> torch.Tensor:
+        """Cell-centred planes (f64, (2|1) x ny x nx) of the decoded state."""
+        assert D.layout == "col"
+        r = int(coef.numel()) if ncols is None else ncols
+        coef = coef.reshape(-1).to(device=D.buf.device, dtype=torch.float64).contiguous()
+        code = {"velocity": 0, "speed": 1}[field]
+        out = torch.empty((2 if code == 0 else 1, ny, nx), dtype=torch.float64, device=D.buf.device)
+        _lib.check(_lib.lib().fdmd_mac_decode(_ptr(D.buf), _DT[D.dtype], D.ld, r, _ptr(coef), nx, ny, code,
+                                              _ptr(out), _stream()), "mac_decode")
+        self.launches += 1
+        return out
+
+    def mac_advect(self, vel: torch.Tensor, nx: int, ny: int, h: float, dt: float,
+                   q: torch.Tensor) -> torch.Tensor:
+        """One semi-Lagrangian step of the cell-centred scalar q (ny x nx f64)."""
+        vel = vel.reshape(-1).contiguous()
+        if vel.dtype not in (torch.float32, torch.float64):
+            vel = vel.to(torch.float64)
+        q = q.to(torch.float64).contiguous()
+        out = torch.empty_like(q)
+        _lib.check(_lib.lib().fdmd_mac_advect(_ptr(vel), _DT[vel.dtype], nx, ny, float(h), float(dt), _ptr(q),
+                                              _ptr(out), _stream()), "mac_advect")
+        self.launches += 1
+        return out
+
+    def mac_inject(self, low: torch.Tensor, nx: int, ny: int, factor: int) -> torch.Tensor:
+        """(nv, n_state_high) fine states from (nv, n_state_low) coarse states."""
+        low = low.to(torch.float64)
+        if low.dim() == 1:
+            low = low[None, :]
+        low = low.contiguous()
+        nh = (nx + 1) * ny + nx * (ny + 1)
+        fine = torch.empty((low.shape[0], nh), dtype=torch.float64, device=low.device)
+        _lib.check(_lib.lib().fdmd_mac_inject(_ptr(low), nx, ny, factor, int(low.shape[0]), low.stride(0),
+                                              fine.stride(0), _ptr(fine), _stream()), "mac_inject")
+        self.launches += 1
+        return fine
+
+    def mac_project(self, H: torch.Tensor, L: torch.Tensor, nx: int, ny: int, factor: int,
+                    gram_diag: float) -> torch.Tensor:
+        H = H.reshape(-1).to(torch.float64).contiguous()
+        L = L.reshape(-1).to(device=H.device, dtype=torch.float64).contiguous()
+        x = torch.empty_like(H)
+        _lib.check(_lib.lib().fdmd_mac_project(_ptr(H), _ptr(L), nx, ny, factor, float(gram_diag), _ptr(x),
+                                               _stream()), "mac_project")
+        self.launches += 1
+        return x
+
     def table_apply(self, R: Tall, src, alpha, beta, D: Tall, ncols: int):
         dev = R.buf.device
         src_t = torch.as_tensor(np.asarray(src, dtype=np.int32), device=dev)

@@ -33,6 +33,7 @@ import torch
 
 from . import device as dv
 from .device import alloc_tall
+from .grid import GridSpec  # noqa: F401  (re-export)
 from .errors import BadMagicError, BadVersionError, ChecksumError, SizeMismatchError
 
 MAGIC = b"KDMD"
@@ -112,22 +113,7 @@ def parse_floats(text: str) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # grid metadata block (model_io.py:107-140)
 # ---------------------------------------------------------------------------
-@dataclasses.dataclass
-class GridSpec:
-    """Grid metadata carried by models and datasets (grid.py:27-56). Only the
-    fields the file formats store; the solver-side behaviour of the
-    reference's GridSpec is outside this package."""
-
-    nx: int
-    ny: int
-    h: float
-    boundary: str = "closed"
-    solid_mask: Optional[np.ndarray] = None
-
-    def solids(self) -> np.ndarray:
-        if self.solid_mask is None:
-            return np.zeros((self.ny, self.nx), dtype=bool)
-        return np.asarray(self.solid_mask, dtype=bool).reshape(self.ny, self.nx)
+# GridSpec lives in grid.py (reference grid.py:27-97); re-exported here.
 
 
 def grid_to_kv(grid) -> dict:

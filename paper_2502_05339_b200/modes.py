@@ -126,6 +126,9 @@ class DeviceModes:
         self.general = general
         self.mix = None if mix is None else np.asarray(mix, dtype=np.float64)
         self._pinv_small = None
+        # Gram of the raw table (D^T D, all raw columns): shared by every model
+        # derived from the same table (editing.apply_edit folds into the mix)
+        self.raw_gram = None
 
     @property
     def n_local(self) -> int:
@@ -153,7 +156,12 @@ class DeviceModes:
         Hermitian Gram phi^H phi = E^H (D^T D) E (eigh on the device)."""
         if self._pinv_small is None:
             D, E = self.basis()
-            G = allreduce(self.shard, dv.get_ops().tall_gram(D, D, symmetric=True))
+            if self.general is None and self.raw_gram is not None:
+                G = self.raw_gram
+            else:
+                G = allreduce(self.shard, dv.get_ops().tall_gram(D, D, symmetric=True))
+                if self.general is None:
+                    self.raw_gram = G
             Et = torch.as_tensor(E, device=G.device)
             H = Et.mH @ G.to(torch.complex128) @ Et
             H = 0.5 * (H + H.mH)

@@ -224,13 +224,22 @@ def rollout(model, z0, frames, ctrl=None, q_seq=None, f_seq=None, edit=None, den
     """Repeatedly step and decode (runtime.py:209-264). The per-frame states are
     advanced on the host (O(r)); all frames are then decoded in one batched
     device GEMM when every state is conjugate-symmetric (the invariant every
-    path here preserves), else frame by frame."""
+    path here preserves), else frame by frame. `edit` folds into the model's
+    mix (editing.apply_edit); `density0` (ScalarField or ny x nx array) is
+    advected on the device through the decoded frames and returned as an
+    (ny, nx, frames) array."""
     if frames < 1:
         raise ValueError("frames must be >= 1")
     if edit is not None:
-        raise NotImplementedError("spectral editing is outside the B200 hot path (SURVEY.md §2.1 row 6)")
+        from .editing import apply_edit
+        model = apply_edit(model, edit)            # folds into the mix; no n-sized copy
+    density = None
     if density0 is not None:
-        raise NotImplementedError("density advection is outside the B200 hot path (SURVEY.md §2.1 row 9)")
+        from .grid import is_grid
+        if not is_grid(model.grid_meta):
+            raise ValueError("density advection needs grid metadata on the model")
+        density = torch.as_tensor(np.asarray(getattr(density0, "values", density0), dtype=np.float64),
+                                  device=_dev(model))
     s = _as_state(z0)
     Z = np.empty((model.r, frames), dtype=np.complex128)
     for k in range(frames):
@@ -243,9 +252,20 @@ def rollout(model, z0, frames, ctrl=None, q_seq=None, f_seq=None, edit=None, den
             s = step(model, s)
         Z[:, k] = s.z
     out = decode_batch(model, Z)
+    densities = None
+    if density is not None:
+        # smoke advected through each decoded frame on the device (runtime.py:255-262)
+        g = model.grid_meta
+        ops = dv.get_ops()
+        dt = -model.dt if backward else model.dt
+        dens = torch.empty((frames, g.ny, g.nx), dtype=torch.float64, device=density.device)
+        for k in range(frames):
+            density = ops.mac_advect(out[k], g.nx, g.ny, g.h, dt, density)
+            dens[k].copy_(density)
+        densities = dens.permute(1, 2, 0).cpu().numpy() if to_host else dens
     if to_host:
-        return _to_host_f64(out).T, None
-    return out, None
+        return _to_host_f64(out).T, densities
+    return out, densities
 
 
 def decode_batch(model, Z, out: Optional[torch.Tensor] = None) -> torch.Tensor:
