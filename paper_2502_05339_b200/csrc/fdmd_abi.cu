@@ -1017,23 +1017,19 @@ int fdmd_mac_decode(const void* D, int dtype, int64_t ldd, int ncol, const doubl
   if (field != FDMD_MAC_VELOCITY && field != FDMD_MAC_SPEED) return fail(FDMD_ERR_INVALID, "mac_decode: bad field");
   const int64_t n = (int64_t)(nx + 1) * ny + (int64_t)nx * (ny + 1);
   if (ldd < n) return fail(FDMD_ERR_INVALID, "mac_decode: ldd < n_state");
-  // TJ cell rows per CTA: faces staged in <= 48 KB of shared memory
-  const size_t per_row = (size_t)(2 * nx + 1) * sizeof(double);
-  const size_t fixed = (size_t)(((ncol + 1) & ~1) + nx) * sizeof(double);
-  if (fixed + per_row > 200 * 1024) return fail(FDMD_ERR_INVALID, "mac_decode: grid row too wide");
-  int tj = (int)std::max<size_t>(1, std::min<size_t>(8, (48 * 1024 - std::min<size_t>(fixed, 48 * 1024)) / per_row));
-  tj = std::min(tj, ny);
-  const size_t smem = fixed + (size_t)tj * per_row;
-  const int blocks = (ny + tj - 1) / tj;
+  const size_t smem = (size_t)(((ncol + 1) & ~1) + fdmd::MAC_TY * (fdmd::MAC_TX + 1) +
+                                (fdmd::MAC_TY + 1) * fdmd::MAC_TX) * sizeof(double);
+  if (smem > 200 * 1024) return fail(FDMD_ERR_INVALID, "mac_decode: too many table columns");
+  const dim3 grid((nx + fdmd::MAC_TX - 1) / fdmd::MAC_TX, (ny + fdmd::MAC_TY - 1) / fdmd::MAC_TY);
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == FDMD_F32) {
     auto k = fdmd::mac_decode_kernel<float>;
     if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<blocks, 256, smem, s>>>((const float*)D, ldd, ncol, coef, nx, ny, tj, field, out);
+    k<<<grid, 256, smem, s>>>((const float*)D, ldd, ncol, coef, nx, ny, field, out);
   } else {
     auto k = fdmd::mac_decode_kernel<double>;
     if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<blocks, 256, smem, s>>>((const double*)D, ldd, ncol, coef, nx, ny, tj, field, out);
+    k<<<grid, 256, smem, s>>>((const double*)D, ldd, ncol, coef, nx, ny, field, out);
   }
   LAUNCH_CHECK("mac_decode");
   return FDMD_OK;

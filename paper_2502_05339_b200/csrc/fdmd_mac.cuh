@@ -22,40 +22,66 @@ namespace fdmd {
 constexpr int MAC_VELOCITY = 0;
 constexpr int MAC_SPEED = 1;
 
-// One CTA per TJ cell rows: the faces those rows need (u rows j0..j0+TJ-1,
-// v rows j0..j0+TJ) are decoded into shared memory once (HBM-coalesced over
-// the column-major table, one face per thread per pass), then centred.
+// One CTA per tile of MAC_TY x MAC_TX cells: the faces the tile needs
+// (u rows j0..j0+TY-1 x cols i0..i0+TX, v rows j0..j0+TY x cols i0..i0+TX-1)
+// are decoded into shared memory (consecutive threads take consecutive faces
+// of a row, so every table load is a coalesced 256-B warp access; the k loop
+// keeps 8 independent loads in flight per thread), then centred. Halo
+// overhead: 1/TX of the u faces and 1/TY of the v faces are decoded twice.
+constexpr int MAC_TX = 128;
+constexpr int MAC_TY = 8;
+
 template <typename T>
 __global__ void __launch_bounds__(256) mac_decode_kernel(const T* __restrict__ D, int64_t ldd, int ncol,
-                                                         const double* __restrict__ coef, int nx, int ny, int TJ,
+                                                         const double* __restrict__ coef, int nx, int ny,
                                                          int field, double* __restrict__ out) {
   extern __shared__ __align__(16) double msm[];
-  double* cs = msm;                          // ncol
-  double* us = cs + ((ncol + 1) & ~1);       // TJ x (nx+1)
-  double* vs = us + (int64_t)TJ * (nx + 1);  // (TJ+1) x nx
+  double* cs = msm;                                  // ncol (padded to even)
+  double* us = cs + ((ncol + 1) & ~1);               // TY x (TX+1)
+  double* vs = us + MAC_TY * (MAC_TX + 1);           // (TY+1) x TX
   for (int k = threadIdx.x; k < ncol; k += blockDim.x) cs[k] = coef[k];
   __syncthreads();
-  const int j0 = blockIdx.x * TJ;
-  const int rows = min(TJ, ny - j0);
+  const int i0 = blockIdx.x * MAC_TX, j0 = blockIdx.y * MAC_TY;
+  const int cols = min(MAC_TX, nx - i0), rows = min(MAC_TY, ny - j0);
   const int64_t n_u = (int64_t)(nx + 1) * ny;
-  const int nu_loc = rows * (nx + 1), nv_loc = (rows + 1) * nx;
+  const int uw = cols + 1;
+  const int nu_loc = rows * uw, nv_loc = (rows + 1) * cols;
   for (int e = threadIdx.x; e < nu_loc + nv_loc; e += blockDim.x) {
-    const int64_t idx = e < nu_loc ? (int64_t)j0 * (nx + 1) + e : n_u + (int64_t)j0 * nx + (e - nu_loc);
-    double acc = 0.0;
+    int64_t idx;
+    int slot;
+    if (e < nu_loc) {
+      const int jj = e / uw, ii = e - jj * uw;
+      idx = (int64_t)(j0 + jj) * (nx + 1) + i0 + ii;
+      slot = jj * (MAC_TX + 1) + ii;
+    } else {
+      const int ev = e - nu_loc, jj = ev / cols, ii = ev - jj * cols;
+      idx = n_u + (int64_t)(j0 + jj) * nx + i0 + ii;
+      slot = MAC_TY * (MAC_TX + 1) + jj * MAC_TX + ii;
+    }
     const T* d = D + idx;
-#pragma unroll 4
-    for (int k = 0; k < ncol; ++k) acc = fma((double)d[(int64_t)k * ldd], cs[k], acc);
-    if (e < nu_loc) us[e] = acc;
-    else vs[e - nu_loc] = acc;
+    double a0 = 0.0, a1 = 0.0;
+    int k = 0;
+    for (; k + 8 <= ncol; k += 8) {
+      T x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldcs(d + (int64_t)(k + u) * ldd);
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        a0 = fma((double)x[u], cs[k + u], a0);
+        a1 = fma((double)x[u + 1], cs[k + u + 1], a1);
+      }
+    }
+    for (; k < ncol; ++k) a0 = fma((double)__ldcs(d + (int64_t)k * ldd), cs[k], a0);
+    msm[((ncol + 1) & ~1) + slot] = a0 + a1;
   }
   __syncthreads();
   const int64_t plane = (int64_t)nx * ny;
-  for (int e = threadIdx.x; e < rows * nx; e += blockDim.x) {
-    const int jj = e / nx, i = e - jj * nx;
+  for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+    const int jj = e / cols, ii = e - jj * cols;
     // 0.5 * (u[:, :-1] + u[:, 1:]), 0.5 * (v[:-1, :] + v[1:, :])
-    const double uc = __dmul_rn(0.5, __dadd_rn(us[jj * (nx + 1) + i], us[jj * (nx + 1) + i + 1]));
-    const double vc = __dmul_rn(0.5, __dadd_rn(vs[jj * nx + i], vs[(jj + 1) * nx + i]));
-    const int64_t o = (int64_t)(j0 + jj) * nx + i;
+    const double uc = __dmul_rn(0.5, __dadd_rn(us[jj * (MAC_TX + 1) + ii], us[jj * (MAC_TX + 1) + ii + 1]));
+    const double vc = __dmul_rn(0.5, __dadd_rn(vs[jj * MAC_TX + ii], vs[(jj + 1) * MAC_TX + ii]));
+    const int64_t o = (int64_t)(j0 + jj) * nx + i0 + ii;
     if (field == MAC_VELOCITY) {
       out[o] = uc;
       out[plane + o] = vc;

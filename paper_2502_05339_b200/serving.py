@@ -26,6 +26,8 @@ the calling thread's current CUDA stream.
 
 from __future__ import annotations
 
+import contextlib
+import functools
 import threading
 import uuid
 
@@ -38,6 +40,35 @@ from .errors import EigenvalueFloorError
 from .grid import ScalarField, component_positions, is_grid
 from .runtime import INVERSE_FLOOR, ReducedState, _conjugate_symmetry_defect, encode, step_forced, step_k
 from . import upres as _upres
+
+
+_tls = threading.local()
+
+
+@contextlib.contextmanager
+def request_stream(device):
+    """Each server thread issues its requests on its own CUDA stream: the
+    stream-keyed scratch buffers (device.CudaOps workspaces) and the
+    allocator's per-stream pools then never interleave between requests
+    running concurrently on different threads."""
+    streams = getattr(_tls, "streams", None)
+    if streams is None:
+        streams = _tls.streams = {}
+    st = streams.get(str(device))
+    if st is None:
+        st = streams[str(device)] = torch.cuda.Stream(device=device)
+    st.wait_stream(torch.cuda.default_stream(device))   # inputs staged on the default stream
+    with torch.cuda.stream(st):
+        yield st
+    st.synchronize()   # synchronous on return: session tensors are complete for any thread
+
+
+def _on_request_stream(fn):
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        with request_stream(_device(self.model)):
+            return fn(self, *args, **kwargs)
+    return wrapper
 
 
 def shift_state(model, z, delta, floor=INVERSE_FLOOR):
@@ -118,6 +149,16 @@ def _center_planes(flat: torch.Tensor, grid, field):
     return torch.sqrt(uc * uc + vc * vc)[None]
 
 
+def _host(t: torch.Tensor) -> np.ndarray:
+    """Device -> host through a pinned staging buffer (one DMA at link speed)."""
+    if t.device.type != "cuda":
+        return t.numpy()
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return h.numpy()
+
+
 def encode_planes(planes, fmt):
     """12-byte header (u32 nx, ny, channels) + row-major f32 or u8 planes
     (server.py:288-302); planes may be a device tensor or a numpy array."""
@@ -126,7 +167,15 @@ def encode_planes(planes, fmt):
     channels, ny, nx = planes.shape
     header = np.asarray([nx, ny, channels], dtype="<u4").tobytes()
     if fmt == "bin":
-        return header + planes.to(torch.float32).cpu().numpy().astype("<f4").tobytes(), "application/octet-stream"
+        if planes.device.type == "cuda":
+            # one pinned staging buffer laid out as the payload (header + f32
+            # planes): a single DMA, then one copy into the returned bytes
+            buf = torch.empty(3 + planes.numel(), dtype=torch.float32, pin_memory=True)
+            buf[:3].view(torch.int32).copy_(torch.tensor([nx, ny, channels], dtype=torch.int32))
+            buf[3:].copy_(planes.reshape(-1).to(torch.float32), non_blocking=True)
+            torch.cuda.current_stream(planes.device).synchronize()
+            return buf.numpy().tobytes(), "application/octet-stream"
+        return header + _host(planes.to(torch.float32)).tobytes(), "application/octet-stream"
     if fmt == "raster":
         p = planes.to(torch.float64)
         lo = p.min()
@@ -136,7 +185,7 @@ def encode_planes(planes, fmt):
             data = torch.zeros(p.shape, dtype=torch.uint8)
         else:
             data = torch.clamp((p - lo) / span * 255.0, 0, 255).to(torch.uint8)
-        return header + data.cpu().numpy().tobytes(), "application/octet-stream"
+        return header + _host(data).tobytes(), "application/octet-stream"
     raise ValueError(f"unknown format {fmt!r}")
 
 
@@ -210,6 +259,7 @@ class ModelServer:
             raise ValueError(f"start_frame {start} outside dataset (0..{frames - 1})")
         return ds.states[:, start]
 
+    @_on_request_stream
     def create_session(self, body):
         model = self.model
         r = model.r
@@ -268,6 +318,7 @@ class ModelServer:
             return self._advected_density(model, z_ref, frame_ref, density_ref, k)[None]
         raise ValueError(f"unknown field {field!r}")
 
+    @_on_request_stream
     def frame_payload(self, session, k, field, fmt):
         planes = self.frame_planes(session, k, field)   # decode first, then format errors (server.py:225)
         return encode_planes(planes, fmt)
@@ -283,6 +334,7 @@ class ModelServer:
         return density
 
     # -- force / upres (server.py:237-285) -------------------------------------
+    @_on_request_stream
     def apply_force(self, session, body):
         model = session.model
         grid = model.grid_meta
@@ -306,6 +358,7 @@ class ModelServer:
                 session.density_ref = advect_density(model, session.density_ref, new.z, model.dt)
             return session.frame_ref
 
+    @_on_request_stream
     def upres_preview(self, session, body):
         model = session.model
         factor = int(body["factor"])

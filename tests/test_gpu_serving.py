@@ -235,3 +235,40 @@ def test_mac_kernel_argument_errors(fd):
         ops.mac_decode(T, torch.ones(2), 3, 3, "velocity")   # n_state 24 > 10 rows
     with pytest.raises(ValueError):
         ops.mac_inject(torch.ones(5, device="cuda"), 7, 4, 2)  # 7 not divisible by 2
+
+
+def test_concurrent_sessions_match_serial(fd, sg, model):
+    """ThreadingHTTPServer-style concurrency (server.py:1-21, test_server.py:224):
+    8 threads, each its own session (half edited, with forces), produce the
+    same payload bytes as the same requests issued serially."""
+    import threading
+    srv = _server(fd, sg, model)
+    bodies = [{} if i % 2 == 0 else _edit_body(sg, model) for i in range(8)]
+
+    def script(sess):
+        out = []
+        for k in (0, 3, 7):
+            out.append(srv.frame_payload(sess, k, "speed", "bin")[0])
+            out.append(srv.frame_payload(sess, k, "density", "raster")[0])
+        srv.apply_force(sess, {"x": 0.4, "y": 0.5, "dx": 0.2, "dy": 0.1})
+        out.append(srv.frame_payload(sess, 2, "velocity", "bin")[0])
+        return out
+
+    serial = [script(srv.get_session(srv.create_session(b))) for b in bodies]
+    results = [None] * len(bodies)
+    errors = []
+
+    def run(i):
+        try:
+            results[i] = script(srv.get_session(srv.create_session(bodies[i])))
+        except Exception as exc:   # pragma: no cover - surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(bodies))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for a, b in zip(results, serial):
+        assert a == b
