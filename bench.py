@@ -349,8 +349,8 @@ def main():
     recon["B=1024"] = {"frames_per_s": round(len(times) / b1024, 1), "ms": round(b1024 * 1e3, 2),
                        "hbm_GBps_per_gpu": round(byt / b1024 / 1e9 / world, 1),
                        "frac_hbm": round(byt / b1024 / 1e9 / world / hbm_peak(), 3),
-                       "kernel": f"tc_decode, {CHUNK}-frame launches (clusters of up to 8 CTAs multicasting each "
-                                 "basis chunk) streamed through one buffer"}
+                       "kernel": f"tc_decode2 (tcgen05 cta_group::2 CTA pairs, 256 frames per pair tile), "
+                                 f"{CHUNK}-frame launches streamed through one buffer"}
     recon["basis_split_ms"] = round(rec["split"] * 1e3, 2)
 
     # ---- e2e through the public API from pinned host memory ----

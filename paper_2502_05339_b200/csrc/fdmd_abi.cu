@@ -591,6 +591,60 @@ int launch_tc_decode_mc(const void* uh, const void* ul, int64_t ldu, int64_t n, 
   return FDMD_OK;
 }
 
+// CTA-pair variant (cta_group::2, M = 256 rows x N = 256 frames per pair tile)
+int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch,
+                          const void* cl, int ldk, int nf, const float* fscale, float* out, int64_t ldo,
+                          void* stream) {
+  auto encode = tensor_map_encoder();
+  if (!encode) return fail(FDMD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap maps[4];
+  const void* ptrs[4] = {uh, ul, ch, cl};
+  for (int i = 0; i < 4; ++i) {
+    const bool a = i < 2;
+    cuuint64_t dims[2] = {(cuuint64_t)r, (cuuint64_t)(a ? n : nf)};
+    cuuint64_t strides[1] = {(cuuint64_t)((a ? ldu : ldk) * 2)};
+    cuuint32_t box[2] = {(cuuint32_t)fdmd::tc2::BKC, (cuuint32_t)(a ? fdmd::tc2::BM : fdmd::tc2::BNH)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult res = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptrs[i]), dims, strides,
+                          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) return fail(FDMD_ERR_CUDA, "tc_decode2: tensor map encode failed (%d)", (int)res);
+  }
+  auto kern = fdmd::tc_decode2_kernel;
+  const int smem = (int)sizeof(fdmd::TC2Smem) + 1024;
+  static thread_local int configured = -1;
+  static thread_local int max_clusters = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(fdmd::tc2::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  if (configured != dev) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cfg.gridDim = dim3(2, 1);
+    int nc = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveClusters(&nc, (void*)kern, &cfg));
+    max_clusters = std::max(1, nc);
+    configured = dev;
+  }
+  fdmd::TCArgs ta{out, ldo, n, r, nf, fscale};
+  const int64_t ptiles = (n + 2 * fdmd::tc2::BM - 1) / (2 * fdmd::tc2::BM);
+  const int gy = (nf + fdmd::tc2::BN - 1) / fdmd::tc2::BN;
+  const int64_t npairs = std::max<int64_t>(1, std::min<int64_t>(ptiles, std::max(1, max_clusters / gy)));
+  cfg.gridDim = dim3((unsigned)(2 * npairs), gy);
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], ta));
+  LAUNCH_CHECK("tc_decode2");
+  return FDMD_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1001,6 +1055,12 @@ int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r
   // sharing every basis chunk through TMA multicast (basis read once per
   // MC * 128 frames).
   const int ny = (nf + 127) / 128;
+  // > 128 frames: CTA pairs (cta_group::2, 256 frames per pair tile; B = 256
+  // at n = 50.3M: 16.5 ms vs 21.3 ms for MC = 2 clusters); FDMD_TC_IMPL=mc
+  // selects the multicast clusters instead
+  static const int pair_on = [] { const char* e = getenv("FDMD_TC_IMPL"); return e ? (strcmp(e, "mc") == 0 ? 0 : 1) : 1; }();
+  if (ny > 1 && pair_on)
+    return launch_tc_decode_pair(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
   static const int mc_cap = [] { const char* e = getenv("FDMD_TC_MAX_CLUSTER"); return e ? atoi(e) : 8; }();
   if (ny == 1 || mc_cap <= 1)
     return launch_tc_decode_mc<128, 3, 0, 1>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);

@@ -13,5 +13,6 @@
 #include "fdmd_gram_tma.cuh"
 #include "fdmd_gram_panel.cuh"
 #include "fdmd_tc_decode.cuh"
+#include "fdmd_tc_decode2.cuh"
 #include "fdmd_stream.cuh"
 #include "fdmd_mac.cuh"

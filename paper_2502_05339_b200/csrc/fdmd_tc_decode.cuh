@@ -38,7 +38,10 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BKC = 64;          // K per chunk (128 B of fp16 = one SW128 row)
 constexpr int MAXKC = 4;         // r <= 256
-constexpr int EPI = 8;           // epilogue warps (2 per TMEM lane quadrant, half the columns each; 4: 14.4 ms, 8: 11.8, 16: 12.3 at B = 128)
+#ifndef FDMD_TC_EPI
+#define FDMD_TC_EPI 8
+#endif
+constexpr int EPI = FDMD_TC_EPI;  // epilogue warps (2 per TMEM lane quadrant, half the columns each; 4: 14.4 ms, 8: 11.8, 16: 12.3 at B = 128)
 constexpr int THREADS = 64 + 32 * EPI;
 constexpr int A_CHUNK_BYTES = BM * BKC * 2;   // 16 KB per plane
 }  // namespace tc
@@ -265,16 +268,20 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cb), v);
         if (row < args.n) {
+          float* o = args.out + (int64_t)(f0 + cb) * args.ldo + row;
+          const float* fsg = args.fscale + f0 + cb;
+          const int jn = min(32, args.nf - (f0 + cb));
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int f = f0 + cb + j;
-            if (f < args.nf) __stcs(args.out + (int64_t)f * args.ldo + row, v[j] * __ldg(args.fscale + f));
-          }
+          for (int j = 0; j < 32; ++j)
+            if (j < jn) { __stcs(o, v[j] * __ldg(fsg + j)); o += args.ldo; }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.tempty[acc]);
+      // relaxed: the TMEM reads (waited) must precede the arrive, the global
+      // stores need not (a release arrive fences every store of the tile)
+      if (lane == 0) asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];\n"
+                                  ::"r"(smem_u32(&sm.tempty[acc])) : "memory");
     }
   }
   __syncwarp();

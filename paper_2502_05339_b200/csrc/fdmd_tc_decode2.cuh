@@ -1,0 +1,237 @@
+// tcgen05 reconstruction on CTA PAIRS (cta_group::2): frames[f][i] =
+// sum_k U[i][k] C[k][f], same FP16 2-way split as fdmd_tc_decode.cuh.
+//
+// Why pairs: the single-CTA kernel keeps all 128 frames' coefficients
+// resident (128 KB) and streams the basis through a 3-stage ring; every
+// 128-row basis tile (128 KB of hi/lo planes) then yields only 128 frames,
+// and the ring's 96 KB in flight caps the rate (ncu: MMA warp waiting on
+// afull, tensor pipe ~45%). A pair issues M = 256 (128 rows per CTA), N = 256
+// frames, with each CTA holding HALF the coefficients (128 frames): same smem
+// per CTA, but every basis byte an SM ingests now produces twice the frames.
+//
+// Protocol (cluster = 2 CTAs along x, rank 0 = leader):
+//   * both CTAs TMA their own 128 basis rows and their 128-frame coefficient
+//     half into local smem, signalling the LEADER's full barriers
+//     (.cta_group::2 TMA with the leader's mbarrier address from mapa);
+//   * the leader's elected thread issues tcgen05.mma.cta_group::2 and commits
+//     with .multicast::cluster to both CTAs' empty / accumulator-full barriers;
+//   * each CTA's 8 epilogue warps drain their own TMEM half (128 rows x 256
+//     frames) and arrive on the leader's accumulator-empty barrier (count 16);
+//   * TMEM (512 columns = 2 accumulators x 256) is allocated / freed by one
+//     warp in each CTA with cta_group::2.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include "fdmd_tc_decode.cuh"
+
+namespace fdmd {
+
+namespace tc2 {
+constexpr int BM = 128;           // basis rows per CTA (pair tile: 256)
+constexpr int BN = 256;           // frames per pair tile
+constexpr int BNH = 128;          // coefficient rows held per CTA
+constexpr int BKC = 64;
+constexpr int MAXKC = 4;          // r <= 256
+constexpr int AST = 3;
+#ifndef FDMD_TC2_EPI
+#define FDMD_TC2_EPI 16
+#endif
+constexpr int EPI = FDMD_TC2_EPI;   // epilogue warps (4 per TMEM lane quadrant)
+constexpr int THREADS = 64 + 32 * EPI;
+constexpr int A_CHUNK_BYTES = BM * BKC * 2;    // 16 KB per plane
+constexpr int B_CHUNK_BYTES = BNH * BKC * 2;   // 16 KB per plane
+}  // namespace tc2
+
+struct TC2Smem {
+  __half A[tc2::AST][2][tc2::BM * tc2::BKC];
+  __half B[tc2::MAXKC][2][tc2::BNH * tc2::BKC];
+  alignas(16) float fs[tc2::BN];
+  uint64_t afull[tc2::AST], aempty[tc2::AST];
+  uint64_t bfull;
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// TMA tile into local smem, completion signalled on a (possibly peer) barrier
+__device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* map, int x, int y, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(bar_cluster) : "memory");
+}
+__device__ __forceinline__ void umma2_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma2_commit_mc(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+               ::"r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  // relaxed: only the (already waited) TMEM reads must precede the arrive, not the
+  // epilogue's global stores (a release would MEMBAR on every store of the tile)
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(tc2::THREADS, 1)
+tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_constant__ CUtensorMap amap_l,
+                  const __grid_constant__ CUtensorMap bmap_h, const __grid_constant__ CUtensorMap bmap_l,
+                  const TCArgs args) {
+  using SM = TC2Smem;
+  constexpr uint32_t TCOLS = 2 * tc2::BN;   // 512: two 256-column accumulators
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int nkc = (args.r + tc2::BKC - 1) / tc2::BKC;
+  const int ksteps_last = ((args.r - (nkc - 1) * tc2::BKC) + 15) / 16;
+  const int64_t ptiles = (args.n + 2 * tc2::BM - 1) / (2 * tc2::BM);
+  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int64_t my_tiles = pair < ptiles ? (ptiles - pair + npairs - 1) / npairs : 0;
+  const int f0 = blockIdx.y * tc2::BN;
+
+  for (int f = threadIdx.x; f < tc2::BN; f += blockDim.x)
+    sm.fs[f] = (f0 + f < args.nf) ? args.fscale[f0 + f] : 0.f;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < tc2::AST; ++s) { mbar_init(&sm.afull[s], 1); mbar_init(&sm.aempty[s], 1); }
+    mbar_init(&sm.bfull, 1);
+    for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], 2 * tc2::EPI); }
+    mbar_fence_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                 ::"r"(smem_u32(&sm.tmem_base)), "n"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // coefficient half: frames f0 + rank * 128 .. +127, every K chunk
+      const uint32_t bfull_l = mapa_u32(&sm.bfull, 0);
+      if (leader) mbar_expect_tx(&sm.bfull, (uint32_t)(2 * nkc * 2 * tc2::B_CHUNK_BYTES));
+      for (int c = 0; c < nkc; ++c) {
+        tma_load_2d_cg2(sm.B[c][0], &bmap_h, c * tc2::BKC, f0 + (int)rank * tc2::BNH, bfull_l);
+        tma_load_2d_cg2(sm.B[c][1], &bmap_l, c * tc2::BKC, f0 + (int)rank * tc2::BNH, bfull_l);
+      }
+      int sa = 0;
+      uint32_t pa = 0;
+      for (int64_t t = 0; t < my_tiles; ++t) {
+        const int row0 = (int)((pair + t * npairs) * (2 * tc2::BM) + rank * tc2::BM);
+        for (int c = 0; c < nkc; ++c) {
+          mbar_wait(&sm.aempty[sa], pa ^ 1);                          // leader's MMAs released it
+          if (leader) mbar_expect_tx(&sm.afull[sa], 2 * 2 * tc2::A_CHUNK_BYTES);   // both CTAs' planes
+          const uint32_t afull_l = mapa_u32(&sm.afull[sa], 0);
+          tma_load_2d_cg2(sm.A[sa][0], &amap_h, c * tc2::BKC, row0, afull_l);
+          tma_load_2d_cg2(sm.A[sa][1], &amap_l, c * tc2::BKC, row0, afull_l);
+          if (++sa == tc2::AST) { sa = 0; pa ^= 1; }
+        }
+      }
+      // tail: the leader's last releases of this CTA's ring have landed
+      for (int s = 0; s < tc2::AST; ++s) {
+        mbar_wait(&sm.aempty[sa], pa ^ 1);
+        if (++sa == tc2::AST) { sa = 0; pa ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // kind::f16, fp16 x fp16 -> fp32, K-major A and B, M = 256, N = 256
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(tc2::BN >> 3) << 17) | ((uint32_t)((2 * tc2::BM) >> 4) << 24);
+      int sa = 0;
+      uint32_t pa = 0;
+      mbar_wait(&sm.bfull, 0);
+      for (int64_t t = 0; t < my_tiles; ++t) {
+        const int acc = (int)(t & 1);
+        mbar_wait(&sm.tempty[acc], (uint32_t)(((t >> 1) & 1) ^ 1));   // both CTAs' epilogues drained it
+        tc_fence_after();
+        const uint32_t d = tmem + acc * tc2::BN;
+        uint32_t first = 1;
+        for (int c = 0; c < nkc; ++c) {
+          mbar_wait(&sm.afull[sa], pa);
+          tc_fence_after();
+          const int ksteps = (c == nkc - 1) ? ksteps_last : tc2::BKC / 16;
+          const uint64_t ah = umma_desc_sw128(sm.A[sa][0]), al = umma_desc_sw128(sm.A[sa][1]);
+          const uint64_t bh = umma_desc_sw128(sm.B[c][0]), bl = umma_desc_sw128(sm.B[c][1]);
+          for (int k = 0; k < ksteps; ++k) {
+            const uint64_t adv = (uint64_t)((k * 32) >> 4);
+            umma2_f16(d, ah + adv, bh + adv, idesc, first ? 0u : 1u);
+            umma2_f16(d, ah + adv, bl + adv, idesc, 1u);
+            umma2_f16(d, al + adv, bh + adv, idesc, 1u);
+            first = 0;
+          }
+          umma2_commit_mc(&sm.aempty[sa]);          // both CTAs may refill this stage
+          if (++sa == tc2::AST) { sa = 0; pa ^= 1; }
+        }
+        umma2_commit_mc(&sm.tfull[acc]);            // both CTAs' TMEM halves ready
+      }
+      // every peer epilogue arrival on our tempty has landed before teardown
+      for (int64_t t = my_tiles; t < my_tiles + 2; ++t)
+        mbar_wait(&sm.tempty[t & 1], (uint32_t)(((t >> 1) & 1) ^ 1));
+    }
+  } else {
+    const int q = warp & 3;
+    constexpr int SPLIT = tc2::EPI / 4;
+    const int part = (warp - 2) / 4;
+    const int c_lo = part * (tc2::BN / SPLIT), c_hi = c_lo + tc2::BN / SPLIT;
+    const uint32_t tempty_l[2] = {mapa_u32(&sm.tempty[0], 0), mapa_u32(&sm.tempty[1], 0)};
+    for (int64_t t = 0; t < my_tiles; ++t) {
+      const int acc = (int)(t & 1);
+      mbar_wait(&sm.tfull[acc], (uint32_t)((t >> 1) & 1));
+      tc_fence_after();
+      const int64_t row = (pair + t * npairs) * (2 * tc2::BM) + rank * tc2::BM + q * 32 + lane;
+#pragma unroll 1
+      for (int cb = c_lo; cb < c_hi; cb += 32) {
+        if (f0 + cb >= args.nf) break;
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * tc2::BN + cb), v);
+        if (row < args.n) {
+          float* o = args.out + (int64_t)(f0 + cb) * args.ldo + row;
+          const int jn = min(32, args.nf - (f0 + cb));
+          const float4* fs4 = reinterpret_cast<const float4*>(sm.fs + cb);
+          if (jn == 32) {
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+              const float4 s = fs4[j4];
+              __stcs(o, v[4 * j4] * s.x); o += args.ldo;
+              __stcs(o, v[4 * j4 + 1] * s.y); o += args.ldo;
+              __stcs(o, v[4 * j4 + 2] * s.z); o += args.ldo;
+              __stcs(o, v[4 * j4 + 3] * s.w); o += args.ldo;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < jn) { __stcs(o, v[j] * sm.fs[cb + j]); o += args.ldo; }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_l[acc]);
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS));
+  }
+}
+
+}  // namespace fdmd
