@@ -525,3 +525,32 @@ def load_dataset_density(path):
     if "nx" in kv and "ny" in kv:
         return dens.reshape((int(kv["ny"]), int(kv["nx"]), frames))
     return dens
+
+
+# ---------------------------------------------------------------------------
+# edit spec files (model_io.py:429-466)
+# ---------------------------------------------------------------------------
+def edit_to_kv(spec):
+    return {"kind": "editspec", "r": spec.r, "cluster_threshold": spec.cluster_threshold,
+            "weights": spec.weights, "growth_scale": spec.growth_scale, "freq_scale": spec.freq_scale}
+
+
+def edit_from_kv(kv):
+    from .editing import EditSpec
+    if kv.get("kind", "editspec") != "editspec":
+        raise ValueError("not an edit spec")
+    spec = EditSpec(parse_floats(kv["weights"]), parse_floats(kv["growth_scale"]), parse_floats(kv["freq_scale"]),
+                    float(kv.get("cluster_threshold", "0.01")))
+    if "r" in kv and int(kv["r"]) != spec.r:
+        raise ValueError(f"edit spec declares r = {kv['r']} but carries {spec.r} entries")
+    return spec
+
+
+def save_edit(path, spec):
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write(kv_dumps({k: format_value(v) for k, v in edit_to_kv(spec).items()}))
+
+
+def load_edit(path):
+    with open(path, "r", encoding="utf-8") as fh:
+        return edit_from_kv(kv_loads(fh.read()))

@@ -109,3 +109,67 @@ def test_cli_errors_match_reference(fd, tmp_path, ref_out):
     assert run([])[0] == 2
     rc, _, se = run(["simulate", "scene.txt", "-o", str(tmp_path / "y")])
     assert rc == 1 and "outside the B200 hot path" in se
+
+
+# ---- commands using editing / density / guided upscaling (§8(f) rows 2-3) ----
+SCLI = os.path.join(ROOT, "tests", "golden", "serving_cli")
+
+
+@pytest.fixture(scope="module")
+def ref_out2():
+    text = open(os.path.join(SCLI, "outputs.txt")).read()
+    out = {}
+    for block in text.split("## ")[1:]:
+        head, rest = block.split("\n", 1)
+        name, rc = head.split(" rc=")
+        so, se = rest.split("--stderr--\n", 1)
+        out[name] = (int(rc), so, se)
+    return out
+
+
+def _compare_dataset(mio, got_dir, want_dir, tol):
+    got = np.fromfile(os.path.join(got_dir, "snapshots.bin"), dtype="<f8")
+    want = np.fromfile(os.path.join(want_dir, "snapshots.bin"), dtype="<f8")
+    assert got.size == want.size
+    assert np.linalg.norm(got - want) <= tol * np.linalg.norm(want)
+    kg = mio.kv_loads(open(os.path.join(got_dir, "manifest")).read())
+    kw = mio.kv_loads(open(os.path.join(want_dir, "manifest")).read())
+    for k in ("snapshots_crc32", "density_crc32"):
+        kg.pop(k, None), kw.pop(k, None)
+    assert kg == kw
+    if os.path.exists(os.path.join(want_dir, "density.bin")):
+        dg = np.fromfile(os.path.join(got_dir, "density.bin"), dtype="<f8")
+        dw = np.fromfile(os.path.join(want_dir, "density.bin"), dtype="<f8")
+        assert dg.size == dw.size and np.linalg.norm(dg - dw) <= tol * np.linalg.norm(dw)
+
+
+@pytest.mark.parametrize("name,argv,sub", [
+    ("rollout_edit_density", ["rollout", "--start-frame", "1", "--k", "2", "--frames", "4", "--edit",
+                              "<SCLI>/edit.kv", "--density"], "rollout_ed"),
+    ("reverse_density", ["reverse", "--start-frame", "8", "--frames", "3", "--density"], "reverse_d")])
+def test_edit_density_commands_match_reference_cli(fd, tmp_path, ref_out2, name, argv, sub):
+    from paper_2502_05339_b200 import model_io as mio
+    argv = [a.replace("<SCLI>", SCLI) for a in argv]
+    out = tmp_path / sub
+    rc, so, se = run(argv + ["--model", os.path.join(SCLI, "model.kdmd"), "--dataset",
+                             os.path.join(SCLI, "dataset"), "--out", str(out)])
+    rrc, rso, _ = ref_out2[name]
+    assert rc == rrc == 0, se
+    assert strip_paths(so) == strip_paths(rso)
+    _compare_dataset(mio, str(out), os.path.join(SCLI, sub), 1e-9)
+
+
+@pytest.mark.parametrize("name,extra,sub", [("upres_on", ["--split", "4"], "upres_on"),
+                                            ("upres_off", ["--split", "3", "--project", "off"], "upres_off")])
+def test_upres_command_matches_reference_cli(fd, tmp_path, ref_out2, name, extra, sub):
+    from paper_2502_05339_b200 import model_io as mio
+    out = tmp_path / sub
+    rc, so, se = run(["upres", "--low", os.path.join(SCLI, "low"), "--model", os.path.join(SCLI, "model.kdmd"),
+                      "--factor", "2", "--out", str(out)] + extra)
+    rrc, rso, _ = ref_out2[name]
+    assert rc == rrc == 0, se
+    assert strip_paths(so) == strip_paths(rso)
+    _compare_dataset(mio, str(out), os.path.join(SCLI, sub), 1e-9)
+    rc, so, se = run(["upres", "--low", os.path.join(SCLI, "low"), "--model", os.path.join(SCLI, "model.kdmd"),
+                      "--split", "4", "--factor", "3", "--out", str(tmp_path / "nope")])
+    assert (rc, se) == (ref_out2["upres_bad_factor"][0], ref_out2["upres_bad_factor"][2])
