@@ -1024,9 +1024,13 @@ int fdmd_geev(int n, double* A, double* w_host, double* vr_host, void* stream) {
 
 int fdmd_split_basis(const float* D, int64_t ldd, int64_t n, int r, float scale, void* uh, void* ul, int64_t ldu,
                      void* stream) {
-  if (!D || !uh || !ul || n <= 0 || r <= 0 || ldu < r || ldd < n) return fail(FDMD_ERR_INVALID, "split_basis: bad arguments");
-  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((ldu + 31) / 32));
-  fdmd::split_basis_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(D, ldd, n, r, scale, (__half*)uh, (__half*)ul, ldu);
+  if (!D || !uh || !ul || n <= 0 || r <= 0 || ldu < r || ldd < n || ldu % 8 || ldu > 256)
+    return fail(FDMD_ERR_INVALID, "split_basis: bad arguments (ldu must be a multiple of 8, <= 256)");
+  const size_t smem = (size_t)ldu * (fdmd::SPLIT_ROWS + 1) * sizeof(float);
+  auto k = fdmd::split_basis_kernel;
+  if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<(unsigned)((n + fdmd::SPLIT_ROWS - 1) / fdmd::SPLIT_ROWS), 256, smem, (cudaStream_t)stream>>>(
+      D, ldd, n, r, scale, (__half*)uh, (__half*)ul, ldu);
   LAUNCH_CHECK("split_basis");
   return FDMD_OK;
 }

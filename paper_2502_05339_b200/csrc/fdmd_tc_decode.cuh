@@ -295,27 +295,50 @@ tc_decode_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_consta
 
 // ------------------------------------------------------------ split kernels --
 // Us[i][k] (hi, lo planes, row-major, ld = ldu) from a column-major fp32 table
-// D[k][i] (ld = ldd), scaled by 2^su. Tiled transpose through smem.
-__global__ void split_basis_kernel(const float* __restrict__ D, int64_t ldd, int64_t n, int r, float scale,
-                                   __half* __restrict__ uh, __half* __restrict__ ul, int64_t ldu) {
-  __shared__ float tile[32][33];
-  const int64_t i0 = (int64_t)blockIdx.x * 32;
-  const int k0 = blockIdx.y * 32;
-  for (int kk = threadIdx.y; kk < 32; kk += blockDim.y) {
-    const int k = k0 + kk;
-    const int64_t i = i0 + threadIdx.x;
-    tile[kk][threadIdx.x] = (k < r && i < n) ? D[(int64_t)k * ldd + i] * scale : 0.f;
+// D[k][i] (ld = ldd), scaled by 2^su. One CTA per 64 rows: the whole 64 x r
+// column-major block is staged in shared memory (coalesced 256-B reads per k),
+// then each row's ldu halves per plane are written as 16-B vectors along the
+// row (one contiguous 2*ldu-byte run per row and plane): the table is read
+// once and the planes written once.
+constexpr int SPLIT_ROWS = 64;
+__global__ void __launch_bounds__(256) split_basis_kernel(const float* __restrict__ D, int64_t ldd, int64_t n, int r,
+                                                          float scale, __half* __restrict__ uh,
+                                                          __half* __restrict__ ul, int64_t ldu) {
+  extern __shared__ float stile[];                    // [ldu][SPLIT_ROWS + 1]
+  const int64_t i0 = (int64_t)blockIdx.x * SPLIT_ROWS;
+  const int rows = (int)(n - i0 < SPLIT_ROWS ? n - i0 : SPLIT_ROWS);
+  const int kp = (int)ldu;
+  // 16 independent loads in flight per thread (thread = row ii, k strided by 4)
+  const int ii = threadIdx.x & (SPLIT_ROWS - 1), kq = threadIdx.x / SPLIT_ROWS;   // 4 k-lanes
+  const bool live = ii < rows;
+  for (int k0 = kq; k0 < kp; k0 += 64) {
+    float x[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int k = k0 + 4 * j;
+      x[j] = (live && k < r) ? __ldcs(D + (int64_t)k * ldd + i0 + ii) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int k = k0 + 4 * j;
+      if (k < kp) stile[k * (SPLIT_ROWS + 1) + ii] = x[j] * scale;
+    }
   }
   __syncthreads();
-  for (int ii = threadIdx.y; ii < 32; ii += blockDim.y) {
-    const int64_t i = i0 + ii;
-    const int k = k0 + threadIdx.x;
-    if (i < n && k < ldu) {
-      const float x = tile[threadIdx.x][ii];
-      const __half h = __float2half_rn(x);
-      uh[i * ldu + k] = h;
-      ul[i * ldu + k] = __float2half_rn(x - __half2float(h));
+  const int vpr = kp / 8;                              // 16-B vectors (8 halves) per row and plane
+  for (int e = threadIdx.x; e < rows * vpr; e += blockDim.x) {
+    const int ri = e / vpr, v = e - ri * vpr;
+    __align__(16) __half h[8];
+    __align__(16) __half l[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float x = stile[(8 * v + j) * (SPLIT_ROWS + 1) + ri];
+      h[j] = __float2half_rn(x);
+      l[j] = __float2half_rn(x - __half2float(h[j]));
     }
+    const int64_t o = (i0 + ri) * ldu + 8 * v;
+    __stcs(reinterpret_cast<float4*>(uh + o), *reinterpret_cast<const float4*>(h));
+    __stcs(reinterpret_cast<float4*>(ul + o), *reinterpret_cast<const float4*>(l));
   }
 }
 

@@ -217,7 +217,11 @@ class CudaOps:
         r = D.k if ncols is None else ncols
         n = D.n
         ldu = round_up(r, 8)
-        mx = float(D.buf[:r, :n].abs().max().item()) if n else 0.0
+        if n:   # one read pass, no |U| temporary (a 40 GB abs() copy at config 4)
+            lo, hi = torch.aminmax(D.buf[:r, :n])
+            mx = max(-float(lo.item()), float(hi.item()))
+        else:
+            mx = 0.0
         e = math.frexp(mx)[1] if mx > 0 else 0
         su = math.ldexp(1.0, 14 - e)
         uh = torch.empty((n, ldu), dtype=torch.float16, device=D.buf.device)
