@@ -158,6 +158,36 @@ int fdmd_mac_inject(const double* low, int nx_high, int ny_high, int factor, int
 int fdmd_mac_project(const double* H, const double* L, int nx_high, int ny_high, int factor, double gram_diag,
                      double* x, void* stream);
 
+/* ---- 2-D smoke solver (reference solver.py) --------
+ * vel: flat MAC state (f64, u block then v block); cell arrays ny x nx f64;
+ * solid: ny x nx uint8 (NULL = no obstacles); closed/open: boundary kind. */
+#define FDMD_SOL_REDUCE_BLOCKS 296
+int fdmd_sol_mask(double* vel, int nx, int ny, const unsigned char* solid, int closed, void* stream);
+/* apply_solid_mask (grid.py:264-272) */
+int fdmd_sol_advect(const double* vel, const double* q, int which, int nx, int ny, double h, double dt,
+                    int maccormack, double* scratch, double* out, void* stream);
+/* _advect_array (solver.py:133-150): which 0 = u, 1 = v, 2 = cell centres;
+ * scratch holds 3 arrays of q's size (MacCormack predictor and extrema). */
+int fdmd_sol_emit(double* dens, double* temp, int nx, int ny, double h, double cx, double cy, double r2, double dadd,
+                  double tadd, void* stream);                                  /* _emit (solver.py:323-334) */
+int fdmd_sol_buoyancy(double* vel, const double* dens, const double* temp, int nx, int ny, double alpha, double beta,
+                      double dt, void* stream);                                /* add_body_forces (solver.py:181-194) */
+int fdmd_sol_vorticity(double* vel, int nx, int ny, double h, double eps, double dt, double* scratch, void* stream);
+/* vorticity_confinement (solver.py:197-222), scratch = 3 cell arrays */
+int fdmd_sol_reduce(const double* a, const double* b, const unsigned char* solid, int64_t n, int op, double* part,
+                    double* out, void* stream);
+/* op 0: sum a*b (np.vdot), 1: max |a|, 2: sum of a over fluid cells; fixed
+ * order; part holds FDMD_SOL_REDUCE_BLOCKS doubles; *out is device memory. */
+int fdmd_sol_rhs(const double* vel, int nx, int ny, double h, const unsigned char* solid, int closed, double nfluid,
+                 double* b, double* part, double* sum, void* stream);
+/* b = -divergence (0 on solids), mean-free on fluid cells when closed (solver.py:262-268) */
+int fdmd_sol_poisson(const double* p, int nx, int ny, double h2, const unsigned char* solid, int open, double* out,
+                     void* stream);                                            /* _apply_poisson (solver.py:248-258) */
+int fdmd_sol_cg_step(double* p, double* r, const double* d, const double* Ad, double alpha, int64_t n, void* stream);
+int fdmd_sol_cg_dir(double* d, const double* r, double beta, int64_t n, void* stream);
+int fdmd_sol_pressure_apply(double* vel, const double* p, int nx, int ny, double h, const unsigned char* solid,
+                            int open, void* stream);                           /* _project tail (solver.py:311-315) */
+
 /* FP64 tensor-pipe (DMMA.8x8x4) throughput probe on the current device:
  * a register-only mma.sync f64 loop lasting ~`seconds`/4; writes TFLOP/s.
  * The fit's roofline denominator (MEASURED_PEAKS.json has no FP64 figure). */

@@ -661,3 +661,68 @@ def upres_step(phi, lam, z, L, nx, ny, f, split):
     P = encode(phi, build_inject(nx, ny, f) @ L)
     zn = np.concatenate([P[:split], (lam * z)[split:]])
     return zn, decode(phi, lam, zn)
+
+
+# --------------------------------------------------------------------------
+# §8(f) row 4: solver pieces (solver.py) used to check the device kernels
+# --------------------------------------------------------------------------
+
+def _bilinear_ex(f, col, row):
+    """solver.py:79-101 with extrema."""
+    nr, nc = f.shape
+    col = np.clip(col, 0.0, nc - 1.0)
+    row = np.clip(row, 0.0, nr - 1.0)
+    i0 = np.minimum(col.astype(np.int64), nc - 2)
+    j0 = np.minimum(row.astype(np.int64), nr - 2)
+    tx = col - i0
+    ty = row - j0
+    f00, f10, f01, f11 = f[j0, i0], f[j0, i0 + 1], f[j0 + 1, i0], f[j0 + 1, i0 + 1]
+    val = f00 * (1 - tx) * (1 - ty) + f10 * tx * (1 - ty) + f01 * (1 - tx) * ty + f11 * tx * ty
+    lo = np.minimum(np.minimum(f00, f10), np.minimum(f01, f11))
+    hi = np.maximum(np.maximum(f00, f10), np.maximum(f01, f11))
+    return val, lo, hi
+
+
+def advect_array(u, v, q, which, h, dt, maccormack=True):
+    """solver.py:111-150 — transport of one component array (u faces, v faces or 'c')."""
+    ny, nxp = u.shape
+    nx = nxp - 1
+    if which == "u":
+        j, i = np.meshgrid(np.arange(ny), np.arange(nx + 1), indexing="ij")
+        X, Y = i * h, (j + 0.5) * h
+        samp = lambda f, x, y: _bilinear_ex(f, x / h, y / h - 0.5)            # noqa: E731
+    elif which == "v":
+        j, i = np.meshgrid(np.arange(ny + 1), np.arange(nx), indexing="ij")
+        X, Y = (i + 0.5) * h, j * h
+        samp = lambda f, x, y: _bilinear_ex(f, x / h - 0.5, y / h)            # noqa: E731
+    else:
+        j, i = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+        X, Y = (i + 0.5) * h, (j + 0.5) * h
+        samp = lambda f, x, y: _bilinear_ex(f, x / h - 0.5, y / h - 0.5)      # noqa: E731
+    up = bilinear(u, X / h, Y / h - 0.5)
+    vp = bilinear(v, X / h - 0.5, Y / h)
+    q_hat, lo, hi = samp(q, X - dt * up, Y - dt * vp)
+    if not maccormack:
+        return q_hat
+    q_back = samp(q_hat, X + dt * up, Y + dt * vp)[0]
+    return np.clip(q_hat + 0.5 * (q - q_back), lo, hi)
+
+
+def apply_poisson(p, nx, ny, h, solid=None, boundary="open"):
+    """solver.py:229-258 — negative masked Laplacian."""
+    fluid = ~(np.zeros((ny, nx), dtype=bool) if solid is None else solid)
+    cx = np.zeros((ny, nx + 1))
+    cy = np.zeros((ny + 1, nx))
+    cx[:, 1:-1] = (fluid[:, :-1] & fluid[:, 1:]).astype(np.float64)
+    cy[1:-1, :] = (fluid[:-1, :] & fluid[1:, :]).astype(np.float64)
+    if boundary == "open":
+        cy[-1, :] = fluid[-1, :].astype(np.float64)
+    out = np.zeros_like(p)
+    fe = cx[:, 1:-1] * (p[:, 1:] - p[:, :-1])
+    out[:, :-1] += fe
+    out[:, 1:] -= fe
+    fn = cy[1:-1, :] * (p[1:, :] - p[:-1, :])
+    out[:-1, :] += fn
+    out[1:, :] -= fn
+    out[-1, :] -= cy[-1, :] * p[-1, :]
+    return -out / (h * h)

@@ -54,7 +54,10 @@ def main():
     spec.freq_scale[high] = 1.25
     epath = os.path.join(OUT, "edit.kv")
     model_io.save_edit(epath, spec)
+    spath = os.path.join(OUT, "scene.kv")
+    model_io.save_scene(spath, SceneConfig(kind="plume", nx=16, ny=32, h=1.0 / 16, frames=6, warmup=2))
     runs = {
+        "simulate": ["simulate", spath, "-o", os.path.join(OUT, "sim")],
         "rollout_edit_density": ["rollout", "--model", mpath, "--dataset", ds, "--start-frame", "1", "--k", "2",
                                  "--frames", "4", "--edit", epath, "--density",
                                  "--out", os.path.join(OUT, "rollout_ed")],

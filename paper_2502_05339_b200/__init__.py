@@ -20,6 +20,7 @@ from . import model_io
 from .editing import EditSpec, apply_edit, band_energy, cluster_modes, omega
 from .grid import GridSpec, MacField, ScalarField, coarse_grid, flatten, unflatten
 from .serving import ModelServer, Session, shift_state
+from . import solver
 from .upres import UpresConfig, blend_fields, build_projector, constrained_project, guided_rollout, upres_step
 from .errors import (
     BadMagicError,

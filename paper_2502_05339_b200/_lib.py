@@ -55,6 +55,17 @@ SIGNATURES = {
     "fdmd_mac_advect": (_i, [_vp, _i, _i, _i, _d, _d, _vp, _vp, _vp]),
     "fdmd_mac_inject": (_i, [_vp, _i, _i, _i, _i, _i64, _i64, _vp, _vp]),
     "fdmd_mac_project": (_i, [_vp, _vp, _i, _i, _i, _d, _vp, _vp]),
+    "fdmd_sol_mask": (_i, [_vp, _i, _i, _vp, _i, _vp]),
+    "fdmd_sol_advect": (_i, [_vp, _vp, _i, _i, _i, _d, _d, _i, _vp, _vp, _vp]),
+    "fdmd_sol_emit": (_i, [_vp, _vp, _i, _i, _d, _d, _d, _d, _d, _d, _vp]),
+    "fdmd_sol_buoyancy": (_i, [_vp, _vp, _vp, _i, _i, _d, _d, _d, _vp]),
+    "fdmd_sol_vorticity": (_i, [_vp, _i, _i, _d, _d, _d, _vp, _vp]),
+    "fdmd_sol_reduce": (_i, [_vp, _vp, _vp, _i64, _i, _vp, _vp, _vp]),
+    "fdmd_sol_rhs": (_i, [_vp, _i, _i, _d, _vp, _i, _d, _vp, _vp, _vp, _vp]),
+    "fdmd_sol_poisson": (_i, [_vp, _i, _i, _d, _vp, _i, _vp, _vp]),
+    "fdmd_sol_cg_step": (_i, [_vp, _vp, _vp, _vp, _d, _i64, _vp]),
+    "fdmd_sol_cg_dir": (_i, [_vp, _vp, _d, _i64, _vp]),
+    "fdmd_sol_pressure_apply": (_i, [_vp, _vp, _i, _i, _d, _vp, _i, _vp]),
     "fdmd_synth3d": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _d, _u64, _i64, _i64, _vp, _i, _i64, _vp]),
 }
 

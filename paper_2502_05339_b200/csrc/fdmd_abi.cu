@@ -1140,6 +1140,129 @@ int fdmd_mac_project(const double* H, const double* L, int nx_high, int ny_high,
   return FDMD_OK;
 }
 
+// ---- 2-D smoke solver (fdmd_solver.cuh) ------------------------------------
+static inline unsigned sol_blocks(int64_t n) { return (unsigned)((n + 255) / 256); }
+static inline int64_t sol_nstate(int nx, int ny) { return (int64_t)(nx + 1) * ny + (int64_t)nx * (ny + 1); }
+#define SOL_CHECK_GRID() \
+  if (nx < 2 || ny < 2) return fail(FDMD_ERR_INVALID, "solver: grid must be at least 2x2")
+
+int fdmd_sol_mask(double* vel, int nx, int ny, const unsigned char* solid, int closed, void* stream) {
+  SOL_CHECK_GRID();
+  const int64_t n = sol_nstate(nx, ny);
+  fdmd::sol_mask_kernel<<<sol_blocks(n), 256, 0, (cudaStream_t)stream>>>(vel, nx, ny, solid, closed);
+  LAUNCH_CHECK("sol_mask");
+  return FDMD_OK;
+}
+
+int fdmd_sol_advect(const double* vel, const double* q, int which, int nx, int ny, double h, double dt,
+                    int maccormack, double* scratch, double* out, void* stream) {
+  SOL_CHECK_GRID();
+  if (which < 0 || which > 2 || !vel || !q || !out || !scratch) return fail(FDMD_ERR_INVALID, "sol_advect: bad arguments");
+  if (out == q) return fail(FDMD_ERR_INVALID, "sol_advect: out must not alias q");
+  const int64_t len = which == 0 ? (int64_t)(nx + 1) * ny : which == 1 ? (int64_t)nx * (ny + 1) : (int64_t)nx * ny;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!maccormack) {
+    fdmd::sol_advect_pred_kernel<<<sol_blocks(len), 256, 0, s>>>(vel, q, which, nx, ny, h, dt, out, nullptr, nullptr);
+  } else {
+    double* qhat = scratch;
+    double* lo = scratch + len;
+    double* hi = scratch + 2 * len;
+    fdmd::sol_advect_pred_kernel<<<sol_blocks(len), 256, 0, s>>>(vel, q, which, nx, ny, h, dt, qhat, lo, hi);
+    fdmd::sol_advect_corr_kernel<<<sol_blocks(len), 256, 0, s>>>(vel, q, qhat, lo, hi, which, nx, ny, h, dt, out);
+  }
+  LAUNCH_CHECK("sol_advect");
+  return FDMD_OK;
+}
+
+int fdmd_sol_emit(double* dens, double* temp, int nx, int ny, double h, double cx, double cy, double r2, double dadd,
+                  double tadd, void* stream) {
+  SOL_CHECK_GRID();
+  fdmd::sol_emit_kernel<<<sol_blocks((int64_t)nx * ny), 256, 0, (cudaStream_t)stream>>>(dens, temp, nx, ny, h, cx, cy,
+                                                                                        r2, dadd, tadd);
+  LAUNCH_CHECK("sol_emit");
+  return FDMD_OK;
+}
+
+int fdmd_sol_buoyancy(double* vel, const double* dens, const double* temp, int nx, int ny, double alpha, double beta,
+                      double dt, void* stream) {
+  SOL_CHECK_GRID();
+  fdmd::sol_buoyancy_kernel<<<sol_blocks((int64_t)(ny + 1) * nx), 256, 0, (cudaStream_t)stream>>>(
+      vel, dens, temp, nx, ny, -alpha, beta, dt);
+  LAUNCH_CHECK("sol_buoyancy");
+  return FDMD_OK;
+}
+
+int fdmd_sol_vorticity(double* vel, int nx, int ny, double h, double eps, double dt, double* scratch, void* stream) {
+  SOL_CHECK_GRID();
+  const int64_t cells = (int64_t)nx * ny;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* omega = scratch;
+  double* fx = scratch + cells;
+  double* fy = scratch + 2 * cells;
+  fdmd::sol_omega_kernel<<<sol_blocks(cells), 256, 0, s>>>(vel, nx, ny, h, omega);
+  fdmd::sol_confine_force_kernel<<<sol_blocks(cells), 256, 0, s>>>(omega, nx, ny, h, eps * h, fx, fy);
+  fdmd::sol_confine_apply_kernel<<<sol_blocks(sol_nstate(nx, ny)), 256, 0, s>>>(vel, fx, fy, nx, ny, dt * 0.5);
+  LAUNCH_CHECK("sol_vorticity");
+  return FDMD_OK;
+}
+
+int fdmd_sol_reduce(const double* a, const double* b, const unsigned char* solid, int64_t n, int op, double* part,
+                    double* out, void* stream) {
+  if (!a || !out || !part || n <= 0 || op < 0 || op > 2 || (op == 0 && !b))
+    return fail(FDMD_ERR_INVALID, "sol_reduce: bad arguments");
+  const int blocks = (int)std::min<int64_t>(FDMD_SOL_REDUCE_BLOCKS, (n + 255) / 256);
+  cudaStream_t s = (cudaStream_t)stream;
+  fdmd::sol_reduce_kernel<<<blocks, 256, 0, s>>>(a, b, solid, n, op, part);
+  fdmd::sol_reduce_final_kernel<<<1, 32, 0, s>>>(part, blocks, op, out);
+  LAUNCH_CHECK("sol_reduce");
+  return FDMD_OK;
+}
+
+int fdmd_sol_rhs(const double* vel, int nx, int ny, double h, const unsigned char* solid, int closed, double nfluid,
+                 double* b, double* part, double* sum, void* stream) {
+  SOL_CHECK_GRID();
+  const int64_t cells = (int64_t)nx * ny;
+  cudaStream_t s = (cudaStream_t)stream;
+  fdmd::sol_rhs_kernel<<<sol_blocks(cells), 256, 0, s>>>(vel, nx, ny, h, solid, b);
+  if (closed) {
+    int rc = fdmd_sol_reduce(b, nullptr, solid, cells, 2, part, sum, stream);
+    if (rc) return rc;
+    fdmd::sol_sub_mean_kernel<<<sol_blocks(cells), 256, 0, s>>>(b, nx, ny, solid, sum, nfluid);
+  }
+  LAUNCH_CHECK("sol_rhs");
+  return FDMD_OK;
+}
+
+int fdmd_sol_poisson(const double* p, int nx, int ny, double h2, const unsigned char* solid, int open, double* out,
+                     void* stream) {
+  SOL_CHECK_GRID();
+  fdmd::sol_poisson_kernel<<<sol_blocks((int64_t)nx * ny), 256, 0, (cudaStream_t)stream>>>(p, nx, ny, h2, solid, open,
+                                                                                           out);
+  LAUNCH_CHECK("sol_poisson");
+  return FDMD_OK;
+}
+
+int fdmd_sol_cg_step(double* p, double* r, const double* d, const double* Ad, double alpha, int64_t n, void* stream) {
+  fdmd::sol_cg_step_kernel<<<sol_blocks(n), 256, 0, (cudaStream_t)stream>>>(p, r, d, Ad, alpha, n);
+  LAUNCH_CHECK("sol_cg_step");
+  return FDMD_OK;
+}
+
+int fdmd_sol_cg_dir(double* d, const double* r, double beta, int64_t n, void* stream) {
+  fdmd::sol_cg_dir_kernel<<<sol_blocks(n), 256, 0, (cudaStream_t)stream>>>(d, r, beta, n);
+  LAUNCH_CHECK("sol_cg_dir");
+  return FDMD_OK;
+}
+
+int fdmd_sol_pressure_apply(double* vel, const double* p, int nx, int ny, double h, const unsigned char* solid,
+                            int open, void* stream) {
+  SOL_CHECK_GRID();
+  fdmd::sol_pressure_apply_kernel<<<sol_blocks(sol_nstate(nx, ny)), 256, 0, (cudaStream_t)stream>>>(vel, p, nx, ny, h,
+                                                                                                  solid, open);
+  LAUNCH_CHECK("sol_pressure_apply");
+  return FDMD_OK;
+}
+
 int fdmd_dmma_peak(double seconds, double* tflops) {
   if (!tflops || seconds <= 0) return fail(FDMD_ERR_INVALID, "dmma_peak: bad arguments");
   double* d = nullptr;

@@ -16,3 +16,4 @@
 #include "fdmd_tc_decode2.cuh"
 #include "fdmd_stream.cuh"
 #include "fdmd_mac.cuh"
+#include "fdmd_solver.cuh"

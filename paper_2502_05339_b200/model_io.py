@@ -554,3 +554,65 @@ def save_edit(path, spec):
 def load_edit(path):
     with open(path, "r", encoding="utf-8") as fh:
         return edit_from_kv(kv_loads(fh.read()))
+
+
+# ---------------------------------------------------------------------------
+# scene files (model_io.py:361-422)
+# ---------------------------------------------------------------------------
+def _scene_fields():
+    from .solver import SceneConfig
+    return SceneConfig, {f.name: f for f in dataclasses.fields(SceneConfig)}
+
+
+def scene_to_kv(scene):
+    _, fields = _scene_fields()
+    out = {}
+    for name in fields:
+        value = getattr(scene, name)
+        if name == "region_disks":
+            value = [x for d in value for x in d]
+        out[name] = format_value(value)
+    return out
+
+
+def scene_from_kv(kv):
+    SceneConfig, fields = _scene_fields()
+    kwargs = {}
+    for name, fld in fields.items():
+        if name not in kv:
+            continue
+        raw = kv[name]
+        if name == "region_disks":
+            flat = parse_floats(raw)
+            if flat.size % 3:
+                raise ValueError("region_disks needs cx,cy,r triples")
+            kwargs[name] = tuple(tuple(flat[k:k + 3]) for k in range(0, flat.size, 3))
+        elif fld.type in ("int", int):
+            kwargs[name] = int(raw)
+        elif fld.type in ("float", float):
+            kwargs[name] = float(raw)
+        elif fld.type in ("bool", bool):
+            kwargs[name] = parse_bool(raw)
+        elif name == "region_down":
+            kwargs[name] = None if raw == "none" else float(raw)
+        else:
+            kwargs[name] = raw
+    return SceneConfig(**kwargs)
+
+
+def save_scene(path, scene):
+    kv = {"kind": "scene"}
+    for key, value in scene_to_kv(scene).items():
+        kv["scene_kind" if key == "kind" else key] = value
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write(kv_dumps(kv))
+
+
+def load_scene(path):
+    with open(path, "r", encoding="utf-8") as fh:
+        kv = kv_loads(fh.read())
+    if kv.pop("kind", "scene") != "scene":
+        raise ValueError(f"{path}: not a scene file")
+    if "scene_kind" in kv:
+        kv["kind"] = kv.pop("scene_kind")
+    return scene_from_kv(kv)

@@ -190,3 +190,25 @@ def test_model_info_fields(sg):
     info = json.loads(str(sg["model_info"]))
     assert set(info) == {"n", "r", "dt", "grid", "eigenvalues", "clusters"}
     assert info["grid"]["kind"] == "grid"
+
+
+def test_scene_and_edit_files_roundtrip_reference_bytes(tmp_path):
+    """Scene / edit-spec files written by the reference (tests/golden/serving_cli)
+    load into this package's SceneConfig / EditSpec and re-save byte-identically."""
+    from paper_2502_05339_b200 import model_io as mio
+    d = os.path.join(GOLDEN, "serving_cli")
+    scene = mio.load_scene(os.path.join(d, "scene.kv"))
+    assert (scene.kind, scene.nx, scene.ny, scene.frames, scene.warmup) == ("plume", 16, 32, 6, 2)
+    mio.save_scene(tmp_path / "s.kv", scene)
+    assert (tmp_path / "s.kv").read_bytes() == open(os.path.join(d, "scene.kv"), "rb").read()
+    spec = mio.load_edit(os.path.join(d, "edit.kv"))
+    mio.save_edit(tmp_path / "e.kv", spec)
+    assert (tmp_path / "e.kv").read_bytes() == open(os.path.join(d, "edit.kv"), "rb").read()
+
+
+def test_sim_params_validation():
+    from paper_2502_05339_b200.solver import SimParams
+    for kw, msg in [({"dt": 0.0}, "dt must be positive"), ({"dt": 0.1, "cg_tol": 1.0}, "cg_tol"),
+                    ({"dt": 0.1, "cg_max_iters": 0}, "cg_max_iters"), ({"dt": 0.1, "vorticity_eps": -1}, "eps")]:
+        with pytest.raises(ValueError, match=msg):
+            SimParams(**kw)

@@ -107,7 +107,7 @@ def test_cli_errors_match_reference(fd, tmp_path, ref_out):
     rrc, _, rse = ref_out["bad_start"]
     assert rc == rrc == 1 and se == rse
     assert run([])[0] == 2
-    rc, _, se = run(["simulate", "scene.txt", "-o", str(tmp_path / "y")])
+    rc, _, se = run(["serve", "--model", os.path.join(GOLD, "model.kdmd")])
     assert rc == 1 and "outside the B200 hot path" in se
 
 
@@ -173,3 +173,13 @@ def test_upres_command_matches_reference_cli(fd, tmp_path, ref_out2, name, extra
     rc, so, se = run(["upres", "--low", os.path.join(SCLI, "low"), "--model", os.path.join(SCLI, "model.kdmd"),
                       "--split", "4", "--factor", "3", "--out", str(tmp_path / "nope")])
     assert (rc, se) == (ref_out2["upres_bad_factor"][0], ref_out2["upres_bad_factor"][2])
+
+
+def test_simulate_matches_reference_cli(fd, tmp_path, ref_out2):
+    from paper_2502_05339_b200 import model_io as mio
+    out = tmp_path / "sim"
+    rc, so, se = run(["simulate", os.path.join(SCLI, "scene.kv"), "-o", str(out)])
+    rrc, rso, _ = ref_out2["simulate"]
+    assert rc == rrc == 0, se
+    assert strip_paths(so) == strip_paths(rso)
+    _compare_dataset(mio, str(out), os.path.join(SCLI, "sim"), 1e-6)
