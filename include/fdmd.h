@@ -185,6 +185,12 @@ int fdmd_sol_poisson(const double* p, int nx, int ny, double h2, const unsigned 
                      void* stream);                                            /* _apply_poisson (solver.py:248-258) */
 int fdmd_sol_cg_step(double* p, double* r, const double* d, const double* Ad, double alpha, int64_t n, void* stream);
 int fdmd_sol_cg_dir(double* d, const double* r, double beta, int64_t n, void* stream);
+int fdmd_sol_cg_single(const double* b, double* p, double* r, double* d, double* Ad, int nx, int ny, double h2,
+                       const unsigned char* solid, int open, double cg_tol, int max_iters, double* status,
+                       void* stream);
+/* The complete CG loop of _project (solver.py:270-309) in one 1024-thread CTA
+ * for grids <= 131072 cells; status (device, 4 doubles) = final max|r|,
+ * iterations, ran-out flag, max|b|. */
 int fdmd_sol_pressure_apply(double* vel, const double* p, int nx, int ny, double h, const unsigned char* solid,
                             int open, void* stream);                           /* _project tail (solver.py:311-315) */
 

@@ -1263,6 +1263,17 @@ int fdmd_sol_pressure_apply(double* vel, const double* p, int nx, int ny, double
   return FDMD_OK;
 }
 
+int fdmd_sol_cg_single(const double* b, double* p, double* r, double* d, double* Ad, int nx, int ny, double h2,
+                       const unsigned char* solid, int open, double cg_tol, int max_iters, double* status,
+                       void* stream) {
+  SOL_CHECK_GRID();
+  if ((int64_t)nx * ny > fdmd::SOL_CG1_MAX_CELLS) return fail(FDMD_ERR_INVALID, "sol_cg_single: grid too large");
+  fdmd::sol_cg_single_kernel<<<1, fdmd::SOL_CG1_THREADS, 0, (cudaStream_t)stream>>>(
+      b, p, r, d, Ad, nx, ny, h2, solid, open, cg_tol, max_iters, status);
+  LAUNCH_CHECK("sol_cg_single");
+  return FDMD_OK;
+}
+
 int fdmd_dmma_peak(double seconds, double* tflops) {
   if (!tflops || seconds <= 0) return fail(FDMD_ERR_INVALID, "dmma_peak: bad arguments");
   double* d = nullptr;

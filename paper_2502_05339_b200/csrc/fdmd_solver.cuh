@@ -344,3 +344,115 @@ __global__ void sol_pressure_apply_kernel(double* __restrict__ vel, const double
 }
 
 }  // namespace fdmd
+
+namespace fdmd {
+
+// ---------------------------------------------- single-CTA CG (small grids) --
+// The whole conjugate-gradient solve of solver.py:_project (same iteration,
+// break conditions and tolerance) in ONE 1024-thread CTA: vectors stay in
+// L2/L1, reductions are fixed-order block tree sums, and the host reads the
+// status once per solve instead of two scalars per iteration. Used for grids
+// up to SOL_CG1_MAX_CELLS cells (the reference scenes: 64 x 128 .. 128 x 256).
+constexpr int SOL_CG1_THREADS = 1024;
+constexpr int64_t SOL_CG1_MAX_CELLS = 1 << 17;
+
+__device__ __forceinline__ double sol_block_reduce(double v, int op, double* red) {
+  // op 0: sum, 1: max
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = SOL_CG1_THREADS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      red[threadIdx.x] = op ? fmax(red[threadIdx.x], red[threadIdx.x + s]) : __dadd_rn(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  const double out = red[0];
+  __syncthreads();
+  return out;
+}
+
+__device__ __forceinline__ double sol_poisson_at(const double* __restrict__ p, int nx, int ny, double h2,
+                                                 const unsigned char* __restrict__ solid, int open, int64_t e) {
+  const int j = (int)(e / nx), i = (int)(e - (int64_t)j * nx);
+  const double pc = p[e];
+  double o = 0.0;
+  if (i < nx - 1) o = __dadd_rn(o, __dmul_rn(sol_cx(solid, nx, j, i + 1), __dsub_rn(p[e + 1], pc)));
+  if (i > 0) o = __dsub_rn(o, __dmul_rn(sol_cx(solid, nx, j, i), __dsub_rn(pc, p[e - 1])));
+  if (j < ny - 1) o = __dadd_rn(o, __dmul_rn(sol_cy(solid, nx, ny, open, j + 1, i), __dsub_rn(p[e + nx], pc)));
+  if (j > 0) o = __dsub_rn(o, __dmul_rn(sol_cy(solid, nx, ny, open, j, i), __dsub_rn(pc, p[e - nx])));
+  if (j == ny - 1) o = __dsub_rn(o, __dmul_rn(sol_cy(solid, nx, ny, open, ny, i), pc));
+  return __ddiv_rn(-o, h2);
+}
+
+// status[0] = final max|r|, status[1] = iterations, status[2] = 1 if the loop
+// ran out without a break (solver.py's for/else), status[3] = bnorm
+__global__ void __launch_bounds__(SOL_CG1_THREADS, 1)
+sol_cg_single_kernel(const double* __restrict__ b, double* __restrict__ p, double* __restrict__ r,
+                     double* __restrict__ d, double* __restrict__ Ad, int nx, int ny, double h2,
+                     const unsigned char* __restrict__ solid, int open, double cg_tol, int max_iters,
+                     double* __restrict__ status) {
+  __shared__ double red[SOL_CG1_THREADS];
+  const int64_t n = (int64_t)nx * ny;
+  const int t = threadIdx.x;
+  double m = 0.0;
+  for (int64_t e = t; e < n; e += SOL_CG1_THREADS) m = fmax(m, fabs(b[e]));
+  const double bnorm = sol_block_reduce(m, 1, red);
+  if (bnorm == 0.0) {
+    if (t == 0) { status[0] = 0.0; status[1] = 0; status[2] = 0; status[3] = 0.0; }
+    return;
+  }
+  const double tol_abs = cg_tol * bnorm;
+  m = 0.0;
+  for (int64_t e = t; e < n; e += SOL_CG1_THREADS) {
+    const double re = __dsub_rn(b[e], sol_poisson_at(p, nx, ny, h2, solid, open, e));
+    r[e] = re;
+    m = fmax(m, fabs(re));
+  }
+  double rmax = sol_block_reduce(m, 1, red);
+  int iters = 0, ran_out = 0;
+  if (rmax > tol_abs) {
+    double acc = 0.0;
+    for (int64_t e = t; e < n; e += SOL_CG1_THREADS) {
+      const double re = r[e];
+      d[e] = re;
+      acc = __dadd_rn(acc, __dmul_rn(re, re));
+    }
+    double rs = sol_block_reduce(acc, 0, red);   // also orders the d writes before A d
+    ran_out = 1;
+    for (iters = 1; iters <= max_iters; ++iters) {
+      acc = 0.0;
+      for (int64_t e = t; e < n; e += SOL_CG1_THREADS) {
+        const double a = sol_poisson_at(d, nx, ny, h2, solid, open, e);
+        Ad[e] = a;
+        acc = __dadd_rn(acc, __dmul_rn(d[e], a));
+      }
+      const double dAd = sol_block_reduce(acc, 0, red);
+      if (dAd <= 0.0) { ran_out = 0; break; }
+      const double alpha = rs / dAd;
+      m = 0.0;
+      acc = 0.0;
+      for (int64_t e = t; e < n; e += SOL_CG1_THREADS) {
+        p[e] = __dadd_rn(p[e], __dmul_rn(alpha, d[e]));
+        const double re = __dsub_rn(r[e], __dmul_rn(alpha, Ad[e]));
+        r[e] = re;
+        m = fmax(m, fabs(re));
+        acc = __dadd_rn(acc, __dmul_rn(re, re));
+      }
+      rmax = sol_block_reduce(m, 1, red);
+      if (rmax <= tol_abs) { ran_out = 0; break; }
+      const double rs_new = sol_block_reduce(acc, 0, red);
+      const double beta = rs_new / rs;
+      for (int64_t e = t; e < n; e += SOL_CG1_THREADS) d[e] = __dadd_rn(r[e], __dmul_rn(beta, d[e]));
+      rs = rs_new;
+      __syncthreads();
+    }
+    if (ran_out) iters = max_iters;
+  }
+  if (t == 0) {
+    status[0] = rmax;
+    status[1] = (double)iters;
+    status[2] = (double)ran_out;
+    status[3] = bnorm;
+  }
+}
+
+}  // namespace fdmd

@@ -171,6 +171,8 @@ def _project(vel: torch.Tensor, G: _Grid, cg_tol, cg_max_iters, p0=None):
     b = torch.empty((G.ny, G.nx), dtype=torch.float64, device=dev)
     _sol("fdmd_sol_rhs", _ptr(vel), G.nx, G.ny, float(h), G.sp, G.closed, float(G.nfluid), _ptr(b), _ptr(G.part),
          _ptr(G.scal[1:]), _stream())
+    if n <= _CG1_MAX_CELLS:
+        return _project_single(vel, G, b, cg_tol, cg_max_iters, p0)
     red = lambda a, bb, op: _sol("fdmd_sol_reduce", _ptr(a), _ptr(bb), G.sp, n, op, _ptr(G.part), _ptr(G.scal),
                                  _stream())   # noqa: E731
     red(b, None, 1)
@@ -220,6 +222,38 @@ def _project(vel: torch.Tensor, G: _Grid, cg_tol, cg_max_iters, p0=None):
                 residual=rmax, iterations=iters)
     out = vel.clone()
     _sol("fdmd_sol_pressure_apply", _ptr(out), _ptr(p), G.nx, G.ny, float(h), G.sp, 1 - G.closed, _stream())
+    return out, p, rmax, iters
+
+
+_CG1_MAX_CELLS = 1 << 17   # SOL_CG1_MAX_CELLS: one-CTA CG below this size
+
+
+def _project_single(vel, G: _Grid, b, cg_tol, cg_max_iters, p0):
+    """The CG loop in one 1024-thread CTA (fdmd_sol_cg_single): same
+    iteration and stopping rules, one status read per solve."""
+    p = torch.zeros_like(b) if p0 is None else p0.clone()
+    if p0 is not None and G.solid is not None:
+        p[G.solid.bool()] = 0.0
+    r = torch.empty_like(b)
+    d = torch.empty_like(b)
+    Ad = torch.empty_like(b)
+    _sol("fdmd_sol_cg_single", _ptr(b), _ptr(p), _ptr(r), _ptr(d), _ptr(Ad), G.nx, G.ny, float(G.h * G.h), G.sp,
+         1 - G.closed, float(cg_tol), int(cg_max_iters), _ptr(G.scal), _stream())
+    rmax, iters, ran_out, bnorm = (float(v) for v in G.scal.cpu())
+    if bnorm == 0.0:
+        return vel.clone(), p, 0.0, 0
+    tol_abs = cg_tol * bnorm
+    iters = int(iters)
+    if ran_out:
+        raise ConvergenceError(
+            f"pressure solve stalled at residual {rmax:.3e} (target {tol_abs:.3e}) after {cg_max_iters} "
+            "iterations", residual=rmax, iterations=cg_max_iters)
+    if rmax > tol_abs:
+        raise ConvergenceError(
+            f"pressure solve stalled at residual {rmax:.3e} (target {tol_abs:.3e}) after {iters} iterations",
+            residual=rmax, iterations=iters)
+    out = vel.clone()
+    _sol("fdmd_sol_pressure_apply", _ptr(out), _ptr(p), G.nx, G.ny, float(G.h), G.sp, 1 - G.closed, _stream())
     return out, p, rmax, iters
 
 
