@@ -151,3 +151,51 @@ def test_streamed_upload_fit_matches_resident(fd, q):
             fd.exact_dmd(bad, 8, svd_mode="randomized", seed=2, oversample=10, power_iters=q)
     finally:
         la.PendingUpload.__init__ = old
+
+
+def test_config3_config4_full_size_properties(fd):
+    """BASELINE config 3 at FULL size (n = 50,331,648, 40 GB of f32
+    snapshots, OptDMD r = 200 with 10 LM iterations) and the config-4
+    reconstruction from its basis, through size-independent properties: the
+    CPU oracle cannot run here (~850 GB RAM)."""
+    import gc
+    from paper_2502_05339_b200 import device as dv
+    from paper_2502_05339_b200 import synth
+    from paper_2502_05339_b200.runtime import ModalBasis
+    p, S = _device_config(3, seed=3)
+    assert p.n == 50331648
+    data = fd.SnapshotMatrix(S, synth.DT)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        model = fd.optdmd(data, 200, lm_config=fd.LMConfig(max_iters=10), svd_mode="randomized", seed=3,
+                          oversample=10, power_iters=1, keep_basis=True)
+    lam, sigma = model.lam, model.sigma
+    assert lam.size == 200 and np.all(np.isfinite(lam))
+    assert max(np.abs(lam - np.conj(v)).min() for v in lam) <= 1e-12    # exact conjugate closure
+    assert np.all(np.diff(sigma) <= 0) and sigma[-1] > 0
+    assert np.abs(lam).max() < 1.05
+    U = model.basis_U
+    G = dv.get_ops().tall_gram(U, U, symmetric=True).cpu().numpy()     # U^T U over 50M rows
+    assert np.abs(G - np.eye(200)).max() < 1e-5                         # orthonormal (f32 storage)
+    del model, data, S
+    gc.collect()
+    torch.cuda.empty_cache()
+    # config 4: u(t) = U Re(W Lam^t b) at continuous times, batched tcgen05 vs GEMV vs fp64 rows
+    rng = np.random.default_rng(4)
+    lam4 = np.concatenate([p.lam, np.conj(p.lam)])[:200]
+    b4 = np.concatenate([p.b, np.conj(p.b)])[:200]
+    W4 = (rng.standard_normal((200, 200)) + 1j * rng.standard_normal((200, 200))) / np.sqrt(400)
+    mb = ModalBasis(U, W4, lam4, b4, dt=1.0)
+    times = rng.uniform(0.0, 300.0, 256)
+    gemv = mb.reconstruct(times[:2]).double()                          # SIMT GEMV (fp32 basis)
+    mb.release_fp32()
+    batch = mb.reconstruct(times)                                       # CTA-pair tcgen05 kernel
+    f2 = batch[:2].double()
+    assert float(torch.linalg.vector_norm(f2 - gemv) / torch.linalg.vector_norm(gemv)) < 2e-6
+    rows = torch.as_tensor(np.sort(rng.choice(p.n, 4096, replace=False)), device="cuda")
+    Ur = U.buf[:200][:, rows].t().double().cpu().numpy()                # n_rows x r fp64
+    C = mb.coefficients(times).double().cpu().numpy().astype(np.float32).astype(np.float64)
+    want = (Ur @ C).T
+    got = batch[:, rows].double().cpu().numpy()
+    err = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert err.max() < 2e-6, err.max()
