@@ -17,6 +17,8 @@
  *   fdmd_residual      provenance["residual"] (dmd.py:269-272)
  *   fdmd_geev          np.linalg.eig in eig_small (linalg.py:120) — cuSOLVER Xgeev
  *   fdmd_synth3d       BASELINE.json configs 1-4 snapshot generator (device)
+ *   fdmd_rsvd          randomized_svd (linalg.py:62-90) as one call (sketch, power
+ *                      iterations, CholeskyQR2, projection, svd, canonical signs, lift)
  *   fdmd_mac_*         2-D serving / guided upscaling: frame planes (server.py:205-214),
  *                      density transport (solver.py:133-150), injection and the
  *                      guide projection (upres.py:21-50, 154-169)
@@ -193,6 +195,16 @@ int fdmd_sol_cg_single(const double* b, double* p, double* r, double* d, double*
  * iterations, ran-out flag, max|b|. */
 int fdmd_sol_pressure_apply(double* vel, const double* p, int nx, int ny, double h, const unsigned char* solid,
                             int open, void* stream);                           /* _project tail (solver.py:311-315) */
+
+/* Randomized SVD of X (n x T, f32/f64 row-major, ld ldx) in one call —
+ * randomized_svd(M, r, oversample=l-r, power_iters=q) of linalg.py:62-90 with
+ * the host-drawn Omega (T x l f64 row-major, default_rng(seed).standard_normal).
+ * Outputs: sigma_host (r), V_host (T x r row-major), U (device, column-major
+ * r x n f64, ld ldu >= n), canonicalised as linalg.py:29-44. Synchronous.
+ * Requires r <= l <= min(T, 256). */
+int fdmd_rsvd(const void* X, int x_dtype, int64_t ldx, int64_t n, int T, int r, int l, int q,
+              const double* omega_host, double* sigma_host, double* V_host, double* U, int64_t ldu,
+              void* stream);
 
 /* FP64 tensor-pipe (DMMA.8x8x4) throughput probe on the current device:
  * a register-only mma.sync f64 loop lasting ~`seconds`/4; writes TFLOP/s.

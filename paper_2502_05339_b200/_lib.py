@@ -67,6 +67,7 @@ SIGNATURES = {
     "fdmd_sol_cg_dir": (_i, [_vp, _vp, _d, _i64, _vp]),
     "fdmd_sol_cg_single": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _d, _vp, _i, _d, _i, _vp, _vp]),
     "fdmd_sol_pressure_apply": (_i, [_vp, _vp, _i, _i, _d, _vp, _i, _vp]),
+    "fdmd_rsvd": (_i, [_vp, _i, _i64, _i64, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i64, _vp]),
     "fdmd_synth3d": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _d, _u64, _i64, _i64, _vp, _i, _i64, _vp]),
 }
 

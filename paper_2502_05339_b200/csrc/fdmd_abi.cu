@@ -1328,3 +1328,5 @@ int fdmd_synth3d(const double* sx, const double* sy, const double* sz, const dou
 }
 
 }  // extern "C"
+
+#include "fdmd_rsvd.inc"
