@@ -126,6 +126,17 @@ int fdmd_split_basis(const float* D, int64_t ldd, int64_t n, int r, float scale,
                      void* stream);
 int fdmd_split_coef(const float* coef, int ldc, int r, int nf, float su_inv, void* ch, void* cl, int ldk,
                     float* fscale, void* stream);
+/* fp16 hi/lo planes (row-major n x ldu) of a row-major fp64 tall matrix
+ * (n x K, ld lda) scaled by `scale` — the sketch basis Q for the tcgen05
+ * lift U = Q Ub (linalg.py:88) and modes Q (Ub B^T) (dmd.py:414). */
+int fdmd_split_rows_f64(const double* A, int64_t lda, int64_t n, int K, double scale, void* uh, void* ul,
+                        int64_t ldu, void* stream);
+/* Per unit u of a column-major fp32 table (columns 2u, 2u+1 = Re, Im):
+ * out[3u..3u+2] = [sum |phi|^2, max |phi|^2, first argmax + row_offset] —
+ * the normalisation / phase-pivot statistics of _order_and_pair (dmd.py:189-206). */
+size_t fdmd_pair_stats_workspace(int64_t n, int units);
+int fdmd_pair_stats(const float* raw, int64_t ld, int64_t n, int units, int64_t row_offset, double* out,
+                    void* workspace, size_t workspace_bytes, void* stream);
 int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch, const void* cl,
                    int ldk, int nf, const float* fscale, float* out, int64_t ldo, void* stream);
 

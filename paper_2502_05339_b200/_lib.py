@@ -50,6 +50,9 @@ SIGNATURES = {
     "fdmd_dmma_peak": (_i, [_d, _c.POINTER(_d)]),
     "fdmd_split_basis": (_i, [_vp, _i64, _i64, _i, _c.c_float, _vp, _vp, _i64, _vp]),
     "fdmd_split_coef": (_i, [_vp, _i, _i, _i, _c.c_float, _vp, _vp, _i, _vp, _vp]),
+    "fdmd_split_rows_f64": (_i, [_vp, _i64, _i64, _i, _d, _vp, _vp, _i64, _vp]),
+    "fdmd_pair_stats_workspace": (_sz, [_i64, _i]),
+    "fdmd_pair_stats": (_i, [_vp, _i64, _i64, _i, _i64, _vp, _vp, _sz, _vp]),
     "fdmd_tc_decode": (_i, [_vp, _vp, _i64, _i64, _i, _vp, _vp, _i, _i, _vp, _vp, _i64, _vp]),
     "fdmd_mac_decode": (_i, [_vp, _i, _i64, _i, _vp, _i, _i, _i, _vp, _vp]),
     "fdmd_mac_advect": (_i, [_vp, _i, _i, _i, _d, _d, _vp, _vp, _vp]),

@@ -1035,6 +1035,37 @@ int fdmd_split_basis(const float* D, int64_t ldd, int64_t n, int r, float scale,
   return FDMD_OK;
 }
 
+int fdmd_split_rows_f64(const double* A, int64_t lda, int64_t n, int K, double scale, void* uh, void* ul,
+                        int64_t ldu, void* stream) {
+  if (!A || !uh || !ul || n <= 0 || K <= 0 || ldu < K || lda < K || ldu % 8 || ldu > 256)
+    return fail(FDMD_ERR_INVALID, "split_rows_f64: bad arguments (ldu must be a multiple of 8, <= 256)");
+  const int64_t items = n * (ldu / 8);
+  fdmd::split_rows_f64_kernel<<<(unsigned)((items + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      A, lda, n, K, scale, (__half*)uh, (__half*)ul, ldu);
+  LAUNCH_CHECK("split_rows_f64");
+  return FDMD_OK;
+}
+
+size_t fdmd_pair_stats_workspace(int64_t n, int units) {
+  const int64_t splits = std::max<int64_t>(1, std::min<int64_t>((n + 65535) / 65536, 4 * sm_count_cached() / std::max(1, units) + 1));
+  return (size_t)splits * units * 3 * sizeof(double) + 256;
+}
+
+int fdmd_pair_stats(const float* raw, int64_t ld, int64_t n, int units, int64_t row_offset, double* out,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  if (!raw || !out || n <= 0 || units <= 0 || ld < n) return fail(FDMD_ERR_INVALID, "pair_stats: bad arguments");
+  const int64_t splits = std::max<int64_t>(1, std::min<int64_t>((n + 65535) / 65536, 4 * sm_count_cached() / std::max(1, units) + 1));
+  if (!workspace || workspace_bytes < (size_t)splits * units * 3 * sizeof(double))
+    return fail(FDMD_ERR_WORKSPACE, "pair_stats workspace");
+  const int64_t rps = (n + splits - 1) / splits;
+  cudaStream_t s = (cudaStream_t)stream;
+  fdmd::pair_stats_kernel<<<dim3(units, (unsigned)splits), 256, 0, s>>>(raw, ld, n, units, rps, (double*)workspace);
+  fdmd::pair_stats_final_kernel<<<(units + 127) / 128, 128, 0, s>>>((const double*)workspace, (int)splits, units,
+                                                                   row_offset, out);
+  LAUNCH_CHECK("pair_stats");
+  return FDMD_OK;
+}
+
 int fdmd_split_coef(const float* coef, int ldc, int r, int nf, float su_inv, void* ch, void* cl, int ldk,
                     float* fscale, void* stream) {
   if (!coef || !ch || !cl || !fscale || r <= 0 || nf <= 0 || ldk < r || ldc < nf)

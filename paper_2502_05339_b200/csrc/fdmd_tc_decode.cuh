@@ -375,3 +375,93 @@ __global__ void split_coef_kernel(const float* __restrict__ coef, int ldc, int r
 }
 
 }  // namespace fdmd
+
+namespace fdmd {
+
+// Us[i][k] (hi, lo fp16 planes, row-major, ld = ldu) from a row-major fp64
+// tall matrix A[i][k] (ld = lda, k < K; zero for K <= k < ldu), scaled by
+// 2^su — the sketch basis Q for the tcgen05 lift / modes products. One
+// thread per 8 consecutive k of a row: 64-B reads, 16-B plane stores.
+__global__ void split_rows_f64_kernel(const double* __restrict__ A, int64_t lda, int64_t n, int K, double scale,
+                                      __half* __restrict__ uh, __half* __restrict__ ul, int64_t ldu) {
+  const int vpr = (int)(ldu / 8);
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * vpr) return;
+  const int64_t i = e / vpr;
+  const int v = (int)(e - i * vpr);
+  __align__(16) __half h[8];
+  __align__(16) __half l[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int k = 8 * v + j;
+    const double x = k < K ? __ldcs(A + i * lda + k) * scale : 0.0;
+    h[j] = __double2half(x);
+    l[j] = __double2half(x - (double)__half2float(h[j]));
+  }
+  __stcs(reinterpret_cast<float4*>(uh + i * ldu + 8 * v), *reinterpret_cast<const float4*>(h));
+  __stcs(reinterpret_cast<float4*>(ul + i * ldu + 8 * v), *reinterpret_cast<const float4*>(l));
+}
+
+// Per unit u (columns 2u = Re, 2u+1 = Im of a column-major fp32 table):
+// [sum_i |phi_i|^2, max_i |phi_i|^2, first argmax i + row_offset] — the
+// statistics tall_gemm fuses into its DMMA epilogue, for tables produced by
+// the tcgen05 kernels. Fixed-order two-stage reduction (ties -> lowest row).
+__global__ void pair_stats_kernel(const float* __restrict__ raw, int64_t ld, int64_t n, int units,
+                                  int64_t rows_per_split, double* __restrict__ part) {
+  const int u = blockIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t r1 = min(n, r0 + rows_per_split);
+  const float* re = raw + (int64_t)(2 * u) * ld;
+  const float* im = raw + (int64_t)(2 * u + 1) * ld;
+  double sum = 0.0, mx = -1.0;
+  int64_t idx = INT64_MAX;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const double a = re[i], b = im[i];
+    const double v = a * a + b * b;
+    sum += v;
+    if (v > mx) { mx = v; idx = i; }
+  }
+  __shared__ double ss[256], sm[256];
+  __shared__ int64_t si[256];
+  ss[threadIdx.x] = sum;
+  sm[threadIdx.x] = mx;
+  si[threadIdx.x] = idx;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      ss[threadIdx.x] += ss[threadIdx.x + s];
+      const double om = sm[threadIdx.x + s];
+      const int64_t oi = si[threadIdx.x + s];
+      if (om > sm[threadIdx.x] || (om == sm[threadIdx.x] && oi < si[threadIdx.x])) {
+        sm[threadIdx.x] = om;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double* p = part + ((int64_t)blockIdx.y * units + u) * 3;
+    p[0] = ss[0];
+    p[1] = sm[0];
+    p[2] = __longlong_as_double((long long)si[0]);
+  }
+}
+
+__global__ void pair_stats_final_kernel(const double* __restrict__ part, int splits, int units, int64_t row_offset,
+                                        double* __restrict__ out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= units) return;
+  double sum = 0.0, mx = -1.0;
+  int64_t idx = INT64_MAX;
+  for (int s = 0; s < splits; ++s) {
+    const double* p = part + ((int64_t)s * units + u) * 3;
+    sum += p[0];
+    const int64_t pi = (int64_t)__double_as_longlong(p[2]);
+    if (p[1] > mx || (p[1] == mx && pi < idx)) { mx = p[1]; idx = pi; }
+  }
+  out[3 * u] = sum;
+  out[3 * u + 1] = mx;
+  out[3 * u + 2] = (double)(idx + row_offset);
+}
+
+}  // namespace fdmd

@@ -231,6 +231,37 @@ class CudaOps:
         self.launches += 1
         return {"uh": uh, "ul": ul, "ldu": ldu, "su": su, "n": n, "r": r}
 
+    def tc_rows(self, A: Tall, ncols: Optional[int] = None):
+        """fp16 hi/lo planes of a row-major fp64 tall matrix (the sketch basis
+        Q) for tc_decode: products Q @ M on tcgen05, FP32-accurate."""
+        import math
+        assert A.layout == "row" and A.dtype == torch.float64
+        K = A.k if ncols is None else ncols
+        n = A.n
+        ldu = round_up(K, 8)
+        lo, hi = torch.aminmax(A.buf[:n, :K])
+        mx = max(-float(lo.item()), float(hi.item()))
+        e = math.frexp(mx)[1] if mx > 0 else 0
+        su = math.ldexp(1.0, 14 - e)
+        uh = torch.empty((n, ldu), dtype=torch.float16, device=A.buf.device)
+        ul = torch.empty_like(uh)
+        _lib.check(_lib.lib().fdmd_split_rows_f64(_ptr(A.buf), A.ld, n, K, float(su), _ptr(uh), _ptr(ul), ldu,
+                                                  _stream()), "split_rows_f64")
+        self.launches += 1
+        return {"uh": uh, "ul": ul, "ldu": ldu, "su": su, "n": n, "r": K}
+
+    def pair_stats(self, raw: Tall, units: int, row_offset: int = 0) -> torch.Tensor:
+        """(units, 3) [sum |phi|^2, max |phi|^2, argmax row] of a col-major fp32 table."""
+        assert raw.layout == "col" and raw.dtype == torch.float32
+        L = _lib.lib()
+        out = torch.empty((units, 3), dtype=torch.float64, device=raw.buf.device)
+        wsb = int(L.fdmd_pair_stats_workspace(raw.n, units))
+        ws = self.ws.get(wsb, raw.buf.device)
+        _lib.check(L.fdmd_pair_stats(_ptr(raw.buf), raw.ld, raw.n, units, int(row_offset), _ptr(out), _ptr(ws), wsb,
+                                     _stream()), "pair_stats")
+        self.launches += 2
+        return out
+
     def tc_decode(self, tcb: dict, coef: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """frames (B x n fp32) = basis @ coef (r x B) on tcgen05."""
         r, n = tcb["r"], tcb["n"]

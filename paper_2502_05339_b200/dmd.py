@@ -13,6 +13,7 @@ the diagnostic, ``table_dtype`` for the decode table, ``timings`` dict.
 from __future__ import annotations
 
 import contextlib
+import os
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -264,7 +265,8 @@ def pair_plan(lam_raw) -> PairPlan:
 
 
 def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, shard: Optional[Shard],
-                table_dtype, timings: Optional[dict] = None, a_orthonormal: bool = False) -> DeviceModes:
+                table_dtype, timings: Optional[dict] = None, a_orthonormal: bool = False,
+                tc_src: Optional[dict] = None) -> DeviceModes:
     """phi_raw = A @ [0_top; Cmap] for every computed unit, with fused
     column statistics; then normalise + phase-canonicalise + lock conjugates
     + build the decode table (dmd.py:189-213 and 92-120) in one HBM pass.
@@ -272,18 +274,21 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
     Cmap: K x r complex (device) with phi_raw[:, j] = A[:, top:top+K] @ Cmap[:, j].
     a_orthonormal: A's columns are orthonormal (the POD basis U), which bounds
     the real-ification test of dmd.py:210 without an extra pass.
+    tc_src: {"planes": fp16 planes of Q, "Umap": l x r} with A = Q @ Umap —
+    the raw modes are then Q @ (Umap [Re|Im]) on tcgen05 (FP32-accurate,
+    fp32 table) and the statistics come from a streaming pass over the table.
     """
     ops = dv.get_ops()
-    dev = A.buf.device
+    dev = Cmap.device
     U = len(plan.src)
     K = int(Cmap.shape[0])
-    mA = A.k
+    mA = K + row_pad_top if A is None else A.k
     Bm = torch.zeros((mA, 2 * U), dtype=torch.float64, device=dev)
     src_t = torch.as_tensor(plan.src, device=dev, dtype=torch.long)
     Cs = Cmap[:, src_t]
     Bm[row_pad_top:row_pad_top + K, 0::2] = Cs.real
     Bm[row_pad_top:row_pad_top + K, 1::2] = Cs.imag
-    n_loc = A.n
+    n_loc = tc_src["n"] if A is None else A.n
     with stage("modes.alloc_raw"):
         raw = alloc_tall(n_loc, 2 * U, table_dtype, "col", device=dev)
     row0 = 0 if shard is None else shard.row0
@@ -292,8 +297,13 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
     # one column of each conjugate pair is executed, so the kernel is credited
     # with its executed 2 n K (2U) flops (the fit-level metric keeps the formula)
     with stage("modes.raw+stats"):
-        st = ops.tall_gemm(A, Bm, raw, stats=True, row_offset=row0,
-                           alg_flops=2.0 * n_loc * K * 2 * U)  # (U, 3)
+        if tc_src is not None:
+            coef = (tc_src["Umap"] @ Bm).to(torch.float32)                 # l x 2U
+            ops.tc_decode(tc_src["planes"], coef, out=raw.buf[: 2 * U])
+            st = ops.pair_stats(raw, U, row_offset=row0)
+        else:
+            st = ops.tall_gemm(A, Bm, raw, stats=True, row_offset=row0,
+                               alg_flops=2.0 * n_loc * K * 2 * U)  # (U, 3)
     post = stage("modes.post")
     post.__enter__()
     st = la._reduce_pair_stats(st, shard)
@@ -348,8 +358,22 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
         for k, (u, im_col) in enumerate(check):
             Bq[row_pad_top:row_pad_top + K, 2 * k] = torch.as_tensor(im_col, device=dev)
         with stage("modes.realify_pass"):
-            stq = la._reduce_pair_stats(ops.tall_gemm(A, Bq, None, stats=True, row_offset=row0), shard)
-            mx = torch.sqrt(stq[:, 1]).cpu().numpy()
+            if A is not None:
+                stq = la._reduce_pair_stats(ops.tall_gemm(A, Bq, None, stats=True, row_offset=row0), shard)
+                mx = torch.sqrt(stq[:, 1]).cpu().numpy()
+            else:
+                # no basis buffer (tcgen05 modes straight from Q): Im(phi_u s_u) from
+                # the raw table columns, re * Im(s) + im * Re(s) (rare path)
+                vals = []
+                for u, _ in check:
+                    su = complex(s[u])
+                    col = (raw.buf[2 * u, :n_loc].double() * su.imag + raw.buf[2 * u + 1, :n_loc].double() * su.real)
+                    vals.append(col.abs().max())
+                mxt = torch.stack(vals)
+                if shard is not None and shard.world > 1:
+                    import torch.distributed as tdist
+                    tdist.all_reduce(mxt, op=tdist.ReduceOp.MAX, group=shard.group)
+                mx = mxt.cpu().numpy()
         for k, (u, _) in enumerate(check):
             if mx[k] <= 1e-10:
                 realified_phi.add(u)
@@ -495,6 +519,9 @@ def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, po
 
 
 _SIDE = {}
+
+# OptDMD on fp32 tables: lift and modes on tcgen05 (FDMD_TC_FIT=0 keeps them on FP64 DMMA)
+_TC_FIT = os.environ.get("FDMD_TC_FIT", "1") != "0"
 
 
 def _side_stream(dev) -> torch.cuda.Stream:
@@ -711,8 +738,26 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
     # The lift does not depend on the eigenvalues: it is launched first, on all
     # but 8 SMs, and the r x r work below (eig, variable projection) runs on a
     # side stream in its shadow.
+    tc_src = None
     if basis.Umap is None:
         U = basis.A
+    elif (_TC_FIT and on_cuda and tdt == torch.float32 and basis.A.dtype == torch.float64
+          and basis.A.layout == "row" and basis.A.k <= 256):
+        # fp32 tables: the lift U = Q Ub and the modes Q (Ub B^T) run on tcgen05
+        # (FP16 2-way split, FP32-accurate — the precision of the fp32 tables
+        # they fill) from one fp16 copy of Q; Q itself is released before U
+        # is allocated (peak S + Q + planes = S + U + planes + table)
+        ops = dv.get_ops()
+        with stage("lift.split_Q"):
+            qt = ops.tc_rows(basis.A)
+        n_loc = basis.A.n
+        basis.A = None
+        U = None
+        if keep_basis:          # the config-4 basis; the model itself never needs U
+            with stage("lift.U=QUb"):
+                U = alloc_tall(n_loc, r, tdt, "col", device=dev)
+                ops.tc_decode(qt, basis.Umap.to(torch.float32), out=U.buf[:r])
+        tc_src = {"planes": qt, "Umap": basis.Umap, "n": n_loc}
     else:
         with stage("lift.U=QUb"):
             U = alloc_tall(basis.A.n, r, tdt, "col", device=basis.A.buf.device)
@@ -765,7 +810,9 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
     if basis.Umap is not None:
         basis.A = None                                                       # release Q
     with stage("optdmd.modes_total"):
-        modes = _modes_pass(U, Bt, plan, 0, data.shard, tdt, timings, a_orthonormal=True)
+        modes = _modes_pass(U if tc_src is None else None, Bt, plan, 0, data.shard, tdt, timings,
+                            a_orthonormal=True, tc_src=tc_src)
+    tc_src = None
     model = ReducedModel(None, plan.lam, Sv, data.dt, grid_meta=data.grid_meta,
                          provenance={"method": "optdmd", "svd": svd_mode, "seed": seed,
                                      "objective_history": history, "converged": converged},

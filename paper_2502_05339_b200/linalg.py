@@ -347,7 +347,12 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     stats: dict = {}
     if Q is None:
         with stage("sketch.alloc_Q"):
-            Q = alloc_tall(S.n, l, torch.float64, "row", device=dev)
+            # slack rows: once Q is released, the two fp32 tables that follow it
+            # (basis U, n x r, and the raw modes, n x (r + #real modes)) fit in
+            # its block — together Q's size plus a few fp32 columns
+            slack = (16 * S.n + (64 << 20)) // (8 * max(l, 1)) + 1
+            Qb = alloc_tall(S.n + slack, l, torch.float64, "row", device=dev)
+            Q = Tall(Qb.buf, "row", S.n, l)
     Om = torch.as_tensor(np.asarray(omega, dtype=np.float64), device=dev)
     Omp = _pad_rows(Om, m)
     nl = float(S.n)

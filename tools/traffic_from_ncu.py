@@ -90,7 +90,10 @@ def main():
     js = {"kernel": dom, "source": os.path.relpath(dst, ROOT), "launches": n,
           "traffic_bytes_per_launch": (rd + wr) / n, "dram_read_bytes_per_launch": rd / n,
           "dram_write_bytes_per_launch": wr / n, "share_of_device_time_under_ncu": round(t / total, 4),
-          "per_launch": per}
+          "per_launch": per,
+          "kernels": {s: {"launches": a[0], "traffic_bytes_per_launch": (a[2] + a[3]) / a[0],
+                          "share_of_device_time_under_ncu": round(a[1] / total, 4)}
+                      for s, a in agg.items() if any(o in s for o in OURS)}}
     with open(os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json"), "w") as f:
         json.dump(js, f, indent=1)
     print("\n".join(out[:30]))
