@@ -139,6 +139,10 @@ int fdmd_pair_stats(const float* raw, int64_t ld, int64_t n, int units, int64_t 
                     void* workspace, size_t workspace_bytes, void* stream);
 int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch, const void* cl,
                    int ldk, int nf, const float* fscale, float* out, int64_t ldo, void* stream);
+/* same, with flags: FDMD_SHARE_SMS leaves 8 SMs to work on another stream
+ * (the OptDMD eigen / variable-projection solves overlapping the lift) */
+int fdmd_tc_decode_ex(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch, const void* cl,
+                      int ldk, int nf, const float* fscale, float* out, int64_t ldo, int flags, void* stream);
 
 /* ---- 2-D MAC-grid serving / guided upscaling ----
  * State layout (grid.py:1-18): u block ny x (nx+1), then v block (ny+1) x nx. */

@@ -594,7 +594,7 @@ int launch_tc_decode_mc(const void* uh, const void* ul, int64_t ldu, int64_t n, 
 // CTA-pair variant (cta_group::2, M = 256 rows x N = 256 frames per pair tile)
 int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch,
                           const void* cl, int ldk, int nf, const float* fscale, float* out, int64_t ldo,
-                          void* stream) {
+                          void* stream, int reserve_pairs = 0) {
   auto encode = tensor_map_encoder();
   if (!encode) return fail(FDMD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap maps[4];
@@ -638,7 +638,7 @@ int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n
   fdmd::TCArgs ta{out, ldo, n, r, nf, fscale};
   const int64_t ptiles = (n + 2 * fdmd::tc2::BM - 1) / (2 * fdmd::tc2::BM);
   const int gy = (nf + fdmd::tc2::BN - 1) / fdmd::tc2::BN;
-  const int64_t npairs = std::max<int64_t>(1, std::min<int64_t>(ptiles, std::max(1, max_clusters / gy)));
+  const int64_t npairs = std::max<int64_t>(1, std::min<int64_t>(ptiles, std::max(1, max_clusters / gy - reserve_pairs)));
   cfg.gridDim = dim3((unsigned)(2 * npairs), gy);
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], ta));
   LAUNCH_CHECK("tc_decode2");
@@ -1077,6 +1077,11 @@ int fdmd_split_coef(const float* coef, int ldc, int r, int nf, float su_inv, voi
 
 int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch, const void* cl,
                    int ldk, int nf, const float* fscale, float* out, int64_t ldo, void* stream) {
+  return fdmd_tc_decode_ex(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, 0, stream);
+}
+
+int fdmd_tc_decode_ex(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch, const void* cl,
+                      int ldk, int nf, const float* fscale, float* out, int64_t ldo, int flags, void* stream) {
   if (!uh || !ul || !ch || !cl || !fscale || !out || n <= 0 || r <= 0 || nf <= 0 || r > fdmd::tc::BKC * fdmd::tc::MAXKC)
     return fail(FDMD_ERR_INVALID, "tc_decode: bad arguments (r must be <= %d)", fdmd::tc::BKC * fdmd::tc::MAXKC);
   if ((ldu * 2) % 16 || (ldk * 2) % 16 || ldu < r || ldk < r || ldo < n || n >= (int64_t)UINT32_MAX)
@@ -1094,8 +1099,9 @@ int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r
   // at n = 50.3M: 16.5 ms vs 21.3 ms for MC = 2 clusters); FDMD_TC_IMPL=mc
   // selects the multicast clusters instead
   static const int pair_on = [] { const char* e = getenv("FDMD_TC_IMPL"); return e ? (strcmp(e, "mc") == 0 ? 0 : 1) : 1; }();
-  if (ny > 1 && pair_on)
-    return launch_tc_decode_pair(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
+  if (ny > 1 && pair_on)   // FDMD_SHARE_SMS: leave 4 SM pairs to a concurrent stream
+    return launch_tc_decode_pair(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream,
+                                 (flags & FDMD_SHARE_SMS) ? 4 : 0);
   static const int mc_cap = [] { const char* e = getenv("FDMD_TC_MAX_CLUSTER"); return e ? atoi(e) : 8; }();
   if (ny == 1 || mc_cap <= 1)
     return launch_tc_decode_mc<128, 3, 0, 1>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);

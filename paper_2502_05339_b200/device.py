@@ -231,16 +231,21 @@ class CudaOps:
         self.launches += 1
         return {"uh": uh, "ul": ul, "ldu": ldu, "su": su, "n": n, "r": r}
 
-    def tc_rows(self, A: Tall, ncols: Optional[int] = None):
+    def tc_rows(self, A: Tall, ncols: Optional[int] = None, bound: Optional[float] = None):
         """fp16 hi/lo planes of a row-major fp64 tall matrix (the sketch basis
-        Q) for tc_decode: products Q @ M on tcgen05, FP32-accurate."""
+        Q) for tc_decode: products Q @ M on tcgen05, FP32-accurate. `bound`:
+        a known max |A| (an orthonormal basis: ~1) skips the scan and its host
+        sync, so the launch overlaps host-side small work."""
         import math
         assert A.layout == "row" and A.dtype == torch.float64
         K = A.k if ncols is None else ncols
         n = A.n
         ldu = round_up(K, 8)
-        lo, hi = torch.aminmax(A.buf[:n, :K])
-        mx = max(-float(lo.item()), float(hi.item()))
+        if bound is not None:
+            mx = float(bound)
+        else:
+            lo, hi = torch.aminmax(A.buf[:n, :K])
+            mx = max(-float(lo.item()), float(hi.item()))
         e = math.frexp(mx)[1] if mx > 0 else 0
         su = math.ldexp(1.0, 14 - e)
         uh = torch.empty((n, ldu), dtype=torch.float16, device=A.buf.device)
@@ -262,7 +267,8 @@ class CudaOps:
         self.launches += 2
         return out
 
-    def tc_decode(self, tcb: dict, coef: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def tc_decode(self, tcb: dict, coef: torch.Tensor, out: Optional[torch.Tensor] = None,
+                  share_sms: bool = False) -> torch.Tensor:
         """frames (B x n fp32) = basis @ coef (r x B) on tcgen05."""
         r, n = tcb["r"], tcb["n"]
         coef = coef.to(torch.float32).contiguous()
@@ -278,8 +284,9 @@ class CudaOps:
         L = _lib.lib()
         _lib.check(L.fdmd_split_coef(_ptr(coef), coef.stride(0), r, B, ctypes.c_float(1.0 / tcb["su"]), _ptr(ch),
                                      _ptr(cl), ldk, _ptr(fs), _stream()), "split_coef")
-        _lib.check(L.fdmd_tc_decode(_ptr(tcb["uh"]), _ptr(tcb["ul"]), tcb["ldu"], n, r, _ptr(ch), _ptr(cl), ldk, B,
-                                    _ptr(fs), _ptr(out), out.stride(0), _stream()), "tc_decode")
+        _lib.check(L.fdmd_tc_decode_ex(_ptr(tcb["uh"]), _ptr(tcb["ul"]), tcb["ldu"], n, r, _ptr(ch), _ptr(cl), ldk,
+                                       B, _ptr(fs), _ptr(out), out.stride(0), 2 if share_sms else 0, _stream()),
+                   "tc_decode")
         self._done("tc_decode", 2.0 * n * r * B, e0)
         self.launches += 2
         return out

@@ -749,14 +749,16 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
         # is allocated (peak S + Q + planes = S + U + planes + table)
         ops = dv.get_ops()
         with stage("lift.split_Q"):
-            qt = ops.tc_rows(basis.A)
+            # the buffer holds (near-)orthonormal columns (CholeskyQR2 output,
+            # Q = buffer @ fix with fix ~ I): |entries| <= ~1, no scan needed
+            qt = ops.tc_rows(basis.A, bound=2.0)
         n_loc = basis.A.n
         basis.A = None
         U = None
         if keep_basis:          # the config-4 basis; the model itself never needs U
             with stage("lift.U=QUb"):
                 U = alloc_tall(n_loc, r, tdt, "col", device=dev)
-                ops.tc_decode(qt, basis.Umap.to(torch.float32), out=U.buf[:r])
+                ops.tc_decode(qt, basis.Umap.to(torch.float32), out=U.buf[:r], share_sms=True)
         tc_src = {"planes": qt, "Umap": basis.Umap, "n": n_loc}
     else:
         with stage("lift.U=QUb"):
