@@ -28,7 +28,10 @@ namespace fdmd {
 
 namespace tgp {
 constexpr int BR = 16;
-constexpr int STAGES = 4;
+#ifndef FDMD_GRAM_STAGES
+#define FDMD_GRAM_STAGES 4
+#endif
+constexpr int STAGES = FDMD_GRAM_STAGES;
 constexpr int THREADS = 256;            // 8 warps = 2 per SM sub-partition -> up to 255 regs
 constexpr int MAXP = 8;                 // partitions (x 8 warp tiles) per launch
 constexpr int BOX_BYTES = BR * 128;
