@@ -476,10 +476,11 @@ class _Basis:
     V: torch.Tensor
     UtS: torch.Tensor
     stats: dict
+    pre: Optional[dict] = None
 
 
 def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, power_iters,
-               timings: Optional[dict]) -> _Basis:
+               timings: Optional[dict], pre_svd=None) -> _Basis:
     S, pending = data.take_pending() if svd_mode == "randomized" else (data.S, None)
     T = S.k - 1
     n_tot = data.n
@@ -494,7 +495,7 @@ def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, po
             raise ValueError(f"rank {r} out of range [1, {min(n_tot, T)}]")
         omega = la.draw_omega(T, l, seed)
         try:
-            f = la.sketch_factors(S, T, l, q, omega, data.shard, pending=pending)
+            f = la.sketch_factors(S, T, l, q, omega, data.shard, pending=pending, pre_svd=pre_svd)
         except BaseException:
             data.pending = pending      # a streamed upload that failed is redone by the next consumer
             raise
@@ -503,6 +504,7 @@ def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, po
         basis = _Basis(f.Q, f.right(Ub_r).contiguous(), f.s[:r].contiguous(), f.Vh[:r].t().contiguous(),
                        UtS, f.stats)
         basis.stats.update(l=l, p=p, q=q)
+        basis.pre = getattr(f, "pre", None)
     elif svd_mode == "full":
         X = Tall(S.buf, "row", S.n, T)                       # X = states[:, :-1] (dmd.py:248)
         svd = la.truncated_svd(X, r, shard=data.shard, keep_device=True)
@@ -528,7 +530,7 @@ def _side_stream(dev) -> torch.cuda.Stream:
     """Per-device stream for r x r work that overlaps a tall kernel."""
     key = str(dev)
     if key not in _SIDE:
-        _SIDE[key] = torch.cuda.Stream(device=dev)
+        _SIDE[key] = torch.cuda.Stream(device=dev, priority=-1)   # small solves go first
     return _SIDE[key]
 
 
@@ -721,8 +723,19 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
     n, T = data.n, data.n_transitions
     if not 1 <= r <= min(n, T):
         raise ValueError(f"rank {r} out of range [1, {min(n, T)}]")
+    use_tc = (_TC_FIT and svd_mode == "randomized" and torch.cuda.is_available()
+              and (table_dtype or _default_table_dtype(data)) == torch.float32 and data._S.buf.is_cuda)
+
+    def _pre_svd(Q, fix):
+        # the fp16 split of the CholeskyQR2 buffer (|entries| <= ~1: no scan)
+        # is issued under svd(B); Q = buffer @ fix, and fix is folded into Umap
+        if Q.dtype != torch.float64 or Q.layout != "row" or Q.k > 256:
+            return None
+        return dv.get_ops().tc_rows(Q, bound=2.0)
+
     with stage("optdmd.basis"):
-        basis = _fit_basis(data, r, svd_mode, seed, oversample, power_iters, timings)
+        basis = _fit_basis(data, r, svd_mode, seed, oversample, power_iters, timings,
+                           pre_svd=_pre_svd if use_tc else None)
     Sv = basis.S.cpu().numpy()
     _check_sigma(Sv)
     t0 = time.perf_counter()
@@ -750,8 +763,9 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
         ops = dv.get_ops()
         with stage("lift.split_Q"):
             # the buffer holds (near-)orthonormal columns (CholeskyQR2 output,
-            # Q = buffer @ fix with fix ~ I): |entries| <= ~1, no scan needed
-            qt = ops.tc_rows(basis.A, bound=2.0)
+            # Q = buffer @ fix with fix ~ I): |entries| <= ~1, no scan needed;
+            # normally already issued under svd(B) (sketch_factors pre_svd)
+            qt = getattr(basis, "pre", None) or ops.tc_rows(basis.A, bound=2.0)
         n_loc = basis.A.n
         basis.A = None
         U = None

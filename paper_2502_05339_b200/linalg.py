@@ -330,7 +330,8 @@ def _rows(T: Tall, r0: int, rr: int) -> Tall:
 
 
 def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Optional[Shard] = None,
-                   Q: Optional[Tall] = None, pending: Optional[PendingUpload] = None) -> SketchFactors:
+                   Q: Optional[Tall] = None, pending: Optional[PendingUpload] = None,
+                   pre_svd=None) -> SketchFactors:
     """Range finder + power passes + projection for X = S[:, :T].
 
     Kernel sequence (DESIGN.md §Fit pipeline): Y = S[Omega;0] -> CholQR2 ->
@@ -401,10 +402,40 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
         QtS = allreduce(shard, ops.tall_gram(Q, S, alg_flops=2 * nl * m * l))     # l x m
         if fix is not None:
             QtS = fix.t() @ QtS
+    pre = None
     with stage("small.svd(B)"):
         B = QtS[:, :T]
-        Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvdj" if B.is_cuda else None)
-    return SketchFactors(Q, Ub, s, Vh, QtS, stats, fix)
+        if pre_svd is not None and B.is_cuda:
+            # tall work that needs only Q (the caller's fp16 split of it) runs on
+            # the main stream while the small SVD runs on a side stream
+            main = torch.cuda.current_stream(B.device)
+            ready = torch.cuda.Event()
+            ready.record(main)
+            pre = pre_svd(Q, fix)
+            side = _svd_stream(B.device)
+            side.wait_event(ready)
+            with torch.cuda.stream(side):
+                Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvdj")
+            main.wait_stream(side)
+            for t in (B, Ub, s, Vh):
+                t.record_stream(side)
+        else:
+            Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvdj" if B.is_cuda else None)
+    f = SketchFactors(Q, Ub, s, Vh, QtS, stats, fix)
+    f.pre = pre
+    return f
+
+
+_SVD_STREAMS = {}
+
+
+def _svd_stream(dev) -> torch.cuda.Stream:
+    key = str(dev)
+    if key not in _SVD_STREAMS:
+        # high priority: its latency-bound small kernels take SMs ahead of the
+        # bulk split kernel queued on the main stream
+        _SVD_STREAMS[key] = torch.cuda.Stream(device=dev, priority=-1)
+    return _SVD_STREAMS[key]
 
 
 def _canonical_signs(Q: Tall, Ub_r: torch.Tensor, shard: Optional[Shard]) -> torch.Tensor:
