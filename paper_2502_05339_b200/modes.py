@@ -24,6 +24,10 @@ import torch
 from . import device as dv
 from .device import Shard, Tall, allreduce, alloc_tall
 
+# fp32 tables: batches of at least this many frames decode on tcgen05
+TC_MIN_FRAMES = 16
+_TC_DECODE = __import__("os").environ.get("FDMD_TC_DECODE", "1") != "0"
+
 
 def conjugate_pairs(lam, tol=1e-8):
     """partner[i] = j with lam[j] ~ conj(lam[i]); i itself if real or unmatched
@@ -126,6 +130,7 @@ class DeviceModes:
         self.general = general
         self.mix = None if mix is None else np.asarray(mix, dtype=np.float64)
         self._pinv_small = None
+        self._tc_planes = None     # fp16 hi/lo planes of the table for batched decodes
         # Gram of the raw table (D^T D, all raw columns): shared by every model
         # derived from the same table (editing.apply_edit folds into the mix)
         self.raw_gram = None
@@ -195,7 +200,15 @@ class DeviceModes:
         if self.mix is not None and not basis_coords:
             M = torch.as_tensor(self.mix[:, : int(C.shape[0])], device=C.device)
             C = M @ C.to(torch.float64)
-        return dv.get_ops().decode(self.table, C, out=out, ncols=int(C.shape[0]))
+        k = int(C.shape[0])
+        if (C.dim() == 2 and int(C.shape[1]) >= TC_MIN_FRAMES and self.table.dtype == torch.float32
+                and self.table.buf.is_cuda and k <= 256 and _TC_DECODE):
+            # frame batches on tcgen05 (FP32-accurate 2-way FP16 split): the
+            # table is read once per 256 frames instead of once per 32
+            if self._tc_planes is None or self._tc_planes["r"] != k:
+                self._tc_planes = dv.get_ops().tc_basis(self.table, ncols=k)
+            return dv.get_ops().tc_decode(self._tc_planes, C, out=out)
+        return dv.get_ops().decode(self.table, C, out=out, ncols=k)
 
     def host_table(self) -> np.ndarray:
         """n x ncol_table float64 (the reference's decode_table cols)."""

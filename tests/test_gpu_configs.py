@@ -65,6 +65,17 @@ def test_config1_full_size_properties(fd):
     rec = fd.decode(model, z0, to_host=False).double()
     rel = float(torch.linalg.vector_norm(rec - x0) / torch.linalg.vector_norm(x0))
     assert rel < 5e-3, rel
+    # BASELINE config 1: 200 integer steps (one tcgen05 batch over the fp32
+    # table) + 1 interactive single-frame GEMV — the batch equals per-frame
+    # GEMV decodes of the same states to FP32 accuracy
+    frames, _ = fd.rollout(model, z0, 200, to_host=False)
+    assert frames.shape == (200, p.n) and model.modes._tc_planes is not None
+    s = z0
+    for k in (1, 57, 200):
+        sk = fd.step_k(model, z0, k)
+        one = fd.decode(model, sk, to_host=False).double()
+        err = float(torch.linalg.vector_norm(frames[k - 1].double() - one) / torch.linalg.vector_norm(one))
+        assert err < 2e-6, (k, err)
 
 
 def test_config3_reduced_grid_device_generator_matches_host(fd):
