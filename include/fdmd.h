@@ -131,6 +131,10 @@ int fdmd_split_coef(const float* coef, int ldc, int r, int nf, float su_inv, voi
  * lift U = Q Ub (linalg.py:88) and modes Q (Ub B^T) (dmd.py:414). */
 int fdmd_split_rows_f64(const double* A, int64_t lda, int64_t n, int K, double scale, void* uh, void* ul,
                         int64_t ldu, void* stream);
+/* same for an fp32 or fp64 row-major matrix (dtype FDMD_F32 / FDMD_F64): the
+ * snapshot matrix S for the tcgen05 exact-DMD modes X' (V S^-1 W) (dmd.py:255,258) */
+int fdmd_split_rows(const void* A, int dtype, int64_t lda, int64_t n, int K, double scale, void* uh, void* ul,
+                    int64_t ldu, void* stream);
 /* Per unit u of a column-major fp32 table (columns 2u, 2u+1 = Re, Im):
  * out[3u..3u+2] = [sum |phi|^2, max |phi|^2, first argmax + row_offset] —
  * the normalisation / phase-pivot statistics of _order_and_pair (dmd.py:189-206). */

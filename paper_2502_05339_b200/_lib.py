@@ -51,6 +51,7 @@ SIGNATURES = {
     "fdmd_split_basis": (_i, [_vp, _i64, _i64, _i, _c.c_float, _vp, _vp, _i64, _vp]),
     "fdmd_split_coef": (_i, [_vp, _i, _i, _i, _c.c_float, _vp, _vp, _i, _vp, _vp]),
     "fdmd_split_rows_f64": (_i, [_vp, _i64, _i64, _i, _d, _vp, _vp, _i64, _vp]),
+    "fdmd_split_rows": (_i, [_vp, _i, _i64, _i64, _i, _d, _vp, _vp, _i64, _vp]),
     "fdmd_pair_stats_workspace": (_sz, [_i64, _i]),
     "fdmd_pair_stats": (_i, [_vp, _i64, _i64, _i, _i64, _vp, _vp, _sz, _vp]),
     "fdmd_tc_decode": (_i, [_vp, _vp, _i64, _i64, _i, _vp, _vp, _i, _i, _vp, _vp, _i64, _vp]),

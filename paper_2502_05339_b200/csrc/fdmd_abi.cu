@@ -1040,9 +1040,22 @@ int fdmd_split_rows_f64(const double* A, int64_t lda, int64_t n, int K, double s
   if (!A || !uh || !ul || n <= 0 || K <= 0 || ldu < K || lda < K || ldu % 8 || ldu > 256)
     return fail(FDMD_ERR_INVALID, "split_rows_f64: bad arguments (ldu must be a multiple of 8, <= 256)");
   const int64_t items = n * (ldu / 8);
-  fdmd::split_rows_f64_kernel<<<(unsigned)((items + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+  fdmd::split_rows_kernel<double><<<(unsigned)((items + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       A, lda, n, K, scale, (__half*)uh, (__half*)ul, ldu);
   LAUNCH_CHECK("split_rows_f64");
+  return FDMD_OK;
+}
+
+int fdmd_split_rows(const void* A, int dtype, int64_t lda, int64_t n, int K, double scale, void* uh, void* ul,
+                    int64_t ldu, void* stream) {
+  if (dtype == FDMD_F64) return fdmd_split_rows_f64((const double*)A, lda, n, K, scale, uh, ul, ldu, stream);
+  if (dtype != FDMD_F32) return fail(FDMD_ERR_INVALID, "split_rows: bad dtype");
+  if (!A || !uh || !ul || n <= 0 || K <= 0 || ldu < K || lda < K || ldu % 8 || ldu > 256)
+    return fail(FDMD_ERR_INVALID, "split_rows: bad arguments (ldu must be a multiple of 8, <= 256)");
+  const int64_t items = n * (ldu / 8);
+  fdmd::split_rows_kernel<float><<<(unsigned)((items + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      (const float*)A, lda, n, K, scale, (__half*)uh, (__half*)ul, ldu);
+  LAUNCH_CHECK("split_rows");
   return FDMD_OK;
 }
 

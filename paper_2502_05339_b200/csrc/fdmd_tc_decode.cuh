@@ -378,12 +378,13 @@ __global__ void split_coef_kernel(const float* __restrict__ coef, int ldc, int r
 
 namespace fdmd {
 
-// Us[i][k] (hi, lo fp16 planes, row-major, ld = ldu) from a row-major fp64
-// tall matrix A[i][k] (ld = lda, k < K; zero for K <= k < ldu), scaled by
+// Us[i][k] (hi, lo fp16 planes, row-major, ld = ldu) from a row-major fp64 /
+// fp32 tall matrix A[i][k] (ld = lda, k < K; zero for K <= k < ldu), scaled by
 // 2^su — the sketch basis Q for the tcgen05 lift / modes products. One
 // thread per 8 consecutive k of a row: 64-B reads, 16-B plane stores.
-__global__ void split_rows_f64_kernel(const double* __restrict__ A, int64_t lda, int64_t n, int K, double scale,
-                                      __half* __restrict__ uh, __half* __restrict__ ul, int64_t ldu) {
+template <typename TA>
+__global__ void split_rows_kernel(const TA* __restrict__ A, int64_t lda, int64_t n, int K, double scale,
+                                  __half* __restrict__ uh, __half* __restrict__ ul, int64_t ldu) {
   const int vpr = (int)(ldu / 8);
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n * vpr) return;
@@ -394,7 +395,7 @@ __global__ void split_rows_f64_kernel(const double* __restrict__ A, int64_t lda,
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int k = 8 * v + j;
-    const double x = k < K ? __ldcs(A + i * lda + k) * scale : 0.0;
+    const double x = k < K ? (double)__ldcs(A + i * lda + k) * scale : 0.0;
     h[j] = __double2half(x);
     l[j] = __double2half(x - (double)__half2float(h[j]));
   }

@@ -237,7 +237,7 @@ class CudaOps:
         a known max |A| (an orthonormal basis: ~1) skips the scan and its host
         sync, so the launch overlaps host-side small work."""
         import math
-        assert A.layout == "row" and A.dtype == torch.float64
+        assert A.layout == "row" and A.dtype in (torch.float64, torch.float32)
         K = A.k if ncols is None else ncols
         n = A.n
         ldu = round_up(K, 8)
@@ -250,8 +250,8 @@ class CudaOps:
         su = math.ldexp(1.0, 14 - e)
         uh = torch.empty((n, ldu), dtype=torch.float16, device=A.buf.device)
         ul = torch.empty_like(uh)
-        _lib.check(_lib.lib().fdmd_split_rows_f64(_ptr(A.buf), A.ld, n, K, float(su), _ptr(uh), _ptr(ul), ldu,
-                                                  _stream()), "split_rows_f64")
+        _lib.check(_lib.lib().fdmd_split_rows(_ptr(A.buf), _DT[A.dtype], A.ld, n, K, float(su), _ptr(uh), _ptr(ul),
+                                              ldu, _stream()), "split_rows")
         self.launches += 1
         return {"uh": uh, "ul": ul, "ldu": ldu, "su": su, "n": n, "r": K}
 

@@ -298,7 +298,8 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
     # with its executed 2 n K (2U) flops (the fit-level metric keeps the formula)
     with stage("modes.raw+stats"):
         if tc_src is not None:
-            coef = (tc_src["Umap"] @ Bm).to(torch.float32)                 # l x 2U
+            M = Bm if tc_src.get("Umap") is None else tc_src["Umap"] @ Bm
+            coef = M.to(torch.float32)                                       # (l | m) x 2U
             ops.tc_decode(tc_src["planes"], coef, out=raw.buf[: 2 * U])
             st = ops.pair_stats(raw, U, row_offset=row0)
         else:
@@ -587,6 +588,10 @@ def exact_dmd(data, r, svd_mode="full", seed=None, *, oversample=None, power_ite
     A, top = data.S, 1
     basis.A = None
     tdt = table_dtype or _default_table_dtype(data)
+    # (stays on FP64 DMMA: Phi = X' V S^-1 W amplifies the operand error by
+    # sigma_1 / sigma_r, so an FP32-accurate product is not enough here —
+    # measured 5% on a cancellation-prone frame checksum of config 1; the
+    # OptDMD modes U B^T have no such amplification and run on tcgen05)
     modes = _modes_pass(A, Cmap, plan, top, data.shard, tdt, timings)
     model = ReducedModel(None, plan.lam, Sv, data.dt, grid_meta=data.grid_meta,
                          provenance={"method": "exact", "svd": svd_mode, "seed": seed}, _modes=modes)
