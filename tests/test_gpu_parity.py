@@ -261,3 +261,34 @@ def test_modal_basis_config4_formula(fd):
         want = (Uh.astype(np.float64) @ np.real(W @ (lam[:, None] ** t[None, :] * b[:, None]))).T
         err = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
         assert err.max() <= FRAME_TOL
+
+
+def test_optdmd_tcgen05_lift_and_modes_match_dmma(fd):
+    """fp32 tables: the tcgen05 lift / modes (FP16 2-way split, FP32-accurate)
+    against the FP64 DMMA path on the same fit — eigenvalues identical (they
+    never touch the tall products), modes and frames to FP32 accuracy."""
+    from conftest import phase_aligned_error
+    from paper_2502_05339_b200 import dmd, synth
+    p = synth.config_params(3, seed=3, grid=16)
+    X = synth.generate_host(p)
+    assert X.dtype == np.float32
+    kw = dict(lm_config=fd.LMConfig(max_iters=10), svd_mode="randomized", seed=3, oversample=10, power_iters=1,
+              keep_basis=True)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        a = fd.optdmd(fd.SnapshotMatrix(X, synth.DT), 200, **kw)
+        old = dmd._TC_FIT
+        dmd._TC_FIT = False
+        try:
+            b = fd.optdmd(fd.SnapshotMatrix(X, synth.DT), 200, **kw)
+        finally:
+            dmd._TC_FIT = old
+    np.testing.assert_array_equal(a.lam, b.lam)
+    assert phase_aligned_error(a.phi, b.phi) <= 1e-5
+    Ua = a.basis_U.view().double().cpu().numpy()
+    Ub = b.basis_U.view().double().cpu().numpy()
+    assert np.abs(Ua - Ub).max() <= 5e-6 * np.abs(Ub).max()      # FP32-accurate products, fp32 storage
+    z0 = fd.encode(b, X[:, 0])
+    fa = fd.decode(a, fd.step_k(a, z0, 50))
+    fb = fd.decode(b, fd.step_k(b, z0, 50))
+    assert rel(fa, fb) <= 1e-5
