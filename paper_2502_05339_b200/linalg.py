@@ -383,21 +383,43 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     with stage("sketch.cholqr2"):
         # power iterations only need the span: one CholeskyQR pass unless this
         # is the last orthonormalisation (q = 0)
-        _, fix = cholqr2_deferred(Q, shard, stats, passes=2 if q == 0 else 1, G=G0)
+        R, fix = cholqr2_deferred(Q, shard, stats, passes=2 if q == 0 else 1, G=G0)
+    # Power iterations use only span(Z), Z = X^T Q. Whatever CholeskyQR
+    # variant ran, Q = X M R^-1 (M = Omega, then W; R its first return), so
+    # Z = (X^T X) M R^-1: one symmetric Gram of the snapshots replaces the
+    # q general X^T Q passes (an algebraically equivalent restructuring of
+    # the 2nTl power terms; the final projection Q^T S stays a tall Gram — it
+    # feeds the SVD directly and needs the direct product's accuracy).
+    GX = None
+    if q > 1 or (q == 1 and Zp is None):
+        with stage("power.XtX"):
+            GX = allreduce(shard, ops.tall_gram(S, S, K1=T, K2=T, symmetric=True,
+                                                alg_flops=1.0 * nl * T * T))   # T x T
+    M = Om
     for it in range(q):
         with stage("power.Z=XtQ"):
+            Z = None
             if it == 0 and Zp is not None and fix is not None:
                 Z = Zp @ fix            # streamed X^T Y, buffer untouched (R1^-1 folded)
-            else:
+            elif GX is not None:
+                # needs an invertible R (a rank-deficient sketch takes the
+                # Householder fallback, whose R may be singular: direct pass then)
+                dR = torch.diagonal(R).abs()
+                if float(dR.min()) > 1e-10 * float(dR.max()):
+                    eye = torch.eye(l, dtype=torch.float64, device=dev)
+                    Rinv = torch.linalg.solve_triangular(R, eye, upper=True)
+                    Z = GX @ (M @ Rinv)                                    # T x l = X^T Q
+            if Z is None:
                 Z = allreduce(shard, ops.tall_gram(S, Q, K1=T, alg_flops=2 * nl * T * l))   # T x l (X^T Q)
                 if fix is not None:
                     Z = Z @ fix
         with stage("power.qr(Z)"):
             W, _ = torch.linalg.qr(Z[:T], mode="reduced")    # T x l (Householder, device)
+        M = W
         with stage("power.Y=XW"):
             ops.tall_gemm(S, _pad_rows(W, m), Q, alg_flops=2 * nl * T * l)
         with stage("power.cholqr2"):
-            _, fix = cholqr2_deferred(Q, shard, stats, passes=2 if it == q - 1 else 1)
+            R, fix = cholqr2_deferred(Q, shard, stats, passes=2 if it == q - 1 else 1)
     with stage("project.QtS"):
         QtS = allreduce(shard, ops.tall_gram(Q, S, alg_flops=2 * nl * m * l))     # l x m
         if fix is not None:
@@ -448,6 +470,8 @@ def _canonical_signs(Q: Tall, Ub_r: torch.Tensor, shard: Optional[Shard]) -> tor
     row0 = 0 if shard is None else shard.row0
     st = ops.tall_gemm(Q, Bp, None, stats=True, row_offset=row0)   # (r, 3)
     st = _reduce_pair_stats(st, shard)
+    if not bool(torch.isfinite(st[:, :2]).all()):
+        raise ConvergenceError("randomized SVD: non-finite basis (degenerate sketch)")
     idx = st[:, 2].round().long()
     local = idx - row0
     if shard is not None and shard.world > 1:
