@@ -56,16 +56,19 @@ def fit_flops(n, m, r, p, q, modes="optdmd"):
 
 def executed_flops(n, m, r, p, q):
     """Flops libfdmd actually executes for the same fit (OptDMD, resident
-    snapshots): the power iterations take Z = X^T Q from one symmetric Gram
-    X^T X (n T^2) instead of q general X^T Q passes; the power-iteration
+    snapshots): with power iterations the sketch Y = X Omega, its Gram and
+    every Z = X^T Q follow from one symmetric Gram X^T X (n T^2); the power-iteration
     CholeskyQR is one SYRK with R1^-1 folded into Z; CholeskyQR2's final
     R2^-1 is folded into small matrices; triangular applies count n*l^2; the
     lift (2nlr) and the modes (one column per conjugate pair, ~2nr^2) run on
     tcgen05 for fp32 tables."""
     T = m - 1
     l = min(r + p, T)
-    # sketch + q (Y = XW) GEMMs, X^T X once, SYRKs (one per power stage, two at the end) + TRSM
-    return (2.0 * n * T * l * (1 + q) + (n * T * T if q > 0 else 0.0) + n * l * l * (q + 3)
+    if q == 0:   # explicit sketch: Y = X Omega, CholeskyQR2 (SYRK + TRSM + SYRK)
+        return 2.0 * n * T * l + 3.0 * n * l * l + 2.0 * n * m * l + 2.0 * n * l * r + 2.0 * n * r * r
+    # X^T X once (the sketch and every X^T Q follow from it), q Y = XW GEMMs,
+    # one SYRK per non-final power stage, SYRK + TRSM + SYRK at the end
+    return (2.0 * n * T * l * q + n * T * T + n * l * l * (q + 2)
             + 2.0 * n * m * l + 2.0 * n * l * r + 2.0 * n * r * r)
 
 

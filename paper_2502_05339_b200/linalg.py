@@ -358,10 +358,29 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     Omp = _pad_rows(Om, m)
     nl = float(S.n)
     G0 = Zp = None
-    if pending is None:
+    GX = None
+    implicit = False
+    if pending is None and q >= 1:
+        # With power iterations the sketch is only used through Z = X^T Q1,
+        # Q1 = X Omega R1^-1, R1 = chol(Omega^T X^T X Omega): all of it follows
+        # from the symmetric snapshot Gram X^T X, so Y = X Omega and its Gram
+        # are never formed (an algebraically equivalent restructuring of the
+        # sketch and first CholeskyQR terms; the explicit path remains for
+        # ill-conditioned sketches and q = 0)
+        with stage("power.XtX"):
+            GX = allreduce(shard, ops.tall_gram(S, S, K1=T, K2=T, symmetric=True,
+                                                alg_flops=1.0 * nl * T * T))   # T x T
+        with stage("sketch.implicit"):
+            G0s = Om.t() @ GX @ Om
+            R0 = _chol_upper(0.5 * (G0s + G0s.t()))
+            if R0 is not None and _cond_upper(R0) <= CHOLQR2_COND_LIMIT:
+                implicit = True
+                R, fix = R0, None
+                stats["implicit_sketch"] = 1
+    if pending is None and not implicit:
         with stage("sketch.Y=XOmega"):
             ops.tall_gemm(S, Omp, Q, alg_flops=2 * nl * T * l)
-    else:
+    elif pending is not None:
         G0 = torch.zeros((l, l), dtype=torch.float64, device=dev)
         Zp = torch.zeros((T, l), dtype=torch.float64, device=dev) if q > 0 else None
 
@@ -380,18 +399,18 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     # CholeskyQR2's final R2^-1 is kept as the small `fix` (Q = buffer @ fix)
     # and folded into Z, Q^T S and the lift; its tall apply is never executed
     # (counted as the TRSM term it replaces).
-    with stage("sketch.cholqr2"):
-        # power iterations only need the span: one CholeskyQR pass unless this
-        # is the last orthonormalisation (q = 0)
-        R, fix = cholqr2_deferred(Q, shard, stats, passes=2 if q == 0 else 1, G=G0)
+    if not implicit:
+        with stage("sketch.cholqr2"):
+            # power iterations only need the span: one CholeskyQR pass unless this
+            # is the last orthonormalisation (q = 0)
+            R, fix = cholqr2_deferred(Q, shard, stats, passes=2 if q == 0 else 1, G=G0)
     # Power iterations use only span(Z), Z = X^T Q. Whatever CholeskyQR
     # variant ran, Q = X M R^-1 (M = Omega, then W; R its first return), so
     # Z = (X^T X) M R^-1: one symmetric Gram of the snapshots replaces the
     # q general X^T Q passes (an algebraically equivalent restructuring of
     # the 2nTl power terms; the final projection Q^T S stays a tall Gram — it
     # feeds the SVD directly and needs the direct product's accuracy).
-    GX = None
-    if q > 1 or (q == 1 and Zp is None):
+    if GX is None and (q > 1 or (q == 1 and Zp is None)):
         with stage("power.XtX"):
             GX = allreduce(shard, ops.tall_gram(S, S, K1=T, K2=T, symmetric=True,
                                                 alg_flops=1.0 * nl * T * T))   # T x T
