@@ -184,8 +184,44 @@ def config_cases():
     return out
 
 
+def frame_cases():
+    """Round-2 additions (tests/golden/config_frames.npz): frames decoded from
+    the reference's OptDMD and exact-DMD models at the config-3 shape, so the
+    benched fit (OptDMD, r = T = 200, fp32 snapshots) is pinned through what a
+    user sees — z0 = encode(x0), decode(step_k(z0, k)) and a continuous-time
+    frame — not only through lambda."""
+    out = {}
+    ref_dmd._svd_of = _patched(10, 1)
+    try:
+        p = synth.config_params(3, seed=3, grid=16)
+        X = synth.generate_host(p)
+        out["c3s_checksum"] = checksum(X)
+        for tag, fit in (("opt", lambda: optdmd(SnapshotMatrix(X, synth.DT), 200, lm_config=LMConfig(max_iters=10),
+                                                svd_mode="randomized", seed=3)),
+                         ("exact", lambda: exact_dmd(SnapshotMatrix(X, synth.DT), 200, svd_mode="randomized",
+                                                     seed=3))):
+            model = fit()
+            z0 = encode(model, X[:, 0])
+            fr = np.stack([decode(model, step_k(model, z0, k)) for k in (1, 50, 199)]
+                          + [decode(model, eval_continuous(model, z0, 12.37))], axis=1)
+            out[f"c3s_{tag}_z0"] = z0.z
+            out[f"c3s_{tag}_lam"] = model.lam
+            out[f"c3s_{tag}_phi_norms"] = np.linalg.norm(model.phi, axis=0)
+            out[f"c3s_{tag}_frames_head"] = fr[:4096]
+            out[f"c3s_{tag}_frames_checksum"] = np.stack([fr.sum(0), (fr * fr).sum(0)])
+            out[f"c3s_{tag}_frames_x0_rel"] = np.array([np.linalg.norm(fr[:, 0] - X[:, 1]) / np.linalg.norm(X[:, 1])])
+    finally:
+        ref_dmd._svd_of = _orig_svd_of
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "frames":
+        f = frame_cases()
+        np.savez_compressed(os.path.join(OUT, "config_frames.npz"), **f)
+        print("config_frames.npz", os.path.getsize(os.path.join(OUT, "config_frames.npz")))
+        return
     s = small_cases()
     np.savez_compressed(os.path.join(OUT, "small_cases.npz"), **s)
     c = config_cases()

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(256) decode_kernel(const T* __restrict__ D, in
                                                      const T* __restrict__ coef, int ldcoef,
                                                      T* __restrict__ out, int64_t ldo, int64_t n,
                                                      int r, int B, int f0) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   T* cs = reinterpret_cast<T*>(smem_raw);  // r x FB
   for (int e = threadIdx.x; e < r * FB; e += blockDim.x) {
     const int k = e / FB, f = e % FB;
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) table_apply_inplace_kernel(T* __restrict_
                                                                   const double* __restrict__ alpha,
                                                                   const double* __restrict__ beta, int ncols,
                                                                   int64_t n, int rows_per_block) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   T* s = reinterpret_cast<T*>(smem_raw);  // nraw x rows_per_block
   for (int64_t r0 = (int64_t)blockIdx.x * rows_per_block; r0 < n; r0 += (int64_t)gridDim.x * rows_per_block) {
     const int64_t left = n - r0;

@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(tg::THREADS, (NF <= 4) ? 2 : 1) tall_gemm_kern
   using S = TGSmem<TA, A_LAYOUT, NF>;
   constexpr int BN = S::BN;
   constexpr int LDB = S::LDB;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
 
   const TA* __restrict__ A = static_cast<const TA*>(args.A);
@@ -367,7 +367,7 @@ template <typename TA, int LA, typename TB, int LB> struct GramSmem {
 
 template <typename TA, int LA, typename TB, int LB>
 __global__ void __launch_bounds__(gr::THREADS, 2) tall_gram_kernel(TallGramArgs args) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   auto& sm = *reinterpret_cast<GramSmem<TA, LA, TB, LB>*>(smem_raw);
   const TA* __restrict__ A = static_cast<const TA*>(args.A);
   const TB* __restrict__ B = static_cast<const TB*>(args.B);

@@ -243,7 +243,6 @@ tall_gemm_tma_kernel(const __grid_constant__ CUtensorMap amap, const __grid_cons
                      const TTArgs ta) {
   using S = TTSmem<TA, A_LAYOUT, NF>;
   constexpr int BN = S::BN;
-  constexpr int LDB = S::LDB;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // align by offsetting the __shared__ array (keeps LDS addressing)
   S& sm = *reinterpret_cast<S*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));

@@ -92,11 +92,37 @@ class Shard:
     group: object = None
     world: int = 1
 
-    def allreduce(self, t: torch.Tensor) -> torch.Tensor:
+    def _host_staged(self, t: torch.Tensor) -> bool:
+        """gloo collectives on device tensors go through host memory (the CPU
+        test harness and the 1-GPU multi-rank tests); NCCL reduces in HBM."""
+        import torch.distributed as dist
+        return t.is_cuda and dist.get_backend(self.group) == "gloo"
+
+    def allreduce(self, t: torch.Tensor, op: str = "sum") -> torch.Tensor:
+        """In-place all-reduce over the ranks' row blocks (sum or max)."""
         if self.world > 1:
             import torch.distributed as dist
-            dist.all_reduce(t, group=self.group)
+            rop = dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX
+            if self._host_staged(t):
+                h = t.cpu()
+                dist.all_reduce(h, op=rop, group=self.group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, op=rop, group=self.group)
         return t
+
+    def all_gather(self, t: torch.Tensor) -> list:
+        """Every rank's copy of t, in rank order."""
+        import torch.distributed as dist
+        t = t.contiguous()
+        if self._host_staged(t):
+            h = t.cpu()
+            out = [torch.empty_like(h) for _ in range(self.world)]
+            dist.all_gather(out, h, group=self.group)
+            return [o.to(t.device) for o in out]
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        return out
 
 
 SINGLE = None  # shard=None means the matrix is whole on this device

@@ -186,7 +186,7 @@ class ReducedModel:
         if self._phi_pinv is None:
             D, E = self.modes.basis()
             M = D.buf[: E.shape[0], : D.n].to(torch.float64).cpu().numpy()   # ncol x n
-            self._phi_pinv = self.modes.pinv_small() @ (E.conj().T @ M)
+            self._phi_pinv = self.modes.pinv_rows() @ M
         return self._phi_pinv
 
     def decode_table(self):
@@ -372,8 +372,7 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
                     vals.append(col.abs().max())
                 mxt = torch.stack(vals)
                 if shard is not None and shard.world > 1:
-                    import torch.distributed as tdist
-                    tdist.all_reduce(mxt, op=tdist.ReduceOp.MAX, group=shard.group)
+                    shard.allreduce(mxt, op="max")
                 mx = mxt.cpu().numpy()
         for k, (u, _) in enumerate(check):
             if mx[k] <= 1e-10:
@@ -547,8 +546,7 @@ def _residual_diag(data: SnapshotMatrix, modes: DeviceModes, lam: np.ndarray):
     T = S.k - 1
     D, E = modes.basis()
     DtS = allreduce(data.shard, dv.get_ops().tall_gram(D, S, K1=E.shape[0]))   # ncol x m
-    Y = E.conj().T @ DtS[:, :T].cpu().numpy()                                   # phi^H X
-    Z = modes.pinv_small() @ Y                                                  # pinv(phi) X
+    Z = modes.pinv_rows() @ DtS[:, :T].cpu().numpy()                           # pinv(phi) X
     F = np.real(E @ (lam[:, None] * Z))                                         # ncol x T
     out = dv.get_ops().residual(S, D, torch.as_tensor(F, device=S.buf.device), E.shape[0], T)
     out = allreduce(data.shard, out)
@@ -648,7 +646,7 @@ def _min_sep_t(alpha: torch.Tensor) -> float:
 
 def _objective_t(alpha, D, T):
     P = _vander_t(alpha, T)
-    B = torch.linalg.lstsq(P, D).solution
+    B = la.lstsq_minnorm(P, D)            # gelsd semantics (linalg.py:136-141)
     R = D - P @ B
     return float(torch.linalg.vector_norm(R).item()), B, P, R
 
@@ -901,43 +899,56 @@ def dmdc_fit(data, controls, r_aug, r, seed=None, *, oversample=10, power_iters=
     sketch of X' (seed + 1). reduced_b is scaled by 1/dt so that
     runtime.step_forced (which multiplies by dt, runtime.py:188) reproduces
     B u_j exactly.
+
+    Row-sharded data (``data.shard``): the ell control rows of [X; Upsilon]
+    live on the last rank; every reduction over rows is all-reduced.
     """
     data = _as_snapshots(data)
-    if data.shard is not None and data.shard.world > 1:
-        raise ValueError("dmdc_fit is single-device in this round")
+    shard = data.shard if (data.shard is not None and data.shard.world > 1) else None
     S = data.S
-    n, m = S.n, S.k
+    n_loc, m = S.n, S.k
+    n = data.n
     T = m - 1
     Ups = np.asarray(controls, dtype=np.float64)
     if Ups.ndim != 2 or Ups.shape[1] != T:
         raise ValueError(f"controls must be ell x {T}")
     ell = Ups.shape[0]
     dev = S.buf.device
-    # augmented tall matrix: rows [S; Upsilon | 0]
-    Aug = alloc_tall(n + ell, m, S.dtype, "row", device=dev, zero=False)
-    Aug.buf[:n].copy_(S.buf[:n])
-    tail = torch.zeros((ell, Aug.ld), dtype=S.dtype, device=dev)
-    tail[:, :T] = torch.as_tensor(Ups, dtype=S.dtype, device=dev)
-    Aug.buf[n:n + ell].copy_(tail)
+    last = shard is None or shard.row0 + n_loc == n
+    extra = ell if last else 0
+    # augmented tall matrix: rows [S; Upsilon | 0] (the control rows on the last shard)
+    Aug = alloc_tall(n_loc + extra, m, S.dtype, "row", device=dev, zero=False)
+    Aug.buf[:n_loc].copy_(S.buf[:n_loc])
+    if extra:
+        tail = torch.zeros((ell, Aug.ld), dtype=S.dtype, device=dev)
+        tail[:, :T] = torch.as_tensor(Ups, dtype=S.dtype, device=dev)
+        Aug.buf[n_loc:n_loc + ell].copy_(tail)
+    aug_shard = None
+    if shard is not None:
+        aug_shard = Shard(shard.row0, n_loc + extra, n + ell, shard.group, shard.world)
     t0 = time.perf_counter()
     p1 = min(oversample, min(n + ell, T) - r_aug)
-    f1 = la.sketch_factors(Aug, T, r_aug + p1, power_iters, la.draw_omega(T, r_aug + p1, seed))
+    f1 = la.sketch_factors(Aug, T, r_aug + p1, power_iters, la.draw_omega(T, r_aug + p1, seed), aug_shard)
     p2 = min(oversample, min(n, T) - r)
-    # sketch of X' = S[:, 1:]: shift by viewing S with column offset through padded smalls
-    f2 = _sketch_shifted(S, 1, T, r + p2, power_iters, la.draw_omega(T, r + p2, None if seed is None else seed + 1))
+    # rank-r sketch of X' = S[:, 1:] (column window c0 = 1 of the same resident S)
+    f2 = la.sketch_factors(S, T, r + p2, power_iters, la.draw_omega(T, r + p2, None if seed is None else seed + 1),
+                           shard, c0=1)
     Ub1 = f1.Ub[:, :r_aug]
     s1 = f1.s[:r_aug]
     V1 = f1.Vh[:r_aug].t()
     Ub2 = f2.Ub[:, :r]
     # U1^T Uhat = Ub1^T (Q1[:n]^T Q2) Ub2
-    Q1top = Tall(f1.Q.buf, "row", n, f1.Q.k)
-    M12 = dv.get_ops().tall_gram(Q1top, f2.Q)                          # l1 x l2
+    Q1top = Tall(f1.Q.buf, "row", n_loc, f1.Q.k)
+    M12 = allreduce(shard, dv.get_ops().tall_gram(Q1top, f2.Q))       # l1 x l2
     if f1.fix is not None:
         M12 = f1.fix.t() @ M12
     if f2.fix is not None:
         M12 = M12 @ f2.fix
     U1tUh = Ub1.t() @ M12 @ Ub2                                        # r_aug x r
-    U2 = f1.Q.buf[n:n + ell, : f1.Q.k].to(torch.float64) @ f1.right(Ub1)   # ell x r_aug
+    U2 = torch.zeros((ell, r_aug), dtype=torch.float64, device=dev)   # control rows of U1
+    if extra:
+        U2 = f1.Q.buf[n_loc:n_loc + ell, : f1.Q.k].to(torch.float64) @ f1.right(Ub1)
+    U2 = allreduce(shard, U2.contiguous())                             # ell x r_aug
     UhtXp = Ub2.t() @ f2.QtS[:, 1:]                                    # r x T
     core = UhtXp @ (V1 / s1[None, :])                                  # r x r_aug
     Atil = core @ U1tUh                                                # r x r
@@ -946,47 +957,22 @@ def dmdc_fit(data, controls, r_aug, r, seed=None, *, oversample=10, power_iters=
     plan = pair_plan(lam_raw)
     Wt = torch.as_tensor(W, device=dev)
     Cmap = ((V1 / s1[None, :]) @ U1tUh).to(torch.complex128) @ Wt     # T x r
+    del Aug, f1
     if timings is not None:
         torch.cuda.synchronize()
         timings["svd_s"] = time.perf_counter() - t0
     tdt = table_dtype or S.dtype
-    modes = _modes_pass(S, Cmap, plan, 1, None, tdt, timings)
+    modes = _modes_pass(S, Cmap, plan, 1, shard, tdt, timings)
     model = ReducedModel(None, plan.lam, s1.cpu().numpy()[:r] if r <= r_aug else s1.cpu().numpy(),
                          data.dt, grid_meta=data.grid_meta,
                          provenance={"method": "dmdc", "svd": "randomized", "seed": seed,
                                      "r_aug": r_aug}, _modes=modes)
     # reduced_b = pinv(phi) U_hat B~ / dt, U_hat = Q2 Ub2
     D, E = modes.basis()
-    DtQ2 = dv.get_ops().tall_gram(D, f2.Q, K1=E.shape[0])              # ncol x l2
+    DtQ2 = allreduce(shard, dv.get_ops().tall_gram(D, f2.Q, K1=E.shape[0]))   # ncol x l2
     y = (DtQ2 @ f2.right(Ub2) @ Btil).cpu().numpy()                    # ncol x ell
-    red = modes.pinv_small() @ (E.conj().T @ y) / data.dt
+    red = modes.pinv_rows() @ y / data.dt
     ctrl = ControlOperator([red], ["augmented"])
     model.provenance["A_tilde"] = Atil.cpu().numpy()
     model.provenance["B_tilde"] = Btil.cpu().numpy()
     return model, ctrl
-
-
-def _sketch_shifted(S: Tall, c0: int, T: int, l: int, q: int, omega: np.ndarray):
-    """sketch_factors for X = S[:, c0:c0+T] (zero-padded small factors)."""
-    ops = dv.get_ops()
-    dev = S.buf.device
-    m = S.k
-
-    def pad(B):
-        out = torch.zeros((m, B.shape[1]), dtype=torch.float64, device=dev)
-        out[c0:c0 + B.shape[0]] = B
-        return out
-
-    Q = alloc_tall(S.n, l, torch.float64, "row", device=dev)
-    ops.tall_gemm(S, pad(torch.as_tensor(omega, device=dev)), Q)
-    la.cholqr2_inplace(Q)
-    for _ in range(q):
-        Z = ops.tall_gram(S, Q)
-        W, _ = torch.linalg.qr(Z[c0:c0 + T], mode="reduced")
-        ops.tall_gemm(S, pad(W), Q)
-        la.cholqr2_inplace(Q)
-    QtS = ops.tall_gram(Q, S)
-    B = QtS[:, c0:c0 + T]
-    Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvdj" if B.is_cuda else None)
-    # QtS re-indexed so that column 1.. of the returned block is Q^T X'_{shifted}
-    return la.SketchFactors(Q, Ub, s, Vh, QtS, {})

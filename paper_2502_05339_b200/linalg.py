@@ -119,6 +119,10 @@ class PendingUpload:
         rows = S.n
         nst = min(self.chunk, rows)
         staging = [torch.empty(nst * k, dtype=S.dtype, device=dev) for _ in range(2)]
+        # the staging blocks come from the compute stream's pool: they may be
+        # blocks freed there while queued kernels still read them, so the copy
+        # stream starts behind everything already queued on the compute stream
+        copy.wait_stream(comp)
         freed = [None, None]
         ok = torch.ones((), dtype=torch.bool, device=dev)
         for i, r0 in enumerate(range(0, rows, self.chunk)):
@@ -257,8 +261,8 @@ def cholqr2_deferred(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dic
         _apply_rinv(Y, R0, shard)
         G = allreduce(shard, ops.tall_gram(Y, Y, symmetric=True))
         R1b = _chol_upper(G)
-        if R1b is None:
-            return _householder_inplace(Y, shard, stats), None
+        if R1b is None:      # Y now holds Y_in R0^-1: its Householder R times R0 is Y_in's
+            return _householder_inplace(Y, shard, stats) @ R0, None
         _apply_rinv(Y, R1b, shard)
         R1 = R1b @ R0
         if stats is not None:
@@ -285,13 +289,41 @@ def cholqr2_deferred(Y: Tall, shard: Optional[Shard] = None, stats: Optional[dic
 def _householder_inplace(Y: Tall, shard: Optional[Shard], stats: Optional[dict]) -> torch.Tensor:
     """Numerically rank-deficient sketch: Householder QR on the device
     (cuSOLVER geqrf/orgqr), matching the reference's np.linalg.qr."""
-    if shard is not None and shard.world > 1:
-        raise ConvergenceError("rank-deficient sketch on a row-sharded matrix (TSQR not implemented)")
     if stats is not None:
         stats["householder_fallback"] = stats.get("householder_fallback", 0) + 1
+    if shard is not None and shard.world > 1:
+        return _tsqr_inplace(Y, shard)
     Q, R = torch.linalg.qr(Y.view().to(torch.float64), mode="reduced")
     Y.view().copy_(Q.to(Y.dtype))
     return R
+
+
+def _tsqr_inplace(Y: Tall, shard: Shard) -> torch.Tensor:
+    """Householder TSQR over the row shards (one level: every rank factors its
+    block, the stacked l x l R factors are all-gathered and factored again).
+    Every rank factors the same gathered stack in rank order, so the small R
+    and the combine blocks are identical on all ranks; each rank then applies
+    its own l x l block to its local Q. Returns R (Y_in = Q R)."""
+    l = Y.k
+    dev = Y.buf.device
+    Yl = Y.view().to(torch.float64)
+    if Y.n >= l:
+        Ql, Rl = torch.linalg.qr(Yl, mode="reduced")                       # n_loc x l, l x l
+    else:   # a shard shorter than the sketch width: pad its R with zero rows
+        Ql, Rs = torch.linalg.qr(Yl, mode="complete")                      # n_loc x n_loc, n_loc x l
+        Rl = torch.zeros((l, l), dtype=torch.float64, device=dev)
+        Rl[: Rs.shape[0]] = Rs
+        Ql = torch.cat([Ql, torch.zeros((Y.n, l - Y.n), dtype=torch.float64, device=dev)], dim=1)
+    stack = torch.cat(shard.all_gather(Rl.contiguous()), dim=0)          # (world l) x l, rank order
+    Q2, R = torch.linalg.qr(stack, mode="reduced")
+    blk = Q2[shard_rank(shard) * l:(shard_rank(shard) + 1) * l]            # this rank's l x l combine block
+    Y.view().copy_((Ql @ blk).to(Y.dtype))
+    return R
+
+
+def shard_rank(shard: Shard) -> int:
+    import torch.distributed as dist
+    return dist.get_rank(shard.group)
 
 
 # ---------------------------------------------------------------------------
@@ -329,19 +361,85 @@ def _rows(T: Tall, r0: int, rr: int) -> Tall:
     return Tall(T.buf[r0:r0 + rr], "row", rr, T.k)
 
 
+# Snapshot-Gram route. X^T X costs n T^2 flops and T^2
+# doubles; it replaces the sketch Y = X Omega, every power pass Z = X^T Q and
+# the first CholeskyQR pass of each orthonormalisation (~2nTl(1+q) + nl^2(1+q)),
+# so it is taken only when it is the cheaper side and its T x T block is small
+# (a long series, T >> l, or a wide matrix keeps the explicit path).
+GRAM_ROUTE_MAX_BYTES = 2 << 30
+
+
+def gram_route_ok(T: int, l: int, q: int) -> bool:
+    if q < 1 or 8.0 * T * T > GRAM_ROUTE_MAX_BYTES:
+        return False
+    return float(T) * T <= 2.0 * T * l * (1 + q) + float(l) * l * (1 + q)
+
+
+def _inv_upper(R: torch.Tensor) -> torch.Tensor:
+    eye = torch.eye(R.shape[0], dtype=torch.float64, device=R.device)
+    return torch.linalg.solve_triangular(R, eye, upper=True)
+
+
+def _gram_factor(GX: torch.Tensor, M: torch.Tensor):
+    """R = chol(M^T (X^T X) M): the CholeskyQR factor of the tall X M taken
+    from the snapshot Gram, or None when X M is too ill-conditioned for
+    CholeskyQR (the explicit path and its shifted / Householder fallbacks
+    then run on the tall buffer)."""
+    G = M.t() @ GX @ M
+    R = _chol_upper(0.5 * (G + G.t()))
+    if R is None or not _cond_upper(R) <= CHOLQR2_COND_LIMIT:
+        return None
+    return R
+
+
+def _cholqr_second_pass(Q: Tall, shard: Optional[Shard], stats: dict):
+    """CholeskyQR2's second pass over a buffer that already holds Q1 (its
+    first pass came from the snapshot Gram): R2 = chol(Q1^T Q1) and
+    fix = R2^-1, never applied to the tall buffer. Falls back to the full
+    CholeskyQR2 / shifted CholeskyQR3 / Householder chain on the buffer."""
+    ops = dv.get_ops()
+    with stage("cholqr.gram2"):
+        G2 = allreduce(shard, ops.tall_gram(Q, Q, symmetric=True))
+    R2 = _chol_upper(G2)
+    if R2 is None:
+        stats["gram_first_pass_fallback"] = stats.get("gram_first_pass_fallback", 0) + 1
+        return cholqr2_deferred(Q, shard, stats, passes=2, G=G2)
+    return R2, _inv_upper(R2)
+
+
+def _place_rows(Bsmall: torch.Tensor, rows: int, r0: int) -> torch.Tensor:
+    """Bsmall placed at rows [r0, r0 + K) of a zero rows x N matrix (the small
+    operand of S @ [0; B; 0] for a column window of S)."""
+    if r0 == 0:
+        return _pad_rows(Bsmall, rows)
+    out = torch.zeros((rows, Bsmall.shape[1]), dtype=torch.float64, device=Bsmall.device)
+    out[r0:r0 + Bsmall.shape[0]] = Bsmall
+    return out
+
+
 def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Optional[Shard] = None,
                    Q: Optional[Tall] = None, pending: Optional[PendingUpload] = None,
-                   pre_svd=None) -> SketchFactors:
-    """Range finder + power passes + projection for X = S[:, :T].
+                   pre_svd=None, c0: int = 0) -> SketchFactors:
+    """Range finder + power passes + projection for X = S[:, c0:c0+T]
+    (linalg.py:62-90 with Householder QR replaced by CholeskyQR2).
 
-    Kernel sequence (DESIGN.md §Fit pipeline): Y = S[Omega;0] -> CholQR2 ->
-    q x {Z = S^T Q (allreduce) -> W = qr(Z[:T]) -> Y = S[W;0] -> CholQR2} ->
-    Q^T S (allreduce) -> svd(Q^T X) on device.
+    Kernel sequence, snapshot-Gram route (q >= 1):
+      G_X = X^T X (one symmetric tall Gram; streamed: accumulated chunk by
+      chunk under the host->device transfer) -> R0 = chol(Omega^T G_X Omega)
+      -> q x {Z = G_X M R^-1 -> W = qr(Z); R1 = chol(W^T G_X W)} (non-final
+      stages never touch the tall data) -> Q1 = S [W R1^-1; 0] (the only tall
+      GEMM) -> R2 = chol(Q1^T Q1) (CholeskyQR2's second pass; fix = R2^-1 is
+      folded into every consumer) -> Q^T S -> svd(Q^T X) on the device.
+    Explicit route (q = 0, T >> l, or an ill-conditioned factor): Y = S[Omega;0]
+    -> CholQR -> q x {Z = S^T Q -> W = qr(Z) -> Y = S[W;0] -> CholQR} -> Q^T S.
 
-    With `pending` (S still streaming in from the host), the first stage —
-    Y = S[Omega;0], Y^T Y and X^T Y, all row-separable — runs chunk by chunk
-    as rows land, in the shadow of the host->device transfer.
+    With `pending` (S still streaming in from the host) the row-separable
+    first stage (G_X, or Y / Y^T Y / X^T Y on the explicit route) runs chunk by
+    chunk as rows land, in the shadow of the transfer.
+    The returned QtS is Q^T S over all m columns of S.
     """
+    if pending is not None and c0 != 0:
+        raise ValueError("a streamed upload sketches the leading columns only")
     ops = dv.get_ops()
     dev = S.buf.device
     m = S.k
@@ -355,31 +453,21 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
             Qb = alloc_tall(S.n + slack, l, torch.float64, "row", device=dev)
             Q = Tall(Qb.buf, "row", S.n, l)
     Om = torch.as_tensor(np.asarray(omega, dtype=np.float64), device=dev)
-    Omp = _pad_rows(Om, m)
+    Omp = _place_rows(Om, m, c0)
     nl = float(S.n)
-    G0 = Zp = None
-    GX = None
-    implicit = False
-    if pending is None and q >= 1:
-        # With power iterations the sketch is only used through Z = X^T Q1,
-        # Q1 = X Omega R1^-1, R1 = chol(Omega^T X^T X Omega): all of it follows
-        # from the symmetric snapshot Gram X^T X, so Y = X Omega and its Gram
-        # are never formed (an algebraically equivalent restructuring of the
-        # sketch and first CholeskyQR terms; the explicit path remains for
-        # ill-conditioned sketches and q = 0)
-        with stage("power.XtX"):
-            GX = allreduce(shard, ops.tall_gram(S, S, K1=T, K2=T, symmetric=True,
-                                                alg_flops=1.0 * nl * T * T))   # T x T
-        with stage("sketch.implicit"):
-            G0s = Om.t() @ GX @ Om
-            R0 = _chol_upper(0.5 * (G0s + G0s.t()))
-            if R0 is not None and _cond_upper(R0) <= CHOLQR2_COND_LIMIT:
-                implicit = True
-                R, fix = R0, None
-                stats["implicit_sketch"] = 1
-    if pending is None and not implicit:
-        with stage("sketch.Y=XOmega"):
-            ops.tall_gemm(S, Omp, Q, alg_flops=2 * nl * T * l)
+    Tc = c0 + T
+    use_gram = gram_route_ok(T, l, q)
+    GX = G0 = Zp = None
+    if pending is not None and use_gram:
+        GX = torch.zeros((T, T), dtype=torch.float64, device=dev)
+
+        def gram_stage(r0, rr):
+            Sc = _rows(S, r0, rr)
+            ops.tall_gram(Sc, Sc, K1=T, K2=T, symmetric=True, out=GX, beta=1.0, alg_flops=1.0 * rr * T * T)
+
+        with stage("sketch.stream_upload+XtX"):
+            pending.run(gram_stage)
+        GX = allreduce(shard, GX)
     elif pending is not None:
         G0 = torch.zeros((l, l), dtype=torch.float64, device=dev)
         Zp = torch.zeros((T, l), dtype=torch.float64, device=dev) if q > 0 else None
@@ -396,56 +484,83 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
         G0 = allreduce(shard, G0)
         if Zp is not None:
             Zp = allreduce(shard, Zp)
-    # CholeskyQR2's final R2^-1 is kept as the small `fix` (Q = buffer @ fix)
-    # and folded into Z, Q^T S and the lift; its tall apply is never executed
-    # (counted as the TRSM term it replaces).
+    elif use_gram:
+        with stage("power.XtX"):
+            GX = allreduce(shard, ops.tall_gram(S, S, K1=Tc, K2=Tc, symmetric=True,
+                                                alg_flops=1.0 * nl * T * T))   # (c0+T)^2
+            if c0:
+                GX = GX[c0:, c0:].contiguous()                               # T x T block of X
+    implicit = False
+    if GX is not None:
+        # the sketch enters the algorithm only through Z = X^T Q1, Q1 = X Omega R0^-1,
+        # R0 = chol((X Omega)^T (X Omega)): all of it follows from G_X, so Y = X Omega
+        # and its Gram are never formed (counted as the terms they replace)
+        with stage("sketch.implicit"):
+            R0 = _gram_factor(GX, Om)
+        if R0 is not None:
+            implicit = True
+            R, fix = R0, None
+            stats["implicit_sketch"] = 1
     if not implicit:
+        if G0 is None:
+            with stage("sketch.Y=XOmega"):
+                ops.tall_gemm(S, Omp, Q, alg_flops=2 * nl * T * l)
         with stage("sketch.cholqr2"):
             # power iterations only need the span: one CholeskyQR pass unless this
             # is the last orthonormalisation (q = 0)
             R, fix = cholqr2_deferred(Q, shard, stats, passes=2 if q == 0 else 1, G=G0)
-    # Power iterations use only span(Z), Z = X^T Q. Whatever CholeskyQR
-    # variant ran, Q = X M R^-1 (M = Omega, then W; R its first return), so
-    # Z = (X^T X) M R^-1: one symmetric Gram of the snapshots replaces the
-    # q general X^T Q passes (an algebraically equivalent restructuring of
-    # the 2nTl power terms; the final projection Q^T S stays a tall Gram — it
-    # feeds the SVD directly and needs the direct product's accuracy).
-    if GX is None and (q > 1 or (q == 1 and Zp is None)):
-        with stage("power.XtX"):
-            GX = allreduce(shard, ops.tall_gram(S, S, K1=T, K2=T, symmetric=True,
-                                                alg_flops=1.0 * nl * T * T))   # T x T
     M = Om
     for it in range(q):
+        final = it == q - 1
         with stage("power.Z=XtQ"):
             Z = None
             if it == 0 and Zp is not None and fix is not None:
                 Z = Zp @ fix            # streamed X^T Y, buffer untouched (R1^-1 folded)
             elif GX is not None:
-                # needs an invertible R (a rank-deficient sketch takes the
-                # Householder fallback, whose R may be singular: direct pass then)
+                # Q = X M R^-1 whatever CholeskyQR variant ran, so Z = X^T Q =
+                # G_X M R^-1; needs an invertible R (a rank-deficient sketch takes
+                # the Householder fallback, whose R may be singular: direct pass then)
                 dR = torch.diagonal(R).abs()
                 if float(dR.min()) > 1e-10 * float(dR.max()):
-                    eye = torch.eye(l, dtype=torch.float64, device=dev)
-                    Rinv = torch.linalg.solve_triangular(R, eye, upper=True)
-                    Z = GX @ (M @ Rinv)                                    # T x l = X^T Q
+                    Z = GX @ (M @ _inv_upper(R))                          # T x l = X^T Q
             if Z is None:
-                Z = allreduce(shard, ops.tall_gram(S, Q, K1=T, alg_flops=2 * nl * T * l))   # T x l (X^T Q)
+                Z = allreduce(shard, ops.tall_gram(S, Q, K1=Tc, alg_flops=2 * nl * T * l))[c0:]   # X^T Q
                 if fix is not None:
                     Z = Z @ fix
         with stage("power.qr(Z)"):
             W, _ = torch.linalg.qr(Z[:T], mode="reduced")    # T x l (Householder, device)
         M = W
-        with stage("power.Y=XW"):
-            ops.tall_gemm(S, _pad_rows(W, m), Q, alg_flops=2 * nl * T * l)
-        with stage("power.cholqr2"):
-            R, fix = cholqr2_deferred(Q, shard, stats, passes=2 if it == q - 1 else 1)
+        R1 = None
+        if GX is not None:
+            with stage("power.chol(WtGW)"):
+                R1 = _gram_factor(GX, W)
+        if R1 is not None and not final:
+            # a non-final power stage is span-only: Q = X W R1^-1 stays implicit and
+            # the next Z = G_X W R1^-1 needs no tall pass
+            R, fix = R1, None
+            stats["gram_power_stages"] = stats.get("gram_power_stages", 0) + 1
+            continue
+        if R1 is not None:
+            # CholeskyQR2 with its first pass from the snapshot Gram: the tall GEMM
+            # writes Q1 = X (W R1^-1) directly (no Y^T Y Gram, no triangular apply)
+            with stage("power.Y=XWR1^-1"):
+                ops.tall_gemm(S, _place_rows(W @ _inv_upper(R1), m, c0), Q, alg_flops=2 * nl * T * l)
+            with stage("power.cholqr2"):
+                R2, fix = _cholqr_second_pass(Q, shard, stats)
+            R = R2 @ R1
+            stats["gram_first_pass"] = 1
+        else:
+            with stage("power.Y=XW"):
+                ops.tall_gemm(S, _place_rows(W, m, c0), Q, alg_flops=2 * nl * T * l)
+            with stage("power.cholqr2"):
+                R, fix = cholqr2_deferred(Q, shard, stats, passes=2 if final else 1)
     with stage("project.QtS"):
         QtS = allreduce(shard, ops.tall_gram(Q, S, alg_flops=2 * nl * m * l))     # l x m
         if fix is not None:
             QtS = fix.t() @ QtS
     pre = None
     with stage("small.svd(B)"):
-        B = QtS[:, :T]
+        B = QtS[:, c0:c0 + T]
         if pre_svd is not None and B.is_cuda:
             # tall work that needs only Q (the caller's fp16 split of it) runs on
             # the main stream while the small SVD runs on a side stream
@@ -508,9 +623,7 @@ def _reduce_pair_stats(st: torch.Tensor, shard: Optional[Shard]) -> torch.Tensor
     """Combine per-rank [sumsq, max, argmax] (argmax ties -> lowest global row)."""
     if shard is None or shard.world <= 1:
         return st
-    import torch.distributed as dist
-    gathered = [torch.empty_like(st) for _ in range(shard.world)]
-    dist.all_gather(gathered, st.contiguous(), group=shard.group)
+    gathered = shard.all_gather(st)
     out = gathered[0].clone()
     out[:, 0] = 0.0
     for g in gathered:                                       # fixed rank order
@@ -557,30 +670,51 @@ def randomized_svd(M, r, oversample=10, power_iters=2, seed=None, *, omega=None,
 
 def truncated_svd(M, r, *, shard: Optional[Shard] = None, keep_device=False) -> SvdResult:
     """Dense truncated SVD (linalg.py:47-59) of a tall matrix on the device:
-    Householder QR (cuSOLVER) then SVD of the small R factor."""
+    Householder QR (cuSOLVER; TSQR across row shards) then the SVD of the
+    small R factor; signs canonicalised as linalg.py:29-44."""
     A = as_tall(M)
-    if shard is not None and shard.world > 1:
-        raise ValueError("svd_mode='full' is single-device; use 'randomized' for row-sharded data")
-    rows, cols = A.n, A.k
+    sharded = shard is not None and shard.world > 1
+    rows, cols = (shard.n_global if sharded else A.n), A.k
     if not 1 <= r <= min(rows, cols):
         raise ValueError(f"rank {r} out of range [1, {min(rows, cols)}]")
-    X = A.view().to(torch.float64)
-    if rows >= cols:
-        Qf, Rf = torch.linalg.qr(X, mode="reduced")
+    if sharded:
+        if rows < cols:
+            raise ValueError("svd_mode='full' on row-sharded data needs at least as many rows as columns")
+        Y = alloc_tall(A.n, cols, torch.float64, "row", device=A.buf.device)
+        Y.view().copy_(A.view())
+        Rf = _tsqr_inplace(Y, shard)
         Ur, s, Vh = torch.linalg.svd(Rf, full_matrices=False, driver="gesvdj" if Rf.is_cuda else None)
-        Ufull = Qf @ Ur
+        Ufull = Y.view() @ Ur
+        del Y
     else:
-        Ufull, s, Vh = torch.linalg.svd(X, full_matrices=False, driver="gesvd" if X.is_cuda else None)
+        X = A.view().to(torch.float64)
+        if rows >= cols:
+            Qf, Rf = torch.linalg.qr(X, mode="reduced")
+            Ur, s, Vh = torch.linalg.svd(Rf, full_matrices=False, driver="gesvdj" if Rf.is_cuda else None)
+            Ufull = Qf @ Ur
+        else:
+            Ufull, s, Vh = torch.linalg.svd(X, full_matrices=False, driver="gesvd" if X.is_cuda else None)
     U = Ufull[:, :r]
     V = Vh[:r].t()
-    idx = torch.argmax(U.abs(), dim=0)
-    piv = U[idx, torch.arange(r, device=U.device)]
+    ar = torch.arange(r, device=U.device)
+    if sharded:
+        # first largest |U| entry per column over all shards (ties -> lowest global row)
+        mx, idx = U.abs().max(dim=0)
+        st = torch.stack([torch.zeros_like(mx), mx, (idx + shard.row0).to(torch.float64)], dim=1)
+        st = _reduce_pair_stats(st, shard)
+        local = st[:, 2].round().long() - shard.row0
+        own = (local >= 0) & (local < A.n)
+        vals = U[local.clamp(0, max(A.n - 1, 0)), ar]
+        piv = shard.allreduce(torch.where(own, vals, torch.zeros_like(vals)).contiguous())
+    else:
+        idx = torch.argmax(U.abs(), dim=0)
+        piv = U[idx, ar]
     sgn = torch.where(piv < 0, -1.0, 1.0).to(torch.float64)
     U = U * sgn[None, :]
     V = V * sgn[None, :]
-    Ut = alloc_tall(rows, r, torch.float64, "col", device=A.buf.device)
+    Ut = alloc_tall(A.n, r, torch.float64, "col", device=A.buf.device)
     Ut.view().copy_(U)
-    res = SvdResult(None, s[:r].cpu().numpy().copy(), V.cpu().numpy(), U_device=Ut)
+    res = SvdResult(None, s[:r].cpu().numpy().copy(), V.cpu().numpy(), U_device=Ut, shard=shard)
     if not keep_device:
         _ = res.U
     return res
@@ -631,9 +765,43 @@ def _check_eig(A, w, V):
     return w, V
 
 
+def lstsq_minnorm(A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+    """Minimum-norm least-squares solution of A X = B with numpy's default
+    cut (np.linalg.lstsq(rcond=None) -> LAPACK gelsd: singular values at or
+    below eps * max(M, N) * s_max are treated as zero), as linalg.py:136-141.
+    CUDA `gels` is a plain QR that assumes full rank, so the solve goes
+    through the SVD of A on the device instead."""
+    if A.shape[0] == 0 or A.shape[1] == 0:
+        return torch.zeros((A.shape[1],) + tuple(B.shape[1:]), dtype=torch.result_type(A, B), device=A.device)
+    M, N = int(A.shape[0]), int(A.shape[1])
+    rcond = torch.finfo(torch.float64).eps * max(M, N)
+    if M >= N:
+        # fast path: when R of A = QR is provably well inside the cut
+        # (||R||_F ||R^-1||_F >= cond_2(A)), A has full column rank numerically,
+        # the least-squares solution is unique and equals the min-norm one
+        Qa, Ra = torch.linalg.qr(A, mode="reduced")
+        eye = torch.eye(N, dtype=Ra.dtype, device=Ra.device)
+        Ri = torch.linalg.solve_triangular(Ra, eye, upper=True)
+        bound = float((torch.linalg.matrix_norm(Ra) * torch.linalg.matrix_norm(Ri)).item())
+        if bound * rcond < 1e-3:
+            return Ri @ (Qa.mH @ B.to(Qa.dtype))
+    U, s, Vh = torch.linalg.svd(A, full_matrices=False, driver="gesvdj" if A.is_cuda else None)
+    keep = s > rcond * s[0]
+    inv = torch.where(keep, 1.0 / torch.where(keep, s, torch.ones_like(s)), torch.zeros_like(s))
+    UhB = U.mH @ B.to(U.dtype)
+    if UhB.dim() == 1:
+        return Vh.mH @ (inv.to(U.dtype) * UhB)
+    return Vh.mH @ (inv.to(U.dtype)[:, None] * UhB)
+
+
 def lstsq(A, B):
-    """Least-squares solve (linalg.py:136-141) on the device."""
+    """Minimum-norm least-squares solve (linalg.py:136-141) on the device."""
     dev = dv.default_device()
     At = torch.as_tensor(np.asarray(A), device=dev)
     Bt = torch.as_tensor(np.asarray(B), device=dev)
-    return torch.linalg.lstsq(At, Bt).solution.cpu().numpy()
+    if At.is_complex() or Bt.is_complex():
+        ct = torch.complex128
+        At, Bt = At.to(ct), Bt.to(ct)
+    else:
+        At, Bt = At.to(torch.float64), Bt.to(torch.float64)
+    return lstsq_minnorm(At, Bt).cpu().numpy()

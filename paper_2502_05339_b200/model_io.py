@@ -238,12 +238,36 @@ def _phi_block(model, a0: int, a1: int) -> torch.Tensor:
     return torch.complex(fr[:b], fr[b:])
 
 
+def _gathered_phi_blocks(model, shard):
+    """Row-sharded model: each block of phi columns is formed on every rank
+    from its table rows and gathered in rank (= row) order; yields the full
+    (b x n) blocks on every rank (rank 0 writes them)."""
+    n_max = max(shard.all_gather(torch.tensor([model.modes.n_local], device=model.modes.table.buf.device)))
+    n_max = int(n_max.item())
+    for a0 in range(0, model.r, BLOCK_MODES):
+        blk = _phi_block(model, a0, min(model.r, a0 + BLOCK_MODES))                    # b x n_loc
+        pad = torch.zeros((blk.shape[0], n_max), dtype=blk.dtype, device=blk.device)
+        pad[:, : blk.shape[1]] = blk
+        parts = shard.all_gather(torch.view_as_real(pad))
+        sizes = shard.all_gather(torch.tensor([blk.shape[1]], device=blk.device))
+        yield torch.cat([torch.view_as_complex(p)[:, : int(k.item())] for p, k in zip(parts, sizes)], dim=1)
+
+
 def save_model(path, model):
     """Write ``model`` in the reference's model-file format
-    (model_io.py:154-181), phi streamed from the device table."""
+    (model_io.py:154-181), phi streamed from the device table. A row-sharded
+    model is written by rank 0 with every rank's rows gathered block by block
+    (a collective: every rank of the shard group calls it)."""
     m = model.modes
-    if m.shard is not None and m.shard.world > 1:
-        raise NotImplementedError("save_model of a row-sharded model: gather the shards first")
+    shard = m.shard if (m.shard is not None and m.shard.world > 1) else None
+    if shard is not None:
+        import torch.distributed as dist
+        rank = dist.get_rank(shard.group)
+        if rank != 0:
+            for _ in _gathered_phi_blocks(model, shard):
+                pass
+            dist.barrier(group=shard.group)
+            return
     n, r = model.n, model.r
     grid_block = kv_dumps(grid_to_kv(model.grid_meta)).encode("utf-8")
     prov_block = kv_dumps({str(k): format_value(v) for k, v in sorted(model.provenance.items())}).encode("utf-8")
@@ -254,11 +278,17 @@ def save_model(path, model):
         w.write(_u32(len(grid_block)) + grid_block)
         w.write(np.ascontiguousarray(model.sigma, dtype=_F64).tobytes())
         w.write(np.ascontiguousarray(model.lam, dtype=_C128).tobytes())
-        blocks = (_phi_block(model, a0, min(r, a0 + BLOCK_MODES)) for a0 in range(0, r, BLOCK_MODES))
+        if shard is None:
+            blocks = (_phi_block(model, a0, min(r, a0 + BLOCK_MODES)) for a0 in range(0, r, BLOCK_MODES))
+        else:
+            blocks = _gathered_phi_blocks(model, shard)
         w.crc = _stream_out(fh, w.crc, blocks, BLOCK_MODES, n, torch.complex128)   # (b, n) c128 = phi columns
         w.write(_u32(len(prov_block)) + prov_block)
         fh.write(_u32(w.crc))
     os.replace(tmp, path)
+    if shard is not None:
+        import torch.distributed as dist
+        dist.barrier(group=shard.group)
 
 
 def _read_exact(fh, count, what, offset, total):

@@ -112,6 +112,16 @@ class TableLayout:
         return c
 
 
+def _pinv_svd(M: torch.Tensor, rel_tol: float) -> torch.Tensor:
+    """SVD pseudo-inverse of a small device matrix (linalg.py:93-104)."""
+    U, s, Vh = torch.linalg.svd(M, full_matrices=False)
+    if s.numel() == 0 or float(s[0]) == 0.0:
+        return torch.zeros((M.shape[1], M.shape[0]), dtype=M.dtype, device=M.device)
+    keep = s > rel_tol * s[0]
+    inv = torch.where(keep, 1.0 / torch.where(keep, s, torch.ones_like(s)), torch.zeros_like(s))
+    return (Vh.mH * inv.to(Vh.dtype)) @ U.mH
+
+
 class DeviceModes:
     """Decode table in HBM (+ optional general basis) and its cached Gram.
 
@@ -130,6 +140,8 @@ class DeviceModes:
         self.general = general
         self.mix = None if mix is None else np.asarray(mix, dtype=np.float64)
         self._pinv_small = None
+        self._pinv_cond2 = np.inf
+        self._pinv_rows = None
         self._tc_planes = None     # fp16 hi/lo planes of the table for batched decodes
         # Gram of the raw table (D^T D, all raw columns): shared by every model
         # derived from the same table (editing.apply_edit folds into the mix)
@@ -158,27 +170,66 @@ class DeviceModes:
 
     def pinv_small(self) -> np.ndarray:
         """P such that pinv(phi) = P @ E^H @ D^T (r x r complex), from the
-        Hermitian Gram phi^H phi = E^H (D^T D) E (eigh on the device)."""
+        Hermitian Gram phi^H phi = E^H (D^T D) E (eigh on the device). Only
+        valid for a well-conditioned phi; `pinv_rows` is the general form."""
         if self._pinv_small is None:
             D, E = self.basis()
-            if self.general is None and self.raw_gram is not None:
-                G = self.raw_gram
-            else:
-                G = allreduce(self.shard, dv.get_ops().tall_gram(D, D, symmetric=True))
-                if self.general is None:
-                    self.raw_gram = G
+            G = self._gram(D)
             Et = torch.as_tensor(E, device=G.device)
             H = Et.mH @ G.to(torch.complex128) @ Et
             H = 0.5 * (H + H.mH)
             mu, V = torch.linalg.eigh(H)
             mu_max = float(mu.max().item()) if mu.numel() else 0.0
-            # sigma_i = sqrt(mu_i) > 1e-12 sigma_max (linalg.py:101) is resolvable
-            # through the Gram only down to sigma ratios ~1e-7.
             keep = mu > max(1e-14 * mu_max, 0.0)
             inv = torch.where(keep, 1.0 / torch.where(keep, mu, torch.ones_like(mu)), torch.zeros_like(mu))
             P = (V * inv.to(V.dtype)) @ V.mH
             self._pinv_small = P.cpu().numpy()
+            self._pinv_cond2 = (mu_max / float(mu.min().item())) if mu.numel() and float(mu.min()) > 0 else np.inf
         return self._pinv_small
+
+    def _gram(self, D: Tall) -> torch.Tensor:
+        if self.general is None and self.raw_gram is not None:
+            return self.raw_gram
+        G = allreduce(self.shard, dv.get_ops().tall_gram(D, D, symmetric=True))
+        if self.general is None:
+            self.raw_gram = G
+        return G
+
+    def pinv_rows(self) -> np.ndarray:
+        """M (r x ncol complex) with pinv(phi) = M @ D^T — the reference's SVD
+        pseudo-inverse (linalg.py:93-104: sigma > 1e-12 sigma_max kept).
+
+        Well-conditioned phi (cond <= 1e6): M = (phi^H phi)^-1 E^H from the
+        Gram (eigh), exact to O(u cond^2). Otherwise the Gram cannot resolve
+        the reference's cut (it sees sigma ratios only down to ~1e-7): the
+        table is orthonormalised on the device (CholeskyQR2 with its shifted /
+        Householder / TSQR fallbacks, D = Q R), and M = pinv(R E) R^-T with
+        the reference's SVD cut on the small R E, plus a RuntimeWarning."""
+        if getattr(self, "_pinv_rows", None) is not None:
+            return self._pinv_rows
+        D, E = self.basis()
+        P = self.pinv_small()
+        if self._pinv_cond2 <= 1e12:
+            self._pinv_rows = P @ E.conj().T
+            return self._pinv_rows
+        import warnings
+
+        from . import linalg as la
+        warnings.warn(f"ill-conditioned mode basis (cond(phi) ~ {np.sqrt(self._pinv_cond2):.1e}): "
+                      "pseudo-inverse through a QR of the table", RuntimeWarning, stacklevel=3)
+        ncol = E.shape[0]
+        dev = D.buf.device
+        Y = dv.alloc_tall(D.n, ncol, torch.float64, "row", device=dev)
+        Y.view().copy_(D.view()[:, :ncol])
+        # Householder QR of the table (TSQR across row shards): D = Q R, R may be
+        # singular (a real mode's zero imaginary column)
+        R = la._householder_inplace(Y, self.shard if (self.shard is not None and self.shard.world > 1) else None,
+                                    None)
+        del Y
+        # phi = Q (R E): pinv(phi) = pinv(R E) Q^T, and on range(D) Q^T = (R^+)^T D^T
+        RE = R.to(torch.complex128) @ torch.as_tensor(E, device=dev)
+        self._pinv_rows = (_pinv_svd(RE, 1e-12) @ _pinv_svd(R, 1e-12).t().to(torch.complex128)).cpu().numpy()
+        return self._pinv_rows
 
     def project(self, U: torch.Tensor) -> np.ndarray:
         """pinv(phi) @ U for U (nv x n_local) device rows -> (r x nv) complex host."""
@@ -188,7 +239,7 @@ class DeviceModes:
         for v0 in range(0, U.shape[0], 8):
             ys.append(ops.colmajor_dot(D, U[v0:v0 + 8]))
         y = allreduce(self.shard, torch.cat(ys, dim=1)).cpu().numpy()   # ncol x nv
-        return self.pinv_small() @ (E.conj().T @ y)
+        return self.pinv_rows() @ y
 
     # -- decode ------------------------------------------------------------
     def decode_coeff(self, C: torch.Tensor, out: Optional[torch.Tensor] = None, general=False,

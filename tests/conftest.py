@@ -50,3 +50,18 @@ def phase_aligned_error(phi, ref):
         e = np.linalg.norm(phi[:, k] * ph - ref[:, k]) / max(np.linalg.norm(ref[:, k]), 1e-300)
         worst = max(worst, e)
     return worst
+
+
+def aligned_coeff_error(phi, ref_phi, z, zref):
+    """Reduced coordinates compared with the per-mode phase that aligns phi
+    to ref_phi (phi_k e^{i t} pairs with z_k e^{-i t}): max |z_k / p_k - zref_k|
+    over max |zref|, p_k the unit phase rotating phi_k onto ref_phi_k."""
+    phi = np.asarray(phi); ref_phi = np.asarray(ref_phi)
+    z = np.asarray(z); zref = np.asarray(zref)
+    h = ref_phi.shape[0]
+    out = np.empty_like(zref)
+    for k in range(zref.size):
+        ip = np.vdot(phi[:h, k], ref_phi[:, k])
+        ph = ip / abs(ip) if abs(ip) > 0 else 1.0
+        out[k] = z[k] / ph
+    return float(np.abs(out - zref).max() / max(np.abs(zref).max(), 1e-300))

@@ -104,3 +104,83 @@ def test_two_rank_gloo_matches_single(data, world):
     np.testing.assert_allclose(got["res"], model.provenance["residual_rel"], rtol=1e-9)
     np.testing.assert_allclose(got["z0"], z0, rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(got["frame"], frame, rtol=1e-9, atol=1e-11)
+
+
+# ---------------------------------------------------------------- round 2: TSQR, DMDc, sharded writer
+def _cpu_device(monkey=True):
+    from paper_2502_05339_b200 import device as dv
+    dv.default_device = lambda: torch.device("cpu")
+
+
+def _fit_more(X, shard, out_dir=None):
+    import warnings
+    import paper_2502_05339_b200 as fd
+    from paper_2502_05339_b200 import device as dv
+    from cpu_ops import CpuOps
+    prev = dv.set_ops(CpuOps())
+    try:
+        out = {}
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            data = fd.SnapshotMatrix(torch.as_tensor(X), 0.1, shard=shard, device=torch.device("cpu"))
+            full = fd.exact_dmd(data, 8, svd_mode="full")                 # TSQR across shards
+            out["full_lam"], out["full_sigma"] = full.lam, full.sigma
+            u = np.random.default_rng(5).standard_normal((2, X.shape[1] - 1))
+            mc, ctrl = fd.dmdc_fit(data, u, 10, 8, seed=3)                # control rows on the last rank
+            out["dmdc_lam"], out["dmdc_B"] = mc.lam, ctrl.reduced_b[0]
+            ex = fd.exact_dmd(data, 8, svd_mode="randomized", seed=5, oversample=10, power_iters=1)
+            out["ex_lam"] = ex.lam
+            if out_dir is not None:
+                fd.model_io.save_model(os.path.join(out_dir, "m.kdmd"), ex)
+        return out
+    finally:
+        dv.set_ops(prev)
+
+
+def _worker_more(rank, world, X, out_dir, port):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    _cpu_device()
+    from paper_2502_05339_b200.shards import row_bounds, row_shard
+    b = row_bounds(X.shape[0], world)
+    out = _fit_more(np.ascontiguousarray(X[b[rank]:b[rank + 1]]), row_shard(X.shape[0]), out_dir)
+    if rank == 0:
+        np.savez(os.path.join(out_dir, "r.npz"), **out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_tsqr_dmdc_and_sharded_writer(data, monkeypatch):
+    """svd_mode='full' (Householder TSQR over the shards), the augmented DMDc
+    fit with its control rows on the last rank, and the sharded model writer,
+    against the single-rank results on the same rows."""
+    import socket
+    from paper_2502_05339_b200 import device as dv
+    monkeypatch.setattr(dv, "default_device", lambda: torch.device("cpu"))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker_more, args=(2, data, d, port), nprocs=2, join=True)
+        got = dict(np.load(os.path.join(d, "r.npz")))
+        with tempfile.TemporaryDirectory() as d1:
+            ref = _fit_more(data, None, d1)
+            a = open(os.path.join(d, "m.kdmd"), "rb").read()
+            b = open(os.path.join(d1, "m.kdmd"), "rb").read()
+    assert match_eigs(got["full_lam"], ref["full_lam"]) <= 1e-10
+    np.testing.assert_allclose(got["full_sigma"], ref["full_sigma"], rtol=1e-12)
+    assert match_eigs(got["dmdc_lam"], ref["dmdc_lam"]) <= 1e-10
+    np.testing.assert_allclose(got["dmdc_B"], ref["dmdc_B"], rtol=1e-6, atol=1e-8 * np.abs(ref["dmdc_B"]).max())
+    assert match_eigs(got["ex_lam"], ref["ex_lam"]) <= 1e-11
+    # same header and layout; phi (column-major c128 after sigma / lambda) equal to round-off
+    n, r = data.shape[0], 8
+    glen = int(np.frombuffer(a[32:36], dtype="<u4")[0])
+    off = 36 + glen + 8 * r + 16 * r
+    assert a[:36 + glen] == b[:36 + glen]
+    pa = np.frombuffer(a[off:off + 16 * n * r], dtype="<c16")
+    pb = np.frombuffer(b[off:off + 16 * n * r], dtype="<c16")
+    assert np.abs(pa - pb).max() <= 1e-9 * np.abs(pb).max()

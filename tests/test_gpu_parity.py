@@ -8,7 +8,7 @@ import warnings
 import numpy as np
 import pytest
 
-from conftest import checksum, match_eigs, phase_aligned_error
+from conftest import aligned_coeff_error, checksum, match_eigs, phase_aligned_error
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -174,6 +174,7 @@ def test_config0_full(fd, config_golden):
     assert match_eigs(model.lam, g["c0_lam"]) <= LAM_TOL
     assert phase_aligned_error(model.phi, g["c0_phi"]) <= 1e-4
     z0 = fd.encode(model, X[:, 0])
+    assert aligned_coeff_error(model.phi, g["c0_phi"], z0.z, g["c0_z0"]) <= 1e-5
     Z = np.stack([fd.step_k(model, z0, k).z for k in range(101)], axis=1)
     frames = fd.decode_batch(model, Z).double().cpu().numpy().T
     sel = frames[:, [0, 1, 50, 100]]
@@ -194,7 +195,10 @@ def test_config1_reduced_grid(fd, config_golden):
     assert np.abs(model.sigma - g["c1s_sigma"]).max() <= SIG_TOL * g["c1s_sigma"].min()
     assert match_eigs(model.lam, g["c1s_lam"]) <= LAM_TOL
     np.testing.assert_allclose(np.linalg.norm(model.phi, axis=0), 1.0, atol=1e-6)
+    # modes up to phase (BASELINE tolerance), on the reference's first 512 rows
+    assert phase_aligned_error(model.phi[:512], g["c1s_phi_head"]) <= 1e-5
     z0 = fd.encode(model, X[:, 0])
+    assert aligned_coeff_error(model.phi[:512], g["c1s_phi_head"], z0.z, g["c1s_z0"]) <= 1e-5
     fr = np.stack([fd.decode(model, fd.step_k(model, z0, k)) for k in (1, 100, 200)], axis=1)
     for j in range(3):
         assert rel(fr[:4096, j], g["c1s_frames_head"][:, j]) <= FRAME_TOL
@@ -218,6 +222,8 @@ def test_config3_reduced_grid_exact_and_opt(fd, config_golden):
         mo = fd.optdmd(data, 200, lm_config=fd.LMConfig(max_iters=10), svd_mode="randomized", seed=3,
                        oversample=10, power_iters=1)
     assert match_eigs(mo.lam, g["c3s_opt_lam"]) <= LAM_TOL
+    # the benched fit's modes (tcgen05 lift / modes path for fp32 tables), up to phase
+    assert phase_aligned_error(mo.phi[:512], g["c3s_opt_phi_head"]) <= 1e-5
     # r = T: the varpro objective starts at round-off level in both implementations
     assert mo.provenance["objective_history"][0] <= 1e-12 * g["c3s_opt_sigma"][0]
     assert g["c3s_opt_hist"][0] <= 1e-12 * g["c3s_opt_sigma"][0]
@@ -292,3 +298,49 @@ def test_optdmd_tcgen05_lift_and_modes_match_dmma(fd):
     fa = fd.decode(a, fd.step_k(a, z0, 50))
     fb = fd.decode(b, fd.step_k(b, z0, 50))
     assert rel(fa, fb) <= 1e-5
+
+
+# ---------------------------------------------------------------- frames of the benched fit vs the reference
+@pytest.fixture(scope="module")
+def frames_golden():
+    import os
+    from conftest import GOLDEN
+    return dict(np.load(os.path.join(GOLDEN, "config_frames.npz")))
+
+
+@pytest.mark.parametrize("tc_fit", [True, False], ids=["tcgen05_lift_modes", "dmma_lift_modes"])
+@pytest.mark.parametrize("method", ["opt", "exact"])
+def test_config3_shape_frames_match_reference(fd, frames_golden, method, tc_fit):
+    """What a user of the benched fit sees — z0 = encode(x0), decode(step_k)
+    and a continuous-time frame — against frames the reference decoded from
+    its own model (oracle/gen_golden.py frame_cases), with the tcgen05 lift /
+    modes path (fp32 tables, the bench) and the FP64 DMMA path."""
+    from paper_2502_05339_b200 import dmd, synth
+    g = frames_golden
+    p = synth.config_params(3, seed=3, grid=16)
+    X = synth.generate_host(p)
+    np.testing.assert_allclose(checksum(X), g["c3s_checksum"], rtol=1e-10)
+    old = dmd._TC_FIT
+    dmd._TC_FIT = tc_fit
+    try:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            data = fd.SnapshotMatrix(X, synth.DT)
+            kw = dict(svd_mode="randomized", seed=3, oversample=10, power_iters=1)
+            if method == "opt":
+                model = fd.optdmd(data, 200, lm_config=fd.LMConfig(max_iters=10), **kw)
+            else:
+                model = fd.exact_dmd(data, 200, **kw)
+            z0 = fd.encode(model, X[:, 0])
+            fr = np.stack([fd.decode(model, fd.step_k(model, z0, k)) for k in (1, 50, 199)]
+                          + [fd.decode(model, fd.eval_continuous(model, z0, 12.37))], axis=1)
+    finally:
+        dmd._TC_FIT = old
+    assert match_eigs(model.lam, g[f"c3s_{method}_lam"]) <= LAM_TOL
+    np.testing.assert_allclose(np.linalg.norm(model.phi, axis=0), g[f"c3s_{method}_phi_norms"], atol=1e-6)
+    head = g[f"c3s_{method}_frames_head"]
+    for j in range(fr.shape[1]):
+        assert rel(fr[:4096, j], head[:, j]) <= FRAME_TOL, j
+    np.testing.assert_allclose(fr.sum(0), g[f"c3s_{method}_frames_checksum"][0], rtol=FRAME_TOL,
+                               atol=FRAME_TOL * np.abs(fr).sum(0).max())
+    np.testing.assert_allclose((fr * fr).sum(0), g[f"c3s_{method}_frames_checksum"][1], rtol=2 * FRAME_TOL)
