@@ -37,6 +37,8 @@ CONFIGS = {
     "c3": dict(cfg=3, grid=256, r=200, p=10, q=1, lm_iters=10, times=1024, seed=3),
     "c1": dict(cfg=1, grid=128, r=150, p=10, q=1, lm_iters=10, times=1024, seed=1),
     "c3s": dict(cfg=3, grid=64, r=200, p=10, q=1, lm_iters=10, times=1024, seed=3),
+    # config 2 (DMDc): augmented fit r_aug = 158 + 200 controlled frames (a side line, not the headline)
+    "c2": dict(cfg=2, grid=128, r=150, r_aug=158, p=10, q=1, ell=8, steps=200, seed=2),
 }
 
 
@@ -54,22 +56,31 @@ def fit_flops(n, m, r, p, q, modes="optdmd"):
     return sum(terms.values()), terms, l
 
 
-def executed_flops(n, m, r, p, q):
+def executed_terms(n, m, r, p, q):
     """Flops libfdmd actually executes for the same fit (OptDMD, resident
-    snapshots): with power iterations the sketch Y = X Omega, its Gram and
-    every Z = X^T Q follow from one symmetric Gram X^T X (n T^2); the power-iteration
-    CholeskyQR is one SYRK with R1^-1 folded into Z; CholeskyQR2's final
-    R2^-1 is folded into small matrices; triangular applies count n*l^2; the
-    lift (2nlr) and the modes (one column per conjugate pair, ~2nr^2) run on
-    tcgen05 for fp32 tables."""
+    snapshots), split by arithmetic. Snapshot-Gram route
+    (q >= 1): the sketch, every power pass Z = X^T Q and the first CholeskyQR
+    pass of each orthonormalisation follow from one symmetric Gram X^T X
+    (n T^2); the only tall GEMM is the final Q1 = X (W R1^-1) (2nTl);
+    CholeskyQR2's second pass is one SYRK (n l^2) whose R2^-1 is folded into
+    small matrices; the projection Q^T S (2nml). Those run in FP64 (DMMA).
+    The lift U = Q Ub (2nlr) and the modes (one column per conjugate pair,
+    ~2nr^2) run on tcgen05 with an FP16 2-way split, FP32-accurate, into the
+    fp32 tables."""
     T = m - 1
     l = min(r + p, T)
     if q == 0:   # explicit sketch: Y = X Omega, CholeskyQR2 (SYRK + TRSM + SYRK)
-        return 2.0 * n * T * l + 3.0 * n * l * l + 2.0 * n * m * l + 2.0 * n * l * r + 2.0 * n * r * r
-    # X^T X once (the sketch and every X^T Q follow from it), q Y = XW GEMMs,
-    # one SYRK per non-final power stage, SYRK + TRSM + SYRK at the end
-    return (2.0 * n * T * l * q + n * T * T + n * l * l * (q + 2)
-            + 2.0 * n * m * l + 2.0 * n * l * r + 2.0 * n * r * r)
+        fp64 = {"sketch 2nTl": 2.0 * n * T * l, "CholQR2 3nl^2": 3.0 * n * l * l, "projection 2nml": 2.0 * n * m * l}
+    else:
+        fp64 = {"snapshot Gram nT^2": 1.0 * n * T * T, "Q1 = X W R1^-1 2nTl": 2.0 * n * T * l,
+                "CholQR2 second pass nl^2": 1.0 * n * l * l, "projection 2nml": 2.0 * n * m * l}
+    tc = {"lift U 2nlr": 2.0 * n * l * r, "modes 2nr^2": 2.0 * n * r * r}
+    return fp64, tc
+
+
+def executed_flops(n, m, r, p, q):
+    fp64, tc = executed_terms(n, m, r, p, q)
+    return sum(fp64.values()) + sum(tc.values())
 
 
 # ---------------------------------------------------------------------------
@@ -128,21 +139,90 @@ def _dist_init():
     return world, rank, local
 
 
+def _relaunch_distributed(args):
+    """`bench.py --gpus N` outside torchrun: one process per GPU through
+    torch.distributed.run (127.0.0.1 rendezvous), after checking that N GPUs
+    are visible — never silently run fewer ranks than asked."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+class CpuArm:
+    """The reference's own CPU implementation of the path, timed on the host.
+
+    Preferred: the UNMODIFIED reference package `flowdmd` installed offline
+    into baseline/_ref (pip --target) — `optdmd` from
+    flowdmd/dmd.py:366-436 with its init exact_dmd (pinv + residual) — with
+    only `_svd_of` (dmd.py:216-222) patched to honour the config's (p, q), as
+    SURVEY §8(d) prescribes. Fallback when baseline/_ref is absent: the oracle
+    port oracle/flowdmd_oracle.py (kind "port")."""
+
+    def __init__(self):
+        ref = os.path.join(ROOT, "baseline", "_ref")
+        self.kind = "port"
+        if os.path.isdir(os.path.join(ref, "flowdmd")):
+            sys.path.insert(0, ref)
+            try:
+                import flowdmd.dmd as rdmd
+                import flowdmd.linalg as rlin
+                self.rdmd, self.rlin, self.kind = rdmd, rlin, "reference"
+            except Exception:
+                self.kind = "port"
+        if self.kind == "port":
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import flowdmd_oracle as orc
+            self.orc = orc
+
+    def describe(self):
+        return ("flowdmd (reference package, unmodified, baseline/_ref) optdmd" if self.kind == "reference"
+                else "oracle port (oracle/flowdmd_oracle.py) optdmd")
+
+    def fit(self, X, cfg):
+        if self.kind == "port":
+            return self.orc.optdmd(X, cfg["r"], max_iters=cfg["lm_iters"], svd_mode="randomized", seed=cfg["seed"],
+                                   p=cfg["p"], q=cfg["q"])
+        rdmd, rlin = self.rdmd, self.rlin
+        orig = rdmd._svd_of
+
+        def svd_of(Xm, r, svd_mode, seed):      # dmd.py:216-222 with the config's (p, q)
+            T = min(Xm.shape)
+            return rlin.randomized_svd(Xm, r, oversample=min(cfg["p"], T - r), power_iters=cfg["q"], seed=seed)
+
+        rdmd._svd_of = svd_of
+        try:
+            import warnings
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                return rdmd.optdmd(rdmd.SnapshotMatrix(X, 0.1), cfg["r"],
+                                   lm_config=rdmd.LMConfig(max_iters=cfg["lm_iters"]),
+                                   svd_mode="randomized", seed=cfg["seed"])
+        finally:
+            rdmd._svd_of = orig
+
+
 def run_reference(args, cfg):
-    """--impl reference: the reference algorithm's CPU implementation (the
-    oracle port, oracle/flowdmd_oracle.py — the reference is pure Python and
-    not importable on the GPU box) on a bounded row sample of the workload."""
+    """--impl reference: the reference's CPU implementation (CpuArm) on a
+    bounded row sample of the workload, all host cores."""
     world, rank, _ = _dist_init()
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import flowdmd_oracle as orc
     from paper_2502_05339_b200 import synth
-    res = cpu_sample(orc, synth, cfg, args.cpu_rows)
+    arm = CpuArm()
+    res = cpu_sample(arm, synth, cfg, args.cpu_rows)
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        cpu_fit(orc, res["X"], cfg)
+        arm.fit(res["X"], cfg)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
@@ -155,7 +235,7 @@ def run_reference(args, cfg):
         "impl": "reference",
         "config": dict(arm_config(cfg, res["n"], res["m"], cfg["r"], res["l"], f"cpu{os.cpu_count()}threads"),
                        sample_rows=res["rows"]),
-        "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
+        "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": arm.kind,
                          "sample": res["sample"]},
         "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -169,22 +249,103 @@ def arm_config(cfg, n, m, r, l, parallelism):
             "snapshot_dtype": "f32", "parallelism": parallelism, "l2": "inputs larger than L2 (X >= 3.8 GB)"}
 
 
-def cpu_sample(orc, synth, cfg, rows):
+def cpu_sample(arm, synth, cfg, rows):
     p = synth.config_params(cfg["cfg"], seed=cfg["seed"], grid=cfg["grid"])
     n_full = p.n
     rows = min(rows, p.n)
     X = synth.generate_host(p, 0, rows).astype(np.float64)
     flops, _, _ = fit_flops(rows, p.m, cfg["r"], cfg["p"], cfg["q"])
-    sample = (f"config{cfg['cfg']} rows [0,{rows}) x {p.m} snapshots; oracle optdmd r={cfg['r']} "
-              f"p={cfg['p']} q={cfg['q']} {cfg['lm_iters']} LM iters, numpy/OpenBLAS fp64; "
-              f"GFLOP/s from the SURVEY §8d formula at n={rows}")
+    sample = (f"config{cfg['cfg']} rows [0,{rows}) x {p.m} snapshots (same generator, first {rows} rows of the "
+              f"{n_full}-row matrix); {arm.describe()} r={cfg['r']} p={cfg['p']} q={cfg['q']} "
+              f"{cfg['lm_iters']} LM iters, numpy/OpenBLAS fp64, all host threads; GFLOP/s from the SURVEY "
+              f"§8d formula at n={rows} (every n-dependent cost of the reference is linear in n)")
     _, _, l = fit_flops(n_full, p.m, cfg["r"], cfg["p"], cfg["q"])
     return {"X": X, "rows": rows, "flops": flops, "sample": sample, "n": n_full, "m": p.m, "l": l}
 
 
-def cpu_fit(orc, X, cfg):
-    return orc.optdmd(X, cfg["r"], max_iters=cfg["lm_iters"], svd_mode="randomized", seed=cfg["seed"],
-                      p=cfg["p"], q=cfg["q"])
+def dmdc_flops(n, m, r_aug, r, p, q, ell):
+    """Config-2 fit work (SURVEY §8(d) formula for C2 plus the output-basis
+    sketch that §8(c) leaves to the builder): the augmented sketch of
+    [X; Upsilon] at l1 = r_aug + p, the rank-r sketch of X' at l2 = r + p,
+    the cross product Q1^T Q2 and the modes X' V S^-1 (4nTr)."""
+    T = m - 1
+    l1, l2 = min(r_aug + p, T), min(r + p, T)
+    na = n + ell
+    terms = {"aug sketch+power 2nTl1(1+2q)": 2.0 * na * T * l1 * (1 + 2 * q),
+             "aug CholQR2 4nl1^2(1+q)": 4.0 * na * l1 * l1 * (1 + q),
+             "aug projection 2nml1": 2.0 * na * m * l1,
+             "X' sketch+power 2nTl2(1+2q)": 2.0 * n * T * l2 * (1 + 2 * q),
+             "X' CholQR2 4nl2^2(1+q)": 4.0 * n * l2 * l2 * (1 + q),
+             "X' projection 2nml2": 2.0 * n * m * l2,
+             "cross Q1^T Q2 2nl1l2": 2.0 * n * l1 * l2,
+             "modes 4nTr": 4.0 * n * T * r}
+    return sum(terms.values()), terms
+
+
+def run_c2(args, cfg):
+    """Config 2: the augmented DMDc fit of a 128^3 x 3 controlled system
+    (synth.config2_params) from HBM-resident snapshots, then 200 controlled
+    steps driven by a fresh seeded control sequence (rollout(q_seq=...)),
+    all frames decoded on the device. One JSON line (a side workload)."""
+    import warnings
+
+    import torch
+
+    import paper_2502_05339_b200 as fd
+    from paper_2502_05339_b200 import device as dv
+    from paper_2502_05339_b200 import synth
+    torch.cuda.set_device(0)
+    p = synth.config2_params(cfg["seed"], grid=cfg["grid"], ell=cfg["ell"])
+    n, m = p.n, p.m
+
+    def states(u):
+        S = dv.alloc_tall(n, u.shape[1] + 1, torch.float32, "row")
+        S.buf[:, u.shape[1] + 1:].zero_()
+        tabs = [torch.as_tensor(np.ascontiguousarray(t), device="cuda") for t in p.sep_tables(u)]
+        dv.get_ops().synth3d(tabs, u.shape[1] + 1, 0.0, 0, 0, n, S)
+        return S
+
+    u = p.controls(5)
+    S = states(u)
+    u2 = p.controls(77, cfg["steps"])
+    truth = states(u2)
+    x0 = truth.buf[:n, 0].clone()
+    q_seq = [[u2[:, k]] for k in range(cfg["steps"])]
+    F, terms = dmdc_flops(n, m, cfg["r_aug"], cfg["r"], cfg["p"], cfg["q"], cfg["ell"])
+
+    def one():
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            model, ctrl = fd.dmdc_fit(fd.SnapshotMatrix(S, 1.0), u, cfg["r_aug"], cfg["r"], seed=3,
+                                      oversample=cfg["p"], power_iters=cfg["q"])
+            e[1].record()
+            z0 = fd.encode(model, x0)
+            frames, _ = fd.rollout(model, z0, cfg["steps"], ctrl=ctrl, q_seq=q_seq, to_host=False)
+        e[2].record()
+        torch.cuda.synchronize()
+        return e[0].elapsed_time(e[1]) / 1e3, e[1].elapsed_time(e[2]) / 1e3, frames
+
+    for _ in range(args.warmup):
+        one()
+    ts = [one() for _ in range(args.steps)]
+    fit_t = float(np.mean([t[0] for t in ts]))
+    roll_t = float(np.mean([t[1] for t in ts]))
+    frames = ts[-1][2]
+    tr = truth.buf[:n, 1:cfg["steps"] + 1].t().double()
+    err = float(((frames.double() - tr).norm(dim=1) / tr.norm(dim=1)).max())
+    line = {"metric": "config-2 DMDc fit GFLOP/s + controlled rollout frames/s", "value": round(F / fit_t / 1e9, 1),
+            "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round((fit_t + roll_t) * 1e3, 1), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2 DMDc fit ([X;Upsilon] r_aug=158, p=10, q=1; output basis r=150) + "
+                                   "200 controlled steps with fresh seeded controls", "n": n, "m": m, "ell": cfg["ell"],
+                       "grid": "128^3x3", "snapshot_dtype": "f32", "l2": "inputs larger than L2"},
+            "fit": {"s": round(fit_t, 4), "flops": F, "terms": terms},
+            "rollout": {"frames": cfg["steps"], "s": round(roll_t, 4), "frames_per_s": round(cfg["steps"] / roll_t, 1),
+                        "max_rel_err_vs_generator": err}}
+    print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
@@ -195,22 +356,28 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="fdmd", choices=["fdmd", "reference"])
-    ap.add_argument("--cpu-rows", type=int, default=98304)
+    ap.add_argument("--cpu-rows", type=int, default=65536)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.config == "c2":
+        return run_c2(args, cfg)
     if args.impl == "reference":
         return run_reference(args, cfg)
 
     import torch
     world, rank, local = _dist_init()
-    torch.cuda.set_device(local)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _relaunch_distributed(args)
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    from paper_2502_05339_b200 import shards
+    shards.init_process_group("nccl")          # NCCL_ALGO / NCCL_PROTO pinned (deterministic sums)
     group = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
 
     import paper_2502_05339_b200 as fd
@@ -251,7 +418,8 @@ def main():
     b4 = np.concatenate([p.b, np.conj(p.b)])[:r]
     W4 = (rng.standard_normal((r, r)) + 1j * rng.standard_normal((r, r))) / np.sqrt(2 * r)
     times = rng.uniform(0.0, 300.0, cfg["times"])
-    peak = ctypes_peak(_lib)
+    peak_burst = ctypes_peak(_lib, 0.4)
+    peak = ctypes_peak(_lib, 8.0)                           # sustained: one ~2 s launch after ~2 s of ramp
     ops = dv.get_ops()
     F_fit, terms, l = fit_flops(n, m, r, cfg["p"], cfg["q"])
     lm = fd.LMConfig(max_iters=cfg["lm_iters"])
@@ -272,17 +440,15 @@ def main():
         mb = ModalBasis(U, W4, lam4, b4, dt=1.0)
         f1 = mb.reconstruct(times[:1])                       # interactive frame (GEMV, fp32 U)
         ev[2].record()
-        if chunk_used[0] is None:                            # fixed at the first (warm-up) step so
-            chunk_used[0] = frame_chunk(n_loc, len(times), keep=4.0 * n_loc * r)
-        chunk = chunk_used[0]
-        # frame buffer before the basis planes: it takes the fit's freed Q block,
-        # so every step allocates into the same blocks (no segment remapping)
-        outb = torch.empty((chunk, n_loc), dtype=torch.float32, device="cuda")
         with trace.stage("reconstruct.basis_split"):
             mb.tc_state()                                    # once per basis: fp16 hi/lo planes
         ev[3].record()
         mb.release_fp32()
         del U                                                # the planes carry the basis from here on
+        if chunk_used[0] is None:                            # fixed at the first (warm-up) step:
+            chunk_used[0] = frame_chunk(n_loc, len(times))   # S + planes resident, fp32 U released
+        chunk = chunk_used[0]
+        outb = torch.empty((chunk, n_loc), dtype=torch.float32, device="cuda")
         mb.reconstruct(times[:32], out=outb[:32])            # one 32-frame batch
         ev[4].record()
         for c0 in range(0, len(times), chunk):               # 1024 frames streamed through one buffer
@@ -351,14 +517,22 @@ def main():
     recon["B=1"]["kernel"] = "decode (SIMT GEMV over fp32 U)"
     recon["B=32"]["kernel"] = "tc_decode (tcgen05, FP16 2-way split)"
     b1024 = rec["rec1024"]
-    # algorithmic bytes: U read once per 128-frame launch + frames written
     CHUNK = chunk_used[0]
-    byt = (4.0 * n * r) * math.ceil(len(times) / CHUNK) + 4.0 * n * len(times)
-    recon["B=1024"] = {"frames_per_s": round(len(times) / b1024, 1), "ms": round(b1024 * 1e3, 2),
-                       "hbm_GBps_per_gpu": round(byt / b1024 / 1e9 / world, 1),
-                       "frac_hbm": round(byt / b1024 / 1e9 / world / hbm_peak(), 3),
-                       "kernel": f"tc_decode2 (tcgen05 cta_group::2 CTA pairs, 256 frames per pair tile), "
-                                 f"{CHUNK}-frame launches streamed through one buffer"}
+    B = len(times)
+    # SURVEY §8(d) algorithmic bytes: the basis read ONCE + frames written (+ coefficients)
+    alg = 4.0 * n * r + 4.0 * n * B + 8.0 * r * B
+    # what the streamed schedule must move: the basis once per launch + frames
+    sched = (4.0 * n * r) * math.ceil(B / CHUNK) + 4.0 * n * B
+    recon["B=1024"] = {"frames_per_s": round(B / b1024, 1), "ms": round(b1024 * 1e3, 2),
+                       "hbm_GBps_per_gpu": round(alg / b1024 / 1e9 / world, 1),
+                       "frac_hbm": round(alg / b1024 / 1e9 / world / hbm_peak(), 3),
+                       "frac_basis": "§8(d) bytes: basis read once + frames written",
+                       "schedule_GBps_per_gpu": round(sched / b1024 / 1e9 / world, 1),
+                       "schedule_bytes": sched,
+                       "frames_per_launch": CHUNK,
+                       "kernel": f"tc_decode2 (tcgen05 cta_group::2 CTA pairs, 256 frames per pair tile; the "
+                                 f"launch's frame tiles walk the basis rows in lock-step), {CHUNK}-frame launches "
+                                 f"streamed through one buffer (1024 frames = {B * 4.0 * n / 1e9:.0f} GB > HBM)"}
     recon["basis_split_ms"] = round(rec["split"] * 1e3, 2)
 
     # ---- e2e through the public API from pinned host memory ----
@@ -378,17 +552,26 @@ def main():
         "fit": {"s": round(fit_t, 4), "gflops": round(value, 1), "flops": F_fit,
                 "per_step_s": [round(x["fit"], 4) for x in res],
                 "terms": {k: v for k, v in terms.items()},
+                "value_kind": "equivalent-work rate: SURVEY §8(d) reference-algorithm flops / fit time (an "
+                              "algebraically equivalent restructuring counts as the terms it replaces); the "
+                              "roofline-comparable rate is executed_tflops",
                 "executed_flops": executed_flops(n, m, r, cfg["p"], cfg["q"]),
+                "executed_terms_fp64_dmma": executed_terms(n, m, r, cfg["p"], cfg["q"])[0],
+                "executed_terms_tcgen05_fp32_accurate": executed_terms(n, m, r, cfg["p"], cfg["q"])[1],
                 "executed_tflops": round(executed_flops(n, m, r, cfg["p"], cfg["q"]) / fit_t / 1e12, 3)},
         "reconstruct": recon,
         "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(DOM_NAMES[dom]),
+                     "frac": round(achieved / peak, 4), "peak_burst": round(peak_burst, 2),
+                     "frac_burst": round(achieved / peak_burst, 4),
+                     "traffic": traffic_from_profiles(DOM_NAMES[dom], args.config),
                      "kernel": DOM_NAMES[dom] + " (FP64 DMMA m8n8k4, TMA-fed); achieved = flops its "
                                "launches execute (symmetric Gram / triangular apply as n*l^2) / their CUDA-event time",
                      "algorithmic_bytes_per_launch": round(g[3] / max(g[2], 1)),
-                     "traffic_source": "profiles/dominant_kernel_traffic.json (ncu dram__bytes_read+write per "
-                                       "launch, config 3, one bench step)",
-                     "peak_source": "in-run DMMA.8x8x4 throughput probe (fdmd_dmma_peak); spec 40 TF/s; "
+                     "traffic_source": f"profiles/dominant_kernel_traffic.json[{args.config}] (ncu "
+                                       "dram__bytes_read+write per launch of this kernel, this config, one bench "
+                                       "step, same code)",
+                     "peak_source": "in-run DMMA.8x8x4 throughput probe (fdmd_dmma_peak): `peak` sustained (one "
+                                    "~2 s launch after ~2 s of ramp), `peak_burst` a ~0.1 s launch; spec 40 TF/s; "
                                     "MEASURED_PEAKS.json has no FP64 figure",
                      "contractions": {"kernels": "tall_gemm + tall_gram (all FP64 DMMA work of the fit)",
                                       "achieved": round(achieved_all, 3), "frac": round(achieved_all / peak, 4),
@@ -402,14 +585,13 @@ def main():
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and not args.no_cpu:
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        import flowdmd_oracle as orc
-        s = cpu_sample(orc, synth, cfg, args.cpu_rows)
+        arm = CpuArm()
+        s = cpu_sample(arm, synth, cfg, args.cpu_rows)
         t0 = time.perf_counter()
-        cpu_fit(orc, s["X"], cfg)
+        arm.fit(s["X"], cfg)
         dt = time.perf_counter() - t0
         line["cpu_baseline"] = {"value": round(s["flops"] / dt / 1e9, 3), "unit": "GFLOP/s", "cores": os.cpu_count(),
-                                "kind": "port", "sample": s["sample"], "s": round(dt, 2)}
+                                "kind": arm.kind, "sample": s["sample"], "s": round(dt, 2)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -458,22 +640,25 @@ def run_e2e(args, fd, host, n_loc, m, r, cfg, lm, shard, F_fit, max_over_ranks, 
                    "sketch stage) -> decode(step_k) to host"}
 
 
-def frame_chunk(n_loc, total, keep=0.0):
+def frame_chunk(n_loc, total, keep=0.0, margin=3e9):
     """Frames per reconstruction launch: the widest 128 * 2^k batch whose
-    frame buffer fits in 90% of free HBM after `keep` more bytes (the basis
-    planes) — the basis is read once per launch."""
+    frame buffer fits in free HBM after `keep` more bytes (the basis planes)
+    with `margin` to spare. A launch's frame tiles walk the basis rows in
+    lock-step, so the basis is fetched from DRAM ~once per launch (L2)."""
     import torch
     free = torch.cuda.mem_get_info()[0] + torch.cuda.memory_reserved() - torch.cuda.memory_allocated() - keep
     chunk = 128
-    while chunk * 2 <= total and chunk * 2 * 4.0 * n_loc <= 0.9 * free:
+    while chunk * 2 <= total and chunk * 2 * 4.0 * n_loc <= free - margin:
         chunk *= 2
     return min(chunk, total)
 
 
-def ctypes_peak(_lib):
+def ctypes_peak(_lib, seconds):
+    """DMMA.8x8x4 throughput probe (fdmd_dmma_peak): the last launch of a
+    growing series lasts ~seconds/4 (0.4 -> burst, 8 -> sustained)."""
     import ctypes
     v = ctypes.c_double(0.0)
-    _lib.check(_lib.lib().fdmd_dmma_peak(0.4, ctypes.byref(v)), "dmma_peak")
+    _lib.check(_lib.lib().fdmd_dmma_peak(float(seconds), ctypes.byref(v)), "dmma_peak")
     return v.value
 
 
@@ -487,18 +672,14 @@ def hbm_peak():
 DOM_NAMES = {"tall_gemm": "tall_gemm_tma_kernel", "tall_gram": "tall_gram_panel_kernel"}
 
 
-def traffic_from_profiles(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu launch-list
-    summary (profiles/dominant_kernel_traffic.json), or None if absent."""
+def traffic_from_profiles(kernel, config="c3"):
+    """dram bytes per launch of `kernel` for this config from the committed
+    ncu summary (profiles/dominant_kernel_traffic.json, keyed by config),
+    or None when that config/kernel was not profiled with the current code."""
     path = os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")
     try:
         js = json.load(open(path))
     except Exception:
         return None
-    if js.get("kernel") == kernel:
-        return js.get("traffic_bytes_per_launch")
-    return js.get("kernels", {}).get(kernel, {}).get("traffic_bytes_per_launch")
-
-
-if __name__ == "__main__":
-    main()
+    ent = js.get("configs", {}).get(config, {})
+    return ent.get("kernels", {}).get(kernel, {}).get("traffic_bytes_per_launch")

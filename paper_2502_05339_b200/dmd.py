@@ -837,6 +837,8 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
                                      "objective_history": history, "converged": converged},
                          _modes=modes)
     model.basis_U = U if keep_basis else None
+    if svd_mode == "randomized":
+        model.provenance["sketch"] = {k: v for k, v in basis.stats.items()}
     warns = _stability_warnings(plan.lam)
     if not converged and cfg.max_iters > 0:
         warns.append(f"variable projection hit max_iters={cfg.max_iters}")

@@ -179,3 +179,126 @@ def generate_host(p: SynthParams, row0: int = 0, rows=None) -> np.ndarray:
     if p.noise:
         out += p.noise * counter_normal(p.seed, idx[:, None], np.arange(p.m)[None, :], p.m)
     return out.astype(p.dtype)
+
+
+# ---------------------------------------------------------------------------
+# Config 2 (DMDc): X_{j+1} = A X_j + B u_j, A = config 1's rank-150 generator
+# ---------------------------------------------------------------------------
+def _sin_tables(kvec, theta, N):
+    """S[d][i, c, x] = sin(2 pi k_icd x / N + th_icd)."""
+    x = np.arange(N)
+    return [np.sin(2.0 * np.pi * kvec[:, :, d, None] * x[None, None, :] / N + theta[:, :, d, None])
+            for d in range(3)]
+
+
+@dataclass
+class ControlledParams:
+    """BASELINE config 2: the 3D mode fields of config 1 (75 complex modes,
+    rank 150) as the generator A, plus ell seeded smooth control fields B.
+
+    A = F M F^+ (F = the 150 real mode fields Re f_i, Im f_i, f_i = amp_ic s_ic
+    per component c; M advances each mode by lambda_i) and B = F F^+ G: the
+    smooth random fields G (separable sinusoids, wavenumbers 1..4) projected
+    onto A's range, so the controlled states stay in A's 150-dim invariant
+    subspace and [X; Upsilon] has rank 150 + ell = 158 — the r = 158 BASELINE
+    fits at. In mode coordinates x = Re(sum_i f_i z_i):
+        z_{j+1} = lambda * z_j + P u_j,   P = the z-coordinates of F^+ G,
+    from z_0 = b; every column is a separable-field superposition generated
+    by the same kernel as configs 1/3/4."""
+
+    base: SynthParams        # config-1 modes (grid, comps, K = 75, m, lambda, b, amp, kvec, theta)
+    ell: int
+    g_amp: np.ndarray        # ell x comps real
+    g_kvec: np.ndarray       # ell x comps x 3 (wavenumbers in [1, 4]: smooth)
+    g_theta: np.ndarray      # ell x comps x 3
+    P: np.ndarray            # K x ell complex: z-coordinates of F^+ g_k
+
+    @property
+    def n(self):
+        return self.base.n
+
+    @property
+    def m(self):
+        return self.base.m
+
+    def controls(self, seed, steps=None) -> np.ndarray:
+        """ell x steps control sequence u_j ~ N(0, 1), seeded."""
+        steps = self.m - 1 if steps is None else steps
+        return np.random.default_rng(seed).standard_normal((self.ell, steps))
+
+    def trajectory(self, u: np.ndarray, z0=None) -> np.ndarray:
+        """Mode coordinates z_j, j = 0..len(u) (K x (s+1) complex)."""
+        K, s = self.base.modes, u.shape[1]
+        z = np.empty((K, s + 1), dtype=np.complex128)
+        z[:, 0] = self.base.b if z0 is None else z0
+        for j in range(s):
+            z[:, j + 1] = self.base.lam * z[:, j] + self.P @ u[:, j]
+        return z
+
+    def sep_tables(self, u: np.ndarray, z0=None):
+        """(sx, sy, sz, A) for the separable generator: one column per state
+        of the trajectory driven by u."""
+        b = self.base
+        z = self.trajectory(u, z0)
+        sx, sy, sz = _sin_tables(b.kvec, b.theta, b.grid)
+        return sx, sy, sz, np.real(b.amp[:, :, None] * z[:, None, :])
+
+    def true_operator_eigs(self) -> np.ndarray:
+        """The nonzero spectrum of A: config 1's lambda and their conjugates."""
+        return np.concatenate([self.base.lam, np.conj(self.base.lam)])
+
+
+def _field_gram(kA, thA, aA, kB, thB, aB, N):
+    """<f_a, f_b> over the N^3 x comps grid for separable fields
+    f(x) = amp_c prod_d sin(2 pi k_cd x_d / N + th_cd) (amplitudes broadcast
+    per component): sums over x factor into three 1-D sums per component."""
+    x = np.arange(N)
+    G = np.zeros((kA.shape[0], kB.shape[0]), dtype=np.result_type(aA, aB, np.float64))
+    for c in range(kA.shape[1]):
+        prod = np.ones((kA.shape[0], kB.shape[0]))
+        for d in range(3):
+            sa = np.sin(2.0 * np.pi * kA[:, c, d, None] * x[None, :] / N + thA[:, c, d, None])
+            sb = np.sin(2.0 * np.pi * kB[:, c, d, None] * x[None, :] / N + thB[:, c, d, None])
+            prod *= sa @ sb.T
+        G += aA[:, c, None] * aB[None, :, c] * prod
+    return G
+
+
+def config2_params(seed: int = 2, grid=None, ell: int = 8) -> ControlledParams:
+    base = config_params(1, seed=seed, grid=grid)
+    rng = np.random.default_rng(seed + 1000)
+    N, C = base.grid, base.comps
+    g_amp = rng.standard_normal((ell, C))
+    g_kvec = rng.integers(1, 5, size=(ell, C, 3))
+    g_theta = rng.uniform(0.0, 2.0 * np.pi, size=(ell, C, 3))
+    # real mode fields R_i = Re(amp_i) s_i, I_i = Im(amp_i) s_i; x = sum R_i Re z_i - I_i Im z_i
+    kF = np.concatenate([base.kvec, base.kvec])
+    thF = np.concatenate([base.theta, base.theta])
+    aF = np.concatenate([base.amp.real, base.amp.imag])
+    FtF = _field_gram(kF, thF, aF, kF, thF, aF, N)
+    FtG = _field_gram(kF, thF, aF, g_kvec, g_theta, g_amp, N)
+    beta = np.linalg.solve(FtF, FtG)                      # 2K x ell: g_k's projection on [R | I]
+    K = base.modes
+    P = beta[:K] - 1j * beta[K:]
+    p = ControlledParams(base, ell, g_amp, g_kvec, g_theta, P)
+    return p
+
+
+def generate_host_tables(tables, n: int, comps: int, grid: int, row0: int = 0, rows=None,
+                         dtype=np.float32) -> np.ndarray:
+    """Rows of sum_i sx[i,c,x] sy[i,c,y] sz[i,c,z] A[i,c,j] (row = c N^3 + (z N + y) N + x),
+    fp64 on the host, cast to dtype (the device generator's formula, no noise)."""
+    sx, sy, sz, A = tables
+    rows = n - row0 if rows is None else rows
+    idx = np.arange(row0, row0 + rows)
+    cells = grid ** 3
+    c = idx // cells
+    rem = idx % cells
+    x, y, z = rem % grid, (rem // grid) % grid, rem // (grid * grid)
+    out = np.empty((rows, A.shape[2]), dtype=np.float64)
+    for cc in range(comps):
+        sel = c == cc
+        if sel.any():
+            S = sx[:, cc, x[sel]] * sy[:, cc, y[sel]] * sz[:, cc, z[sel]]
+            out[sel] = S.T @ A[:, cc, :]
+    return out.astype(dtype)

@@ -138,3 +138,38 @@ def test_synth_generator_properties():
     # counter noise is standard normal
     g = synth.counter_normal(7, np.arange(200000), np.zeros(200000, dtype=np.int64), 1)
     assert abs(g.mean()) < 0.01 and abs(g.std() - 1) < 0.01
+
+
+def test_config2_generator_is_the_controlled_system():
+    """synth.config2_params: every column of the generated matrix satisfies
+    X_{j+1} = A X_j + B u_j with A = F M F^+ (config 1's 75 modes advanced by
+    lambda on span F, zero on its complement) and B = F F^+ G (the smooth
+    fields projected onto A's range), built here from explicit grid fields."""
+    from paper_2502_05339_b200 import synth
+    N = 20
+    p = synth.config2_params(2, grid=N)
+    u = p.controls(5, 30)
+    X = synth.generate_host_tables(p.sep_tables(u), p.n, 3, N, dtype=np.float64)
+    b = p.base
+    idx = np.arange(p.n)
+    c, rem = idx // N ** 3, idx % N ** 3
+    xyz = (rem % N, (rem // N) % N, rem // (N * N))
+
+    def fields(kv, th):
+        s = np.empty((kv.shape[0], p.n))
+        for cc in range(3):
+            sel = c == cc
+            s[:, sel] = np.prod([np.sin(2 * np.pi * kv[:, cc, d, None] * xyz[d][None, sel] / N + th[:, cc, d, None])
+                                 for d in range(3)], axis=0)
+        return s
+    sF, sG = fields(b.kvec, b.theta), fields(p.g_kvec, p.g_theta)
+    F = np.hstack([(sF * b.amp.real[:, c]).T, (sF * b.amp.imag[:, c]).T])
+    G = (sG * p.g_amp[:, c]).T
+    K = b.modes
+    M = np.zeros((2 * K, 2 * K))
+    for i, lv in enumerate(b.lam):        # x = R a + I b, z = a - i b, z' = lam z
+        M[i, i], M[i, K + i], M[K + i, i], M[K + i, K + i] = lv.real, lv.imag, -lv.imag, lv.real
+    Fp = np.linalg.pinv(F)
+    A, B = F @ M @ Fp, F @ (Fp @ G)
+    resid = np.abs(X[:, 1:] - (A @ X[:, :-1] + B @ u)).max() / np.abs(X).max()
+    assert resid <= 1e-11
