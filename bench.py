@@ -683,3 +683,7 @@ def traffic_from_profiles(kernel, config="c3"):
         return None
     ent = js.get("configs", {}).get(config, {})
     return ent.get("kernels", {}).get(kernel, {}).get("traffic_bytes_per_launch")
+
+
+if __name__ == "__main__":
+    main()

@@ -19,6 +19,10 @@
  *   fdmd_synth3d       BASELINE.json configs 1-4 snapshot generator (device)
  *   fdmd_rsvd          randomized_svd (linalg.py:62-90) as one call (sketch, power
  *                      iterations, CholeskyQR2, projection, svd, canonical signs, lift)
+ *   fdmd_dmd_fit       exact_dmd (dmd.py:240-274) / optdmd + _varpro_lm (dmd.py:277-455)
+ *                      as one call over a device-owned SnapshotMatrix (fdmd_mat_upload)
+ *   fdmd_model_*       ReducedModel.phi (dmd.py:53-77, chunked), decode (runtime.py:66-99);
+ *   fdmd_encode        encode (runtime.py:47-52) — model handles from fdmd_dmd_fit
  *   fdmd_mac_*         2-D serving / guided upscaling: frame planes (server.py:205-214),
  *                      density transport (solver.py:133-150), injection and the
  *                      guide projection (upres.py:21-50, 154-169)
@@ -224,6 +228,54 @@ int fdmd_sol_pressure_apply(double* vel, const double* p, int nx, int ny, double
 int fdmd_rsvd(const void* X, int x_dtype, int64_t ldx, int64_t n, int T, int r, int l, int q,
               const double* omega_host, double* sigma_host, double* V_host, double* U, int64_t ldu,
               void* stream);
+
+/* ---- Fit / model handles ----------------------------------
+ * The whole exact-DMD / OptDMD fit, the mode matrix, encode and decode as C
+ * calls over plain host buffers, for a binding without this package's Python
+ * layer. A context owns one device and a pool of streams;
+ * every call takes a stream from the pool for its duration, so concurrent
+ * calls from several host threads (the reference server's request threads,
+ * server.py:57-67) are safe. Host buffers are caller-owned; calls are
+ * synchronous on return. Complex values are interleaved (re, im) doubles. */
+typedef struct fdmd_ctx fdmd_ctx;
+typedef struct fdmd_mat fdmd_mat;
+typedef struct fdmd_model fdmd_model;
+
+#define FDMD_METHOD_EXACT 0 /* exact_dmd (dmd.py:240-274) */
+#define FDMD_METHOD_OPT 1   /* optdmd (dmd.py:366-436) */
+
+int fdmd_ctx_create(int device, int n_streams, fdmd_ctx** out);
+int fdmd_ctx_destroy(fdmd_ctx* ctx);
+/* SnapshotMatrix(states) (dmd.py:26-50): host C-order n x m (row stride
+ * ld_host elements, FDMD_F32 / FDMD_F64) -> a device-owned row-major copy.
+ * ValueError semantics: n >= 1, m >= 2, every entry finite. */
+int fdmd_mat_upload(fdmd_ctx* ctx, const void* host, int dtype, int64_t n, int64_t m, int64_t ld_host,
+                    fdmd_mat** out);
+int fdmd_mat_free(fdmd_mat* mat);
+/* exact_dmd(data, r, svd_mode="randomized", seed) / optdmd(data, r, init,
+ * LMConfig(max_iters=lm_max_iters), svd_mode="randomized", seed) on the
+ * snapshot columns X = states[:, :-1], X' = states[:, 1:]:
+ * omega_host = default_rng(seed).standard_normal((T, l)) (T = m - 1,
+ * l = r + oversample, linalg.py:76), q power iterations. OPT only:
+ * init_lam_host (2r, NULL = exact-DMD eigenvalues, dmd.py:387), jitter_host
+ * (r values default_rng(seed).random(r) for the collapse retry,
+ * dmd.py:394-399; NULL = fail on collapse). Outputs sigma_host (r), lam_host
+ * (2r) and the model (modes on the device, table dtype = states dtype). */
+int fdmd_dmd_fit(fdmd_ctx* ctx, const fdmd_mat* states, double dt, int r, int l, int q, const double* omega_host,
+                 int method, int lm_max_iters, const double* init_lam_host, const double* jitter_host,
+                 double* sigma_host, double* lam_host, fdmd_model** out);
+int fdmd_model_info(const fdmd_model* model, int64_t* n, int* r, double* dt, int* converged);
+/* the variable-projection objective history (provenance["objective_history"]);
+ * returns its length, copies min(length, cap) values */
+int fdmd_model_history(const fdmd_model* model, double* out, int cap);
+/* rows [row0, row0 + rows) of phi (n x r complex, C-order) -> out_c128 (rows x 2r doubles) */
+int fdmd_model_phi_to_host(fdmd_ctx* ctx, const fdmd_model* model, int64_t row0, int64_t rows, double* out_c128);
+/* encode: z = pinv(phi) u (runtime.py:47-52); u_host n doubles, z_host 2r */
+int fdmd_encode(fdmd_ctx* ctx, const fdmd_model* model, const double* u_host, double* z_host);
+/* decode: frames[f] = Re(phi z_f) (runtime.py:66-99) for B states (z_host B x 2r)
+ * -> out_host (B x n doubles, C-order) */
+int fdmd_model_decode(fdmd_ctx* ctx, const fdmd_model* model, const double* z_host, int B, double* out_host);
+int fdmd_model_free(fdmd_model* model);
 
 /* FP64 tensor-pipe (DMMA.8x8x4) throughput probe on the current device:
  * a register-only mma.sync f64 loop lasting ~`seconds`/4; writes TFLOP/s.

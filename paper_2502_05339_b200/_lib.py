@@ -73,6 +73,17 @@ SIGNATURES = {
     "fdmd_sol_cg_single": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _d, _vp, _i, _d, _i, _vp, _vp]),
     "fdmd_sol_pressure_apply": (_i, [_vp, _vp, _i, _i, _d, _vp, _i, _vp]),
     "fdmd_rsvd": (_i, [_vp, _i, _i64, _i64, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i64, _vp]),
+    "fdmd_ctx_create": (_i, [_i, _i, _c.POINTER(_vp)]),
+    "fdmd_ctx_destroy": (_i, [_vp]),
+    "fdmd_mat_upload": (_i, [_vp, _vp, _i, _i64, _i64, _i64, _c.POINTER(_vp)]),
+    "fdmd_mat_free": (_i, [_vp]),
+    "fdmd_dmd_fit": (_i, [_vp, _vp, _d, _i, _i, _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _c.POINTER(_vp)]),
+    "fdmd_model_info": (_i, [_vp, _c.POINTER(_i64), _c.POINTER(_i), _c.POINTER(_d), _c.POINTER(_i)]),
+    "fdmd_model_history": (_i, [_vp, _vp, _i]),
+    "fdmd_model_phi_to_host": (_i, [_vp, _vp, _i64, _i64, _vp]),
+    "fdmd_encode": (_i, [_vp, _vp, _vp, _vp]),
+    "fdmd_model_decode": (_i, [_vp, _vp, _vp, _i, _vp]),
+    "fdmd_model_free": (_i, [_vp]),
     "fdmd_synth3d": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _d, _u64, _i64, _i64, _vp, _i, _i64, _vp]),
 }
 

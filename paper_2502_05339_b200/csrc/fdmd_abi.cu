@@ -1379,4 +1379,20 @@ int fdmd_synth3d(const double* sx, const double* sy, const double* sz, const dou
 
 }  // extern "C"
 
-#include "fdmd_rsvd.inc"
+// Internal hooks for the host orchestration unit (fdmd_fit.cpp, compiled
+// separately with g++): the thread-local error slot, the stream-ordered scratch
+// pool and the per-thread cuSOLVER handle. Not part of include/fdmd.h.
+extern "C" {
+int fdmdi_set_error(int code, const char* msg) {
+  g_err = msg ? msg : "";
+  return code;
+}
+cudaError_t fdmdi_scratch_alloc(void** p, size_t bytes, void* stream) {
+  return scratch_alloc(p, bytes, (cudaStream_t)stream);
+}
+void* fdmdi_solver_handle(void* stream) {
+  SolverCtx* c = solver_ctx();
+  if (!c || cusolverDnSetStream(c->h, (cudaStream_t)stream) != CUSOLVER_STATUS_SUCCESS) return nullptr;
+  return (void*)c->h;
+}
+}  // extern "C"
