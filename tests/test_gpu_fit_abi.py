@@ -36,6 +36,7 @@ def _bind():
         "fdmd_mat_upload": (i32, [vp, vp, i32, i64, i64, i64, PV]),
         "fdmd_mat_free": (i32, [vp]),
         "fdmd_dmd_fit": (i32, [vp, vp, dbl, i32, i32, i32, vp, i32, i32, vp, vp, vp, vp, PV]),
+        "fdmd_dmdc_fit": (i32, [vp, vp, vp, i32, dbl, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, PV]),
         "fdmd_model_info": (i32, [vp, ctypes.POINTER(i64), ctypes.POINTER(i32), ctypes.POINTER(dbl),
                                   ctypes.POINTER(i32)]),
         "fdmd_model_history": (i32, [vp, vp, i32]),
@@ -213,6 +214,50 @@ def test_config3_shape_optdmd_abi(abi, config_golden):
         assert phase_aligned_error(head, g["c3s_opt_phi_head"]) <= 1e-5
     finally:
         abi[0].fdmd_model_free(model)
+
+
+@pytest.mark.parametrize("noise", [0.0, 1e-4])
+def test_dmdc_abi_against_oracle_and_truth(abi, noise):
+    """fdmd_dmdc_fit on the oracle's controlled system (x_{j+1} = A x_j + B u_j,
+    known spectrum): eigenvalues against the oracle restatement (same Omegas),
+    the generator's spectrum, and a controlled rollout z_{k+1} = lam z_k +
+    reduced_b u_k dt (runtime.step_forced, runtime.py:164-200) against the data."""
+    import flowdmd_oracle as orc
+    L, ctx = abi
+    n, pairs, ell, m = 6000, 5, 3, 61
+    X, U, true_eigs, Bf = orc.controlled_system(n, pairs, ell, m, seed=7, noise=noise)
+    T = m - 1
+    r_aug, r = 2 * pairs + 2 * ell, 2 * pairs + ell
+    l_aug, l = r_aug + 10, r + 10
+    om_aug = np.random.default_rng(5).standard_normal((T, l_aug))
+    om_out = np.random.default_rng(6).standard_normal((T, l))
+    ref = orc.dmdc_fit(X, U, r_aug, r, seed=5, p=10, q=1)
+    M = upload(abi, X)
+    sig, lam, red = np.zeros(r_aug), np.zeros(2 * r), np.zeros(2 * r * ell)
+    model = vp()
+    try:
+        chk(L, L.fdmd_dmdc_fit(ctx, M, _p(np.ascontiguousarray(U, dtype=np.float64)), ell, 1.0, r_aug, l_aug, r, l, 1,
+                               _p(om_aug), _p(om_out), _p(sig), _p(lam), _p(red), ctypes.byref(model)))
+    finally:
+        L.fdmd_mat_free(M)
+    try:
+        lam = lam[0::2] + 1j * lam[1::2]
+        red = (red[0::2] + 1j * red[1::2]).reshape(r, ell)
+        np.testing.assert_allclose(sig, ref["sigma_aug"][:r_aug], rtol=1e-9)
+        assert match_eigs(lam, ref["lam"]) <= 1e-8
+        if noise == 0.0:
+            d = np.array([np.abs(lam - t).min() for t in true_eigs])
+            assert d.max() <= 1e-7, d.max()
+        # controlled rollout through the model handle, from the data's first state
+        z = encode(abi, model, X[:, 0], r)
+        worst = 0.0
+        for k in range(T):
+            z = lam * z + red @ U[:, k]
+            fr = decode(abi, model, z, n)[0]
+            worst = max(worst, rel(fr, X[:, k + 1]))
+        assert worst <= (1e-6 if noise == 0.0 else 5e-2), worst
+    finally:
+        L.fdmd_model_free(model)
 
 
 def test_abi_errors_and_concurrency(abi, small_golden):

@@ -4,7 +4,7 @@ into (a) a per-kernel table (launches, device-time share, DRAM bytes per
 launch) and (b) profiles/dominant_kernel_traffic.json, which bench.py reads
 for roofline.traffic.
 
-  python tools/traffic_from_ncu.py gpurun_out/r01_c3_launches.csv profiles/r01_launches_bench_c3.txt
+  python tools/traffic_from_ncu.py gpurun_out/r2_c3_launches.csv profiles/r02_launches_bench_c3.txt [--config=c3]
 
 Per-launch times under ncu are serialised and cold-cache: compare shares,
 not absolute times. DRAM bytes are per launch and do not depend on that.
@@ -94,8 +94,18 @@ def main():
           "kernels": {s: {"launches": a[0], "traffic_bytes_per_launch": (a[2] + a[3]) / a[0],
                           "share_of_device_time_under_ncu": round(a[1] / total, 4)}
                       for s, a in agg.items() if any(o in s for o in OURS)}}
-    with open(os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json"), "w") as f:
-        json.dump(js, f, indent=1)
+    # keyed by bench config (bench.py's traffic_from_profiles reads configs[<config>])
+    config = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--config=")), "c3")
+    path = os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")
+    try:
+        allj = json.load(open(path))
+    except Exception:
+        allj = {}
+    if "configs" not in allj:
+        allj = {"configs": {}}
+    allj["configs"][config] = js
+    with open(path, "w") as f:
+        json.dump(allj, f, indent=1)
     print("\n".join(out[:30]))
 
 
