@@ -264,6 +264,16 @@ int fdmd_mat_free(fdmd_mat* mat);
 int fdmd_dmd_fit(fdmd_ctx* ctx, const fdmd_mat* states, double dt, int r, int l, int q, const double* omega_host,
                  int method, int lm_max_iters, const double* init_lam_host, const double* jitter_host,
                  double* sigma_host, double* lam_host, fdmd_model** out);
+/* Augmented DMDc (the package's dmd.dmdc_fit; Proctor et al. 2016, SURVEY.md
+ * §8(c) "C2 restatement"): controls_host ell x T row-major (u_j for j < T);
+ * a rank-r_aug sketch of [X; Upsilon] (omega_aug_host T x l_aug) and the
+ * output basis U_hat = a rank-r sketch of X' (omega_out_host T x l).
+ * Outputs sigma_aug_host (r_aug), lam_host (2r), reduced_b_host (r x ell
+ * complex, interleaved) = pinv(phi) U_hat B~ / dt, the ControlOperator matrix
+ * runtime.step_forced consumes (runtime.py:164-200), and the model. */
+int fdmd_dmdc_fit(fdmd_ctx* ctx, const fdmd_mat* states, const double* controls_host, int ell, double dt, int r_aug,
+                  int l_aug, int r, int l, int q, const double* omega_aug_host, const double* omega_out_host,
+                  double* sigma_aug_host, double* lam_host, double* reduced_b_host, fdmd_model** out);
 int fdmd_model_info(const fdmd_model* model, int64_t* n, int* r, double* dt, int* converged);
 /* the variable-projection objective history (provenance["objective_history"]);
  * returns its length, copies min(length, cap) values */

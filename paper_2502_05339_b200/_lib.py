@@ -78,6 +78,7 @@ SIGNATURES = {
     "fdmd_mat_upload": (_i, [_vp, _vp, _i, _i64, _i64, _i64, _c.POINTER(_vp)]),
     "fdmd_mat_free": (_i, [_vp]),
     "fdmd_dmd_fit": (_i, [_vp, _vp, _d, _i, _i, _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _c.POINTER(_vp)]),
+    "fdmd_dmdc_fit": (_i, [_vp, _vp, _vp, _i, _d, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _c.POINTER(_vp)]),
     "fdmd_model_info": (_i, [_vp, _c.POINTER(_i64), _c.POINTER(_i), _c.POINTER(_d), _c.POINTER(_i)]),
     "fdmd_model_history": (_i, [_vp, _vp, _i]),
     "fdmd_model_phi_to_host": (_i, [_vp, _vp, _i64, _i64, _vp]),

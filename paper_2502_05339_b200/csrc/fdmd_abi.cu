@@ -384,9 +384,14 @@ PanelPlan panel_plan(int64_t n, int K1, int K2, int symmetric, size_t ea, size_t
       }
     }
   }
-  // row splits: ~2 waves of one CTA per SM, chunk-aligned (16 rows)
+  // row splits: ~2 waves of one CTA per SM, chunk-aligned (16 rows);
+  // FDMD_GRAM_SPLITS overrides the split count (tools/gram_sweep.py)
   const int64_t max_splits = std::max<int64_t>(1, (n + 15) / 16);
   int64_t splits = std::max<int64_t>(1, ((int64_t)sm_count_cached() * 2 + p.P - 1) / p.P);
+  if (const char* e = getenv("FDMD_GRAM_SPLITS")) {
+    const int64_t v = atoll(e);
+    if (v > 0) splits = v;
+  }
   splits = std::min(splits, max_splits);
   p.rows_per_split = ((n + splits - 1) / splits + 15) / 16 * 16;
   if (p.rows_per_split == 0) p.rows_per_split = 16;

@@ -553,15 +553,16 @@ struct Sketch {
   std::vector<double> QtS;  // l x m = Q^T S over all m columns (fix applied)
 };
 
-// The explicit range finder over X = S[:, :T] (S: n x m, m >= T): Y = X Omega
+// The explicit range finder over X = S[:, c0:c0+T] (S: n x m, m >= c0 + T): Y = X Omega
 // -> CholeskyQR (one pass while power iterating, CholeskyQR2 at the end, the
 // shifted CholeskyQR3 of Fukaya et al. 2020 when the factor is ill-conditioned)
 // -> q x {Z = X^T Q -> W = qr(Z) -> Y = X W -> CholeskyQR} -> Q^T S -> svd(Q^T X).
-int sketch(Dev& d, const Tall& S, int64_t n, int T, int m, int l, int q, const double* omega_host, Sketch& out) {
+int sketch(Dev& d, const Tall& S, int64_t n, int T, int m, int l, int q, const double* omega_host, Sketch& out,
+           int c0 = 0) {
   cudaStream_t s = d.s;
   const int K2max = std::max(m, l);
   const size_t gws = std::max(fdmd_tall_gram_workspace(n, l, l),
-                              std::max(fdmd_tall_gram_workspace(n, T, l), fdmd_tall_gram_workspace(n, l, K2max)));
+                              std::max(fdmd_tall_gram_workspace(n, c0 + T, l), fdmd_tall_gram_workspace(n, l, K2max)));
   double* Q = d.alloc<double>((size_t)n * l);
   double* Bd = d.alloc<double>((size_t)K2max * 2 * l + 16);
   double* Gd = d.alloc<double>((size_t)K2max * l);
@@ -616,15 +617,24 @@ int sketch(Dev& d, const Tall& S, int64_t n, int T, int m, int l, int q, const d
     fix = inv_upper(R2, l);
     return FDMD_OK;
   };
+  // a column window c0 > 0 (X' = S[:, 1:]) multiplies S by the small matrix
+  // padded with c0 zero rows on top (TMA needs the 16-byte aligned base of S)
+  const int Kc = c0 + T;
+  auto placed = [&](const std::vector<double>& M) {
+    std::vector<double> P((size_t)Kc * l, 0.0);
+    std::copy(M.begin(), M.end(), P.begin() + (size_t)c0 * l);
+    return P;
+  };
   std::vector<double> Om(omega_host, omega_host + (size_t)T * l);
-  TRY(gemm(S.p, S.dt, S.ld, Om, T, l, 0));  // Y = X Omega (X = the first T columns)
+  TRY(gemm(S.p, S.dt, S.ld, placed(Om), Kc, l, 0));  // Y = X Omega
   TRY(cholqr(q == 0 ? 2 : 1));
   for (int it = 0; it < q; ++it) {
-    std::vector<double> Z;
-    TRY(gram(S.p, S.dt, S.ld, Q, FDMD_F64, l, T, l, 0, Z));  // T x l = X^T buffer
+    std::vector<double> Zf, Z((size_t)T * l);
+    TRY(gram(S.p, S.dt, S.ld, Q, FDMD_F64, l, Kc, l, 0, Zf));  // (c0 + T) x l; X^T buffer = its last T rows
+    std::copy(Zf.begin() + (size_t)c0 * l, Zf.end(), Z.begin());
     if (!fix.empty()) Z = matmul(Z, fix, T, l, l);
     std::vector<double> W = householder_q(Z, T, l);
-    TRY(gemm(S.p, S.dt, S.ld, W, T, l, 0));
+    TRY(gemm(S.p, S.dt, S.ld, placed(W), Kc, l, 0));
     TRY(cholqr(it == q - 1 ? 2 : 1));
   }
   // Q^T S (l x m) with Q = buffer fix
@@ -635,7 +645,7 @@ int sketch(Dev& d, const Tall& S, int64_t n, int T, int m, int l, int q, const d
   if (!h) return fail(FDMD_ERR_SOLVER, "cusolverDnCreate failed");
   std::vector<double> Bt((size_t)T * l);  // column-major T x l = B^T: A[i + j*T] = B[j][i]
   for (int j = 0; j < l; ++j)
-    for (int i = 0; i < T; ++i) Bt[i + (size_t)j * T] = out.QtS[(size_t)j * m + i];
+    for (int i = 0; i < T; ++i) Bt[i + (size_t)j * T] = out.QtS[(size_t)j * m + c0 + i];
   double* A = d.alloc<double>((size_t)T * l);
   double* Sv = d.alloc<double>(l);
   double* Ua = d.alloc<double>((size_t)T * l);
@@ -1397,6 +1407,142 @@ int fdmd_dmd_fit(fdmd_ctx* ctx, const fdmd_mat* states, double dt, int r, int l,
   if (sigma_host) std::copy(model->sigma.begin(), model->sigma.end(), sigma_host);
   if (lam_host)
     for (int k = 0; k < r; ++k) lam_host[2 * k] = model->lam[k].real(), lam_host[2 * k + 1] = model->lam[k].imag();
+  *out = model;
+  return FDMD_OK;
+}
+
+// Augmented DMDc (Proctor et al. 2016; SURVEY §8(c) "C2 restatement"; the
+// package's dmd.dmdc_fit): rank-r_aug sketch of [X; Upsilon], output basis
+// U_hat = a rank-r sketch of X' (seed + 1), A~ = U_hat^T X' V S^-1 U1^T U_hat,
+// B~ = U_hat^T X' V S^-1 U2^T, phi = X' V S^-1 U1^T U_hat W and the modal
+// control matrix reduced_b = pinv(phi) U_hat B~ / dt (runtime.step_forced
+// multiplies by dt, runtime.py:188).
+int fdmd_dmdc_fit(fdmd_ctx* ctx, const fdmd_mat* states, const double* controls_host, int ell, double dt, int r_aug,
+                  int l_aug, int r, int l, int q, const double* omega_aug_host, const double* omega_out_host,
+                  double* sigma_aug_host, double* lam_host, double* reduced_b_host, fdmd_model** out) {
+  if (!ctx || !states || !controls_host || !omega_aug_host || !omega_out_host || !out)
+    return fail(FDMD_ERR_INVALID, "dmdc_fit: null argument");
+  *out = nullptr;
+  if (!(dt > 0) || !std::isfinite(dt)) return fail(FDMD_ERR_INVALID, "dt must be positive");
+  const int64_t n = states->n;
+  const int m = (int)states->m, T = m - 1;
+  if (ell < 1) return fail(FDMD_ERR_INVALID, "controls must be ell x %d with ell >= 1", T);
+  if (r_aug < 1 || r_aug > std::min<int64_t>(n + ell, T) || l_aug < r_aug || l_aug > T || l_aug > 256)
+    return fail(FDMD_ERR_INVALID, "dmdc_fit: need 1 <= r_aug <= l_aug <= min(T, 256)");
+  if (r < 1 || r > r_aug || r > std::min<int64_t>(n, T) || l < r || l > T || l > 256 || q < 0)
+    return fail(FDMD_ERR_INVALID, "dmdc_fit: need 1 <= r <= min(r_aug, l), l <= min(T, 256), q >= 0");
+  for (size_t i = 0; i < (size_t)ell * T; ++i)
+    if (!std::isfinite(controls_host[i])) return fail(FDMD_ERR_INVALID, "controls contain non-finite values");
+  TRY(set_device(ctx->device));
+  StreamLease lease(ctx);
+  Dev d(lease.s());
+  d.trim = true;
+  const size_t es = esize(states->dt);
+  const int64_t ld = states->ld;
+  // [S; Upsilon | 0]: the ell control rows below the n state rows
+  void* aug = d.alloc<unsigned char>((size_t)(n + ell) * ld * es);
+  if (!aug) return fail(FDMD_ERR_CUDA, "dmdc_fit: device allocation failed");
+  CUDA_TRY(cudaMemcpyAsync(aug, states->p, (size_t)n * ld * es, cudaMemcpyDeviceToDevice, d.s));
+  std::vector<unsigned char> tail((size_t)ell * ld * es, 0);
+  for (int c = 0; c < ell; ++c)
+    for (int j = 0; j < T; ++j) {
+      const double v = controls_host[(size_t)c * T + j];
+      if (states->dt == FDMD_F32)
+        reinterpret_cast<float*>(tail.data())[(size_t)c * ld + j] = (float)v;
+      else
+        reinterpret_cast<double*>(tail.data())[(size_t)c * ld + j] = v;
+    }
+  TRY(d.up(tail.data(), (char*)aug + (size_t)n * ld * es, tail.size()));
+  const Tall S{states->p, states->dt, ld};
+  Sketch f1, f2;
+  TRY(sketch(d, Tall{aug, states->dt, ld}, n + ell, T, m, l_aug, q, omega_aug_host, f1));
+  TRY(sketch(d, S, n, T, m, l, q, omega_out_host, f2, 1));
+  // U1^T U_hat = Ub1^T (Q1[:n]^T Q2) Ub2 with Q = buffer @ fix
+  const size_t gws = std::max(fdmd_tall_gram_workspace(n, l_aug, l), fdmd_tall_gram_workspace(n, 2 * r + 2, l));
+  double* Gd = d.alloc<double>((size_t)std::max(l_aug, 2 * r + 2) * l);
+  void* ws = d.alloc<unsigned char>(gws);
+  if (!Gd || !ws) return fail(FDMD_ERR_CUDA, "dmdc_fit: device allocation failed");
+  TRY(fdmd_tall_gram(f1.Q, FDMD_F64, FDMD_ROW, l_aug, f2.Q, FDMD_F64, FDMD_ROW, l, Gd, l, 0.0, n, l_aug, l, 0, ws, gws,
+                     d.s));
+  std::vector<double> M12((size_t)l_aug * l);
+  TRY(d.down(M12.data(), Gd, M12.size() * sizeof(double)));
+  if (!f1.fix.empty()) M12 = matmul(transpose(f1.fix, l_aug, l_aug), M12, l_aug, l_aug, l);
+  if (!f2.fix.empty()) M12 = matmul(M12, f2.fix, l_aug, l, l);
+  std::vector<double> Ub1((size_t)l_aug * r_aug), Ub2((size_t)l * r);
+  for (int i = 0; i < l_aug; ++i)
+    for (int k = 0; k < r_aug; ++k) Ub1[(size_t)i * r_aug + k] = f1.Ub[(size_t)i * l_aug + k];
+  for (int i = 0; i < l; ++i)
+    for (int k = 0; k < r; ++k) Ub2[(size_t)i * r + k] = f2.Ub[(size_t)i * l + k];
+  std::vector<double> U1tUh = matmul(transpose(Ub1, l_aug, r_aug), matmul(M12, Ub2, l_aug, l, r), r_aug, l_aug, r);
+  // control rows of U1: Q1[n:n+ell] (fix1 Ub1)
+  std::vector<double> qrows((size_t)ell * l_aug);
+  TRY(d.down(qrows.data(), f1.Q + (size_t)n * l_aug, qrows.size() * sizeof(double)));
+  const std::vector<double> R1 = lift_map(f1, r_aug);                       // l_aug x r_aug
+  const std::vector<double> U2 = matmul(qrows, R1, ell, l_aug, r_aug);     // ell x r_aug
+  // U_hat^T X' = Ub2^T (Q2^T S)[:, 1:]; core = U_hat^T X' V1 S1^-1
+  std::vector<double> VS((size_t)T * r_aug);
+  for (int j = 0; j < T; ++j)
+    for (int k = 0; k < r_aug; ++k) VS[(size_t)j * r_aug + k] = f1.V[(size_t)j * l_aug + k] / f1.s[k];
+  std::vector<double> UhtXp((size_t)r * T, 0.0);
+  for (int k = 0; k < r; ++k)
+    for (int i = 0; i < l; ++i) {
+      const double u = f2.Ub[(size_t)i * l + k];
+      for (int j = 0; j < T; ++j) UhtXp[(size_t)k * T + j] += u * f2.QtS[(size_t)i * m + 1 + j];
+    }
+  const std::vector<double> core = matmul(UhtXp, VS, r, T, r_aug);          // r x r_aug
+  const std::vector<double> Atil = matmul(core, U1tUh, r, r_aug, r);        // r x r
+  const std::vector<double> Btil = matmul(core, transpose(U2, ell, r_aug), r, r_aug, ell);   // r x ell
+  fdmd_model* model = new fdmd_model();
+  model->device = ctx->device;
+  model->n = n;
+  model->r = r;
+  model->step_dt = dt;
+  model->sigma.assign(f1.s.begin(), f1.s.begin() + r);
+  std::vector<cd> w;
+  CM W;
+  int rc = eig_checked(d, Atil, r, true, w, W);
+  PairPlan plan;
+  if (rc == FDMD_OK) {
+    plan = pair_plan(w);
+    const std::vector<double> VU = matmul(VS, U1tUh, T, r_aug, r);          // T x r
+    CM Cmap(T, r);
+    for (int j = 0; j < T; ++j)
+      for (int c = 0; c < r; ++c) {
+        cd acc = 0.0;
+        for (int k = 0; k < r; ++k) acc += VU[(size_t)j * r + k] * W(k, c);
+        Cmap(j, c) = acc;
+      }
+    model->lam = plan.lam;
+    rc = modes_pass(d, S, n, m, 1, Cmap, plan, states->dt, model);
+  }
+  std::vector<cd> red((size_t)r * ell, 0.0);
+  if (rc == FDMD_OK) rc = ensure_pinv(d, model);
+  if (rc == FDMD_OK) {
+    // reduced_b = pinv(phi) U_hat B~ / dt with pinv(phi) = P D^T: y = (D^T Q2) (fix2 Ub2) B~
+    const int nc = 2 * model->units;
+    rc = fdmd_tall_gram(model->raw, model->dt, FDMD_COL, model->ldr, f2.Q, FDMD_F64, FDMD_ROW, l, Gd, l, 0.0, n, nc, l,
+                        0, ws, gws, d.s);
+    std::vector<double> DtQ2((size_t)nc * l);
+    if (rc == FDMD_OK) rc = d.down(DtQ2.data(), Gd, DtQ2.size() * sizeof(double));
+    if (rc == FDMD_OK) {
+      const std::vector<double> y = matmul(matmul(DtQ2, lift_map(f2, r), nc, l, r), Btil, nc, r, ell);   // nc x ell
+      for (int a = 0; a < r; ++a)
+        for (int c = 0; c < ell; ++c) {
+          cd acc = 0.0;
+          for (int k = 0; k < nc; ++k) acc += model->pinv[(size_t)a * nc + k] * y[(size_t)k * ell + c];
+          red[(size_t)a * ell + c] = acc / dt;
+        }
+    }
+  }
+  if (rc != FDMD_OK) {
+    free_model(model);
+    return rc;
+  }
+  if (sigma_aug_host) std::copy(f1.s.begin(), f1.s.begin() + r_aug, sigma_aug_host);
+  if (lam_host)
+    for (int k = 0; k < r; ++k) lam_host[2 * k] = model->lam[k].real(), lam_host[2 * k + 1] = model->lam[k].imag();
+  if (reduced_b_host)
+    for (size_t i = 0; i < red.size(); ++i) reduced_b_host[2 * i] = red[i].real(), reduced_b_host[2 * i + 1] = red[i].imag();
   *out = model;
   return FDMD_OK;
 }
