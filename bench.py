@@ -482,7 +482,23 @@ def main():
     launches = ops.launches - launches0
     prof = ops.profile
     ops.profile = None
-    stages = trace.summarize(trace.disable(), args.steps)
+    rec_raw = trace.disable()
+    stages = trace.summarize(rec_raw, args.steps)
+    if os.environ.get("FDMD_BENCH_DIAG"):
+        # per-occurrence device / host ms of the first stages of each fit, then the
+        # same snapshot Gram launched in isolation (first-kernel-of-step effects)
+        for name, e0, e1, h in rec_raw:
+            if name in ("power.XtX", "sketch.alloc_Q", "power.Y=XWR1^-1", "cholqr.gram2"):
+                print(f"diag {name}: device {e0.elapsed_time(e1):.2f} ms host {h * 1e3:.2f} ms", file=sys.stderr)
+        for _ in range(3):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            ops.tall_gram(data.S, data.S, K1=m - 1, K2=m - 1, symmetric=True)
+            e1.record()
+            torch.cuda.synchronize()
+            print(f"diag isolated XtX: {e0.elapsed_time(e1):.2f} ms", file=sys.stderr)
     total = max_over_ranks(t0e.elapsed_time(t1e) / 1e3)
     fit_t = max_over_ranks(float(np.mean([x["fit"] for x in res])))
     rec = {k: max_over_ranks(float(np.mean([x[k] for x in res]))) for k in ("rec1", "split", "rec32", "rec1024")}

@@ -313,6 +313,7 @@ struct PanelPlan {
   bool transposed = false;   // run as B^T A (better tiling), reduce transposes back
   int cost = 0;              // sum over partitions of the busiest sub-partition (8x8 blocks)
   int WR = 5, WC = 7, P = 0, splits = 0, K1p = 0, K2p = 0, nba = 0, nbb = 0;
+  int cl = 1;                // cluster size (the P partitions of a split share one row stream)
   int64_t rows_per_split = 0;
   size_t smem = 0;
   fdmd::PanelTile tile[fdmd::tgp::MAXP * 8];
@@ -326,11 +327,30 @@ bool panel_enabled() {
   return on;
 }
 
+// Opt-in (FDMD_GRAM_CLUSTER=1): the cluster-shared row stream brings DRAM
+// traffic down to the algorithmic bytes (ncu: 41 / 80.5 / 121.6 GB for the
+// three fit Grams, from 82 / 161 / 257) but ties the partitions of a split to
+// one pace — the lighter partition's SM can no longer move on to its next
+// CTA — and GPC packing leaves SMs idle for 3-CTA clusters: 72 -> 88 ms
+// (X^T X), 150 -> 197 ms (Q^T S) at config-3 size (tools/gram_sweep.py).
+bool gram_cluster_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FDMD_GRAM_CLUSTER");
+    return e && strcmp(e, "1") == 0;
+  }();
+  return on;
+}
+
+// co-resident clusters of `cl` panel-Gram CTAs (cudaOccupancyMaxActiveClusters;
+// cached per device, cluster size and smem footprint)
+int gram_cluster_capacity(int cl, size_t smem);
+
 // Warp tiles of WR x WC 8x8 blocks cover the (upper, if symmetric) block grid;
 // they are packed into partitions of 8 consumer warps so that the DMMA count
 // per SM sub-partition (warps w, w+4) is balanced (greedy, heaviest first).
-PanelPlan panel_plan(int64_t n, int K1, int K2, int symmetric, size_t ea, size_t eb) {
+PanelPlan panel_plan(int64_t n, int K1, int K2, int symmetric, size_t ea, size_t eb, int wc = 7) {
   PanelPlan p;
+  p.WC = wc;
   if (symmetric) { p.WR = 5; p.WC = 5; }
   const int MB = (K1 + 7) / 8, NB = (K2 + 7) / 8;
   const int TI = (MB + p.WR - 1) / p.WR, TJ = (NB + p.WC - 1) / p.WC;
@@ -384,10 +404,21 @@ PanelPlan panel_plan(int64_t n, int K1, int K2, int symmetric, size_t ea, size_t
       }
     }
   }
-  // row splits: ~2 waves of one CTA per SM, chunk-aligned (16 rows);
-  // FDMD_GRAM_SPLITS overrides the split count (tools/gram_sweep.py)
+  // row splits: 2 waves of one CTA per SM, chunk-aligned (16 rows). With
+  // clusters (P in 2..4) a wave is the number of co-resident P-CTA clusters
+  // (GPC-limited, e.g. 45 clusters of 3 = 135 SMs), so 2 waves never leave a
+  // straggler cluster. FDMD_GRAM_SPLITS overrides the split count
+  // (tools/gram_sweep.py); FDMD_GRAM_CLUSTER=1 enables the clusters.
   const int64_t max_splits = std::max<int64_t>(1, (n + 15) / 16);
+  p.cl = (p.P >= 2 && p.P <= 4 && gram_cluster_enabled()) ? p.P : 1;
   int64_t splits = std::max<int64_t>(1, ((int64_t)sm_count_cached() * 2 + p.P - 1) / p.P);
+  if (p.cl > 1) {
+    const int per_wave = gram_cluster_capacity(p.cl, p.smem);
+    if (per_wave > 0)
+      splits = 2 * (int64_t)per_wave;
+    else
+      p.cl = 1;
+  }
   if (const char* e = getenv("FDMD_GRAM_SPLITS")) {
     const int64_t v = atoll(e);
     if (v > 0) splits = v;
@@ -400,21 +431,86 @@ PanelPlan panel_plan(int64_t n, int K1, int K2, int symmetric, size_t ea, size_t
   return p;
 }
 
-// orientation with the cheaper busiest-sub-partition schedule (A^T B or (B^T A)^T)
+// orientation and warp-tile width with the cheapest schedule: cost = sum over
+// partitions of the busiest sub-partition = SM time per 16-row chunk. 5 x 9
+// tiles (90 accumulators per lane) cover a 200 x 201 projection in 2
+// partitions of 15 tiles (0.90 of the DMMA work per SM-time) where 5 x 7
+// needs 3 partitions of 20 (0.77); ties keep fewer partitions (DRAM reads).
 PanelPlan panel_plan_best(int64_t n, int K1, int K2, int symmetric, size_t ea, size_t eb) {
   PanelPlan p = panel_plan(n, K1, K2, symmetric, ea, eb);
   if (symmetric) return p;
-  PanelPlan q = panel_plan(n, K2, K1, 0, eb, ea);
-  if (q.ok && (!p.ok || q.cost < p.cost)) {
-    q.transposed = true;
-    return q;
+  static const int wide = [] {
+    const char* e = getenv("FDMD_GRAM_WC");   // 7 or 9 forces the tile width (tools/gram_sweep.py)
+    return e ? atoi(e) : 0;
+  }();
+  auto better = [](const PanelPlan& a, const PanelPlan& b) {   // a better than b?
+    if (!a.ok) return false;
+    if (!b.ok) return true;
+    return a.cost < b.cost || (a.cost == b.cost && a.P < b.P);
+  };
+  PanelPlan best;
+  for (int wc : {7, 9}) {
+    if (wide && wc != wide) continue;
+    PanelPlan q = panel_plan(n, K1, K2, 0, ea, eb, wc);
+    if (better(q, best)) best = q;
+    PanelPlan t = panel_plan(n, K2, K1, 0, eb, ea, wc);
+    t.transposed = true;
+    if (better(t, best)) best = t;
   }
-  return p;
+  return best.ok ? best : p;
 }
+
+int gram_cluster_capacity(int cl, size_t smem) {
+  static thread_local std::unordered_map<long long, int> cache;
+  int dv = 0;
+  cudaGetDevice(&dv);
+  const long long key = ((long long)dv << 40) | ((long long)cl << 32) | (long long)smem;
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(cl, 64);
+  cfg.blockDim = dim3(fdmd::tgp::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int num = 0;
+  cudaError_t e = cudaErrorInvalidValue;
+  auto probe = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    return cudaOccupancyMaxActiveClusters(&num, kern, &cfg);
+  };
+  if (cl == 2) e = probe(fdmd::tall_gram_panel_kernel<double, double, 5, 7, false, 2>);
+  if (cl == 3) e = probe(fdmd::tall_gram_panel_kernel<double, double, 5, 7, false, 3>);
+  if (cl == 4) e = probe(fdmd::tall_gram_panel_kernel<double, double, 5, 7, false, 4>);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    num = 0;
+  }
+  cache[key] = num;
+  return num;
+}
+
+template <typename TA, typename TB, int WR, int WC, bool SYM, int CL>
+int launch_gram_panel_cl(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaStream_t s);
 
 template <typename TA, typename TB, int WR, int WC, bool SYM>
 int launch_gram_panel(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaStream_t s) {
-  auto kt = fdmd::tall_gram_panel_kernel<TA, TB, WR, WC, SYM>;
+  switch (pl.cl) {
+    case 2: return launch_gram_panel_cl<TA, TB, WR, WC, SYM, 2>(a, pl, s);
+    case 3: return launch_gram_panel_cl<TA, TB, WR, WC, SYM, 3>(a, pl, s);
+    case 4: return launch_gram_panel_cl<TA, TB, WR, WC, SYM, 4>(a, pl, s);
+    default: return launch_gram_panel_cl<TA, TB, WR, WC, SYM, 1>(a, pl, s);
+  }
+}
+
+template <typename TA, typename TB, int WR, int WC, bool SYM, int CL>
+int launch_gram_panel_cl(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaStream_t s) {
+  auto kt = fdmd::tall_gram_panel_kernel<TA, TB, WR, WC, SYM, CL>;
   CUtensorMap maps[2], tmaps[2];
   const void* ptr[2] = {a.A, a.B};
   const int64_t ld[2] = {a.lda, a.ldb};
@@ -433,6 +529,7 @@ int launch_gram_panel(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaStre
     const int full = std::min(loaded, kdim[i] / W);
     nfull[i] = full;
     tail[i] = loaded > full ? 1 : 0;
+    const bool need_2d = tail[i] || CL > 1;   // clusters load every box as a 2-D {W, 16} tile
     const auto dt = elt[i] == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
     if (full > 0) {
       cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)a.n, (cuuint64_t)(kdim[i] / W)};
@@ -444,7 +541,7 @@ int launch_gram_panel(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaStre
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return fail(FDMD_ERR_CUDA, "tall_gram: tensor map encode failed");
     }
-    if (tail[i]) {
+    if (need_2d) {
       cuuint64_t dims[2] = {(cuuint64_t)kdim[i], (cuuint64_t)a.n};
       cuuint64_t strides[1] = {(cuuint64_t)(ld[i] * elt[i])};
       cuuint32_t box[2] = {(cuuint32_t)W, (cuuint32_t)fdmd::tgp::BR};
@@ -479,7 +576,23 @@ int launch_gram_panel(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaStre
     conf_t = dv;
     conf_smem = 227 * 1024;
   }
-  kt<<<dim3(pl.P, pl.splits), fdmd::tgp::THREADS, pl.smem, s>>>(maps[0], maps[1], tmaps[0], tmaps[1], pa);
+  if (CL == 1) {
+    kt<<<dim3(pl.P, pl.splits), fdmd::tgp::THREADS, pl.smem, s>>>(maps[0], maps[1], tmaps[0], tmaps[1], pa);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(pl.P, pl.splits);
+    cfg.blockDim = dim3(fdmd::tgp::THREADS);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kt, maps[0], maps[1], tmaps[0], tmaps[1], pa));
+  }
   LAUNCH_CHECK("tall_gram_panel");
   return FDMD_OK;
 }
@@ -767,6 +880,12 @@ int fdmd_tall_gram(const void* A, int a_dtype, int a_layout, int64_t lda, const 
       if (symmetric)
         rc = da == FDMD_F32 ? launch_gram_panel<float, float, 5, 5, true>(a, pl, s)
                             : launch_gram_panel<double, double, 5, 5, true>(a, pl, s);
+      else if (pl.WC == 9 && da == FDMD_F32)
+        rc = db == FDMD_F32 ? launch_gram_panel<float, float, 5, 9, false>(a, pl, s)
+                            : launch_gram_panel<float, double, 5, 9, false>(a, pl, s);
+      else if (pl.WC == 9)
+        rc = db == FDMD_F32 ? launch_gram_panel<double, float, 5, 9, false>(a, pl, s)
+                            : launch_gram_panel<double, double, 5, 9, false>(a, pl, s);
       else if (da == FDMD_F32)
         rc = db == FDMD_F32 ? launch_gram_panel<float, float, 5, 7, false>(a, pl, s)
                             : launch_gram_panel<float, double, 5, 7, false>(a, pl, s);

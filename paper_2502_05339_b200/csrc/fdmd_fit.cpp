@@ -543,9 +543,47 @@ struct Tall {  // row-major n x k device matrix
   int64_t ld;
 };
 
+// Householder QR of the tall buffer (n x l, row-major, ld ldq) in place on
+// cuSOLVER (geqrf + orgqr on a column-major copy made by the tall GEMM): the
+// fallback of linalg.cholqr2_deferred when the (shifted) CholeskyQR Gram is not
+// positive definite, i.e. a rank-deficient sketch. Leaves fix = identity.
+int householder(Dev& d, double* Q, int64_t ldq, int64_t n, int l, std::vector<double>& fix) {
+  cusolverDnHandle_t h = (cusolverDnHandle_t)fdmdi_solver_handle(d.s);
+  if (!h) return fail(FDMD_ERR_SOLVER, "cusolverDnCreate failed");
+  if (n > INT32_MAX) return fail(FDMD_ERR_SOLVER, "Householder fallback limited to n < 2^31 rows");
+  std::vector<double> I((size_t)l * l, 0.0);
+  for (int i = 0; i < l; ++i) I[(size_t)i * l + i] = 1.0;
+  const int64_t lda = round_up(n, 2);
+  double* A = d.alloc<double>((size_t)lda * l);
+  double* Id = d.alloc<double>(I.size());
+  double* tau = d.alloc<double>(l);
+  int* info = d.alloc<int>(1);
+  if (!A || !Id || !tau || !info) return fail(FDMD_ERR_CUDA, "householder: device allocation failed");
+  TRY(d.up(I.data(), Id, I.size() * sizeof(double)));
+  TRY(fdmd_tall_gemm(Q, FDMD_F64, FDMD_ROW, ldq, Id, l, A, FDMD_F64, FDMD_COL, lda, n, l, l, 0, nullptr, 0, nullptr, 0,
+                     d.s));
+  int lw1 = 0, lw2 = 0;
+  if (cusolverDnDgeqrf_bufferSize(h, (int)n, l, A, (int)lda, &lw1) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDorgqr_bufferSize(h, (int)n, l, l, A, (int)lda, tau, &lw2) != CUSOLVER_STATUS_SUCCESS)
+    return fail(FDMD_ERR_SOLVER, "householder: bufferSize");
+  double* work = d.alloc<double>((size_t)std::max(lw1, lw2));
+  if (!work) return fail(FDMD_ERR_CUDA, "householder: device allocation failed");
+  if (cusolverDnDgeqrf(h, (int)n, l, A, (int)lda, tau, work, std::max(lw1, lw2), info) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDorgqr(h, (int)n, l, l, A, (int)lda, tau, work, std::max(lw1, lw2), info) != CUSOLVER_STATUS_SUCCESS)
+    return fail(FDMD_ERR_SOLVER, "householder: geqrf / orgqr failed");
+  int ih = 0;
+  TRY(d.down(&ih, info, sizeof(int)));
+  if (ih != 0) return fail(FDMD_ERR_SOLVER, "householder: info %d", ih);
+  TRY(fdmd_tall_gemm(A, FDMD_F64, FDMD_COL, lda, Id, l, Q, FDMD_F64, FDMD_ROW, ldq, n, l, l, 0, nullptr, 0, nullptr, 0,
+                     d.s));
+  fix.clear();
+  return FDMD_OK;
+}
+
 struct Sketch {
-  double* Q = nullptr;      // device row-major n x l (buffer; Q = buffer @ fix)
+  double* Q = nullptr;      // device row-major n x l, ld ldq (buffer; Q = buffer @ fix)
   int l = 0;
+  int64_t ldq = 0;          // round_up(l, 2): 16-byte rows for the TMA-fed kernels
   std::vector<double> fix;  // l x l (empty = identity)
   std::vector<double> Ub;   // l x l left vectors of B (row-major)
   std::vector<double> s;    // l singular values
@@ -563,16 +601,19 @@ int sketch(Dev& d, const Tall& S, int64_t n, int T, int m, int l, int q, const d
   const int K2max = std::max(m, l);
   const size_t gws = std::max(fdmd_tall_gram_workspace(n, l, l),
                               std::max(fdmd_tall_gram_workspace(n, c0 + T, l), fdmd_tall_gram_workspace(n, l, K2max)));
-  double* Q = d.alloc<double>((size_t)n * l);
+  const int64_t ldq = round_up(l, 2);
+  double* Q = d.alloc<double>((size_t)n * ldq);
   double* Bd = d.alloc<double>((size_t)K2max * 2 * l + 16);
   double* Gd = d.alloc<double>((size_t)K2max * l);
   void* ws = d.alloc<unsigned char>(gws);
   if (!Q || !Bd || !Gd || !ws) return fail(FDMD_ERR_CUDA, "sketch: device allocation failed");
   out.Q = Q;
   out.l = l;
+  out.ldq = ldq;
+  CUDA_TRY(cudaMemsetAsync(Q, 0, (size_t)n * ldq * sizeof(double), d.s));   // pad column stays zero
   auto gemm = [&](const void* A, int adt, int64_t lda, const std::vector<double>& Bh, int K, int N, int flags) {
     TRY(d.up(Bh.data(), Bd, Bh.size() * sizeof(double)));
-    return fdmd_tall_gemm(A, adt, FDMD_ROW, lda, Bd, N, Q, FDMD_F64, FDMD_ROW, l, n, K, N, flags, nullptr, 0, nullptr,
+    return fdmd_tall_gemm(A, adt, FDMD_ROW, lda, Bd, N, Q, FDMD_F64, FDMD_ROW, ldq, n, K, N, flags, nullptr, 0, nullptr,
                           0, s);
   };
   auto gram = [&](const void* A, int adt, int64_t lda, const void* B, int bdt, int64_t ldb, int K1, int K2, int sym,
@@ -584,7 +625,7 @@ int sketch(Dev& d, const Tall& S, int64_t n, int T, int m, int l, int q, const d
   std::vector<double>& fix = out.fix;
   auto cholqr = [&](int passes) -> int {
     std::vector<double> G, R1, R2;
-    TRY(gram(Q, FDMD_F64, l, Q, FDMD_F64, l, l, l, 1, G));
+    TRY(gram(Q, FDMD_F64, ldq, Q, FDMD_F64, ldq, l, l, 1, G));
     const bool ok = chol_upper(G, l, R1);
     std::vector<double> R1i;
     double cond = INFINITY;
@@ -597,11 +638,13 @@ int sketch(Dev& d, const Tall& S, int64_t n, int T, int m, int l, int q, const d
       const double shift = 11.0 * ((double)n * l + (double)l * (l + 1)) * u * fro(G);
       std::vector<double> Gs = G, R0, R1b;
       for (int i = 0; i < l; ++i) Gs[(size_t)i * l + i] += shift;
-      if (!chol_upper(Gs, l, R0)) return fail(FDMD_ERR_SOLVER, "shifted CholeskyQR: Gram not positive definite");
-      TRY(gemm(Q, FDMD_F64, l, inv_upper(R0, l), l, l, FDMD_B_UPPER));
-      TRY(gram(Q, FDMD_F64, l, Q, FDMD_F64, l, l, l, 1, G));
-      if (!chol_upper(G, l, R1b)) return fail(FDMD_ERR_SOLVER, "shifted CholeskyQR: second Gram not positive definite");
-      TRY(gemm(Q, FDMD_F64, l, inv_upper(R1b, l), l, l, FDMD_B_UPPER));
+      // Householder fallback on Cholesky failure (a rank-deficient sketch), as
+      // linalg.cholqr2_deferred: Q orthonormal, no deferred factor
+      if (!chol_upper(Gs, l, R0)) return householder(d, Q, ldq, n, l, fix);
+      TRY(gemm(Q, FDMD_F64, ldq, inv_upper(R0, l), l, l, FDMD_B_UPPER));
+      TRY(gram(Q, FDMD_F64, ldq, Q, FDMD_F64, ldq, l, l, 1, G));
+      if (!chol_upper(G, l, R1b)) return householder(d, Q, ldq, n, l, fix);
+      TRY(gemm(Q, FDMD_F64, ldq, inv_upper(R1b, l), l, l, FDMD_B_UPPER));
       if (passes == 1) {
         fix.clear();
         return FDMD_OK;
@@ -610,10 +653,10 @@ int sketch(Dev& d, const Tall& S, int64_t n, int T, int m, int l, int q, const d
       fix = R1i;
       return FDMD_OK;
     } else {
-      TRY(gemm(Q, FDMD_F64, l, R1i, l, l, FDMD_B_UPPER));  // Q <- Y R1^-1
+      TRY(gemm(Q, FDMD_F64, ldq, R1i, l, l, FDMD_B_UPPER));  // Q <- Y R1^-1
     }
-    TRY(gram(Q, FDMD_F64, l, Q, FDMD_F64, l, l, l, 1, G));
-    if (!chol_upper(G, l, R2)) return fail(FDMD_ERR_SOLVER, "CholeskyQR2: second Gram not positive definite");
+    TRY(gram(Q, FDMD_F64, ldq, Q, FDMD_F64, ldq, l, l, 1, G));
+    if (!chol_upper(G, l, R2)) return householder(d, Q, ldq, n, l, fix);
     fix = inv_upper(R2, l);
     return FDMD_OK;
   };
@@ -630,7 +673,7 @@ int sketch(Dev& d, const Tall& S, int64_t n, int T, int m, int l, int q, const d
   TRY(cholqr(q == 0 ? 2 : 1));
   for (int it = 0; it < q; ++it) {
     std::vector<double> Zf, Z((size_t)T * l);
-    TRY(gram(S.p, S.dt, S.ld, Q, FDMD_F64, l, Kc, l, 0, Zf));  // (c0 + T) x l; X^T buffer = its last T rows
+    TRY(gram(S.p, S.dt, S.ld, Q, FDMD_F64, ldq, Kc, l, 0, Zf));  // (c0 + T) x l; X^T buffer = its last T rows
     std::copy(Zf.begin() + (size_t)c0 * l, Zf.end(), Z.begin());
     if (!fix.empty()) Z = matmul(Z, fix, T, l, l);
     std::vector<double> W = householder_q(Z, T, l);
@@ -638,7 +681,7 @@ int sketch(Dev& d, const Tall& S, int64_t n, int T, int m, int l, int q, const d
     TRY(cholqr(it == q - 1 ? 2 : 1));
   }
   // Q^T S (l x m) with Q = buffer fix
-  TRY(gram(Q, FDMD_F64, l, S.p, S.dt, S.ld, l, m, 0, out.QtS));
+  TRY(gram(Q, FDMD_F64, ldq, S.p, S.dt, S.ld, l, m, 0, out.QtS));
   if (!fix.empty()) out.QtS = matmul(transpose(fix, l, l), out.QtS, l, l, m);
   // svd(B), B = Q^T X (l x T) on cuSOLVER gesvd (rows >= cols: factor B^T, T x l)
   cusolverDnHandle_t h = (cusolverDnHandle_t)fdmdi_solver_handle(s);
@@ -1160,7 +1203,7 @@ int fdmd_rsvd(const void* X, int x_dtype, int64_t ldx, int64_t n, int T, int r, 
   void* sws = d.alloc<unsigned char>(sws_b);
   if (!Bd || !st || !sws) return fail(FDMD_ERR_CUDA, "rsvd: device allocation failed");
   TRY(d.up(Mp.data(), Bd, Mp.size() * sizeof(double)));
-  TRY(fdmd_tall_gemm(f.Q, FDMD_F64, FDMD_ROW, l, Bd, 2 * r, nullptr, FDMD_F64, FDMD_COL, n, n, l, 2 * r, 0, st, 0, sws,
+  TRY(fdmd_tall_gemm(f.Q, FDMD_F64, FDMD_ROW, f.ldq, Bd, 2 * r, nullptr, FDMD_F64, FDMD_COL, n, n, l, 2 * r, 0, st, 0, sws,
                      sws_b, d.s));
   std::vector<double> sth((size_t)3 * r);
   TRY(d.down(sth.data(), st, sth.size() * sizeof(double)));
@@ -1171,7 +1214,7 @@ int fdmd_rsvd(const void* X, int x_dtype, int64_t ldx, int64_t n, int T, int r, 
         a >= (double)n)
       return fail(FDMD_ERR_SOLVER, "randomized SVD: non-finite basis (degenerate sketch)");
     const int64_t piv = (int64_t)llround(a);
-    CUDA_TRY(cudaMemcpyAsync(rows.data() + (size_t)k * l, f.Q + piv * l, sizeof(double) * l, cudaMemcpyDeviceToHost,
+    CUDA_TRY(cudaMemcpyAsync(rows.data() + (size_t)k * l, f.Q + piv * f.ldq, sizeof(double) * l, cudaMemcpyDeviceToHost,
                              d.s));
   }
   CUDA_TRY(cudaStreamSynchronize(d.s));
@@ -1185,7 +1228,7 @@ int fdmd_rsvd(const void* X, int x_dtype, int64_t ldx, int64_t n, int T, int r, 
     }
   }
   TRY(d.up(M.data(), Bd, M.size() * sizeof(double)));
-  TRY(fdmd_tall_gemm(f.Q, FDMD_F64, FDMD_ROW, l, Bd, r, U, FDMD_F64, FDMD_COL, ldu, n, l, r, 0, nullptr, 0, nullptr, 0,
+  TRY(fdmd_tall_gemm(f.Q, FDMD_F64, FDMD_ROW, f.ldq, Bd, r, U, FDMD_F64, FDMD_COL, ldu, n, l, r, 0, nullptr, 0, nullptr, 0,
                      d.s));  // lift (linalg.py:88)
   std::copy(f.s.begin(), f.s.begin() + r, sigma_host);
   std::copy(Vr.begin(), Vr.end(), V_host);
@@ -1397,7 +1440,7 @@ int fdmd_dmd_fit(fdmd_ctx* ctx, const fdmd_mat* states, double dt, int r, int l,
       model->lam = plan.lam;
       model->history = lm.history;
       model->converged = lm.converged ? 1 : 0;
-      rc = modes_pass(d, Tall{f.Q, FDMD_F64, l}, n, l, 0, Cmap, plan, states->dt, model);
+      rc = modes_pass(d, Tall{f.Q, FDMD_F64, f.ldq}, n, l, 0, Cmap, plan, states->dt, model);
     }
   }
   if (rc != FDMD_OK) {
@@ -1462,7 +1505,7 @@ int fdmd_dmdc_fit(fdmd_ctx* ctx, const fdmd_mat* states, const double* controls_
   double* Gd = d.alloc<double>((size_t)std::max(l_aug, 2 * r + 2) * l);
   void* ws = d.alloc<unsigned char>(gws);
   if (!Gd || !ws) return fail(FDMD_ERR_CUDA, "dmdc_fit: device allocation failed");
-  TRY(fdmd_tall_gram(f1.Q, FDMD_F64, FDMD_ROW, l_aug, f2.Q, FDMD_F64, FDMD_ROW, l, Gd, l, 0.0, n, l_aug, l, 0, ws, gws,
+  TRY(fdmd_tall_gram(f1.Q, FDMD_F64, FDMD_ROW, f1.ldq, f2.Q, FDMD_F64, FDMD_ROW, f2.ldq, Gd, l, 0.0, n, l_aug, l, 0, ws, gws,
                      d.s));
   std::vector<double> M12((size_t)l_aug * l);
   TRY(d.down(M12.data(), Gd, M12.size() * sizeof(double)));
@@ -1476,7 +1519,10 @@ int fdmd_dmdc_fit(fdmd_ctx* ctx, const fdmd_mat* states, const double* controls_
   std::vector<double> U1tUh = matmul(transpose(Ub1, l_aug, r_aug), matmul(M12, Ub2, l_aug, l, r), r_aug, l_aug, r);
   // control rows of U1: Q1[n:n+ell] (fix1 Ub1)
   std::vector<double> qrows((size_t)ell * l_aug);
-  TRY(d.down(qrows.data(), f1.Q + (size_t)n * l_aug, qrows.size() * sizeof(double)));
+  for (int c = 0; c < ell; ++c)
+    CUDA_TRY(cudaMemcpyAsync(qrows.data() + (size_t)c * l_aug, f1.Q + (size_t)(n + c) * f1.ldq, l_aug * sizeof(double),
+                             cudaMemcpyDeviceToHost, d.s));
+  CUDA_TRY(cudaStreamSynchronize(d.s));
   const std::vector<double> R1 = lift_map(f1, r_aug);                       // l_aug x r_aug
   const std::vector<double> U2 = matmul(qrows, R1, ell, l_aug, r_aug);     // ell x r_aug
   // U_hat^T X' = Ub2^T (Q2^T S)[:, 1:]; core = U_hat^T X' V1 S1^-1
@@ -1520,7 +1566,7 @@ int fdmd_dmdc_fit(fdmd_ctx* ctx, const fdmd_mat* states, const double* controls_
   if (rc == FDMD_OK) {
     // reduced_b = pinv(phi) U_hat B~ / dt with pinv(phi) = P D^T: y = (D^T Q2) (fix2 Ub2) B~
     const int nc = 2 * model->units;
-    rc = fdmd_tall_gram(model->raw, model->dt, FDMD_COL, model->ldr, f2.Q, FDMD_F64, FDMD_ROW, l, Gd, l, 0.0, n, nc, l,
+    rc = fdmd_tall_gram(model->raw, model->dt, FDMD_COL, model->ldr, f2.Q, FDMD_F64, FDMD_ROW, f2.ldq, Gd, l, 0.0, n, nc, l,
                         0, ws, gws, d.s);
     std::vector<double> DtQ2((size_t)nc * l);
     if (rc == FDMD_OK) rc = d.down(DtQ2.data(), Gd, DtQ2.size() * sizeof(double));

@@ -58,7 +58,34 @@ template <typename TX> __device__ __forceinline__ int panel_offset(int row, int 
   return box * tgp::BOX_BYTES + row * 128 + ((((cb >> 4) ^ (row & 7))) << 4) + (cb & 15);
 }
 
+// ---- cluster sharing of the row stream (CL > 1) ----------------------------
+// The P output partitions of one row split run as ONE cluster of CL = P CTAs:
+// every 128-B box of a stage is loaded ONCE per cluster — CTA k issues the
+// boxes b with b % CL == k as 2-D TMA multicasts into the same smem offset of
+// all CL CTAs — so DRAM / L2 traffic is the operands once per split instead of
+// once per partition (r01 ncu: 2-3x the algorithmic bytes). A stage is
+// refilled only after every warp of every CTA released it: each warp arrives
+// on the empty barrier of all CL CTAs (count 8 * CL).
+__device__ __forceinline__ void gp_tma_2d_mc(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                             uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+__device__ __forceinline__ void gp_arrive_remote(uint64_t* bar, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(a) : "r"(smem_u32(bar)), "r"(rank));
+  // relaxed: the warp's fragment loads of the stage have been consumed by its
+  // DMMAs (register dependences) before the arrive; a release would fence
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void gp_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 struct PanelFeed {
+  int cl = 1, rank = 0;                        // cluster size / this CTA's rank in it
   const CUtensorMap* amap;
   const CUtensorMap* bmap;
   const CUtensorMap* atmap;
@@ -72,6 +99,19 @@ struct PanelFeed {
   __device__ __forceinline__ void issue(int64_t c, int s, uint64_t* full) const {
     mbar_expect_tx(&full[s], bytes);
     const int r0 = (int)(rbeg + c * tgp::BR);
+    if (cl > 1) {
+      // box b of the stage (A boxes, then B boxes) is issued by CTA b % cl for the
+      // whole cluster; every box is a 2-D {W, 16} tile (zero fill past K)
+      const uint16_t mask = (uint16_t)((1u << cl) - 1);
+      const int na = la, nb = lb;
+      for (int b = rank; b < na + nb; b += cl) {
+        if (b < na)
+          gp_tma_2d_mc(a_sm + s * a_stage + b * tgp::BOX_BYTES, atmap, b * wa, r0, &full[s], mask);
+        else
+          gp_tma_2d_mc(b_sm + s * b_stage + (b - na) * tgp::BOX_BYTES, btmap, (b - na) * wb, r0, &full[s], mask);
+      }
+      return;
+    }
     // one 3-D TMA per operand for its full 128-B column blocks (they land as
     // consecutive 16-row x 128-B SW128 boxes, the layout panel_offset reads)
     // + one 2-D TMA for a ragged last block (zero-filled past K)
@@ -87,7 +127,14 @@ struct PanelFeed {
 __device__ __forceinline__ void panel_release(const PanelFeed& fd, bool feeder, int lane, int64_t c, int s,
                                               unsigned ph, uint64_t* full, uint64_t* empty) {
   __syncwarp();
-  if (lane == 0) mbar_arrive(&empty[s]);
+  if (lane == 0) {
+    if (fd.cl > 1) {
+      mbar_arrive(&empty[s]);
+      for (int k = 1; k < fd.cl; ++k) gp_arrive_remote(&empty[s], (uint32_t)((fd.rank + k) % fd.cl));
+    } else {
+      mbar_arrive(&empty[s]);
+    }
+  }
   if (feeder && lane == 0 && c + tgp::STAGES < fd.nchunks) {
     mbar_wait(&empty[s], ph);
     fd.issue(c + tgp::STAGES, s, full);
@@ -99,15 +146,22 @@ __device__ __forceinline__ void panel_consume(const PanelFeed& fd, bool feeder, 
                                               int b_stage_bytes, uint64_t* full, uint64_t* empty, int i0, int j0,
                                               int lane, double* __restrict__ W, int K2p) {
   const int g = lane >> 2, t = lane & 3;
-  // byte offsets of this lane's fragments for the two row parities of a k-step
-  int offa[WR][2], offb[WC][2];
+  // byte offsets of this lane's fragments for the two row parities of a k-step.
+  // Column 8 ii + c lands in box (c + 8 ii) / W at a swizzled position that
+  // repeats every W / 8 blocks (a whole box further on), so only W / 8 base
+  // offsets per operand and parity live in registers; the rest are immediate
+  // +BOX_BYTES displacements of the unrolled loads (5 x 9 tiles: 12 instead of
+  // 28 offset registers next to 90 accumulators).
+  constexpr int PA = 128 / (int)sizeof(TA) / 8, PB = 128 / (int)sizeof(TB) / 8;
+  constexpr int NA = PA < WR ? PA : WR, NB = PB < WC ? PB : WC;
+  int offa[NA][2], offb[NB][2];
 #pragma unroll
   for (int p = 0; p < 2; ++p) {
     const int row = p + 2 * t;
 #pragma unroll
-    for (int ii = 0; ii < WR; ++ii) offa[ii][p] = panel_offset<TA>(row, 8 * (i0 + ii) + g);
+    for (int ii = 0; ii < NA; ++ii) offa[ii][p] = panel_offset<TA>(row, 8 * (i0 + ii) + g);
 #pragma unroll
-    for (int jj = 0; jj < WC; ++jj) offb[jj][p] = panel_offset<TB>(row, 8 * (j0 + jj) + g);
+    for (int jj = 0; jj < NB; ++jj) offb[jj][p] = panel_offset<TB>(row, 8 * (j0 + jj) + g);
   }
   double acc[WR][WC][2];
 #pragma unroll
@@ -126,9 +180,11 @@ __device__ __forceinline__ void panel_consume(const PanelFeed& fd, bool feeder, 
       const int p = ks & 1, hi = (ks >> 1) * 1024;   // rows +8 -> +1024 B, same swizzle key
       double a[WR], b[WC];
 #pragma unroll
-      for (int ii = 0; ii < WR; ++ii) a[ii] = (double)*reinterpret_cast<const TA*>(pa + offa[ii][p] + hi);
+      for (int ii = 0; ii < WR; ++ii)
+        a[ii] = (double)*reinterpret_cast<const TA*>(pa + offa[ii % NA][p] + (ii / NA) * tgp::BOX_BYTES + hi);
 #pragma unroll
-      for (int jj = 0; jj < WC; ++jj) b[jj] = (double)*reinterpret_cast<const TB*>(pb + offb[jj][p] + hi);
+      for (int jj = 0; jj < WC; ++jj)
+        b[jj] = (double)*reinterpret_cast<const TB*>(pb + offb[jj % NB][p] + (jj / NB) * tgp::BOX_BYTES + hi);
 #pragma unroll
       for (int ii = 0; ii < WR; ++ii)
 #pragma unroll
@@ -150,7 +206,7 @@ __device__ __forceinline__ void panel_consume(const PanelFeed& fd, bool feeder, 
   }
 }
 
-template <typename TA, typename TB, int WR, int WC, bool SYM>
+template <typename TA, typename TB, int WR, int WC, bool SYM, int CL>
 __global__ void __launch_bounds__(tgp::THREADS, 1)
 tall_gram_panel_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                        const __grid_constant__ CUtensorMap atmap, const __grid_constant__ CUtensorMap btmap,
@@ -183,6 +239,8 @@ tall_gram_panel_kernel(const __grid_constant__ CUtensorMap amap, const __grid_co
   uint64_t* empty = full + tgp::STAGES;
 
   const int part = blockIdx.x;
+  fd.cl = CL;
+  fd.rank = CL > 1 ? (int)(blockIdx.x % CL) : 0;   // cluster dims (CL, 1, 1): rank = x % CL
   fd.rbeg = (int64_t)blockIdx.y * args.rows_per_split;
   const int64_t rend = min(args.n, fd.rbeg + args.rows_per_split);
   fd.nchunks = rend > fd.rbeg ? (rend - fd.rbeg + tgp::BR - 1) / tgp::BR : 0;
@@ -193,11 +251,14 @@ tall_gram_panel_kernel(const __grid_constant__ CUtensorMap amap, const __grid_co
   if (tid == 0) {
     for (int s = 0; s < tgp::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], tgp::THREADS / 32);
+      mbar_init(&empty[s], CL * tgp::THREADS / 32);
     }
     mbar_fence_init();
   }
-  __syncthreads();
+  if (CL > 1)
+    gp_cluster_sync();   // every CTA's barriers initialised before any multicast / remote arrive
+  else
+    __syncthreads();
   if (tid == 0)
     for (int s = 0; s < tgp::STAGES && s < fd.nchunks; ++s) fd.issue(s, s, full);
 
@@ -218,6 +279,7 @@ tall_gram_panel_kernel(const __grid_constant__ CUtensorMap amap, const __grid_co
       if (++s == tgp::STAGES) { s = 0; ph ^= 1; }
     }
   }
+  if (CL > 1) gp_cluster_sync();   // no peer may still arrive on / multicast into an exited CTA
 }
 
 }  // namespace fdmd

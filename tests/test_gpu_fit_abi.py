@@ -216,18 +216,47 @@ def test_config3_shape_optdmd_abi(abi, config_golden):
         abi[0].fdmd_model_free(model)
 
 
-@pytest.mark.parametrize("noise", [0.0, 1e-4])
+def _controlled(n, pairs, ell, m, seed, noise):
+    """x_{j+1} = A x_j + B u_j with A = Psi Ablk Psi^T (known spectrum) and B in
+    A's range — as BASELINE config 2 projects its control fields (synth.py). A
+    B outside range(A) would add exact-zero eigenvalues whose exact-DMD modes
+    Phi = X' V S^-1 U1^T U_hat W vanish (Phi = U_hat W Lambda), leaving
+    pinv(Phi) undefined in those directions — for the reference algorithm too."""
+    rng = np.random.default_rng(seed)
+    Psi = np.linalg.qr(rng.standard_normal((n, 2 * pairs)))[0]
+    rho = rng.uniform(0.9, 0.999, pairs)
+    th = rng.uniform(0.05, 1.0, pairs)
+    Ab = np.zeros((2 * pairs, 2 * pairs))
+    eigs = []
+    for i in range(pairs):
+        c, s_ = np.cos(th[i]), np.sin(th[i])
+        Ab[2 * i:2 * i + 2, 2 * i:2 * i + 2] = rho[i] * np.array([[c, -s_], [s_, c]])
+        eigs += [rho[i] * np.exp(1j * th[i]), rho[i] * np.exp(-1j * th[i])]
+    Bc = rng.standard_normal((2 * pairs, ell)) / np.sqrt(2 * pairs)
+    U = rng.standard_normal((ell, m - 1))
+    Z = np.empty((2 * pairs, m))
+    Z[:, 0] = rng.standard_normal(2 * pairs)
+    for j in range(m - 1):
+        Z[:, j + 1] = Ab @ Z[:, j] + Bc @ U[:, j]
+    X = Psi @ Z
+    if noise:
+        X = X + noise * rng.standard_normal(X.shape)
+    return X, U, np.asarray(eigs)
+
+
+@pytest.mark.parametrize("noise", [0.0, 1e-5])
 def test_dmdc_abi_against_oracle_and_truth(abi, noise):
-    """fdmd_dmdc_fit on the oracle's controlled system (x_{j+1} = A x_j + B u_j,
-    known spectrum): eigenvalues against the oracle restatement (same Omegas),
-    the generator's spectrum, and a controlled rollout z_{k+1} = lam z_k +
-    reduced_b u_k dt (runtime.step_forced, runtime.py:164-200) against the data."""
+    """fdmd_dmdc_fit on a controlled system with known spectrum: eigenvalues
+    against the oracle restatement (oracle.dmdc_fit, same Omegas) and the
+    generator, and a controlled rollout z_{k+1} = lam z_k + reduced_b u_k dt
+    (runtime.step_forced, runtime.py:164-200) through the model handle against
+    the data."""
     import flowdmd_oracle as orc
     L, ctx = abi
     n, pairs, ell, m = 6000, 5, 3, 61
-    X, U, true_eigs, Bf = orc.controlled_system(n, pairs, ell, m, seed=7, noise=noise)
+    X, U, true_eigs = _controlled(n, pairs, ell, m, seed=7, noise=noise)
     T = m - 1
-    r_aug, r = 2 * pairs + 2 * ell, 2 * pairs + ell
+    r_aug, r = 2 * pairs + ell, 2 * pairs
     l_aug, l = r_aug + 10, r + 10
     om_aug = np.random.default_rng(5).standard_normal((T, l_aug))
     om_out = np.random.default_rng(6).standard_normal((T, l))
@@ -236,8 +265,8 @@ def test_dmdc_abi_against_oracle_and_truth(abi, noise):
     sig, lam, red = np.zeros(r_aug), np.zeros(2 * r), np.zeros(2 * r * ell)
     model = vp()
     try:
-        chk(L, L.fdmd_dmdc_fit(ctx, M, _p(np.ascontiguousarray(U, dtype=np.float64)), ell, 1.0, r_aug, l_aug, r, l, 1,
-                               _p(om_aug), _p(om_out), _p(sig), _p(lam), _p(red), ctypes.byref(model)))
+        chk(L, L.fdmd_dmdc_fit(ctx, M, _p(U), ell, 1.0, r_aug, l_aug, r, l, 1, _p(om_aug), _p(om_out), _p(sig),
+                               _p(lam), _p(red), ctypes.byref(model)))
     finally:
         L.fdmd_mat_free(M)
     try:
@@ -245,9 +274,8 @@ def test_dmdc_abi_against_oracle_and_truth(abi, noise):
         red = (red[0::2] + 1j * red[1::2]).reshape(r, ell)
         np.testing.assert_allclose(sig, ref["sigma_aug"][:r_aug], rtol=1e-9)
         assert match_eigs(lam, ref["lam"]) <= 1e-8
-        if noise == 0.0:
-            d = np.array([np.abs(lam - t).min() for t in true_eigs])
-            assert d.max() <= 1e-7, d.max()
+        d = np.array([np.abs(lam - t).min() for t in true_eigs])
+        assert d.max() <= (1e-7 if noise == 0.0 else 1e-3), d.max()
         # controlled rollout through the model handle, from the data's first state
         z = encode(abi, model, X[:, 0], r)
         worst = 0.0
@@ -255,7 +283,7 @@ def test_dmdc_abi_against_oracle_and_truth(abi, noise):
             z = lam * z + red @ U[:, k]
             fr = decode(abi, model, z, n)[0]
             worst = max(worst, rel(fr, X[:, k + 1]))
-        assert worst <= (1e-6 if noise == 0.0 else 5e-2), worst
+        assert worst <= (1e-6 if noise == 0.0 else 1e-3), worst
     finally:
         L.fdmd_model_free(model)
 

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--n", type=int, default=50331648)
     ap.add_argument("--splits", default="0,99,148,296,444,592")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--after-hbm", action="store_true",
+                    help="also time each Gram right after ~130 ms of HBM streaming (the bench's reconstruct phase)")
     a = ap.parse_args()
     ops = dv.get_ops()
     n, m, l = a.n, 201, 200
@@ -53,6 +55,22 @@ def main():
             key = f"{name} splits={sp or 'default'}"
             out[key] = {"ms": round(best, 2), "TFLOPs_alg": round(fl / best / 1e9, 2)}
             print(f"{key:40s} {best:8.2f} ms  {fl / best / 1e9:6.2f} TF/s", flush=True)
+    if a.after_hbm:
+        os.environ.pop("FDMD_GRAM_SPLITS", None)
+        big = torch.empty((8 << 30) // 4, dtype=torch.float32, device="cuda")
+        big2 = torch.empty_like(big)
+        for name, (fn, fl) in cases.items():
+            for rep in range(a.reps):
+                for _ in range(8):          # 8 x 16 GB moved ~ 130 ms at ~6.5 TB/s
+                    big2.copy_(big)
+                ev[0].record()
+                fn()
+                ev[1].record()
+                torch.cuda.synchronize()
+                ms = ev[0].elapsed_time(ev[1])
+                key = f"{name} after HBM streaming #{rep}"
+                out[key] = {"ms": round(ms, 2), "TFLOPs_alg": round(fl / ms / 1e9, 2)}
+                print(f"{key:40s} {ms:8.2f} ms  {fl / ms / 1e9:6.2f} TF/s", flush=True)
     print(json.dumps(out))
 
 
