@@ -152,6 +152,14 @@ int fdmd_tc_decode(const void* uh, const void* ul, int64_t ldu, int64_t n, int r
 int fdmd_tc_decode_ex(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch, const void* cl,
                       int ldk, int nf, const float* fscale, float* out, int64_t ldo, int flags, void* stream);
 
+/* tc_decode (CTA-pair kernel, nf <= 256) writing its result as the fp16
+ * hi/lo planes of a row-major n x ldp matrix scaled by pscale (ldp % 8 == 0,
+ * ldp >= nf; columns [nf, ldp) are written as zeros): the lift U = Q Ub
+ * (linalg.py:88) straight into the planes of the config-4 basis. */
+int fdmd_tc_decode_planes(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch,
+                          const void* cl, int ldk, int nf, const float* fscale, void* out_h, void* out_l,
+                          int64_t ldp, float pscale, int flags, void* stream);
+
 /* ---- 2-D MAC-grid serving / guided upscaling ----
  * State layout (grid.py:1-18): u block ny x (nx+1), then v block (ny+1) x nx. */
 #define FDMD_MAC_VELOCITY 0

@@ -56,6 +56,8 @@ SIGNATURES = {
     "fdmd_pair_stats": (_i, [_vp, _i64, _i64, _i, _i64, _vp, _vp, _sz, _vp]),
     "fdmd_tc_decode": (_i, [_vp, _vp, _i64, _i64, _i, _vp, _vp, _i, _i, _vp, _vp, _i64, _vp]),
     "fdmd_tc_decode_ex": (_i, [_vp, _vp, _i64, _i64, _i, _vp, _vp, _i, _i, _vp, _vp, _i64, _i, _vp]),
+    "fdmd_tc_decode_planes": (_i, [_vp, _vp, _i64, _i64, _i, _vp, _vp, _i, _i, _vp, _vp, _vp, _i64, _c.c_float, _i,
+                                   _vp]),
     "fdmd_mac_decode": (_i, [_vp, _i, _i64, _i, _vp, _i, _i, _i, _vp, _vp]),
     "fdmd_mac_advect": (_i, [_vp, _i, _i, _i, _d, _d, _vp, _vp, _vp]),
     "fdmd_mac_inject": (_i, [_vp, _i, _i, _i, _i, _i64, _i64, _vp, _vp]),

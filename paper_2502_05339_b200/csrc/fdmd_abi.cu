@@ -712,7 +712,8 @@ int launch_tc_decode_mc(const void* uh, const void* ul, int64_t ldu, int64_t n, 
 // CTA-pair variant (cta_group::2, M = 256 rows x N = 256 frames per pair tile)
 int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch,
                           const void* cl, int ldk, int nf, const float* fscale, float* out, int64_t ldo,
-                          void* stream, int reserve_pairs = 0) {
+                          void* stream, int reserve_pairs = 0, void* ph = nullptr, void* pl = nullptr,
+                          int64_t ldp = 0, float pscale = 1.f) {
   auto encode = tensor_map_encoder();
   if (!encode) return fail(FDMD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap maps[4];
@@ -754,6 +755,10 @@ int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n
     configured = dev;
   }
   fdmd::TCArgs ta{out, ldo, n, r, nf, fscale};
+  ta.ph = static_cast<__half*>(ph);
+  ta.pl = static_cast<__half*>(pl);
+  ta.ldp = ldp;
+  ta.pscale = pscale;
   const int64_t ptiles = (n + 2 * fdmd::tc2::BM - 1) / (2 * fdmd::tc2::BM);
   const int gy = (nf + fdmd::tc2::BN - 1) / fdmd::tc2::BN;
   const int64_t npairs = std::max<int64_t>(1, std::min<int64_t>(ptiles, std::max(1, max_clusters / gy - reserve_pairs)));
@@ -1247,6 +1252,20 @@ int fdmd_tc_decode_ex(const void* uh, const void* ul, int64_t ldu, int64_t n, in
   if (ny <= 4 || mc_cap < 8)
     return launch_tc_decode_mc<128, 3, 0, 4>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
   return launch_tc_decode_mc<128, 3, 0, 8>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
+}
+
+int fdmd_tc_decode_planes(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch,
+                          const void* cl, int ldk, int nf, const float* fscale, void* out_h, void* out_l,
+                          int64_t ldp, float pscale, int flags, void* stream) {
+  if (!uh || !ul || !ch || !cl || !fscale || !out_h || !out_l || n <= 0 || r <= 0 || nf <= 0 ||
+      r > fdmd::tc::BKC * fdmd::tc::MAXKC || nf > fdmd::tc2::BN)
+    return fail(FDMD_ERR_INVALID, "tc_decode_planes: bad arguments (r <= %d, nf <= %d)",
+                fdmd::tc::BKC * fdmd::tc::MAXKC, fdmd::tc2::BN);
+  if ((ldu * 2) % 16 || (ldk * 2) % 16 || ldu < r || ldk < r || ldp % 8 || ldp < nf || n >= (int64_t)UINT32_MAX)
+    return fail(FDMD_ERR_INVALID, "tc_decode_planes: leading dimensions must be multiples of 8 halves, ldp >= nf");
+  // one 256-column tile; the unused out pointer/ld keep the kernel's frame path inert
+  return launch_tc_decode_pair(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, static_cast<float*>(out_h), n, stream,
+                               (flags & FDMD_SHARE_SMS) ? 4 : 0, out_h, out_l, ldp, pscale);
 }
 
 int fdmd_mac_decode(const void* D, int dtype, int64_t ldd, int ncol, const double* coef, int nx, int ny,

@@ -123,6 +123,14 @@ struct TCArgs {
   int r;               // K (modes)
   int nf;              // frames in this launch (<= BN * gridDim.y)
   const float* fscale; // per-frame output scale 2^-(su + sc_f)
+  // plane output (CTA-pair kernel only; ph != nullptr replaces `out`): the
+  // result is written as the fp16 hi/lo planes of a row-major n x ldp matrix
+  // scaled by pscale — the split a later tcgen05 product streams (the lift
+  // U = Q Ub straight into the config-4 basis planes, no fp32 U round trip)
+  __half* ph = nullptr;
+  __half* pl = nullptr;
+  int64_t ldp = 0;
+  float pscale = 1.f;
 };
 
 // TMA maps: amap_h/amap_l over Us planes (dims {r, n}, box {64, 128 / MC}, SW128),

@@ -200,6 +200,42 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
         if (f0 + cb >= args.nf) break;
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * tc2::BN + cb), v);
+        if (args.ph != nullptr) {
+          // planes: this lane's row, 32 consecutive columns -> 64 B of hi and lo
+          if (row < args.n) {
+            const int c0 = f0 + cb;
+            const int cn = (int)min((int64_t)32, args.ldp - c0);   // columns in [nf, ldp) are zero
+            __half* oh = args.ph + row * args.ldp + c0;
+            __half* ol = args.pl + row * args.ldp + c0;
+            if (cn == 32) {
+#pragma unroll
+              for (int j8 = 0; j8 < 4; ++j8) {
+                uint4 hv, lv;
+                __half2* h2 = reinterpret_cast<__half2*>(&hv);
+                __half2* l2 = reinterpret_cast<__half2*>(&lv);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int j = 8 * j8 + 2 * u;
+                  const float x0 = (c0 + j < args.nf ? v[j] * sm.fs[cb + j] : 0.f) * args.pscale;
+                  const float x1 = (c0 + j + 1 < args.nf ? v[j + 1] * sm.fs[cb + j + 1] : 0.f) * args.pscale;
+                  const __half a0 = __float2half_rn(x0), a1 = __float2half_rn(x1);
+                  h2[u] = __halves2half2(a0, a1);
+                  l2[u] = __halves2half2(__float2half_rn(x0 - __half2float(a0)), __float2half_rn(x1 - __half2float(a1)));
+                }
+                *reinterpret_cast<uint4*>(oh + 8 * j8) = hv;
+                *reinterpret_cast<uint4*>(ol + 8 * j8) = lv;
+              }
+            } else {
+              for (int j = 0; j < cn; ++j) {
+                const float x = (c0 + j < args.nf ? v[j] * sm.fs[cb + j] : 0.f) * args.pscale;
+                const __half a = __float2half_rn(x);
+                oh[j] = a;
+                ol[j] = __float2half_rn(x - __half2float(a));
+              }
+            }
+          }
+          continue;
+        }
         if (row < args.n) {
           float* o = args.out + (int64_t)(f0 + cb) * args.ldo + row;
           const int jn = min(32, args.nf - (f0 + cb));

@@ -317,6 +317,37 @@ class CudaOps:
         self.launches += 2
         return out
 
+    def tc_decode_planes(self, tcb: dict, coef: torch.Tensor, bound: float = 2.0, share_sms: bool = False) -> dict:
+        """basis @ coef (r x k, k <= 256) on tcgen05, written straight into the
+        fp16 hi/lo planes of a row-major n x round_up(k, 8) matrix (the lift
+        U = Q Ub into the config-4 basis planes: no fp32 U, no separate split).
+        `bound`: a known max |result| (orthonormal columns: <= 1) fixes the
+        plane scale su = 2^(14 - e) without a scan."""
+        import math
+        r, n = tcb["r"], tcb["n"]
+        coef = coef.to(torch.float32).contiguous()
+        k = int(coef.shape[1])
+        ldk = round_up(r, 8)
+        ldp = round_up(k, 8)
+        dev = coef.device
+        ch = torch.empty((k, ldk), dtype=torch.float16, device=dev)
+        cl = torch.empty_like(ch)
+        fs = torch.empty((k,), dtype=torch.float32, device=dev)
+        e = math.frexp(float(bound))[1]
+        su = math.ldexp(1.0, 14 - e)
+        uh = torch.empty((n, ldp), dtype=torch.float16, device=dev)
+        ul = torch.empty_like(uh)
+        e0 = self._ev()
+        L = _lib.lib()
+        _lib.check(L.fdmd_split_coef(_ptr(coef), coef.stride(0), r, k, ctypes.c_float(1.0 / tcb["su"]), _ptr(ch),
+                                     _ptr(cl), ldk, _ptr(fs), _stream()), "split_coef")
+        _lib.check(L.fdmd_tc_decode_planes(_ptr(tcb["uh"]), _ptr(tcb["ul"]), tcb["ldu"], n, r, _ptr(ch), _ptr(cl),
+                                           ldk, k, _ptr(fs), _ptr(uh), _ptr(ul), ldp, ctypes.c_float(su),
+                                           2 if share_sms else 0, _stream()), "tc_decode_planes")
+        self._done("tc_decode", 2.0 * n * r * k, e0)
+        self.launches += 2
+        return {"uh": uh, "ul": ul, "ldu": ldp, "su": su, "n": n, "r": k}
+
     # -- y[k][v] = sum_i D[k][i] U[v][i] -----------------------------------
     def colmajor_dot(self, D: Tall, U: torch.Tensor, ncols: Optional[int] = None) -> torch.Tensor:
         """U: (nv, n) tensor (nv <= 8), row v contiguous."""

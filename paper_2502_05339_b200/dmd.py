@@ -772,7 +772,12 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
         n_loc = basis.A.n
         basis.A = None
         U = None
-        if keep_basis:          # the config-4 basis; the model itself never needs U
+        if keep_basis == "planes":
+            # the config-4 basis as the fp16 hi/lo planes the batched
+            # reconstruction streams, written by the lift itself (|U| <= 1)
+            with stage("lift.U=QUb"):
+                U = ops.tc_decode_planes(qt, basis.Umap.to(torch.float32), bound=2.0, share_sms=True)
+        elif keep_basis:        # the config-4 basis; the model itself never needs U
             with stage("lift.U=QUb"):
                 U = alloc_tall(n_loc, r, tdt, "col", device=dev)
                 ops.tc_decode(qt, basis.Umap.to(torch.float32), out=U.buf[:r], share_sms=True)

@@ -328,16 +328,24 @@ class ModalBasis:
     # a single frame is a GEMV and stays on the HBM-streaming SIMT kernel
     TC_MIN_BATCH = 16
 
-    def __init__(self, U: Tall, W, lam, b, dt=1.0, use_tc: Optional[bool] = None):
-        assert U.layout == "col"
+    def __init__(self, U, W, lam, b, dt=1.0, use_tc: Optional[bool] = None):
+        """U: the real basis as a column-major Tall, or the fp16 hi/lo planes
+        dict of a tcgen05 lift (optdmd(keep_basis="planes"))."""
+        planes = U if isinstance(U, dict) else None
+        if planes is not None:
+            U = None
+            dev = planes["uh"].device
+            use_tc = True
+        else:
+            assert U.layout == "col"
+            dev = U.buf.device
         self.U = U
-        dev = U.buf.device
         self.W = torch.as_tensor(np.asarray(W, dtype=np.complex128), device=dev)
         self.lam = np.asarray(lam, dtype=np.complex128)
         self.omega = torch.as_tensor(np.log(self.lam) / dt, device=dev)
         self.b = torch.as_tensor(np.asarray(b, dtype=np.complex128), device=dev)
         self.use_tc = (U.dtype == torch.float32 and U.buf.is_cuda) if use_tc is None else use_tc
-        self._tc = None
+        self._tc = planes
 
     def coefficients(self, times) -> torch.Tensor:
         t = torch.as_tensor(np.asarray(times, dtype=np.float64), device=self.W.device)
@@ -355,7 +363,8 @@ class ModalBasis:
         batch size then runs on the tcgen05 kernel."""
         if not self.use_tc:
             raise ValueError("release_fp32 needs the tcgen05 path (fp32 CUDA basis)")
-        self.tc_state()
+        if self.U is not None:
+            self.tc_state()
         self.U = None
 
     def reconstruct(self, times, out: Optional[torch.Tensor] = None) -> torch.Tensor:

@@ -251,6 +251,29 @@ def test_tc_decode_fp16_split(dv, n, r, B):
     assert err.max() <= 2e-6, err.max()
 
 
+@pytest.mark.parametrize("n,K,k", [(100003, 200, 200), (70001, 160, 150), (5000, 64, 37), (300, 200, 256)])
+def test_tc_decode_planes_lift(dv, n, K, k):
+    """The lift U = Q M written straight into fp16 hi/lo planes
+    (fdmd_tc_decode_planes): the planes hold U to FP32 accuracy, columns past k
+    are zero, and reconstructing frames from them equals U @ C."""
+    rng = np.random.default_rng(n + K + k)
+    Q = np.linalg.qr(rng.standard_normal((n, K)))[0] if n >= K else rng.standard_normal((n, K)) / np.sqrt(n)
+    M = np.linalg.qr(rng.standard_normal((K, K)))[0][:, :k]          # U = Q M: orthonormal columns, |U| <= 1
+    ops = dv.get_ops()
+    Qt = _tall_from(dv, Q, "row", torch.float64)
+    qt = ops.tc_rows(Qt, bound=2.0)
+    pl = ops.tc_decode_planes(qt, torch.as_tensor(M, device="cuda"), bound=2.0)
+    U = (pl["uh"].double() + pl["ul"].double()).cpu().numpy() / pl["su"]
+    want = Q @ M
+    assert pl["ldu"] % 8 == 0 and np.all(U[:, k:] == 0.0)
+    err = np.linalg.norm(U[:, :k] - want, axis=0) / np.linalg.norm(want, axis=0)
+    assert err.max() <= 2e-6, err.max()
+    C = rng.standard_normal((k, 40))
+    fr = ops.tc_decode(pl, torch.as_tensor(C, device="cuda")).double().cpu().numpy()
+    wf = (want @ C.astype(np.float32).astype(np.float64)).T
+    assert (np.linalg.norm(fr - wf, axis=1) / np.linalg.norm(wf, axis=1)).max() <= 4e-6
+
+
 @pytest.mark.parametrize("nv", [1, 3, 8])
 def test_colmajor_dot(dv, nv):
     rng = np.random.default_rng(nv)

@@ -300,6 +300,38 @@ def test_optdmd_tcgen05_lift_and_modes_match_dmma(fd):
     assert rel(fa, fb) <= 1e-5
 
 
+def test_optdmd_basis_planes_match_fp32_basis(fd):
+    """keep_basis="planes" (the lift writes the config-4 basis straight into
+    the fp16 hi/lo planes, the bench's schedule) against keep_basis=True (fp32
+    U, then the split): same eigenvalues, U to FP32 accuracy, and the same
+    config-4 frames u(t) = U Re(W Lam^t b)."""
+    from paper_2502_05339_b200 import synth
+    from paper_2502_05339_b200.runtime import ModalBasis
+    p = synth.config_params(3, seed=3, grid=16)
+    X = synth.generate_host(p)
+    kw = dict(lm_config=fd.LMConfig(max_iters=10), svd_mode="randomized", seed=3, oversample=10, power_iters=1)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        a = fd.optdmd(fd.SnapshotMatrix(X, synth.DT), 200, keep_basis=True, **kw)
+        b = fd.optdmd(fd.SnapshotMatrix(X, synth.DT), 200, keep_basis="planes", **kw)
+    np.testing.assert_array_equal(a.lam, b.lam)
+    pl = b.basis_U
+    Ua = a.basis_U.view().double().cpu().numpy()
+    Ub = ((pl["uh"].double() + pl["ul"].double()) / pl["su"]).t().cpu().numpy()[:200]
+    assert np.abs(Ua - Ub).max() <= 2e-6 * np.abs(Ua).max()
+    rng = np.random.default_rng(4)
+    lam4 = rng.uniform(0.9, 0.999, 200) * np.exp(1j * rng.uniform(0.05, 1.0, 200))
+    W4 = (rng.standard_normal((200, 200)) + 1j * rng.standard_normal((200, 200))) / np.sqrt(400)
+    b4 = rng.standard_normal(200) + 1j * rng.standard_normal(200)
+    times = rng.uniform(0.0, 300.0, 300)
+    fa = ModalBasis(a.basis_U, W4, lam4, b4).reconstruct(times).double()
+    fb = ModalBasis(pl, W4, lam4, b4).reconstruct(times).double()
+    err = torch.linalg.vector_norm(fa - fb, dim=1) / torch.linalg.vector_norm(fa, dim=1)
+    assert float(err.max()) <= 4e-6
+    f1 = ModalBasis(pl, W4, lam4, b4).reconstruct(times[:1]).double()     # B = 1 from the planes
+    assert float(torch.linalg.vector_norm(f1[0] - fa[0]) / torch.linalg.vector_norm(fa[0])) <= 4e-6
+
+
 # ---------------------------------------------------------------- frames of the benched fit vs the reference
 @pytest.fixture(scope="module")
 def frames_golden():
