@@ -729,10 +729,13 @@ int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res != CUDA_SUCCESS) return fail(FDMD_ERR_CUDA, "tc_decode2: tensor map encode failed (%d)", (int)res);
   }
-  auto kern = fdmd::tc_decode2_kernel;
+  // the plane-output epilogue is a separate instantiation: sharing one body
+  // pushed the frame path over the 113-register budget of 576 threads (spills)
+  auto kern = ph ? fdmd::tc_decode2_kernel<true> : fdmd::tc_decode2_kernel<false>;
   const int smem = (int)sizeof(fdmd::TC2Smem) + 1024;
-  static thread_local int configured = -1;
-  static thread_local int max_clusters = 0;
+  static thread_local int configured[2] = {-1, -1};
+  static thread_local int max_clusters[2] = {0, 0};
+  const int kv = ph ? 1 : 0;
   int dev = 0;
   cudaGetDevice(&dev);
   cudaLaunchConfig_t cfg = {};
@@ -746,13 +749,13 @@ int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n
   cfg.blockDim = dim3(fdmd::tc2::THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = (cudaStream_t)stream;
-  if (configured != dev) {
+  if (configured[kv] != dev) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cfg.gridDim = dim3(2, 1);
     int nc = 0;
     CUDA_TRY(cudaOccupancyMaxActiveClusters(&nc, (void*)kern, &cfg));
-    max_clusters = std::max(1, nc);
-    configured = dev;
+    max_clusters[kv] = std::max(1, nc);
+    configured[kv] = dev;
   }
   fdmd::TCArgs ta{out, ldo, n, r, nf, fscale};
   ta.ph = static_cast<__half*>(ph);
@@ -761,7 +764,8 @@ int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n
   ta.pscale = pscale;
   const int64_t ptiles = (n + 2 * fdmd::tc2::BM - 1) / (2 * fdmd::tc2::BM);
   const int gy = (nf + fdmd::tc2::BN - 1) / fdmd::tc2::BN;
-  const int64_t npairs = std::max<int64_t>(1, std::min<int64_t>(ptiles, std::max(1, max_clusters / gy - reserve_pairs)));
+  const int64_t npairs =
+      std::max<int64_t>(1, std::min<int64_t>(ptiles, std::max(1, max_clusters[kv] / gy - reserve_pairs)));
   cfg.gridDim = dim3((unsigned)(2 * npairs), gy);
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], ta));
   LAUNCH_CHECK("tc_decode2");

@@ -85,6 +85,7 @@ __device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, unsigned byte
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
+template <bool PLANES>
 __global__ void __launch_bounds__(tc2::THREADS, 1)
 tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_constant__ CUtensorMap amap_l,
                   const __grid_constant__ CUtensorMap bmap_h, const __grid_constant__ CUtensorMap bmap_l,
@@ -200,38 +201,48 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
         if (f0 + cb >= args.nf) break;
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * tc2::BN + cb), v);
-        if (args.ph != nullptr) {
-          // planes: this lane's row, 32 consecutive columns -> 64 B of hi and lo
-          if (row < args.n) {
-            const int c0 = f0 + cb;
-            const int cn = (int)min((int64_t)32, args.ldp - c0);   // columns in [nf, ldp) are zero
-            __half* oh = args.ph + row * args.ldp + c0;
-            __half* ol = args.pl + row * args.ldp + c0;
-            if (cn == 32) {
+        if constexpr (PLANES) {
+          // planes: lane = row (q * 32 + lane), 32 consecutive columns. The hi / lo
+          // halves are packed into half2 registers and transposed across the warp
+          // with shuffles so every store instruction writes 8 rows x 64 contiguous
+          // bytes (one uint4 per lane) instead of 32 rows' scattered 16-B pieces.
+          const int c0 = f0 + cb;
+          uint32_t hp[16], lp[16];
 #pragma unroll
-              for (int j8 = 0; j8 < 4; ++j8) {
-                uint4 hv, lv;
-                __half2* h2 = reinterpret_cast<__half2*>(&hv);
-                __half2* l2 = reinterpret_cast<__half2*>(&lv);
+          for (int u = 0; u < 16; ++u) {
+            const int j = 2 * u;
+            const float x0 = (c0 + j < args.nf ? v[j] * sm.fs[cb + j] : 0.f) * args.pscale;
+            const float x1 = (c0 + j + 1 < args.nf ? v[j + 1] * sm.fs[cb + j + 1] : 0.f) * args.pscale;
+            const __half a0 = __float2half_rn(x0), a1 = __float2half_rn(x1);
+            const __half2 h = __halves2half2(a0, a1);
+            const __half2 l = __halves2half2(__float2half_rn(x0 - __half2float(a0)), __float2half_rn(x1 - __half2float(a1)));
+            hp[u] = *reinterpret_cast<const uint32_t*>(&h);
+            lp[u] = *reinterpret_cast<const uint32_t*>(&l);
+          }
+          const int64_t rowbase = row - lane;
+          const int cq = lane & 3;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                  const int j = 8 * j8 + 2 * u;
-                  const float x0 = (c0 + j < args.nf ? v[j] * sm.fs[cb + j] : 0.f) * args.pscale;
-                  const float x1 = (c0 + j + 1 < args.nf ? v[j + 1] * sm.fs[cb + j + 1] : 0.f) * args.pscale;
-                  const __half a0 = __float2half_rn(x0), a1 = __float2half_rn(x1);
-                  h2[u] = __halves2half2(a0, a1);
-                  l2[u] = __halves2half2(__float2half_rn(x0 - __half2float(a0)), __float2half_rn(x1 - __half2float(a1)));
-                }
-                *reinterpret_cast<uint4*>(oh + 8 * j8) = hv;
-                *reinterpret_cast<uint4*>(ol + 8 * j8) = lv;
+          for (int k = 0; k < 4; ++k) {
+            const int src = 8 * k + (lane >> 2);
+            uint4 oh, ol;
+            uint32_t* ohp = reinterpret_cast<uint32_t*>(&oh);
+            uint32_t* olp = reinterpret_cast<uint32_t*>(&ol);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint32_t hc[4], lc[4];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                hc[c] = __shfl_sync(0xffffffffu, hp[4 * c + j], src);
+                lc[c] = __shfl_sync(0xffffffffu, lp[4 * c + j], src);
               }
-            } else {
-              for (int j = 0; j < cn; ++j) {
-                const float x = (c0 + j < args.nf ? v[j] * sm.fs[cb + j] : 0.f) * args.pscale;
-                const __half a = __float2half_rn(x);
-                oh[j] = a;
-                ol[j] = __float2half_rn(x - __half2float(a));
-              }
+              ohp[j] = cq == 0 ? hc[0] : cq == 1 ? hc[1] : cq == 2 ? hc[2] : hc[3];
+              olp[j] = cq == 0 ? lc[0] : cq == 1 ? lc[1] : cq == 2 ? lc[2] : lc[3];
+            }
+            const int64_t r_out = rowbase + src;
+            const int col = c0 + 8 * cq;
+            if (r_out < args.n && col < args.ldp) {
+              *reinterpret_cast<uint4*>(args.ph + r_out * args.ldp + col) = oh;
+              *reinterpret_cast<uint4*>(args.pl + r_out * args.ldp + col) = ol;
             }
           }
           continue;

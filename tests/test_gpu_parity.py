@@ -317,7 +317,7 @@ def test_optdmd_basis_planes_match_fp32_basis(fd):
     np.testing.assert_array_equal(a.lam, b.lam)
     pl = b.basis_U
     Ua = a.basis_U.view().double().cpu().numpy()
-    Ub = ((pl["uh"].double() + pl["ul"].double()) / pl["su"]).t().cpu().numpy()[:200]
+    Ub = ((pl["uh"].double() + pl["ul"].double()) / pl["su"]).cpu().numpy()[:, :200]
     assert np.abs(Ua - Ub).max() <= 2e-6 * np.abs(Ua).max()
     rng = np.random.default_rng(4)
     lam4 = rng.uniform(0.9, 0.999, 200) * np.exp(1j * rng.uniform(0.05, 1.0, 200))
