@@ -730,12 +730,31 @@ int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n
     if (res != CUDA_SUCCESS) return fail(FDMD_ERR_CUDA, "tc_decode2: tensor map encode failed (%d)", (int)res);
   }
   // the plane-output epilogue is a separate instantiation: sharing one body
-  // pushed the frame path over the 113-register budget of 576 threads (spills)
-  auto kern = ph ? fdmd::tc_decode2_kernel<true> : fdmd::tc_decode2_kernel<false>;
-  const int smem = (int)sizeof(fdmd::TC2Smem) + 1024;
-  static thread_local int configured[2] = {-1, -1};
-  static thread_local int max_clusters[2] = {0, 0};
-  const int kv = ph ? 1 : 0;
+  // pushed the frame path over the 113-register budget of 576 threads (spills).
+  // FDMD_TC2_TMAO=1: frames go out through TMA stores of 16-frame x 128-row
+  // staged chunks (2-deep basis ring) when the output rows are 16-byte aligned.
+  // Measured at n = 50.3M: B = 256 18.2 ms vs 16.7 ms with register stores,
+  // B = 512 equal (33.4 ms) — off by default.
+  static const bool tmao_on = [] { const char* e = getenv("FDMD_TC2_TMAO"); return e && strcmp(e, "1") == 0; }();
+  const bool tmao = !ph && tmao_on && (ldo * 4) % 16 == 0 && ((uintptr_t)out % 16) == 0;
+  auto kern = ph ? fdmd::tc_decode2_kernel<true, false, fdmd::tc2::AST>
+                 : (tmao ? fdmd::tc_decode2_kernel<false, true, 2> : fdmd::tc_decode2_kernel<false, false, fdmd::tc2::AST>);
+  const int smem = (int)(tmao ? sizeof(fdmd::TC2SmemT<2, true>) : sizeof(fdmd::TC2Smem)) + 1024;
+  static thread_local int configured[3] = {-1, -1, -1};
+  static thread_local int max_clusters[3] = {0, 0, 0};
+  const int kv = ph ? 1 : (tmao ? 2 : 0);
+  CUtensorMap omap;
+  memset(&omap, 0, sizeof(omap));
+  if (tmao) {
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)nf};
+    cuuint64_t strides[1] = {(cuuint64_t)(ldo * 4)};
+    cuuint32_t box[2] = {(cuuint32_t)fdmd::tc2::BM, (cuuint32_t)fdmd::TMAO_FR};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult res = encode(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) return fail(FDMD_ERR_CUDA, "tc_decode2: output tensor map encode failed (%d)", (int)res);
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   cudaLaunchConfig_t cfg = {};
@@ -766,8 +785,8 @@ int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n
   const int gy = (nf + fdmd::tc2::BN - 1) / fdmd::tc2::BN;
   const int64_t npairs =
       std::max<int64_t>(1, std::min<int64_t>(ptiles, std::max(1, max_clusters[kv] / gy - reserve_pairs)));
-  cfg.gridDim = dim3((unsigned)(2 * npairs), gy);
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], ta));
+  cfg.gridDim = dim3((unsigned)(2 * npairs * gy), 1);
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], omap, ta));
   LAUNCH_CHECK("tc_decode2");
   return FDMD_OK;
 }

@@ -43,15 +43,43 @@ constexpr int A_CHUNK_BYTES = BM * BKC * 2;    // 16 KB per plane
 constexpr int B_CHUNK_BYTES = BNH * BKC * 2;   // 16 KB per plane
 }  // namespace tc2
 
-struct TC2Smem {
-  __half A[tc2::AST][2][tc2::BM * tc2::BKC];
+// TMAO (TMA-store epilogue): each of the 4 epilogue parts stages 16 frames x
+// 128 rows (8 KB) and writes them with ONE 2-D TMA store — 512 contiguous
+// bytes per frame per CTA tile. Register stores from the TMEM lane layout
+// (lane = row) write 128 B per frame per warp instruction, which HBM absorbs
+// at 4.5 TB/s against 6.0-6.3 TB/s for 512-B runs (tools/write_pattern.cu,
+// profiles/r02_write_pattern.txt). The staging space comes from a 2-deep
+// basis ring (3 before): at 256 frames per basis tile a pair SM needs ~15 GB/s
+// of basis, covered by 64 KB in flight.
+constexpr int TMAO_FR = 16;                      // frames per staged chunk
+template <int AST_, bool TMAO>
+struct TC2SmemT {
+  __half A[AST_][2][tc2::BM * tc2::BKC];
   __half B[tc2::MAXKC][2][tc2::BNH * tc2::BKC];
+  alignas(128) float stage[TMAO ? tc2::EPI / 4 : 1][TMAO ? TMAO_FR * tc2::BM : 1];
   alignas(16) float fs[tc2::BN];
-  uint64_t afull[tc2::AST], aempty[tc2::AST];
+  uint64_t afull[AST_], aempty[AST_];
   uint64_t bfull;
   uint64_t tfull[2], tempty[2];
   uint32_t tmem_base;
 };
+using TC2Smem = TC2SmemT<tc2::AST, false>;
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n"
+               ::"l"(map), "r"(x), "r"(y), "r"(smem_u32(src)) : "memory");
+}
 
 __device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
   uint32_t r;
@@ -85,12 +113,12 @@ __device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, unsigned byte
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
-template <bool PLANES>
+template <bool PLANES, bool TMAO, int AST_>
 __global__ void __launch_bounds__(tc2::THREADS, 1)
 tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_constant__ CUtensorMap amap_l,
                   const __grid_constant__ CUtensorMap bmap_h, const __grid_constant__ CUtensorMap bmap_l,
-                  const TCArgs args) {
-  using SM = TC2Smem;
+                  const __grid_constant__ CUtensorMap omap, const TCArgs args) {
+  using SM = TC2SmemT<AST_, TMAO>;
   constexpr uint32_t TCOLS = 2 * tc2::BN;   // 512: two 256-column accumulators
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
@@ -100,14 +128,21 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
   const int nkc = (args.r + tc2::BKC - 1) / tc2::BKC;
   const int ksteps_last = ((args.r - (nkc - 1) * tc2::BKC) + 15) / 16;
   const int64_t ptiles = (args.n + 2 * tc2::BM - 1) / (2 * tc2::BM);
-  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  // frame tiles interleave with the row pairs along x (CTA 2 (gy p + y) + rank):
+  // the gy pairs reading the same basis rows get adjacent CTA ids, hence SMs on
+  // the same die, so the second frame tile's basis reads hit the same L2
+  // (grid (npairs, gy) placed the two frame tiles on different dies: 1.8x
+  // basis DRAM reads at 512 frames)
+  const int gy = (args.nf + tc2::BN - 1) / tc2::BN;
+  const int64_t pid = blockIdx.x >> 1;
+  const int64_t pair = pid / gy, npairs = (gridDim.x >> 1) / gy;
   const int64_t my_tiles = pair < ptiles ? (ptiles - pair + npairs - 1) / npairs : 0;
-  const int f0 = blockIdx.y * tc2::BN;
+  const int f0 = (int)(pid % gy) * tc2::BN;
 
   for (int f = threadIdx.x; f < tc2::BN; f += blockDim.x)
     sm.fs[f] = (f0 + f < args.nf) ? args.fscale[f0 + f] : 0.f;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < tc2::AST; ++s) { mbar_init(&sm.afull[s], 1); mbar_init(&sm.aempty[s], 1); }
+    for (int s = 0; s < AST_; ++s) { mbar_init(&sm.afull[s], 1); mbar_init(&sm.aempty[s], 1); }
     mbar_init(&sm.bfull, 1);
     for (int a = 0; a < 2; ++a) { mbar_init(&sm.tfull[a], 1); mbar_init(&sm.tempty[a], 2 * tc2::EPI); }
     mbar_fence_init();
@@ -141,13 +176,13 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
           const uint32_t afull_l = mapa_u32(&sm.afull[sa], 0);
           tma_load_2d_cg2(sm.A[sa][0], &amap_h, c * tc2::BKC, row0, afull_l);
           tma_load_2d_cg2(sm.A[sa][1], &amap_l, c * tc2::BKC, row0, afull_l);
-          if (++sa == tc2::AST) { sa = 0; pa ^= 1; }
+          if (++sa == AST_) { sa = 0; pa ^= 1; }
         }
       }
       // tail: the leader's last releases of this CTA's ring have landed
-      for (int s = 0; s < tc2::AST; ++s) {
+      for (int s = 0; s < AST_; ++s) {
         mbar_wait(&sm.aempty[sa], pa ^ 1);
-        if (++sa == tc2::AST) { sa = 0; pa ^= 1; }
+        if (++sa == AST_) { sa = 0; pa ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -177,7 +212,7 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
             first = 0;
           }
           umma2_commit_mc(&sm.aempty[sa]);          // both CTAs may refill this stage
-          if (++sa == tc2::AST) { sa = 0; pa ^= 1; }
+          if (++sa == AST_) { sa = 0; pa ^= 1; }
         }
         umma2_commit_mc(&sm.tfull[acc]);            // both CTAs' TMEM halves ready
       }
@@ -196,6 +231,26 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
       mbar_wait(&sm.tfull[acc], (uint32_t)((t >> 1) & 1));
       tc_fence_after();
       const int64_t row = (pair + t * npairs) * (2 * tc2::BM) + rank * tc2::BM + q * 32 + lane;
+      if constexpr (TMAO && !PLANES) {
+        float* stg = sm.stage[part];
+        const int64_t row0 = row - q * 32 - lane;              // first row of this CTA's tile half
+#pragma unroll 1
+        for (int cb = c_lo; cb < c_hi; cb += TMAO_FR) {
+          if (f0 + cb >= args.nf) break;                       // uniform over the part's 4 warps
+          float v[TMAO_FR];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * tc2::BN + cb), v);
+#pragma unroll
+          for (int j = 0; j < TMAO_FR; ++j) stg[j * tc2::BM + q * 32 + lane] = v[j] * sm.fs[cb + j];
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          asm volatile("bar.sync %0, 128;\n" ::"r"(1 + part) : "memory");
+          if (q == 0 && lane == 0) {
+            tma_store_2d(&omap, stg, (int)row0, f0 + cb);       // rows >= n / frames >= nf are clipped
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // staging free again
+          }
+          asm volatile("bar.sync %0, 128;\n" ::"r"(1 + part) : "memory");
+        }
+      } else {
 #pragma unroll 1
       for (int cb = c_lo; cb < c_hi; cb += 32) {
         if (f0 + cb >= args.nf) break;
@@ -267,11 +322,14 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
           }
         }
       }
+      }  // register-store / plane epilogue
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_l[acc]);
     }
   }
+  if constexpr (TMAO && !PLANES)
+    if (warp >= 2) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores complete
   __syncwarp();
   tc_fence_before();
   cluster_sync_all();
