@@ -51,12 +51,12 @@ constexpr int B_CHUNK_BYTES = BNH * BKC * 2;   // 16 KB per plane
 // profiles/r02_write_pattern.txt). The staging space comes from a 2-deep
 // basis ring (3 before): at 256 frames per basis tile a pair SM needs ~15 GB/s
 // of basis, covered by 64 KB in flight.
-constexpr int TMAO_FR = 16;                      // frames per staged chunk
+constexpr int TMAO_FR = 8;                       // frames per staged chunk (2 buffers per part)
 template <int AST_, bool TMAO>
 struct TC2SmemT {
   __half A[AST_][2][tc2::BM * tc2::BKC];
   __half B[tc2::MAXKC][2][tc2::BNH * tc2::BKC];
-  alignas(128) float stage[TMAO ? tc2::EPI / 4 : 1][TMAO ? TMAO_FR * tc2::BM : 1];
+  alignas(128) float stage[TMAO ? tc2::EPI / 4 : 1][2][TMAO ? TMAO_FR * tc2::BM : 1];
   alignas(16) float fs[tc2::BN];
   uint64_t afull[AST_], aempty[AST_];
   uint64_t bfull;
@@ -232,23 +232,31 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
       tc_fence_after();
       const int64_t row = (pair + t * npairs) * (2 * tc2::BM) + rank * tc2::BM + q * 32 + lane;
       if constexpr (TMAO && !PLANES) {
-        float* stg = sm.stage[part];
         const int64_t row0 = row - q * 32 - lane;              // first row of this CTA's tile half
+        int buf = 0;
 #pragma unroll 1
-        for (int cb = c_lo; cb < c_hi; cb += TMAO_FR) {
+        for (int cb = c_lo; cb < c_hi; cb += 2 * TMAO_FR) {
           if (f0 + cb >= args.nf) break;                       // uniform over the part's 4 warps
-          float v[TMAO_FR];
+          float v[2 * TMAO_FR];
           tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * tc2::BN + cb), v);
 #pragma unroll
-          for (int j = 0; j < TMAO_FR; ++j) stg[j * tc2::BM + q * 32 + lane] = v[j] * sm.fs[cb + j];
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          asm volatile("bar.sync %0, 128;\n" ::"r"(1 + part) : "memory");
-          if (q == 0 && lane == 0) {
-            tma_store_2d(&omap, stg, (int)row0, f0 + cb);       // rows >= n / frames >= nf are clipped
-            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // staging free again
+          for (int h = 0; h < 2; ++h) {
+            if (f0 + cb + h * TMAO_FR >= args.nf) break;
+            float* stg = sm.stage[part][buf];
+#pragma unroll
+            for (int j = 0; j < TMAO_FR; ++j)
+              stg[j * tc2::BM + q * 32 + lane] = v[h * TMAO_FR + j] * sm.fs[cb + h * TMAO_FR + j];
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            asm volatile("bar.sync %0, 128;\n" ::"r"(1 + part) : "memory");
+            if (q == 0 && lane == 0) {
+              tma_store_2d(&omap, stg, (int)row0, f0 + cb + h * TMAO_FR);   // rows >= n / frames >= nf clipped
+              asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+              // the OTHER buffer (the store before this one) is free for the next chunk
+              asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            }
+            asm volatile("bar.sync %0, 128;\n" ::"r"(1 + part) : "memory");
+            buf ^= 1;
           }
-          asm volatile("bar.sync %0, 128;\n" ::"r"(1 + part) : "memory");
         }
       } else {
 #pragma unroll 1
