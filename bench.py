@@ -548,7 +548,8 @@ def main():
                        "schedule_bytes": sched,
                        "frames_per_launch": CHUNK,
                        "kernel": f"tc_decode2 (tcgen05 cta_group::2 CTA pairs, 256 frames per pair tile; the "
-                                 f"launch's frame tiles walk the basis rows in lock-step), {CHUNK}-frame launches "
+                                 f"launch's frame tiles interleaved with the row pairs so they share the basis "
+                                 f"rows through one die's L2), {CHUNK}-frame launches "
                                  f"streamed through one buffer (1024 frames = {B * 4.0 * n / 1e9:.0f} GB > HBM)"}
     recon["basis_split_ms"] = round(rec["split"] * 1e3, 2)
 
