@@ -55,3 +55,4 @@ def main():
 
 if __name__ == "__main__":
     main()
+
