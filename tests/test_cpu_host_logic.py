@@ -173,3 +173,14 @@ def test_config2_generator_is_the_controlled_system():
     A, B = F @ M @ Fp, F @ (Fp @ G)
     resid = np.abs(X[:, 1:] - (A @ X[:, :-1] + B @ u)).max() / np.abs(X).max()
     assert resid <= 1e-11
+
+
+def test_snapshot_gram_route_guard():
+    """linalg.gram_route_ok: the X^T X route only when it is the cheaper side
+    and its T x T block stays small (long series / wide inputs)."""
+    from paper_2502_05339_b200 import linalg as la
+    assert la.gram_route_ok(200, 200, 1)          # the benched config-3 shape
+    assert la.gram_route_ok(200, 160, 1)          # config 1
+    assert not la.gram_route_ok(200, 200, 0)      # q = 0: no power stage to replace
+    assert not la.gram_route_ok(1000, 20, 2)      # long series: n T^2 >> 2 n T l (1 + q)
+    assert not la.gram_route_ok(20000, 256, 30)   # T x T f64 block over the 2 GB budget

@@ -376,3 +376,40 @@ def test_config3_shape_frames_match_reference(fd, frames_golden, method, tc_fit)
     np.testing.assert_allclose(fr.sum(0), g[f"c3s_{method}_frames_checksum"][0], rtol=FRAME_TOL,
                                atol=FRAME_TOL * np.abs(fr).sum(0).max())
     np.testing.assert_allclose((fr * fr).sum(0), g[f"c3s_{method}_frames_checksum"][1], rtol=2 * FRAME_TOL)
+
+
+# ---------------------------------------------------------------- which sketch route runs
+def test_long_series_takes_explicit_sketch_route(fd):
+    """T >> l: the snapshot Gram X^T X would cost n T^2 > 2 n T l (1 + q), so
+    the explicit Y = X Omega / X^T Q route runs — with the reference's factors."""
+    import flowdmd_oracle as orc
+    from paper_2502_05339_b200 import linalg as la
+    rng = np.random.default_rng(0)
+    n, T, r, p, q = 20000, 1000, 10, 10, 2
+    M = rng.standard_normal((n, 12)) @ rng.standard_normal((12, T)) + 1e-3 * rng.standard_normal((n, T))
+    assert not la.gram_route_ok(T, r + p, q)
+    f = la.sketch_factors(la.as_tall(M), T, r + p, q, la.draw_omega(T, r + p, 4))
+    assert "implicit_sketch" not in f.stats and "gram_first_pass" not in f.stats
+    res = fd.randomized_svd(M, r, oversample=p, power_iters=q, seed=4)
+    _, S, _ = orc.sketch_svd(M, r, p, q, 4)
+    np.testing.assert_allclose(res.S, S, rtol=1e-10)
+
+
+def test_rank_deficient_sketch_falls_back_under_gram_route(fd):
+    """Exactly rank-5 data sketched at l = 18 with the snapshot-Gram route
+    available: chol(Omega^T G_X Omega) is singular, so the explicit route and
+    its shifted-CholeskyQR3 / Householder fallbacks run; the 5 nonzero singular
+    values still match the reference algorithm (Householder QR)."""
+    import flowdmd_oracle as orc
+    from paper_2502_05339_b200 import linalg as la
+    rng = np.random.default_rng(1)
+    n, T, r, p, q = 5000, 60, 8, 10, 1
+    M = rng.standard_normal((n, 5)) @ rng.standard_normal((5, T))
+    assert la.gram_route_ok(T, r + p, q)
+    f = la.sketch_factors(la.as_tall(M), T, r + p, q, la.draw_omega(T, r + p, 9))
+    assert "implicit_sketch" not in f.stats
+    assert f.stats.get("householder_fallback", 0) + f.stats.get("shifted_cholqr3", 0) >= 1, f.stats
+    res = fd.randomized_svd(M, r, oversample=p, power_iters=q, seed=9)
+    _, S, _ = orc.sketch_svd(M, r, p, q, 9)
+    np.testing.assert_allclose(res.S[:5], S[:5], rtol=1e-9)
+    assert np.all(res.S[5:] <= 1e-9 * res.S[0])
