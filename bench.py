@@ -374,7 +374,10 @@ def main():
     if world != args.gpus:
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     from paper_2502_05339_b200 import shards
-    shards.init_process_group("nccl")          # NCCL_ALGO / NCCL_PROTO pinned (deterministic sums)
+    # NCCL_ALGO / NCCL_PROTO pinned (deterministic sums). FDMD_DIST_BACKEND=gloo is a
+    # functional check of the multi-rank path on a 1-GPU box (every rank on cuda:0,
+    # host-staged collectives): its timings mean nothing
+    shards.init_process_group(os.environ.get("FDMD_DIST_BACKEND", "nccl"))
     group = None
     if world > 1:
         import torch.distributed as dist

@@ -547,7 +547,8 @@ struct Tall {  // row-major n x k device matrix
 // cuSOLVER (geqrf + orgqr on a column-major copy made by the tall GEMM): the
 // fallback of linalg.cholqr2_deferred when the (shifted) CholeskyQR Gram is not
 // positive definite, i.e. a rank-deficient sketch. Leaves fix = identity.
-int householder(Dev& d, double* Q, int64_t ldq, int64_t n, int l, std::vector<double>& fix) {
+int householder(Dev& d, double* Q, int64_t ldq, int64_t n, int l, std::vector<double>& fix,
+                std::vector<double>* R_out = nullptr) {
   cusolverDnHandle_t h = (cusolverDnHandle_t)fdmdi_solver_handle(d.s);
   if (!h) return fail(FDMD_ERR_SOLVER, "cusolverDnCreate failed");
   if (n > INT32_MAX) return fail(FDMD_ERR_SOLVER, "Householder fallback limited to n < 2^31 rows");
@@ -568,9 +569,19 @@ int householder(Dev& d, double* Q, int64_t ldq, int64_t n, int l, std::vector<do
     return fail(FDMD_ERR_SOLVER, "householder: bufferSize");
   double* work = d.alloc<double>((size_t)std::max(lw1, lw2));
   if (!work) return fail(FDMD_ERR_CUDA, "householder: device allocation failed");
-  if (cusolverDnDgeqrf(h, (int)n, l, A, (int)lda, tau, work, std::max(lw1, lw2), info) != CUSOLVER_STATUS_SUCCESS ||
-      cusolverDnDorgqr(h, (int)n, l, l, A, (int)lda, tau, work, std::max(lw1, lw2), info) != CUSOLVER_STATUS_SUCCESS)
-    return fail(FDMD_ERR_SOLVER, "householder: geqrf / orgqr failed");
+  if (cusolverDnDgeqrf(h, (int)n, l, A, (int)lda, tau, work, std::max(lw1, lw2), info) != CUSOLVER_STATUS_SUCCESS)
+    return fail(FDMD_ERR_SOLVER, "householder: geqrf failed");
+  if (R_out) {   // R = upper triangle of the factored block (column-major, ld lda) -> row-major l x l
+    std::vector<double> top((size_t)l * l);
+    CUDA_TRY(cudaMemcpy2DAsync(top.data(), l * sizeof(double), A, lda * sizeof(double), l * sizeof(double), l,
+                               cudaMemcpyDeviceToHost, d.s));
+    CUDA_TRY(cudaStreamSynchronize(d.s));
+    R_out->assign((size_t)l * l, 0.0);
+    for (int j = 0; j < l; ++j)
+      for (int i = 0; i <= j; ++i) (*R_out)[(size_t)i * l + j] = top[(size_t)j * l + i];
+  }
+  if (cusolverDnDorgqr(h, (int)n, l, l, A, (int)lda, tau, work, std::max(lw1, lw2), info) != CUSOLVER_STATUS_SUCCESS)
+    return fail(FDMD_ERR_SOLVER, "householder: orgqr failed");
   int ih = 0;
   TRY(d.down(&ih, info, sizeof(int)));
   if (ih != 0) return fail(FDMD_ERR_SOLVER, "householder: info %d", ih);
@@ -1143,11 +1154,75 @@ int ensure_pinv(Dev& d, fdmd_model* m) {
   csvd(H, Uh, mu, Vh);
   const double mu_max = mu.empty() ? 0.0 : mu[0];
   const double mu_min = mu.empty() ? 0.0 : mu.back();
-  if (!(mu_min > 0) || mu_max / mu_min > 1e12)
-    return fail(FDMD_ERR_SOLVER,
-                "ill-conditioned mode basis (cond(phi) ~ %.1e): the C ABI resolves pinv(phi) through the Gram "
-                "only; use the Python layer's QR route",
-                mu_min > 0 ? std::sqrt(mu_max / mu_min) : INFINITY);
+  if (!(mu_min > 0) || mu_max / mu_min > 1e12) {
+    // The Gram cannot resolve the reference's cut (sigma > 1e-12 sigma_max) for
+    // cond(phi) > 1e6: QR of the table instead (modes.DeviceModes.pinv_rows'
+    // ill-conditioned branch). phi = D M = D' M' over the nonzero raw columns
+    // D' (a real mode's exactly-zero imaginary column carries nothing), D' = Q R
+    // by Householder on the device, pinv(phi) = pinv(R M') Q^T and, on range(D'),
+    // Q^T = pinv(R)^T D'^T: both small pseudo-inverses with the SVD cut 1e-12.
+    std::vector<int> keep;
+    for (int k = 0; k < nc; ++k)
+      if (Gh[(size_t)k * nc + k] > 0.0) keep.push_back(k);
+    const int kc = (int)keep.size();
+    if (kc == 0) return fail(FDMD_ERR_SOLVER, "pinv: empty mode table");
+    const int64_t ldy = round_up(kc, 2);
+    std::vector<double> Isel((size_t)nc * kc, 0.0);
+    for (int j = 0; j < kc; ++j) Isel[(size_t)keep[j] * kc + j] = 1.0;
+    double* Id = d.alloc<double>(Isel.size());
+    double* Y = d.alloc<double>((size_t)m->n * ldy);
+    if (!Id || !Y) return fail(FDMD_ERR_CUDA, "pinv: device allocation failed (QR route)");
+    TRY(d.up(Isel.data(), Id, Isel.size() * sizeof(double)));
+    TRY(fdmd_tall_gemm(m->raw, m->dt, FDMD_COL, m->ldr, Id, kc, Y, FDMD_F64, FDMD_ROW, ldy, m->n, nc, kc, 0, nullptr,
+                       0, nullptr, 0, d.s));
+    std::vector<double> fix, R;
+    TRY(householder(d, Y, ldy, m->n, kc, fix, &R));
+    auto pinv_small = [](const CM& A) {   // SVD pseudo-inverse, cut 1e-12 sigma_max (linalg.py:93-104)
+      CM U, V;
+      std::vector<double> sv;
+      const bool tall = A.m >= A.n;
+      CM B = A;
+      if (!tall) {
+        B = CM(A.n, A.m);
+        for (int i = 0; i < A.m; ++i)
+          for (int j = 0; j < A.n; ++j) B(j, i) = std::conj(A(i, j));
+      }
+      csvd(B, U, sv, V);               // B = U s V^H
+      CM P(B.n, B.m);                  // pinv(B) = V s^-1 U^H
+      for (int i = 0; i < B.n; ++i)
+        for (int j = 0; j < B.m; ++j) {
+          cd acc = 0.0;
+          for (int k = 0; k < (int)sv.size(); ++k)
+            if (sv[0] > 0 && sv[k] > 1e-12 * sv[0]) acc += V(i, k) * std::conj(U(j, k)) / sv[k];
+          P(i, j) = acc;
+        }
+      if (tall) return P;
+      CM Pt(P.n, P.m);                 // pinv(A) = pinv(A^H)^H
+      for (int i = 0; i < P.m; ++i)
+        for (int j = 0; j < P.n; ++j) Pt(j, i) = std::conj(P(i, j));
+      return Pt;
+    };
+    CM RM(kc, r), Rc(kc, kc);
+    for (int i = 0; i < kc; ++i) {
+      for (int j = 0; j < kc; ++j) Rc(i, j) = R[(size_t)i * kc + j];
+      for (int a = 0; a < r; ++a) {
+        cd acc = 0.0;
+        for (int k = i; k < kc; ++k) acc += R[(size_t)i * kc + k] * M(keep[k], a);
+        RM(i, a) = acc;
+      }
+    }
+    const CM P1 = pinv_small(RM);      // r x kc
+    const CM P2 = pinv_small(Rc);      // kc x kc; Q^T = P2^T D'^T on range(D')
+    CM P2t(kc, kc);
+    for (int i = 0; i < kc; ++i)
+      for (int j = 0; j < kc; ++j) P2t(i, j) = P2(j, i);
+    const CM PP = cmul(P1, P2t);       // r x kc, pinv(phi) = PP D'^T
+    m->pinv.assign((size_t)r * nc, 0.0);
+    for (int a = 0; a < r; ++a)
+      for (int j = 0; j < kc; ++j) m->pinv[(size_t)a * nc + keep[j]] = PP(a, j);
+    m->have_pinv = true;
+    return FDMD_OK;
+  }
   CM P(r, r);
   for (int i = 0; i < r; ++i)
     for (int j = 0; j < r; ++j) {

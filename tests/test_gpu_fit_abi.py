@@ -288,6 +288,33 @@ def test_dmdc_abi_against_oracle_and_truth(abi, noise):
         L.fdmd_model_free(model)
 
 
+def test_encode_ill_conditioned_modes_takes_qr_route(abi):
+    """Two nearly parallel spatial modes (cond(phi) ~ 1e9 > 1e6): encode leaves
+    the Gram route for a Householder QR of the table with the reference's SVD
+    cut (pinv, linalg.py:93-104); the projection phi z matches numpy's
+    pinv(phi, rcond=1e-12) u."""
+    L, ctx = abi
+    rng = np.random.default_rng(3)
+    n, m = 400, 40
+    a = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    b = a + 1e-9 * (rng.standard_normal(n) + 1j * rng.standard_normal(n))
+    lam = np.array([0.95 * np.exp(0.3j), 0.9 * np.exp(0.7j)])
+    j = np.arange(m)
+    X = (np.outer(a, lam[0] ** j) + np.outer(b, lam[1] ** j)).real
+    X = X + 1e-12 * rng.standard_normal(X.shape)
+    model, sig, lam_fit = fit(abi, X, 4, 1, p=10, q=2)
+    try:
+        phi = phi_of(abi, model, n, 4)
+        sv = np.linalg.svd(phi, compute_uv=False)
+        assert sv[0] / sv[-1] > 1e6
+        u = X[:, 5]
+        z = encode(abi, model, u, 4)
+        z_np = np.linalg.pinv(phi, rcond=1e-12) @ u
+        assert np.linalg.norm(phi @ z - phi @ z_np) <= 1e-6 * np.linalg.norm(u)
+    finally:
+        L.fdmd_model_free(model)
+
+
 def test_abi_errors_and_concurrency(abi, small_golden):
     L, ctx = abi
     X = small_golden["dmd_rand6_X"]
