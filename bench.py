@@ -56,7 +56,7 @@ def fit_flops(n, m, r, p, q, modes="optdmd"):
     return sum(terms.values()), terms, l
 
 
-def executed_terms(n, m, r, p, q):
+def executed_terms(n, m, r, p, q, route="gram_projection"):
     """Flops libfdmd actually executes for the same fit (OptDMD, resident
     snapshots), split by arithmetic. Snapshot-Gram route
     (q >= 1): the sketch, every power pass Z = X^T Q and the first CholeskyQR
@@ -66,9 +66,20 @@ def executed_terms(n, m, r, p, q):
     small matrices; the projection Q^T S (2nml). Those run in FP64 (DMMA).
     The lift U = Q Ub (2nlr) and the modes (one column per conjugate pair,
     ~2nr^2) run on tcgen05 with an FP16 2-way split, FP32-accurate, into the
-    fp32 tables."""
+    fp32 tables.
+
+    route "gram_projection" (linalg.PROJ_GRAM_TOL: taken when the a-priori
+    error bound allows, e.g. config 3 with r = T): B = Q^T S also follows from
+    the snapshot Gram and its border X^T s_m (2nT), so there is no Q1 buffer,
+    no second CholeskyQR pass and no direct projection; the only tall GEMM is
+    the lift U = S [W R1^-1 Ub; 0] (2nmr, FP64 DMMA, written as the fp16 planes
+    of the tcgen05 modes product)."""
     T = m - 1
     l = min(r + p, T)
+    if q >= 1 and route == "gram_projection":
+        fp64 = {"snapshot Gram nT^2": 1.0 * n * T * T, "border X^T s_m 2nT": 2.0 * n * T,
+                "lift U = S Umap 2nmr": 2.0 * n * m * r}
+        return fp64, {"modes 2nr^2": 2.0 * n * r * r}
     if q == 0:   # explicit sketch: Y = X Omega, CholeskyQR2 (SYRK + TRSM + SYRK)
         fp64 = {"sketch 2nTl": 2.0 * n * T * l, "CholQR2 3nl^2": 3.0 * n * l * l, "projection 2nml": 2.0 * n * m * l}
     else:
@@ -78,8 +89,8 @@ def executed_terms(n, m, r, p, q):
     return fp64, tc
 
 
-def executed_flops(n, m, r, p, q):
-    fp64, tc = executed_terms(n, m, r, p, q)
+def executed_flops(n, m, r, p, q, route="gram_projection"):
+    fp64, tc = executed_terms(n, m, r, p, q, route)
     return sum(fp64.values()) + sum(tc.values())
 
 
@@ -427,6 +438,7 @@ def main():
     F_fit, terms, l = fit_flops(n, m, r, cfg["p"], cfg["q"])
     lm = fd.LMConfig(max_iters=cfg["lm_iters"])
 
+    route_used = [None]   # projection route the fit took (linalg.PROJ_GRAM_TOL)
     chunk_used = [None]   # frames per tcgen05 launch (U streamed once per launch; clusters multicast it)
 
     def one_step(record):
@@ -438,6 +450,7 @@ def main():
             model = fd.optdmd(data, r, lm_config=lm, svd_mode="randomized", seed=cfg["seed"],
                               oversample=cfg["p"], power_iters=cfg["q"], keep_basis=BASIS_MODE)
         ev[1].record()
+        route_used[0] = "gram_projection" if model.provenance["sketch"].get("gram_projection") else "direct"
         U = model.basis_U
         del model                                            # config 4 reconstructs from U, not the table
         mb = ModalBasis(U, W4, lam4, b4, dt=1.0)
@@ -576,10 +589,11 @@ def main():
                 "value_kind": "equivalent-work rate: SURVEY §8(d) reference-algorithm flops / fit time (an "
                               "algebraically equivalent restructuring counts as the terms it replaces); the "
                               "roofline-comparable rate is executed_tflops",
-                "executed_flops": executed_flops(n, m, r, cfg["p"], cfg["q"]),
-                "executed_terms_fp64_dmma": executed_terms(n, m, r, cfg["p"], cfg["q"])[0],
-                "executed_terms_tcgen05_fp32_accurate": executed_terms(n, m, r, cfg["p"], cfg["q"])[1],
-                "executed_tflops": round(executed_flops(n, m, r, cfg["p"], cfg["q"]) / fit_t / 1e12, 3)},
+                "projection_route": route_used[0],
+                "executed_flops": executed_flops(n, m, r, cfg["p"], cfg["q"], route_used[0]),
+                "executed_terms_fp64_dmma": executed_terms(n, m, r, cfg["p"], cfg["q"], route_used[0])[0],
+                "executed_terms_tcgen05_fp32_accurate": executed_terms(n, m, r, cfg["p"], cfg["q"], route_used[0])[1],
+                "executed_tflops": round(executed_flops(n, m, r, cfg["p"], cfg["q"], route_used[0]) / fit_t / 1e12, 3)},
         "reconstruct": recon,
         "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4), "peak_burst": round(peak_burst, 2),

@@ -74,6 +74,14 @@ int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda,
                    double* pair_stats, int64_t row_offset,
                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* C = A[n x K] * B[K x N] (A row-major f32/f64, FP64 DMMA) written as the fp16
+ * hi/lo planes of C * scale (row-major n x ldu, ldu = round_up(N, 8) <= 256,
+ * padding columns zero): the operand format of fdmd_tc_decode_ex. Replaces
+ * the lift U = Q Ub (linalg.py:88) when Q = S M is implicit. */
+int fdmd_tall_gemm_planes(const void* A, int a_dtype, int64_t lda, const double* B, int64_t ldb,
+                          void* uh, void* ul, int64_t ldu, double scale,
+                          int64_t n, int K, int N, int flags, void* stream);
+
 /* C[K1 x K2] (f64 row-major, ld ldc) = beta*C + A[n x K1]^T B[n x K2].
  * Deterministic fixed-order split reduction. symmetric=1 requires A==B, K1==K2. */
 size_t fdmd_tall_gram_workspace(int64_t n, int K1, int K2);
@@ -81,6 +89,15 @@ int fdmd_tall_gram(const void* A, int a_dtype, int a_layout, int64_t lda,
                    const void* B, int b_dtype, int b_layout, int64_t ldb,
                    double* C, int64_t ldc, double beta,
                    int64_t n, int K1, int K2, int symmetric,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* y[k] = beta*y[k] + sum_i A[i*lda + k] v[i*ldv]  (k < K): A^T v over the rows of a
+ * row-major f32/f64 A, v strided in the same dtype (e.g. a column of A), f64 out,
+ * fixed-order (deterministic) split sums. The border X^T s_m of the snapshot Gram
+ * S^T S next to X^T X (linalg.py:82-86: Q^T M with Q = X M1). */
+size_t fdmd_tall_tdot_workspace(int64_t n, int K);
+int fdmd_tall_tdot(const void* A, int dtype, int64_t lda, const void* v, int64_t ldv,
+                   int64_t n, int K, double* y, double beta,
                    void* workspace, size_t workspace_bytes, void* stream);
 
 /* Reconstruction: out[f*ldo + i] = sum_k D[k*ldd + i] * coef[k*ldcoef + f]

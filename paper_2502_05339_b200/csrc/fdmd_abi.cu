@@ -860,6 +860,35 @@ int fdmd_tall_gemm(const void* A, int a_dtype, int a_layout, int64_t lda, const 
   return FDMD_OK;
 }
 
+int fdmd_tall_gemm_planes(const void* A, int a_dtype, int64_t lda, const double* B, int64_t ldb, void* uh, void* ul,
+                          int64_t ldu, double scale, int64_t n, int K, int N, int flags, void* stream) {
+  if (n < 0 || K <= 0 || N <= 0) return fail(FDMD_ERR_INVALID, "tall_gemm_planes: bad sizes");
+  if (!A || !B || !uh || !ul) return fail(FDMD_ERR_INVALID, "tall_gemm_planes: null operand");
+  if (a_dtype != FDMD_F32 && a_dtype != FDMD_F64) return fail(FDMD_ERR_INVALID, "tall_gemm_planes: bad a_dtype");
+  if (lda < K || ldb < N) return fail(FDMD_ERR_INVALID, "tall_gemm_planes: lda < K or ldb < N");
+  if (ldu < N || ldu % 8 || ldu > 256 || ldu > (N + 7) / 8 * 8)
+    return fail(FDMD_ERR_INVALID, "tall_gemm_planes: ldu must be round_up(N, 8) <= 256");
+  if (n == 0) return FDMD_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int gx = tg_grid_x(n);
+  fdmd::TallGemmArgs a{};
+  a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.C = uh; a.C2 = ul; a.ldc = ldu; a.cscale = scale;
+  a.n = n; a.K = K; a.N = N;
+  a.reserve_sms = (flags & FDMD_SHARE_SMS) ? 8 : 0;
+  bool used = false;
+  int rc;
+  const int nf = pick_nf(N);
+#define TGP(TA, NFV) launch_tg_tma<TA, fdmd::LAYOUT_ROW, NFV, __half, fdmd::LAYOUT_PLANES, false>(a, s, gx, used)
+  if (a_dtype == FDMD_F32)
+    rc = nf == 1 ? TGP(float, 1) : nf == 2 ? TGP(float, 2) : nf == 4 ? TGP(float, 4) : TGP(float, 7);
+  else
+    rc = nf == 1 ? TGP(double, 1) : nf == 2 ? TGP(double, 2) : nf == 4 ? TGP(double, 4) : TGP(double, 7);
+#undef TGP
+  if (rc != FDMD_OK) return rc;
+  if (!used) return fail(FDMD_ERR_INVALID, "tall_gemm_planes: A not TMA-eligible (16-B aligned rows needed)");
+  return FDMD_OK;
+}
+
 size_t fdmd_tall_gram_workspace(int64_t n, int K1, int K2) {
   // large enough for either plan (a symmetric Gram has fewer tiles -> more splits)
   size_t need = 0;
@@ -1050,6 +1079,42 @@ int fdmd_colmajor_dot(const void* D, int d_dtype, int64_t ldd, const void* U, in
   const int len = r * nv;
   fdmd::split_sum_kernel<<<(len + 127) / 128, 128, 0, s>>>(part, splits, len, y);
   LAUNCH_CHECK("split_sum");
+  return FDMD_OK;
+}
+
+static int64_t tdot_splits(int64_t n) {
+  return std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, (int64_t)sm_count_cached() * 8));
+}
+
+size_t fdmd_tall_tdot_workspace(int64_t n, int K) {
+  return (size_t)tdot_splits(n) * std::max(K, 1) * sizeof(double) + 256;
+}
+
+int fdmd_tall_tdot(const void* A, int dtype, int64_t lda, const void* v, int64_t ldv, int64_t n, int K, double* y,
+                   double beta, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n < 0 || K <= 0 || lda < K || ldv < 1) return fail(FDMD_ERR_INVALID, "tall_tdot: bad sizes");
+  if (!A || !v || !y) return fail(FDMD_ERR_INVALID, "tall_tdot: null operand");
+  if (dtype != FDMD_F32 && dtype != FDMD_F64) return fail(FDMD_ERR_INVALID, "tall_tdot: bad dtype");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t splits = tdot_splits(n);
+  if (!workspace || workspace_bytes < (size_t)splits * K * sizeof(double))
+    return fail(FDMD_ERR_WORKSPACE, "tall_tdot workspace");
+  double* part = static_cast<double*>(workspace);
+  const int64_t rps = (n + splits - 1) / splits;
+  if (dtype == FDMD_F32)
+    fdmd::tall_tdot_kernel<float><<<(unsigned)splits, 256, 0, s>>>((const float*)A, lda, (const float*)v, ldv, n, K,
+                                                                     rps, part);
+  else
+    fdmd::tall_tdot_kernel<double><<<(unsigned)splits, 256, 0, s>>>((const double*)A, lda, (const double*)v, ldv, n,
+                                                                      K, rps, part);
+  LAUNCH_CHECK("tall_tdot");
+  if (beta == 0.0) {
+    fdmd::split_sum_kernel<<<(K + 127) / 128, 128, 0, s>>>(part, (int)splits, K, y);
+  } else {   // y += sum (streamed accumulation): sum into the tail of the workspace first
+    fdmd::split_sum_kernel<<<(K + 127) / 128, 128, 0, s>>>(part, (int)splits, K, part);
+    fdmd::axpy_kernel<<<(K + 127) / 128, 128, 0, s>>>(part, beta, y, K);
+  }
+  LAUNCH_CHECK("tall_tdot_reduce");
   return FDMD_OK;
 }
 

@@ -779,7 +779,10 @@ struct fdmd_model {
   int converged = 1;
   std::mutex mu;                  // guards the lazily built pseudo-inverse
   bool have_pinv = false;
-  std::vector<cd> pinv;           // r x 2*units: pinv(phi) = pinv @ raw^T
+  std::vector<cd> pinv;           // r x 2*units: pinv(phi) = pinv @ raw^T (or r x qcols: pinv @ Q^T)
+  double* qbuf = nullptr;         // ill-conditioned table: Householder Q (row-major n x ldq) of its columns
+  int64_t ldq = 0;
+  int qcols = 0;
 };
 
 namespace {
@@ -1113,6 +1116,7 @@ void free_model(fdmd_model* m) {
     cudaGetDevice(&prev);
     cudaSetDevice(m->device);
     cudaFree(m->raw);
+    if (m->qbuf) cudaFree(m->qbuf);
     cudaSetDevice(prev);
   }
   delete m;
@@ -1159,8 +1163,9 @@ int ensure_pinv(Dev& d, fdmd_model* m) {
     // cond(phi) > 1e6: QR of the table instead (modes.DeviceModes.pinv_rows'
     // ill-conditioned branch). phi = D M = D' M' over the nonzero raw columns
     // D' (a real mode's exactly-zero imaginary column carries nothing), D' = Q R
-    // by Householder on the device, pinv(phi) = pinv(R M') Q^T and, on range(D'),
-    // Q^T = pinv(R)^T D'^T: both small pseudo-inverses with the SVD cut 1e-12.
+    // by Householder on the device and pinv(phi) = pinv(R M') Q^T: the model keeps
+    // Q, and encode projects u onto it directly (Q^T u on the device) — going
+    // through R^-T D'^T u instead would square cond(D').
     std::vector<int> keep;
     for (int k = 0; k < nc; ++k)
       if (Gh[(size_t)k * nc + k] > 0.0) keep.push_back(k);
@@ -1170,13 +1175,17 @@ int ensure_pinv(Dev& d, fdmd_model* m) {
     std::vector<double> Isel((size_t)nc * kc, 0.0);
     for (int j = 0; j < kc; ++j) Isel[(size_t)keep[j] * kc + j] = 1.0;
     double* Id = d.alloc<double>(Isel.size());
-    double* Y = d.alloc<double>((size_t)m->n * ldy);
-    if (!Id || !Y) return fail(FDMD_ERR_CUDA, "pinv: device allocation failed (QR route)");
-    TRY(d.up(Isel.data(), Id, Isel.size() * sizeof(double)));
-    TRY(fdmd_tall_gemm(m->raw, m->dt, FDMD_COL, m->ldr, Id, kc, Y, FDMD_F64, FDMD_ROW, ldy, m->n, nc, kc, 0, nullptr,
-                       0, nullptr, 0, d.s));
+    double* Y = nullptr;
+    if (!Id || cudaMalloc(&Y, (size_t)m->n * ldy * sizeof(double)) != cudaSuccess)
+      return fail(FDMD_ERR_CUDA, "pinv: device allocation failed (QR route)");
+    auto drop = [&](int rc) { cudaFree(Y); return rc; };
+    if (int rc = d.up(Isel.data(), Id, Isel.size() * sizeof(double))) return drop(rc);
+    if (int rc = fdmd_tall_gemm(m->raw, m->dt, FDMD_COL, m->ldr, Id, kc, Y, FDMD_F64, FDMD_ROW, ldy, m->n, nc, kc, 0,
+                                nullptr, 0, nullptr, 0, d.s))
+      return drop(rc);
     std::vector<double> fix, R;
-    TRY(householder(d, Y, ldy, m->n, kc, fix, &R));
+    if (int rc = householder(d, Y, ldy, m->n, kc, fix, &R)) return drop(rc);
+    if (cudaStreamSynchronize(d.s) != cudaSuccess) return drop(fail(FDMD_ERR_CUDA, "pinv: QR route"));
     auto pinv_small = [](const CM& A) {   // SVD pseudo-inverse, cut 1e-12 sigma_max (linalg.py:93-104)
       CM U, V;
       std::vector<double> sv;
@@ -1202,24 +1211,18 @@ int ensure_pinv(Dev& d, fdmd_model* m) {
         for (int j = 0; j < P.n; ++j) Pt(j, i) = std::conj(P(i, j));
       return Pt;
     };
-    CM RM(kc, r), Rc(kc, kc);
-    for (int i = 0; i < kc; ++i) {
-      for (int j = 0; j < kc; ++j) Rc(i, j) = R[(size_t)i * kc + j];
+    CM RM(kc, r);
+    for (int i = 0; i < kc; ++i)
       for (int a = 0; a < r; ++a) {
         cd acc = 0.0;
         for (int k = i; k < kc; ++k) acc += R[(size_t)i * kc + k] * M(keep[k], a);
         RM(i, a) = acc;
       }
-    }
-    const CM P1 = pinv_small(RM);      // r x kc
-    const CM P2 = pinv_small(Rc);      // kc x kc; Q^T = P2^T D'^T on range(D')
-    CM P2t(kc, kc);
-    for (int i = 0; i < kc; ++i)
-      for (int j = 0; j < kc; ++j) P2t(i, j) = P2(j, i);
-    const CM PP = cmul(P1, P2t);       // r x kc, pinv(phi) = PP D'^T
-    m->pinv.assign((size_t)r * nc, 0.0);
-    for (int a = 0; a < r; ++a)
-      for (int j = 0; j < kc; ++j) m->pinv[(size_t)a * nc + keep[j]] = PP(a, j);
+    const CM P1 = pinv_small(RM);      // r x kc: pinv(phi) u = P1 (Q^T u)
+    m->pinv = P1.a;
+    m->qbuf = Y;
+    m->ldq = ldy;
+    m->qcols = kc;
     m->have_pinv = true;
     return FDMD_OK;
   }
@@ -1640,9 +1643,12 @@ int fdmd_dmdc_fit(fdmd_ctx* ctx, const fdmd_mat* states, const double* controls_
   if (rc == FDMD_OK) rc = ensure_pinv(d, model);
   if (rc == FDMD_OK) {
     // reduced_b = pinv(phi) U_hat B~ / dt with pinv(phi) = P D^T: y = (D^T Q2) (fix2 Ub2) B~
-    const int nc = 2 * model->units;
-    rc = fdmd_tall_gram(model->raw, model->dt, FDMD_COL, model->ldr, f2.Q, FDMD_F64, FDMD_ROW, f2.ldq, Gd, l, 0.0, n, nc, l,
-                        0, ws, gws, d.s);
+    // (ill-conditioned table: pinv(phi) = P Q^T with the table's Householder Q)
+    const int nc = model->qbuf ? model->qcols : 2 * model->units;
+    rc = model->qbuf ? fdmd_tall_gram(model->qbuf, FDMD_F64, FDMD_ROW, model->ldq, f2.Q, FDMD_F64, FDMD_ROW, f2.ldq, Gd,
+                                      l, 0.0, n, nc, l, 0, ws, gws, d.s)
+                     : fdmd_tall_gram(model->raw, model->dt, FDMD_COL, model->ldr, f2.Q, FDMD_F64, FDMD_ROW, f2.ldq, Gd,
+                                      l, 0.0, n, nc, l, 0, ws, gws, d.s);
     std::vector<double> DtQ2((size_t)nc * l);
     if (rc == FDMD_OK) rc = d.down(DtQ2.data(), Gd, DtQ2.size() * sizeof(double));
     if (rc == FDMD_OK) {
@@ -1736,12 +1742,24 @@ int fdmd_encode(fdmd_ctx* ctx, const fdmd_model* cmodel, const double* u_host, d
   void* ws = d.alloc<unsigned char>(wsb);
   if (!u || !y || !ws) return fail(FDMD_ERR_CUDA, "encode: device allocation failed");
   TRY(d.up(u_host, u, (size_t)n * sizeof(double)));
-  TRY(fdmd_colmajor_dot(model->raw, model->dt, model->ldr, u, FDMD_F64, n, n, nc, 1, y, ws, wsb, d.s));
-  std::vector<double> yh(nc);
-  TRY(d.down(yh.data(), y, nc * sizeof(double)));
+  int ny = nc;
+  if (model->qbuf) {   // ill-conditioned table: y = Q^T u (fdmd_tall_gram, K2 = 1)
+    ny = model->qcols;
+    const size_t gws = fdmd_tall_gram_workspace(n, ny, 1);
+    void* gw = d.alloc<unsigned char>(gws);
+    double* yq = d.alloc<double>((size_t)ny);
+    if (!gw || !yq) return fail(FDMD_ERR_CUDA, "encode: device allocation failed");
+    TRY(fdmd_tall_gram(model->qbuf, FDMD_F64, FDMD_ROW, model->ldq, u, FDMD_F64, FDMD_COL, n, yq, 1, 0.0, n, ny, 1,
+                       0, gw, gws, d.s));
+    y = yq;
+  } else {
+    TRY(fdmd_colmajor_dot(model->raw, model->dt, model->ldr, u, FDMD_F64, n, n, nc, 1, y, ws, wsb, d.s));
+  }
+  std::vector<double> yh(ny);
+  TRY(d.down(yh.data(), y, ny * sizeof(double)));
   for (int a = 0; a < r; ++a) {
     cd acc = 0.0;
-    for (int k = 0; k < nc; ++k) acc += model->pinv[(size_t)a * nc + k] * yh[k];
+    for (int k = 0; k < ny; ++k) acc += model->pinv[(size_t)a * ny + k] * yh[k];
     z_host[2 * a] = acc.real();
     z_host[2 * a + 1] = acc.imag();
   }

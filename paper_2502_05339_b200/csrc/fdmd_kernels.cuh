@@ -16,7 +16,7 @@
 
 namespace fdmd {
 
-enum { LAYOUT_ROW = 0, LAYOUT_COL = 1 };
+enum { LAYOUT_ROW = 0, LAYOUT_COL = 1, LAYOUT_PLANES = 2 };  // PLANES: row-major fp16 hi (C) + lo (C2) of C * cscale
 enum { DT_F32 = 0, DT_F64 = 1 };
 
 // ---------------------------------------------------------------------------
@@ -45,6 +45,8 @@ struct TallGemmArgs {
   // per CTA: sum_i |c|^2 and (max_i |c|^2, first argmax i)
   double* pair_stats;  // [gridDim.x][N/2][3] or nullptr
   int64_t row_offset;  // global row index of row 0 (for sharded argmax)
+  void* C2;            // LAYOUT_PLANES: the lo plane (C holds the hi plane), both ld ldc
+  double cscale;       // LAYOUT_PLANES: planes hold C * cscale split as hi + lo
 };
 
 struct TallGramArgs {

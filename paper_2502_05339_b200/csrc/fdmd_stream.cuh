@@ -141,6 +141,38 @@ __global__ void __launch_bounds__(256) colmajor_dot_kernel(const TD* __restrict_
   }
 }
 
+// ===========================================================================
+// Row-major transposed dot: part[split][k] = sum_{i in split} A[i*lda+k] v[i*ldv]
+// (y = A^T v over the rows; v may be a column of A itself, e.g. the last
+// snapshot: the border X^T s_m of the snapshot Gram). One thread per column,
+// a CTA walks its row range: each row is one coalesced read of the CTA's
+// columns; v[i] is a broadcast load. HBM-bound (A read once).
+// ===========================================================================
+template <typename TA>
+__global__ void __launch_bounds__(256) tall_tdot_kernel(const TA* __restrict__ A, int64_t lda,
+                                                        const TA* __restrict__ v, int64_t ldv, int64_t n, int K,
+                                                        int64_t rps, double* __restrict__ part) {
+  const int64_t r0 = (int64_t)blockIdx.x * rps;
+  const int64_t r1 = min(n, r0 + rps);
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t i = r0;
+    for (; i + 4 <= r1; i += 4) {   // four independent chains: loads stay in flight
+      a0 += (double)__ldcs(A + i * lda + k) * (double)v[i * ldv];
+      a1 += (double)__ldcs(A + (i + 1) * lda + k) * (double)v[(i + 1) * ldv];
+      a2 += (double)__ldcs(A + (i + 2) * lda + k) * (double)v[(i + 2) * ldv];
+      a3 += (double)__ldcs(A + (i + 3) * lda + k) * (double)v[(i + 3) * ldv];
+    }
+    for (; i < r1; ++i) a0 += (double)A[i * lda + k] * (double)v[i * ldv];
+    part[(int64_t)blockIdx.x * K + k] = (a0 + a1) + (a2 + a3);
+  }
+}
+
+__global__ void axpy_kernel(const double* __restrict__ x, double beta, double* __restrict__ y, int len) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < len) y[e] = beta * y[e] + x[e];
+}
+
 __global__ void split_sum_kernel(const double* __restrict__ part, int splits, int len,
                                  double* __restrict__ out) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;

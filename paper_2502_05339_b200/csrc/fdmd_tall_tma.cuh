@@ -8,6 +8,7 @@
 // Included by fdmd_kernels.cu after fdmd_tall.cuh (shares tg::, dmma884).
 #pragma once
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "fdmd_tall.cuh"
 
@@ -186,7 +187,20 @@ __device__ __forceinline__ void tt_consume(S& sm, const TallGemmArgs& args, cons
 #pragma unroll
           for (int f = 0; f < NFW; ++f) {
             const int col = wcol0 + f * 8 + 2 * t;
-            if (C != nullptr && !(args.debug & 2)) {
+            if (C_LAYOUT == LAYOUT_PLANES) {
+              // fp16 hi/lo planes of C * cscale (split_rows_kernel's split),
+              // zero in the padding columns N <= col < ldc
+              if (!(args.debug & 2) && col < args.ldc) {
+                const double x0 = col < args.N ? acc[mi][f][0] * args.cscale : 0.0;
+                const double x1 = col + 1 < args.N ? acc[mi][f][1] * args.cscale : 0.0;
+                const __half h0 = __double2half(x0), h1 = __double2half(x1);
+                const __half l0 = __double2half(x0 - (double)__half2float(h0));
+                const __half l1 = __double2half(x1 - (double)__half2float(h1));
+                const int64_t o = row * args.ldc + col;
+                *reinterpret_cast<__half2*>(static_cast<__half*>(args.C) + o) = __halves2half2(h0, h1);
+                *reinterpret_cast<__half2*>(static_cast<__half*>(args.C2) + o) = __halves2half2(l0, l1);
+              }
+            } else if (C != nullptr && !(args.debug & 2)) {
               if (C_LAYOUT == LAYOUT_ROW) {
                 TC* p = C + row * args.ldc + col;
                 if (sizeof(TC) == 8 && col + 1 < args.N && ((args.ldc & 1) == 0)) {

@@ -235,15 +235,56 @@ class CudaOps:
         return out
 
     # -- tcgen05 batched reconstruction (FP16 2-way split) -----------------
-    def tc_basis(self, D: Tall, ncols: Optional[int] = None):
+    def tall_tdot(self, A: Tall, col: int, K: int, out: Optional[torch.Tensor] = None,
+                  beta: float = 0.0) -> torch.Tensor:
+        """y (K, f64) = A[:, :K]^T A[:, col] over the rows of a row-major A (the
+        border X^T s_m of the snapshot Gram); out = beta*out + y when given."""
+        assert A.layout == "row" and 0 <= col < A.k and K <= A.k
+        L = _lib.lib()
+        y = torch.zeros((K,), dtype=torch.float64, device=A.buf.device) if out is None else out
+        wsb = int(L.fdmd_tall_tdot_workspace(A.n, K))
+        ws = self.ws.get(wsb, A.buf.device)
+        e0 = self._ev()
+        vp = A.buf.data_ptr() + col * A.buf.element_size()
+        _lib.check(L.fdmd_tall_tdot(_ptr(A.buf), _DT[A.dtype], A.ld, ctypes.c_void_p(vp), A.ld, A.n, K, _ptr(y),
+                                    float(beta if out is not None else 0.0), _ptr(ws), wsb, _stream()), "tall_tdot")
+        self._done("tall_tdot", 2.0 * A.n * K, e0, A.n * A.ld * A.buf.element_size())
+        self.launches += 2
+        return y
+
+    def tall_gemm_planes(self, A: Tall, B: torch.Tensor, bound: float = 2.0, alg_flops: Optional[float] = None,
+                         share_sms: bool = False) -> dict:
+        """A @ B on FP64 DMMA written straight into the fp16 hi/lo planes
+        tc_decode streams (row-major n x round_up(N, 8)); `bound` = a known
+        max |A @ B| (orthonormal columns: <= 1) fixes the plane scale."""
+        import math
+        assert A.layout == "row"
+        K, N = int(B.shape[0]), int(B.shape[1])
+        B = B.to(torch.float64).contiguous()
+        ldu = round_up(N, 8)
+        su = math.ldexp(1.0, 14 - math.frexp(float(bound))[1])
+        uh = torch.empty((A.n, ldu), dtype=torch.float16, device=A.buf.device)
+        ul = torch.empty_like(uh)
+        e0 = self._ev()
+        _lib.check(_lib.lib().fdmd_tall_gemm_planes(_ptr(A.buf), _DT[A.dtype], A.ld, _ptr(B), N, _ptr(uh), _ptr(ul),
+                                                    ldu, float(su), A.n, K, N, 2 if share_sms else 0, _stream()),
+                   "tall_gemm_planes")
+        self._done("tall_gemm", 2.0 * A.n * K * N if alg_flops is None else alg_flops, e0,
+                   A.n * K * A.buf.element_size() + 4 * A.n * ldu)
+        return {"uh": uh, "ul": ul, "ldu": ldu, "su": su, "n": A.n, "r": N}
+
+    def tc_basis(self, D: Tall, ncols: Optional[int] = None, bound: Optional[float] = None):
         """Split a column-major fp32 basis into the row-major fp16 hi/lo
-        planes the tcgen05 kernel streams (built once per basis)."""
+        planes the tcgen05 kernel streams (built once per basis). `bound`: a
+        known max |D| (orthonormal columns: <= 1) skips the scan and its sync."""
         import math
         assert D.layout == "col" and D.dtype == torch.float32
         r = D.k if ncols is None else ncols
         n = D.n
         ldu = round_up(r, 8)
-        if n:   # one read pass, no |U| temporary (a 40 GB abs() copy at config 4)
+        if bound is not None:
+            mx = float(bound)
+        elif n:   # one read pass, no |U| temporary (a 40 GB abs() copy at config 4)
             lo, hi = torch.aminmax(D.buf[:r, :n])
             mx = max(-float(lo.item()), float(hi.item()))
         else:

@@ -477,6 +477,7 @@ class _Basis:
     UtS: torch.Tensor
     stats: dict
     pre: Optional[dict] = None
+    implicit: bool = False         # A is the snapshot buffer S itself: U = S @ Umap (m x r)
 
 
 def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, power_iters,
@@ -495,7 +496,7 @@ def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, po
             raise ValueError(f"rank {r} out of range [1, {min(n_tot, T)}]")
         omega = la.draw_omega(T, l, seed)
         try:
-            f = la.sketch_factors(S, T, l, q, omega, data.shard, pending=pending, pre_svd=pre_svd)
+            f = la.sketch_factors(S, T, l, q, omega, data.shard, pending=pending, pre_svd=pre_svd, r=r)
         except BaseException:
             data.pending = pending      # a streamed upload that failed is redone by the next consumer
             raise
@@ -505,6 +506,7 @@ def _fit_basis(data: SnapshotMatrix, r: int, svd_mode: str, seed, oversample, po
                        UtS, f.stats)
         basis.stats.update(l=l, p=p, q=q)
         basis.pre = getattr(f, "pre", None)
+        basis.implicit = f.implicit
     elif svd_mode == "full":
         X = Tall(S.buf, "row", S.n, T)                       # X = states[:, :-1] (dmd.py:248)
         svd = la.truncated_svd(X, r, shard=data.shard, keep_device=True)
@@ -757,6 +759,31 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
     tc_src = None
     if basis.Umap is None:
         U = basis.A
+    elif basis.implicit and _TC_FIT and on_cuda and tdt == torch.float32 and r <= 256:
+        # projection from the snapshot Gram: no sketch buffer exists, U = S Umap
+        # is one FP64 DMMA pass over the snapshots (its error is O(u cond) —
+        # it cannot go through a 22-bit split of S), written as fp32 and split
+        # once into the fp16 planes the tcgen05 modes product (and the config-4
+        # reconstruction) stream; |U| <= 1 (orthonormal columns)
+        ops = dv.get_ops()
+        S_ = basis.A
+        n_loc = S_.n
+        U = None
+        if keep_basis and keep_basis != "planes":
+            with stage("lift.U=SM"):
+                U = alloc_tall(n_loc, r, torch.float32, "col", device=dev)
+                ops.tall_gemm(S_, basis.Umap, U, alg_flops=2.0 * n_loc * S_.k * r, share_sms=True)
+            with stage("lift.split_U"):
+                qt = ops.tc_basis(U, bound=2.0)
+        else:
+            # the DMMA epilogue writes the fp16 planes directly (no fp32 U)
+            with stage("lift.U=SM"):
+                qt = ops.tall_gemm_planes(S_, basis.Umap, bound=2.0, alg_flops=2.0 * n_loc * S_.k * r,
+                                          share_sms=True)
+            if keep_basis == "planes":
+                U = qt
+        basis.A = None
+        tc_src = {"planes": qt, "Umap": None, "n": n_loc}
     elif (_TC_FIT and on_cuda and tdt == torch.float32 and basis.A.dtype == torch.float64
           and basis.A.layout == "row" and basis.A.k <= 256):
         # fp32 tables: the lift U = Q Ub and the modes Q (Ub B^T) run on tcgen05

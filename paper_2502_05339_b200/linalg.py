@@ -12,6 +12,7 @@ numerically rank deficient.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -343,6 +344,9 @@ class SketchFactors:
     QtS: torch.Tensor  # l x m (Q^T S: both Q^T X and Q^T X'), fix already applied
     stats: dict
     fix: Optional[torch.Tensor] = None   # l x l upper triangular (None = identity)
+    # implicit: no sketch buffer — Q is S @ fix with fix the m x l map
+    # [W R1^-1; 0] (projection from the snapshot Gram); Q above is S itself
+    implicit: bool = False
 
     def right(self, M: torch.Tensor) -> torch.Tensor:
         """Small matrix to multiply the stored buffer by to get (Q @ M)."""
@@ -382,14 +386,48 @@ def _inv_upper(R: torch.Tensor) -> torch.Tensor:
 
 def _gram_factor(GX: torch.Tensor, M: torch.Tensor):
     """R = chol(M^T (X^T X) M): the CholeskyQR factor of the tall X M taken
-    from the snapshot Gram, or None when X M is too ill-conditioned for
-    CholeskyQR (the explicit path and its shifted / Householder fallbacks
-    then run on the tall buffer)."""
+    from the snapshot Gram, and its condition bound; (None, cond) when X M is
+    too ill-conditioned for CholeskyQR (the explicit path and its shifted /
+    Householder fallbacks then run on the tall buffer)."""
     G = M.t() @ GX @ M
     R = _chol_upper(0.5 * (G + G.t()))
-    if R is None or not _cond_upper(R) <= CHOLQR2_COND_LIMIT:
-        return None
-    return R
+    if R is None:
+        return None, float("inf")
+    cond = _cond_upper(R)
+    if not cond <= CHOLQR2_COND_LIMIT:
+        return None, cond
+    return R, cond
+
+
+# Projection from the snapshot Gram (DESIGN.md §4.3): with Q1 = X W R1^-1 and
+# R1 = chol(W^T G_X W), B = Q1^T S = (W R1^-1)^T (X^T S) follows from the
+# m x m Gram S^T S — no Q1 buffer, no second CholeskyQR pass, no direct Q^T S.
+# The price is accuracy: B's error grows from O(u ||S||) to O(u ||S|| cond(R1)),
+# and the rank-r subspace moves by that over the singular-value gap at r. The
+# route is taken only when the a-priori bound u cond(R1) sigma_1 / (sigma_r -
+# sigma_{r+1}) is below PROJ_GRAM_TOL (sigma from R1; sigma_{r+1} = 0 when
+# r = T, the whole row space). Measured against the reference (CPU probe,
+# configs 0/1/3 recipes): bound 1.6e-8 (config 3, r = T) -> sigma 2e-9,
+# lambda 4e-9; configs 0 / 1 (r inside the noise cluster) give bounds
+# 8e-7 .. 1e-5 and keep the direct route.
+PROJ_GRAM_TOL = float(os.environ.get("FDMD_PROJ_GRAM_TOL", "1e-7"))
+_PROJ_GRAM = os.environ.get("FDMD_PROJ_GRAM", "1") != "0"
+
+
+def _proj_gram_bound(R1: torch.Tensor, r: int, T: int) -> float:
+    """u cond(R1) sigma_1 / (sigma_r - sigma_{r+1}) with sigma = sv(R1) =
+    sv(X W) (exact 2-norm values: the Frobenius bound used for the CholeskyQR
+    switch overestimates cond by up to ~l)."""
+    u = np.finfo(np.float64).eps / 2
+    l = R1.shape[0]
+    if l <= r and r < T:
+        return float("inf")               # no estimate of the gap at r
+    sv = np.linalg.svd(R1.cpu().numpy(), compute_uv=False)
+    if not (sv[-1] > 0 and np.all(np.isfinite(sv))):
+        return float("inf")
+    nxt = float(sv[r]) if r < l else 0.0  # r = l = T: the whole row space, sigma_{r+1} = 0
+    gap = float(sv[r - 1]) - nxt
+    return u * float(sv[0] / sv[-1]) * float(sv[0]) / gap if gap > 0 else float("inf")
 
 
 def _cholqr_second_pass(Q: Tall, shard: Optional[Shard], stats: dict):
@@ -419,7 +457,7 @@ def _place_rows(Bsmall: torch.Tensor, rows: int, r0: int) -> torch.Tensor:
 
 def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Optional[Shard] = None,
                    Q: Optional[Tall] = None, pending: Optional[PendingUpload] = None,
-                   pre_svd=None, c0: int = 0) -> SketchFactors:
+                   pre_svd=None, c0: int = 0, r: Optional[int] = None) -> SketchFactors:
     """Range finder + power passes + projection for X = S[:, c0:c0+T]
     (linalg.py:62-90 with Householder QR replaced by CholeskyQR2).
 
@@ -437,6 +475,11 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     first stage (G_X, or Y / Y^T Y / X^T Y on the explicit route) runs chunk by
     chunk as rows land, in the shadow of the transfer.
     The returned QtS is Q^T S over all m columns of S.
+
+    `r` (the rank the caller truncates to) enables the projection from the
+    snapshot Gram (PROJ_GRAM_TOL): the Gram is then taken over all m columns
+    (S^T S), B = (W R1^-1)^T (X^T S) comes from it, and no n x l buffer is
+    ever written (the result has implicit=True: Q = S @ fix).
     """
     if pending is not None and c0 != 0:
         raise ValueError("a streamed upload sketches the leading columns only")
@@ -444,36 +487,52 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     dev = S.buf.device
     m = S.k
     stats: dict = {}
-    if Q is None:
-        with stage("sketch.alloc_Q"):
-            # slack rows: once Q is released, the two fp32 tables that follow it
-            # (basis U, n x r, and the raw modes, n x (r + #real modes)) fit in
-            # its block — together Q's size plus a few fp32 columns
-            slack = (16 * S.n + (64 << 20)) // (8 * max(l, 1)) + 1
-            Qb = alloc_tall(S.n + slack, l, torch.float64, "row", device=dev)
-            Q = Tall(Qb.buf, "row", S.n, l)
+    Qbox = [Q]
+
+    def _Q() -> Tall:
+        # the n x l sketch buffer, allocated only when a route writes it
+        if Qbox[0] is None:
+            with stage("sketch.alloc_Q"):
+                # slack rows: once Q is released, the two fp32 tables that follow it
+                # (basis U, n x r, and the raw modes, n x (r + #real modes)) fit in
+                # its block — together Q's size plus a few fp32 columns
+                slack = (16 * S.n + (64 << 20)) // (8 * max(l, 1)) + 1
+                Qb = alloc_tall(S.n + slack, l, torch.float64, "row", device=dev)
+                Qbox[0] = Tall(Qb.buf, "row", S.n, l)
+        return Qbox[0]
+
     Om = torch.as_tensor(np.asarray(omega, dtype=np.float64), device=dev)
     Omp = _place_rows(Om, m, c0)
     nl = float(S.n)
     Tc = c0 + T
     use_gram = gram_route_ok(T, l, q)
-    GX = G0 = Zp = None
+    # the projection route needs X^T S = [X^T X | X^T s_m] for a snapshot matrix
+    # (m = T + 1): the symmetric Gram of X plus one HBM-bound border pass
+    # (a 201 x 201 panel plan would pad to 240 and cost 3 partitions)
+    full = use_gram and r is not None and c0 == 0 and m - T in (0, 1)
+    border = full and m == T + 1
+    GX = XtS = bd = G0 = Zp = None
     if pending is not None and use_gram:
         GX = torch.zeros((T, T), dtype=torch.float64, device=dev)
+        bd = torch.zeros((T,), dtype=torch.float64, device=dev) if border else None
 
         def gram_stage(r0, rr):
             Sc = _rows(S, r0, rr)
             ops.tall_gram(Sc, Sc, K1=T, K2=T, symmetric=True, out=GX, beta=1.0, alg_flops=1.0 * rr * T * T)
+            if bd is not None:
+                ops.tall_tdot(Sc, T, T, out=bd, beta=1.0)
 
         with stage("sketch.stream_upload+XtX"):
             pending.run(gram_stage)
         GX = allreduce(shard, GX)
+        if bd is not None:
+            bd = allreduce(shard, bd)
     elif pending is not None:
         G0 = torch.zeros((l, l), dtype=torch.float64, device=dev)
         Zp = torch.zeros((T, l), dtype=torch.float64, device=dev) if q > 0 else None
 
         def first_stage(r0, rr):
-            Sc, Yc = _rows(S, r0, rr), _rows(Q, r0, rr)
+            Sc, Yc = _rows(S, r0, rr), _rows(_Q(), r0, rr)
             ops.tall_gemm(Sc, Omp, Yc, alg_flops=2.0 * rr * T * l)
             ops.tall_gram(Yc, Yc, symmetric=True, out=G0, beta=1.0)
             if Zp is not None:
@@ -490,13 +549,16 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
                                                 alg_flops=1.0 * nl * T * T))   # (c0+T)^2
             if c0:
                 GX = GX[c0:, c0:].contiguous()                               # T x T block of X
+        if border:
+            with stage("power.Xts_m"):
+                bd = allreduce(shard, ops.tall_tdot(S, T, T))                # X^T s_m
     implicit = False
     if GX is not None:
         # the sketch enters the algorithm only through Z = X^T Q1, Q1 = X Omega R0^-1,
         # R0 = chol((X Omega)^T (X Omega)): all of it follows from G_X, so Y = X Omega
         # and its Gram are never formed (counted as the terms they replace)
         with stage("sketch.implicit"):
-            R0 = _gram_factor(GX, Om)
+            R0, _ = _gram_factor(GX, Om)
         if R0 is not None:
             implicit = True
             R, fix = R0, None
@@ -504,11 +566,11 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     if not implicit:
         if G0 is None:
             with stage("sketch.Y=XOmega"):
-                ops.tall_gemm(S, Omp, Q, alg_flops=2 * nl * T * l)
+                ops.tall_gemm(S, Omp, _Q(), alg_flops=2 * nl * T * l)
         with stage("sketch.cholqr2"):
             # power iterations only need the span: one CholeskyQR pass unless this
             # is the last orthonormalisation (q = 0)
-            R, fix = cholqr2_deferred(Q, shard, stats, passes=2 if q == 0 else 1, G=G0)
+            R, fix = cholqr2_deferred(_Q(), shard, stats, passes=2 if q == 0 else 1, G=G0)
     M = Om
     for it in range(q):
         final = it == q - 1
@@ -524,7 +586,7 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
                 if float(dR.min()) > 1e-10 * float(dR.max()):
                     Z = GX @ (M @ _inv_upper(R))                          # T x l = X^T Q
             if Z is None:
-                Z = allreduce(shard, ops.tall_gram(S, Q, K1=Tc, alg_flops=2 * nl * T * l))[c0:]   # X^T Q
+                Z = allreduce(shard, ops.tall_gram(S, _Q(), K1=Tc, alg_flops=2 * nl * T * l))[c0:]   # X^T Q
                 if fix is not None:
                     Z = Z @ fix
         with stage("power.qr(Z)"):
@@ -533,31 +595,52 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
         R1 = None
         if GX is not None:
             with stage("power.chol(WtGW)"):
-                R1 = _gram_factor(GX, W)
+                R1, _ = _gram_factor(GX, W)
         if R1 is not None and not final:
             # a non-final power stage is span-only: Q = X W R1^-1 stays implicit and
             # the next Z = G_X W R1^-1 needs no tall pass
             R, fix = R1, None
             stats["gram_power_stages"] = stats.get("gram_power_stages", 0) + 1
             continue
+        if R1 is not None and full and _PROJ_GRAM:
+            with stage("power.proj_bound"):
+                bound = _proj_gram_bound(R1, r, T)
+            stats["proj_gram_bound"] = bound
+            if bound <= PROJ_GRAM_TOL:
+                # B = Q1^T S = (W R1^-1)^T (X^T S) from the snapshot Gram: Q stays
+                # implicit (Q = S [W R1^-1; 0]); no tall pass at all
+                with stage("project.QtS_from_gram"):
+                    M1 = W @ _inv_upper(R1)
+                    XtS = GX if bd is None else torch.cat([GX, bd[:, None]], dim=1)   # T x m
+                    QtS = M1.t() @ XtS                                       # l x m
+                stats["gram_projection"] = 1
+                return _svd_tail(S, QtS, c0, T, None, stats, _place_rows(M1, m, 0), implicit=True)
         if R1 is not None:
             # CholeskyQR2 with its first pass from the snapshot Gram: the tall GEMM
             # writes Q1 = X (W R1^-1) directly (no Y^T Y Gram, no triangular apply)
             with stage("power.Y=XWR1^-1"):
-                ops.tall_gemm(S, _place_rows(W @ _inv_upper(R1), m, c0), Q, alg_flops=2 * nl * T * l)
+                ops.tall_gemm(S, _place_rows(W @ _inv_upper(R1), m, c0), _Q(), alg_flops=2 * nl * T * l)
             with stage("power.cholqr2"):
-                R2, fix = _cholqr_second_pass(Q, shard, stats)
+                R2, fix = _cholqr_second_pass(_Q(), shard, stats)
             R = R2 @ R1
             stats["gram_first_pass"] = 1
         else:
             with stage("power.Y=XW"):
-                ops.tall_gemm(S, _place_rows(W, m, c0), Q, alg_flops=2 * nl * T * l)
+                ops.tall_gemm(S, _place_rows(W, m, c0), _Q(), alg_flops=2 * nl * T * l)
             with stage("power.cholqr2"):
-                R, fix = cholqr2_deferred(Q, shard, stats, passes=2 if final else 1)
+                R, fix = cholqr2_deferred(_Q(), shard, stats, passes=2 if final else 1)
+    Q = _Q()
     with stage("project.QtS"):
         QtS = allreduce(shard, ops.tall_gram(Q, S, alg_flops=2 * nl * m * l))     # l x m
         if fix is not None:
             QtS = fix.t() @ QtS
+    return _svd_tail(Q, QtS, c0, T, pre_svd, stats, fix)
+
+
+def _svd_tail(Q: Tall, QtS: torch.Tensor, c0: int, T: int, pre_svd, stats: dict, fix,
+              implicit: bool = False) -> SketchFactors:
+    """svd(B), B = Q^T X (the leading block of Q^T S), on the device — on a side
+    stream under the caller's Q-only tall work (`pre_svd`) when given."""
     pre = None
     with stage("small.svd(B)"):
         B = QtS[:, c0:c0 + T]
@@ -577,7 +660,7 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
                 t.record_stream(side)
         else:
             Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvdj" if B.is_cuda else None)
-    f = SketchFactors(Q, Ub, s, Vh, QtS, stats, fix)
+    f = SketchFactors(Q, Ub, s, Vh, QtS, stats, fix, implicit)
     f.pre = pre
     return f
 
@@ -655,7 +738,7 @@ def randomized_svd(M, r, oversample=10, power_iters=2, seed=None, *, omega=None,
     l = r + oversample
     _validate_rank(rows, cols, r, l)
     G = draw_omega(cols, l, seed) if omega is None else np.asarray(omega, dtype=np.float64)
-    f = sketch_factors(A, cols, l, power_iters, G, shard)
+    f = sketch_factors(A, cols, l, power_iters, G, shard, r=r)
     Ub_r = f.Ub[:, :r].contiguous()
     sgn = _canonical_signs(f.Q, f.right(Ub_r), shard)
     Ub_r = Ub_r * sgn[None, :]

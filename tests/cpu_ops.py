@@ -44,6 +44,14 @@ class CpuOps:
             return out
         return G.contiguous()
 
+    def tall_tdot(self, A, col, K, out=None, beta=0.0):
+        Av = _logical(A).to(torch.float64)
+        y = Av[:, :K].t() @ Av[:, col]
+        if out is not None:
+            out.copy_(beta * out + y)
+            return out
+        return y
+
     def decode(self, D, coef, out=None, ncols=None):
         r = D.k if ncols is None else ncols
         Dv = D.buf[:r, : D.n].to(torch.float64)

@@ -274,6 +274,55 @@ def test_tc_decode_planes_lift(dv, n, K, k):
     assert (np.linalg.norm(fr - wf, axis=1) / np.linalg.norm(wf, axis=1)).max() <= 4e-6
 
 
+@pytest.mark.parametrize("n,m,k,dt", [(100003, 201, 200, torch.float32), (70001, 161, 150, torch.float32),
+                                       (5000, 40, 37, torch.float64), (3001, 256, 256, torch.float32)])
+def test_tall_gemm_planes_lift(dv, n, m, k, dt):
+    """The lift U = S Umap on FP64 DMMA written straight into fp16 hi/lo planes
+    (fdmd_tall_gemm_planes, the projection-from-Gram route): S is an
+    ill-conditioned snapshot-like matrix and Umap = (its R factor)^-1 times an
+    orthogonal map, so U has orthonormal columns only through cancellation
+    (~cond(S) = 1e4) — the planes still hold U to FP32 accuracy, padding
+    columns are zero, and tc_decode from them reproduces U @ C."""
+    rng = np.random.default_rng(n + m + k)
+    sv = np.logspace(0, -4, m)
+    S = (np.linalg.qr(rng.standard_normal((n, m)))[0] * sv) @ np.linalg.qr(rng.standard_normal((m, m)))[0]
+    S = S.astype(np.float32 if dt == torch.float32 else np.float64)
+    Sd = S.astype(np.float64)
+    R = np.linalg.qr(Sd)[1]
+    Umap = np.linalg.solve(R, np.linalg.qr(rng.standard_normal((m, m)))[0][:, :k])
+    want = Sd @ Umap
+    ops = dv.get_ops()
+    St = _tall_from(dv, S, "row", dt)
+    pl = ops.tall_gemm_planes(St, torch.as_tensor(Umap, device="cuda"), bound=2.0)
+    U = (pl["uh"].double() + pl["ul"].double()).cpu().numpy() / pl["su"]
+    assert pl["ldu"] % 8 == 0 and np.all(U[:, k:] == 0.0)
+    err = np.linalg.norm(U[:, :k] - want, axis=0) / np.linalg.norm(want, axis=0)
+    assert err.max() <= 2e-6, err.max()
+    C = rng.standard_normal((k, 40))
+    fr = ops.tc_decode(pl, torch.as_tensor(C, device="cuda")).double().cpu().numpy()
+    wf = (want @ C.astype(np.float32).astype(np.float64)).T
+    assert (np.linalg.norm(fr - wf, axis=1) / np.linalg.norm(wf, axis=1)).max() <= 4e-6
+
+
+@pytest.mark.parametrize("n,m,dt", [(1000003, 201, torch.float32), (70001, 41, torch.float64), (5, 3, torch.float32)])
+def test_tall_tdot_border(dv, n, m, dt):
+    """fdmd_tall_tdot: the border X^T s_m of the snapshot Gram (last column of
+    a row-major padded S against the first T = m - 1), fp64 accumulation,
+    bitwise repeatable, and beta accumulation for the streamed upload."""
+    rng = np.random.default_rng(n + m)
+    S = rng.standard_normal((n, m)).astype(np.float32 if dt == torch.float32 else np.float64)
+    Sd = S.astype(np.float64)
+    want = Sd[:, : m - 1].T @ Sd[:, m - 1]
+    St = _tall_from(dv, S, "row", dt)
+    ops = dv.get_ops()
+    y = ops.tall_tdot(St, m - 1, m - 1)
+    np.testing.assert_allclose(y.cpu().numpy(), want, rtol=1e-12, atol=1e-12 * np.abs(Sd).max() ** 2 * n)
+    assert torch.equal(y, ops.tall_tdot(St, m - 1, m - 1))
+    acc = y.clone()
+    ops.tall_tdot(St, m - 1, m - 1, out=acc, beta=1.0)
+    np.testing.assert_allclose(acc.cpu().numpy(), 2 * want, rtol=1e-12, atol=1e-12 * np.abs(Sd).max() ** 2 * n)
+
+
 @pytest.mark.parametrize("nv", [1, 3, 8])
 def test_colmajor_dot(dv, nv):
     rng = np.random.default_rng(nv)
