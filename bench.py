@@ -70,15 +70,16 @@ def executed_terms(n, m, r, p, q, route="gram_projection"):
 
     route "gram_projection" (linalg.PROJ_GRAM_TOL: taken when the a-priori
     error bound allows, e.g. config 3 with r = T): B = Q^T S also follows from
-    the snapshot Gram and its border X^T s_m (2nT), so there is no Q1 buffer,
-    no second CholeskyQR pass and no direct projection; the only tall GEMM is
-    the lift U = S [W R1^-1 Ub; 0] (2nmr, FP64 DMMA, written as the fp16 planes
-    of the tcgen05 modes product)."""
+    the snapshot Gram and its border X^T s_m (2nT, carried by the same panel
+    kernel: fdmd_tall_gram_bordered), so there is no Q1 buffer, no second
+    CholeskyQR pass and no direct projection; the only tall GEMM is the lift
+    U = X (W R1^-1 Ub) (2nTr, FP64 DMMA, written as the fp16 planes of the
+    tcgen05 modes product)."""
     T = m - 1
     l = min(r + p, T)
     if q >= 1 and route == "gram_projection":
-        fp64 = {"snapshot Gram nT^2": 1.0 * n * T * T, "border X^T s_m 2nT": 2.0 * n * T,
-                "lift U = S Umap 2nmr": 2.0 * n * m * r}
+        fp64 = {"snapshot Gram nT^2": 1.0 * n * T * T, "border X^T s_m 2nT (same kernel)": 2.0 * n * T,
+                "lift U = S Umap 2nTr": 2.0 * n * T * r}
         return fp64, {"modes 2nr^2": 2.0 * n * r * r}
     if q == 0:   # explicit sketch: Y = X Omega, CholeskyQR2 (SYRK + TRSM + SYRK)
         fp64 = {"sketch 2nTl": 2.0 * n * T * l, "CholQR2 3nl^2": 3.0 * n * l * l, "projection 2nml": 2.0 * n * m * l}

@@ -91,6 +91,26 @@ int fdmd_tall_gram(const void* A, int a_dtype, int a_layout, int64_t lda,
                    int64_t n, int K1, int K2, int symmetric,
                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* C (K x (K+1), f64, row stride ldc) = beta*C + [A^T A | A^T a_K] over the rows of a
+ * row-major f32/f64 A with at least K + 1 columns (a_K = column K): the snapshot
+ * Gram X^T X together with the border X^T s_m of S^T S in ONE pass over S — what
+ * the projection B = Q^T M takes from a Gram when Q = X M1 (reference
+ * linalg.py:82-86, `Q.T @ M` after the power loop). The border rides in the
+ * symmetric panel kernel as 5 extra 8x8 blocks per diagonal warp tile;
+ * operands that kernel cannot take run the symmetric Gram + fdmd_tall_tdot.
+ * Deterministic fixed-order split reduction. */
+size_t fdmd_tall_gram_bordered_workspace(int64_t n, int K);
+int fdmd_tall_gram_bordered(const void* A, int dtype, int64_t lda, double* C, int64_t ldc, double beta,
+                            int64_t n, int K, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Host-side view of the panel-Gram schedule for a K x K (symmetric / bordered) Gram
+ * over n rows of elt_bytes elements: info[9] = {ok, partitions, cost (sum over
+ * partitions of the busiest SM sub-partition, in 8x8 DMMA blocks per k-step), cuts,
+ * row splits, K1p, K2p, border block column, blocks}; tiles (may be NULL) receives
+ * {i0, j0, kind, 8*partition+warp} per warp tile. Returns the tile count. No device work. */
+int fdmd_gram_plan_info(int64_t n, int K, int symmetric, int border, int elt_bytes, int* info, int* tiles,
+                        int max_tiles);
+
 /* y[k] = beta*y[k] + sum_i A[i*lda + k] v[i*ldv]  (k < K): A^T v over the rows of a
  * row-major f32/f64 A, v strided in the same dtype (e.g. a column of A), f64 out,
  * fixed-order (deterministic) split sums. The border X^T s_m of the snapshot Gram

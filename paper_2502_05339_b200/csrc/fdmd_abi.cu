@@ -314,6 +314,8 @@ struct PanelPlan {
   int cost = 0;              // sum over partitions of the busiest sub-partition (8x8 blocks)
   int WR = 5, WC = 7, P = 0, splits = 0, K1p = 0, K2p = 0, nba = 0, nbb = 0;
   int cl = 1;                // cluster size (the P partitions of a split share one row stream)
+  int border = 0, jb = 0;    // bordered symmetric Gram: extra column K (block column jb when K % 8 == 0)
+  int cuts = 0;              // pairs of adjacent full tiles re-cut into 3 + 4 + 3 block columns
   int64_t rows_per_split = 0;
   size_t smem = 0;
   fdmd::PanelTile tile[fdmd::tgp::MAXP * 8];
@@ -347,28 +349,74 @@ int gram_cluster_capacity(int cl, size_t smem);
 
 // Warp tiles of WR x WC 8x8 blocks cover the (upper, if symmetric) block grid;
 // they are packed into partitions of 8 consumer warps so that the DMMA count
-// per SM sub-partition (warps w, w+4) is balanced (greedy, heaviest first).
-PanelPlan panel_plan(int64_t n, int K1, int K2, int symmetric, size_t ea, size_t eb, int wc = 7) {
+// per SM sub-partition (warps w, w+4) is balanced: tiles sorted by weight, the
+// k-th heaviest sharing a sub-partition with the k-th lightest, sub-partitions
+// grouped into partitions by load (cost = sum over partitions of the busiest
+// sub-partition = SM time per 16-row chunk).
+//
+// Symmetric Grams (r02): 10 full (25 blocks) + 5 diagonal (15) tiles of a
+// 200 x 200 Gram leave two sub-partitions with 25 + 25 next to 25 + 15 (cost
+// 90 for 325 blocks). `cuts` pairs of horizontally adjacent full tiles are
+// re-cut into 3 + 4 + 3 block columns (15 + 20 + 15 blocks, kinds 4 / 5), one
+// more warp tile per cut: one cut gives 7 x 40 + 45 (cost 85). border = 1
+// (bordered Gram: C = [A^T A | A^T a_K], A with K + 1 columns): when K is a
+// multiple of 8 the border column block jb = K / 8 is attached to the diagonal
+// tiles (kind 3: 15 + 5 blocks; with one cut 6 x 45 + 2 x 40, cost 90 for 350
+// blocks — the separate HBM-bound X^T s_m pass is gone); otherwise column K
+// lies inside the last block columns of the tile grid and only has to be
+// loaded. The number of cuts is the one with the cheapest schedule.
+PanelPlan panel_plan(int64_t n, int K1, int K2, int symmetric, size_t ea, size_t eb, int wc = 7, int border = 0,
+                     int cuts = -1) {
   PanelPlan p;
   p.WC = wc;
   if (symmetric) { p.WR = 5; p.WC = 5; }
   const int MB = (K1 + 7) / 8, NB = (K2 + 7) / 8;
   const int TI = (MB + p.WR - 1) / p.WR, TJ = (NB + p.WC - 1) / p.WC;
+  // the border needs its own block column only when column K starts a block the
+  // tile grid does not cover (K % 8 == 0 and the block count a multiple of WR);
+  // otherwise it lies inside the last (possibly padding) block columns of the grid
+  const bool bcol = symmetric && border && K1 % 8 == 0 && K1 / 8 >= TJ * p.WC;
+  if (border && (!symmetric || gram_cluster_enabled())) return p;
+  if (symmetric && cuts < 0) {
+    // cheapest schedule over the number of cuts (ties: fewer partitions, fewer cuts)
+    PanelPlan best;
+    const int max_cuts = gram_cluster_enabled() ? 0 : 4;
+    for (int c = 0; c <= max_cuts; ++c) {
+      PanelPlan q = panel_plan(n, K1, K2, symmetric, ea, eb, wc, border, c);
+      if (!q.ok || q.cuts != c) break;
+      if (!best.ok || q.cost < best.cost || (q.cost == best.cost && q.P < best.P)) best = q;
+    }
+    return best;
+  }
   struct T { short i0, j0, kind; int w; };
   std::vector<T> ts;
+  int ncut = 0;
   for (int I = 0; I < TI; ++I)
     for (int J = 0; J < TJ; ++J) {
       if (symmetric && J < I) continue;
       const bool diag = symmetric && I == J;
-      ts.push_back({(short)(I * p.WR), (short)(J * p.WC), (short)(diag ? 2 : 1),
-                    diag ? p.WR * (p.WR + 1) / 2 : p.WR * p.WC});
+      if (symmetric && !diag && ncut < cuts && J + 1 < TJ) {
+        // (I, J) and (I, J + 1) as 3 + 4 + 3 block columns
+        const short i0 = (short)(I * p.WR), j0 = (short)(J * p.WC);
+        ts.push_back({i0, j0, 4, p.WR * 3});
+        ts.push_back({i0, (short)(j0 + 3), 5, p.WR * 4});
+        ts.push_back({i0, (short)(j0 + 7), 4, p.WR * 3});
+        ++ncut;
+        ++J;
+        continue;
+      }
+      const int w = diag ? p.WR * (p.WR + 1) / 2 + (bcol ? p.WR : 0) : p.WR * p.WC;
+      ts.push_back({(short)(I * p.WR), (short)(J * p.WC), (short)(diag ? (bcol ? 3 : 2) : 1), w});
     }
+  p.cuts = ncut;
+  p.border = border;
+  p.jb = bcol ? K1 / 8 : 0;
   const int ntile = (int)ts.size();
   p.P = (ntile + 7) / 8;
   if (p.P > fdmd::tgp::MAXP) return p;
   p.K1p = TI * p.WR * 8;
-  p.K2p = TJ * p.WC * 8;
-  p.nba = (int)((p.K1p * ea + 127) / 128);
+  p.K2p = std::max(TJ * p.WC * 8, bcol ? 8 * (p.jb + 1) : 0);
+  p.nba = (int)((std::max(p.K1p, bcol ? 8 * (p.jb + 1) : 0) * ea + 127) / 128);
   p.nbb = symmetric ? 0 : (int)((p.K2p * eb + 127) / 128);
   p.smem = (size_t)fdmd::tgp::STAGES * (p.nba + p.nbb) * fdmd::tgp::BOX_BYTES + 2 * fdmd::tgp::STAGES * 8 + 1024;
   if (p.smem > 227 * 1024) return p;
@@ -376,12 +424,23 @@ PanelPlan panel_plan(int64_t n, int K1, int K2, int symmetric, size_t ea, size_t
   const int nbins = p.P * 4;                       // (partition, sub-partition)
   std::vector<int> load(nbins, 0);
   std::vector<std::vector<const T*>> bin(nbins);
-  for (const T& x : ts) {
-    int best = -1;
-    for (int b = 0; b < nbins; ++b)
-      if (bin[b].size() < 2 && (best < 0 || load[b] < load[best])) best = b;
-    bin[best].push_back(&x);
-    load[best] += x.w;
+  // bins in order of their heavy tile; bin k also takes tile 2 * nbins - 1 - k
+  // (the k-th lightest, idle slots counted as weight 0)
+  for (int k = 0; k < nbins; ++k) {
+    if (k < ntile) { bin[k].push_back(&ts[k]); load[k] += ts[k].w; }
+    const int o = 2 * nbins - 1 - k;
+    if (o < ntile && o >= nbins) { bin[k].push_back(&ts[o]); load[k] += ts[o].w; }
+  }
+  // partitions = groups of 4 bins by decreasing load
+  std::vector<int> ord(nbins);
+  for (int k = 0; k < nbins; ++k) ord[k] = k;
+  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return load[x] > load[y]; });
+  {
+    std::vector<int> l2(nbins);
+    std::vector<std::vector<const T*>> b2(nbins);
+    for (int k = 0; k < nbins; ++k) { l2[k] = load[ord[k]]; b2[k] = bin[ord[k]]; }
+    load.swap(l2);
+    bin.swap(b2);
   }
   for (int part = 0; part < p.P; ++part) {
     int mx = 0;
@@ -514,7 +573,7 @@ int launch_gram_panel_cl(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaS
   CUtensorMap maps[2], tmaps[2];
   const void* ptr[2] = {a.A, a.B};
   const int64_t ld[2] = {a.lda, a.ldb};
-  const int kdim[2] = {a.K1, a.K2};
+  const int kdim[2] = {a.K1 + (SYM && pl.border ? 1 : 0), a.K2};   // bordered: column K is loaded too
   const size_t elt[2] = {sizeof(TA), sizeof(TB)};
   int nfull[2] = {0, 0}, tail[2] = {0, 0};
   // Full 128-B column blocks of a row-major n x K operand are one 3-D box
@@ -566,6 +625,7 @@ int launch_gram_panel_cl(const fdmd::TallGramArgs& a, const PanelPlan& pl, cudaS
   pa.b_full = SYM ? 0 : nfull[1];
   pa.a_tail = tail[0];
   pa.b_tail = SYM ? 0 : tail[1];
+  pa.jb = pl.jb;
   for (int i = 0; i < fdmd::tgp::MAXP * 8; ++i) pa.tile[i] = pl.tile[i];
   static thread_local int conf_t = -1;
   static thread_local size_t conf_smem = 0;
@@ -1117,6 +1177,103 @@ int fdmd_tall_tdot(const void* A, int dtype, int64_t lda, const void* v, int64_t
   LAUNCH_CHECK("tall_tdot_reduce");
   return FDMD_OK;
 }
+
+// ---- bordered symmetric Gram: C (K x (K + 1)) = [A^T A | A^T a_K] ----------
+// One pass over the rows of a row-major A with K + 1 columns: the snapshot
+// Gram X^T X and the border X^T s_m of S^T S (S = [X | s_m]) that the
+// projection from the snapshot Gram needs (linalg.sketch_factors). The panel
+// kernel carries the border as 5 extra 8x8 blocks per diagonal warp tile
+// (kind 3); operands the panel path cannot take fall back to the symmetric
+// Gram + fdmd_tall_tdot.
+static PanelPlan bordered_plan(const void* A, int dtype, int64_t lda, int64_t n, int K) {
+  PanelPlan none;
+  if (!panel_enabled() || n <= 0) return none;
+  if (!gram_sw_eligible(A, dtype, FDMD_ROW, lda, A, dtype, FDMD_ROW, lda, n)) return none;
+  return panel_plan(n, K, K, 1, dsize(dtype), dsize(dtype), 7, 1);
+}
+
+// Host-side introspection of the panel-Gram schedule (tests, DESIGN numbers):
+// info = {ok, P, cost, cuts, splits, K1p, K2p, jb, blocks}; tiles (optional, up to
+// 4 * max_tiles ints) = {i0, j0, kind, slot} per non-idle warp tile, slot =
+// 8 * partition + warp. No device work.
+int fdmd_gram_plan_info(int64_t n, int K, int symmetric, int border, int elt_bytes, int* info, int* tiles,
+                        int max_tiles) {
+  if (!info || K <= 0 || (elt_bytes != 4 && elt_bytes != 8)) return fail(FDMD_ERR_INVALID, "gram_plan_info: bad args");
+  PanelPlan pl = symmetric ? panel_plan(n, K, K, 1, (size_t)elt_bytes, (size_t)elt_bytes, 7, border)
+                           : panel_plan_best(n, K, K, 0, (size_t)elt_bytes, (size_t)elt_bytes);
+  int blocks = 0, nt = 0;
+  for (int i = 0; i < fdmd::tgp::MAXP * 8 && pl.ok; ++i) {
+    const fdmd::PanelTile& t = pl.tile[i];
+    if (t.kind == 0) continue;
+    const int w = t.kind == 1 ? pl.WR * pl.WC : t.kind == 2 ? pl.WR * (pl.WR + 1) / 2
+                  : t.kind == 3 ? pl.WR * (pl.WR + 1) / 2 + pl.WR : t.kind == 4 ? pl.WR * 3 : pl.WR * 4;
+    blocks += w;
+    if (tiles && nt < max_tiles) {
+      tiles[4 * nt + 0] = t.i0; tiles[4 * nt + 1] = t.j0; tiles[4 * nt + 2] = t.kind; tiles[4 * nt + 3] = i;
+    }
+    ++nt;
+  }
+  const int v[9] = {pl.ok ? 1 : 0, pl.P, pl.cost, pl.cuts, pl.splits, pl.K1p, pl.K2p, pl.jb, blocks};
+  for (int i = 0; i < 9; ++i) info[i] = v[i];
+  return nt;
+}
+
+size_t fdmd_tall_gram_bordered_workspace(int64_t n, int K) {
+  size_t need = std::max(fdmd_tall_gram_workspace(n, K, K), fdmd_tall_tdot_workspace(n, K));
+  for (size_t ea = 4; ea <= 8; ea += 4) {
+    PanelPlan q = panel_plan(n, K, K, 1, ea, ea, 7, 1);
+    if (q.ok) need = std::max(need, (size_t)q.splits * q.K1p * q.K2p * sizeof(double) + 256);
+  }
+  return need;
+}
+
+int fdmd_tall_gram_bordered(const void* A, int dtype, int64_t lda, double* C, int64_t ldc, double beta, int64_t n,
+                            int K, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n < 0 || K <= 0) return fail(FDMD_ERR_INVALID, "tall_gram_bordered: bad sizes n=%lld K=%d", (long long)n, K);
+  if (!A || !C) return fail(FDMD_ERR_INVALID, "tall_gram_bordered: null operand");
+  if (dtype != FDMD_F32 && dtype != FDMD_F64) return fail(FDMD_ERR_INVALID, "tall_gram_bordered: bad dtype");
+  if (lda < K + 1 || ldc < K + 1) return fail(FDMD_ERR_INVALID, "tall_gram_bordered: lda / ldc < K + 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  PanelPlan pl = bordered_plan(A, dtype, lda, n, K);
+  if (pl.ok) {
+    const size_t need = (size_t)pl.splits * pl.K1p * pl.K2p * sizeof(double);
+    if (!workspace || workspace_bytes < need)
+      return fail(FDMD_ERR_WORKSPACE, "tall_gram_bordered workspace %zu < %zu", workspace_bytes, need);
+    fdmd::TallGramArgs a{};
+    a.A = A; a.lda = lda; a.B = A; a.ldb = lda;
+    a.W = static_cast<double*>(workspace);
+    a.n = n; a.K1 = K; a.K2 = K; a.symmetric = 1;
+    const int rc = dtype == FDMD_F32 ? launch_gram_panel<float, float, 5, 5, true>(a, pl, s)
+                                     : launch_gram_panel<double, double, 5, 5, true>(a, pl, s);
+    if (rc != FDMD_OK) return rc;
+    // the mirror rule of the reduce is per 8x8 block, so column K (its own block
+    // column, or inside the last one) is read where the kernel wrote it
+    dim3 grid((K + 1 + 127) / 128, K);
+    fdmd::gram_reduce_kernel<<<grid, 128, 0, s>>>(a.W, pl.splits, K, K + 1, pl.K1p, pl.K2p, 1, C, ldc, beta, 0);
+    LAUNCH_CHECK("gram_reduce");
+    return FDMD_OK;
+  }
+  int rc = fdmd_tall_gram(A, dtype, FDMD_ROW, lda, A, dtype, FDMD_ROW, lda, C, ldc, beta, n, K, K, 1, workspace,
+                          workspace_bytes, stream);
+  if (rc != FDMD_OK) return rc;
+  const int64_t splits = tdot_splits(n);
+  if (workspace_bytes < (size_t)splits * K * sizeof(double)) return fail(FDMD_ERR_WORKSPACE, "tall_gram_bordered workspace");
+  const char* v = static_cast<const char*>(A) + (size_t)K * dsize(dtype);
+  double* part = static_cast<double*>(workspace);
+  const int64_t rps = (n + splits - 1) / splits;
+  if (dtype == FDMD_F32)
+    fdmd::tall_tdot_kernel<float><<<(unsigned)splits, 256, 0, s>>>((const float*)A, lda, (const float*)v, lda, n, K,
+                                                                     rps, part);
+  else
+    fdmd::tall_tdot_kernel<double><<<(unsigned)splits, 256, 0, s>>>((const double*)A, lda, (const double*)v, lda, n,
+                                                                      K, rps, part);
+  LAUNCH_CHECK("tall_tdot");
+  fdmd::split_sum_kernel<<<(K + 127) / 128, 128, 0, s>>>(part, (int)splits, K, part);
+  fdmd::strided_axpby_kernel<<<(K + 127) / 128, 128, 0, s>>>(part, beta, C + K, ldc, K);
+  LAUNCH_CHECK("tall_tdot_reduce");
+  return FDMD_OK;
+}
+
 
 int fdmd_table_apply(const void* R, int r_dtype, int64_t ldr, const int* src, const double* alpha,
                      const double* beta, void* D, int d_dtype, int64_t ldd, int64_t n, int ncols,

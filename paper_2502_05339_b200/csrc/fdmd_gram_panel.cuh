@@ -39,7 +39,12 @@ constexpr int BOX_BYTES = BR * 128;
 
 struct PanelTile {
   short i0, j0;   // first 8x8 block row / column of the warp tile
-  short kind;     // 0 idle, 1 full, 2 diagonal (symmetric: blocks ii <= jj only)
+  // 0 idle, 1 full WR x WC, 2 diagonal (symmetric: blocks ii <= jj only),
+  // 3 diagonal + its 5 border blocks (ii, jb) (bordered symmetric Gram),
+  // 4 / 5: full 5 x 3 / 5 x 4 (two adjacent 5 x 5 tiles of a symmetric Gram cut
+  // into 3 + 4 + 3 block columns so that every sub-partition carries 40-45
+  // blocks instead of 25 + 25 next to 25 + 15; host: panel_plan)
+  short kind;
   short pad;
 };
 
@@ -48,6 +53,7 @@ struct TallGramPanelArgs {
   int nba, nbb;                               // 128-B boxes per chunk row (A, B; nbb = 0 when symmetric)
   int lda_boxes, ldb_boxes;                   // boxes actually loaded (those holding columns < K)
   int a_full, b_full, a_tail, b_tail;         // full 128-B blocks (one 3-D TMA) + ragged block (2-D TMA)
+  int jb;                                     // bordered symmetric Gram: block column of the border (K / 8)
   PanelTile tile[tgp::MAXP * 8];
 };
 
@@ -141,10 +147,10 @@ __device__ __forceinline__ void panel_release(const PanelFeed& fd, bool feeder, 
   }
 }
 
-template <typename TA, typename TB, int WR, int WC, bool DIAG>
+template <typename TA, typename TB, int WR, int WC, bool DIAG, bool BORDER = false>
 __device__ __forceinline__ void panel_consume(const PanelFeed& fd, bool feeder, const unsigned char* b_base,
                                               int b_stage_bytes, uint64_t* full, uint64_t* empty, int i0, int j0,
-                                              int lane, double* __restrict__ W, int K2p) {
+                                              int lane, double* __restrict__ W, int K2p, int jb = 0) {
   const int g = lane >> 2, t = lane & 3;
   // byte offsets of this lane's fragments for the two row parities of a k-step.
   // Column 8 ii + c lands in box (c + 8 ii) / W at a swizzled position that
@@ -162,6 +168,15 @@ __device__ __forceinline__ void panel_consume(const PanelFeed& fd, bool feeder, 
     for (int ii = 0; ii < NA; ++ii) offa[ii][p] = panel_offset<TA>(row, 8 * (i0 + ii) + g);
 #pragma unroll
     for (int jj = 0; jj < NB; ++jj) offb[jj][p] = panel_offset<TB>(row, 8 * (j0 + jj) + g);
+  }
+  // border blocks (ii, jb): the extra column block of a bordered symmetric Gram
+  int offbd[2] = {0, 0};
+  double accb[BORDER ? WR : 1][2];
+  if (BORDER) {
+#pragma unroll
+    for (int p = 0; p < 2; ++p) offbd[p] = panel_offset<TB>(p + 2 * t, 8 * jb + g);
+#pragma unroll
+    for (int ii = 0; ii < WR; ++ii) accb[ii][0] = accb[ii][1] = 0.0;
   }
   double acc[WR][WC][2];
 #pragma unroll
@@ -190,6 +205,11 @@ __device__ __forceinline__ void panel_consume(const PanelFeed& fd, bool feeder, 
 #pragma unroll
         for (int jj = 0; jj < WC; ++jj)
           if (!DIAG || ii <= jj) dmma884(acc[ii][jj], a[ii], b[jj]);
+      if (BORDER) {
+        const double bd = (double)*reinterpret_cast<const TB*>(pb + offbd[p] + hi);
+#pragma unroll
+        for (int ii = 0; ii < WR; ++ii) dmma884(accb[ii], a[ii], bd);
+      }
     }
     panel_release(fd, feeder, lane, c, s, ph, full, empty);
     if (++s == tgp::STAGES) { s = 0; ph ^= 1; }
@@ -203,6 +223,8 @@ __device__ __forceinline__ void panel_consume(const PanelFeed& fd, bool feeder, 
       const int j = 8 * (j0 + jj) + 2 * t;
       *reinterpret_cast<double2*>(W + (int64_t)i * K2p + j) = make_double2(acc[ii][jj][0], acc[ii][jj][1]);
     }
+    if (BORDER)
+      *reinterpret_cast<double2*>(W + (int64_t)i * K2p + 8 * jb + 2 * t) = make_double2(accb[ii][0], accb[ii][1]);
   }
 }
 
@@ -266,11 +288,27 @@ tall_gram_panel_kernel(const __grid_constant__ CUtensorMap amap, const __grid_co
   double* W = args.W + (int64_t)blockIdx.y * args.K1p * args.K2p;
   const unsigned char* bb = SYM ? fd.a_sm : fd.b_sm;
   const int bst = SYM ? fd.a_stage : fd.b_stage;
+  bool done = true;
   if (tl.kind == 1) {
     panel_consume<TA, TB, WR, WC, false>(fd, feeder, bb, bst, full, empty, tl.i0, tl.j0, lane, W, args.K2p);
   } else if (SYM && tl.kind == 2) {
     panel_consume<TA, TB, WR, WC, true>(fd, feeder, bb, bst, full, empty, tl.i0, tl.j0, lane, W, args.K2p);
-  } else {   // idle slot: keep the ring moving
+  } else {
+    done = false;
+    if constexpr (SYM && CL == 1) {   // bordered / rebalanced symmetric plans (host: panel_plan)
+      done = true;
+      if (tl.kind == 3)
+        panel_consume<TA, TB, WR, WC, true, true>(fd, feeder, bb, bst, full, empty, tl.i0, tl.j0, lane, W,
+                                                  args.K2p, pa.jb);
+      else if (tl.kind == 4)
+        panel_consume<TA, TB, WR, 3, false>(fd, feeder, bb, bst, full, empty, tl.i0, tl.j0, lane, W, args.K2p);
+      else if (tl.kind == 5)
+        panel_consume<TA, TB, WR, 4, false>(fd, feeder, bb, bst, full, empty, tl.i0, tl.j0, lane, W, args.K2p);
+      else
+        done = false;
+    }
+  }
+  if (!done) {   // idle slot: keep the ring moving
     int s = 0;
     unsigned ph = 0;
     for (int64_t c = 0; c < fd.nchunks; ++c) {

@@ -173,6 +173,13 @@ __global__ void axpy_kernel(const double* __restrict__ x, double beta, double* _
   if (e < len) y[e] = beta * y[e] + x[e];
 }
 
+// y[e * ldy] = beta * y[e * ldy] + x[e] (a column of a row-major matrix; beta = 0 overwrites)
+__global__ void strided_axpby_kernel(const double* __restrict__ x, double beta, double* __restrict__ y, int64_t ldy,
+                                     int len) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < len) y[e * ldy] = (beta == 0.0) ? x[e] : beta * y[e * ldy] + x[e];
+}
+
 __global__ void split_sum_kernel(const double* __restrict__ part, int splits, int len,
                                  double* __restrict__ out) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;

@@ -133,6 +133,7 @@ __device__ __forceinline__ void tt_consume(S& sm, const TallGemmArgs& args, cons
   // upper-triangular B (B[k][j] = 0 for k > j): k-chunks past this warp's last
   // column contribute nothing and are skipped (still consumed from the ring)
   const int kc_last = args.b_upper ? (wcol0 + 8 * NFW - 1) / tt::BK : INT32_MAX;
+  const int ks_tail = (args.K - (nk - 1) * tt::BK + 3) / 4;
   double st_sum[NFW], st_max[NFW];
   int64_t st_idx[NFW];
 #pragma unroll
@@ -152,8 +153,12 @@ __device__ __forceinline__ void tt_consume(S& sm, const TallGemmArgs& args, cons
     mbar_wait(&sm.full[s], phase);
     const unsigned char* As = reinterpret_cast<const unsigned char*>(sm.A[s]);
     if (kc <= kc_last) {
+      // the last k-chunk only runs the k-steps that hold columns < K (K = 200:
+      // 12.5 chunks, the zero half of chunk 13 is skipped)
+      const int ksn = (kc == nk - 1) ? ks_tail : tt::BK / 4;
 #pragma unroll
       for (int ks = 0; ks < tt::BK / 4; ++ks) {
+        if (ks >= ksn) break;
         double a[4], b[NFW];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {

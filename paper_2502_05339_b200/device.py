@@ -235,6 +235,25 @@ class CudaOps:
         return out
 
     # -- tcgen05 batched reconstruction (FP16 2-way split) -----------------
+    def tall_gram_bordered(self, A: Tall, K: int, out: Optional[torch.Tensor] = None, beta: float = 0.0,
+                           alg_flops: Optional[float] = None) -> torch.Tensor:
+        """out[K x (K+1)] = beta * out + [A[:, :K]^T A[:, :K] | A[:, :K]^T A[:, K]] in one
+        pass over a row-major A (the snapshot Gram X^T X with the border X^T s_m)."""
+        assert A.layout == "row" and K + 1 <= A.k
+        L = _lib.lib()
+        if out is None:
+            out = torch.empty((K, K + 1), dtype=torch.float64, device=A.buf.device)
+        wsb = int(L.fdmd_tall_gram_bordered_workspace(A.n, K))
+        ws = self.ws.get(wsb, A.buf.device)
+        e0 = self._ev()
+        _lib.check(L.fdmd_tall_gram_bordered(_ptr(A.buf), _DT[A.dtype], A.ld, _ptr(out), out.stride(0), float(beta),
+                                             A.n, K, _ptr(ws), wsb, _stream()), "tall_gram_bordered")
+        if alg_flops is None:
+            alg_flops = 1.0 * A.n * K * K + 2.0 * A.n * K
+        self._done("tall_gram", alg_flops, e0, A.n * (K + 1) * A.buf.element_size())
+        self.launches += 2
+        return out
+
     def tall_tdot(self, A: Tall, col: int, K: int, out: Optional[torch.Tensor] = None,
                   beta: float = 0.0) -> torch.Tensor:
         """y (K, f64) = A[:, :K]^T A[:, col] over the rows of a row-major A (the

@@ -769,17 +769,19 @@ def optdmd(data, r, init=None, lm_config=None, svd_mode="full", seed=None, *, ov
         S_ = basis.A
         n_loc = S_.n
         U = None
+        # rows >= T of the m x r map are zero (X = S[:, :T]): the product runs over
+        # K = T columns, and the kernel skips the empty half of the last k-chunk
+        Um = basis.Umap[:T].contiguous()
         if keep_basis and keep_basis != "planes":
             with stage("lift.U=SM"):
                 U = alloc_tall(n_loc, r, torch.float32, "col", device=dev)
-                ops.tall_gemm(S_, basis.Umap, U, alg_flops=2.0 * n_loc * S_.k * r, share_sms=True)
+                ops.tall_gemm(S_, Um, U, alg_flops=2.0 * n_loc * T * r, share_sms=True)
             with stage("lift.split_U"):
                 qt = ops.tc_basis(U, bound=2.0)
         else:
             # the DMMA epilogue writes the fp16 planes directly (no fp32 U)
             with stage("lift.U=SM"):
-                qt = ops.tall_gemm_planes(S_, basis.Umap, bound=2.0, alg_flops=2.0 * n_loc * S_.k * r,
-                                          share_sms=True)
+                qt = ops.tall_gemm_planes(S_, Um, bound=2.0, alg_flops=2.0 * n_loc * T * r, share_sms=True)
             if keep_basis == "planes":
                 U = qt
         basis.A = None

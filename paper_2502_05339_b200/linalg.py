@@ -507,26 +507,29 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
     Tc = c0 + T
     use_gram = gram_route_ok(T, l, q)
     # the projection route needs X^T S = [X^T X | X^T s_m] for a snapshot matrix
-    # (m = T + 1): the symmetric Gram of X plus one HBM-bound border pass
-    # (a 201 x 201 panel plan would pad to 240 and cost 3 partitions)
+    # (m = T + 1): the bordered symmetric Gram (fdmd_tall_gram_bordered: the border
+    # rides in the panel kernel's diagonal warp tiles; a plain 201 x 201 panel
+    # plan would pad to 240 and cost 3 partitions)
     full = use_gram and r is not None and c0 == 0 and m - T in (0, 1)
     border = full and m == T + 1
     GX = XtS = bd = G0 = Zp = None
     if pending is not None and use_gram:
-        GX = torch.zeros((T, T), dtype=torch.float64, device=dev)
-        bd = torch.zeros((T,), dtype=torch.float64, device=dev) if border else None
+        # bordered: [X^T X | X^T s_m] accumulates in one T x (T + 1) block, one
+        # kernel per chunk (the border rides in the symmetric panel Gram)
+        GXb = torch.zeros((T, T + 1 if border else T), dtype=torch.float64, device=dev)
 
         def gram_stage(r0, rr):
             Sc = _rows(S, r0, rr)
-            ops.tall_gram(Sc, Sc, K1=T, K2=T, symmetric=True, out=GX, beta=1.0, alg_flops=1.0 * rr * T * T)
-            if bd is not None:
-                ops.tall_tdot(Sc, T, T, out=bd, beta=1.0)
+            if border:
+                ops.tall_gram_bordered(Sc, T, out=GXb, beta=1.0, alg_flops=1.0 * rr * T * T + 2.0 * rr * T)
+            else:
+                ops.tall_gram(Sc, Sc, K1=T, K2=T, symmetric=True, out=GXb, beta=1.0, alg_flops=1.0 * rr * T * T)
 
         with stage("sketch.stream_upload+XtX"):
             pending.run(gram_stage)
-        GX = allreduce(shard, GX)
-        if bd is not None:
-            bd = allreduce(shard, bd)
+        GXb = allreduce(shard, GXb)
+        GX = GXb[:, :T].contiguous()
+        bd = GXb[:, T].contiguous() if border else None
     elif pending is not None:
         G0 = torch.zeros((l, l), dtype=torch.float64, device=dev)
         Zp = torch.zeros((T, l), dtype=torch.float64, device=dev) if q > 0 else None
@@ -543,15 +546,18 @@ def sketch_factors(S: Tall, T: int, l: int, q: int, omega: np.ndarray, shard: Op
         G0 = allreduce(shard, G0)
         if Zp is not None:
             Zp = allreduce(shard, Zp)
+    elif use_gram and border:
+        with stage("power.XtX+Xts_m"):
+            # [X^T X | X^T s_m] in one pass (c0 = 0 on this route)
+            GXb = allreduce(shard, ops.tall_gram_bordered(S, T, alg_flops=1.0 * nl * T * T + 2.0 * nl * T))
+            GX = GXb[:, :T].contiguous()
+            bd = GXb[:, T].contiguous()
     elif use_gram:
         with stage("power.XtX"):
             GX = allreduce(shard, ops.tall_gram(S, S, K1=Tc, K2=Tc, symmetric=True,
                                                 alg_flops=1.0 * nl * T * T))   # (c0+T)^2
             if c0:
                 GX = GX[c0:, c0:].contiguous()                               # T x T block of X
-        if border:
-            with stage("power.Xts_m"):
-                bd = allreduce(shard, ops.tall_tdot(S, T, T))                # X^T s_m
     implicit = False
     if GX is not None:
         # the sketch enters the algorithm only through Z = X^T Q1, Q1 = X Omega R0^-1,

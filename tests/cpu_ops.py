@@ -44,6 +44,14 @@ class CpuOps:
             return out
         return G.contiguous()
 
+    def tall_gram_bordered(self, A, K, out=None, beta=0.0, alg_flops=None):
+        Av = _logical(A).to(torch.float64)
+        G = Av[:, :K].t() @ Av[:, :K + 1]
+        if out is not None:
+            out.copy_(G if beta == 0.0 else beta * out + G)
+            return out
+        return G.contiguous()
+
     def tall_tdot(self, A, col, K, out=None, beta=0.0):
         Av = _logical(A).to(torch.float64)
         y = Av[:, :K].t() @ Av[:, col]

@@ -184,3 +184,48 @@ def test_snapshot_gram_route_guard():
     assert not la.gram_route_ok(200, 200, 0)      # q = 0: no power stage to replace
     assert not la.gram_route_ok(1000, 20, 2)      # long series: n T^2 >> 2 n T l (1 + q)
     assert not la.gram_route_ok(20000, 256, 30)   # T x T f64 block over the 2 GB budget
+
+
+@pytest.mark.parametrize("K,border,eb", [(200, 0, 4), (200, 1, 4), (200, 1, 8), (160, 0, 8), (150, 1, 4), (100, 1, 4),
+                                         (256, 1, 4), (24, 1, 8), (8, 1, 8), (7, 1, 4)])
+def test_panel_gram_schedule_covers_every_block_once(K, border, eb):
+    """Host planner of the symmetric / bordered panel Gram (fdmd_gram_plan_info, no
+    device work): the warp tiles — 5 x 5 full, diagonal, diagonal + border blocks,
+    and the 5 x 3 / 5 x 4 re-cut pairs — cover every 8x8 block on or above the
+    diagonal exactly once, the border column block once per block row, with at
+    most one tile per warp slot; cost = sum over partitions of the busiest SM
+    sub-partition (warps w, w + 4)."""
+    from paper_2502_05339_b200 import _lib
+    L = _lib.lib()
+    info = (ctypes.c_int * 9)()
+    tiles = (ctypes.c_int * (4 * 64))()
+    nt = L.fdmd_gram_plan_info(50331648, K, 1, border, eb, info, tiles, 64)
+    ok, P, cost, cuts, splits, K1p, K2p, jb, blocks = list(info)
+    assert ok == 1 and 0 < nt <= 8 * P
+    t = np.array(list(tiles)[:4 * nt]).reshape(nt, 4)
+    MB = (K + 7) // 8
+    cover = np.zeros((K1p // 8, max(K2p // 8, MB + 1)), dtype=int)
+    shape = {1: (5, 5), 2: (5, 5), 3: (5, 5), 4: (5, 3), 5: (5, 4)}
+    load = np.zeros((P, 4), dtype=int)
+    for i0, j0, kind, slot in t:
+        h, w = shape[kind]
+        wgt = 0
+        for ii in range(h):
+            for jj in range(w):
+                if kind in (2, 3) and ii > jj:
+                    continue
+                cover[i0 + ii, j0 + jj] += 1
+                wgt += 1
+            if kind == 3:
+                cover[i0 + ii, jb] += 1
+                wgt += 1
+        load[slot // 8, slot % 4] += wgt
+    assert len(set(t[:, 3].tolist())) == nt                       # one tile per warp slot
+    for bi in range(MB):
+        for bj in range(bi, MB):
+            assert cover[bi, bj] == 1, (bi, bj)
+        if border:   # column K lives in block column K // 8: covered once for every block row
+            assert cover[bi, K // 8] == 1 and K2p >= 8 * (K // 8 + 1), (bi, jb)
+    assert cost == int(load.max(axis=1).sum()) and blocks == int(load.sum())
+    if K == 200:   # the benched shapes: 7 x 40 + 45 (plain), 6 x 45 + 2 x 40 (bordered)
+        assert (P, cuts, cost) == (2, 1, 90 if border else 85)

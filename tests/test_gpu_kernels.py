@@ -323,6 +323,37 @@ def test_tall_tdot_border(dv, n, m, dt):
     np.testing.assert_allclose(acc.cpu().numpy(), 2 * want, rtol=1e-12, atol=1e-12 * np.abs(Sd).max() ** 2 * n)
 
 
+@pytest.mark.parametrize("n,K,dt", [(300007, 200, torch.float32), (70001, 200, torch.float64),
+                                    (50021, 150, torch.float32), (4099, 20, torch.float64),
+                                    (65536, 100, torch.float32), (33333, 256, torch.float32),
+                                    (20011, 8, torch.float64), (5, 3, torch.float32)])
+def test_tall_gram_bordered(dv, n, K, dt):
+    """fdmd_tall_gram_bordered: [X^T X | X^T s_m] in one pass (the border rides in
+    the diagonal warp tiles of the symmetric panel Gram when K % 8 == 0, inside
+    the last block column otherwise; tiny / unaligned operands fall back to the
+    symmetric Gram + tall_tdot) against fp64 products; bitwise repeatable; beta
+    accumulation (streamed upload); identical to the separate Gram + border."""
+    rng = np.random.default_rng(n + K)
+    S = rng.standard_normal((n, K + 1)).astype(np.float32 if dt == torch.float32 else np.float64)
+    Sd = S.astype(np.float64)
+    want = Sd[:, :K].T @ Sd
+    St = _tall_from(dv, S, "row", dt)
+    ops = dv.get_ops()
+    G = ops.tall_gram_bordered(St, K)
+    assert G.shape == (K, K + 1)
+    tol = 1e-12 * np.abs(Sd).max() ** 2 * n
+    np.testing.assert_allclose(G.cpu().numpy(), want, rtol=1e-12, atol=tol)
+    np.testing.assert_allclose(G[:, :K].cpu().numpy(), G[:, :K].t().cpu().numpy(), rtol=1e-14, atol=tol * 1e-2)
+    assert torch.equal(G, ops.tall_gram_bordered(St, K))
+    acc = G.clone()
+    ops.tall_gram_bordered(St, K, out=acc, beta=1.0)
+    np.testing.assert_allclose(acc.cpu().numpy(), 2 * want, rtol=1e-12, atol=2 * tol)
+    G2 = ops.tall_gram(St, St, K1=K, K2=K, symmetric=True)
+    np.testing.assert_allclose(G[:, :K].cpu().numpy(), G2.cpu().numpy(), rtol=1e-13, atol=tol * 0.1)
+    y = ops.tall_tdot(St, K, K)
+    np.testing.assert_allclose(G[:, K].cpu().numpy(), y.cpu().numpy(), rtol=1e-12, atol=tol)
+
+
 @pytest.mark.parametrize("nv", [1, 3, 8])
 def test_colmajor_dot(dv, nv):
     rng = np.random.default_rng(nv)
