@@ -31,8 +31,12 @@ def main():
     Q = dv.alloc_tall(n, l, torch.float64, "row")
     Q.buf.normal_()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    Um = torch.randn((200, 200), dtype=torch.float64, device="cuda") / 200.0
     cases = {
         "XtX f32 sym 200": (lambda: ops.tall_gram(S, S, K1=200, K2=200, symmetric=True), 1.0 * n * 200 * 200),
+        "XtX+border f32 sym 200|1": (lambda: ops.tall_gram_bordered(S, 200), 1.0 * n * 200 * 200 + 2.0 * n * 200),
+        "Xts_m border alone": (lambda: ops.tall_tdot(S, 200, 200), 2.0 * n * 200),
+        "lift S Umap planes K=200": (lambda: ops.tall_gemm_planes(S, Um, bound=1e3), 2.0 * n * 200 * 200),
         "QtQ f64 sym 200": (lambda: ops.tall_gram(Q, Q, symmetric=True), 1.0 * n * 200 * 200),
         "QtS f64xf32 200x201": (lambda: ops.tall_gram(Q, S), 2.0 * n * 200 * 201),
     }
