@@ -196,11 +196,16 @@ __device__ __forceinline__ void tt_consume(S& sm, const TallGemmArgs& args, cons
               // fp16 hi/lo planes of C * cscale (split_rows_kernel's split),
               // zero in the padding columns N <= col < ldc
               if (!(args.debug & 2) && col < args.ldc) {
-                const double x0 = col < args.N ? acc[mi][f][0] * args.cscale : 0.0;
-                const double x1 = col + 1 < args.N ? acc[mi][f][1] * args.cscale : 0.0;
-                const __half h0 = __double2half(x0), h1 = __double2half(x1);
-                const __half l0 = __double2half(x0 - (double)__half2float(h0));
-                const __half l1 = __double2half(x1 - (double)__half2float(h1));
+                // one f64 -> f32 conversion per value (XU pipe), then the split in
+                // fp32 like the tcgen05 plane epilogue: 24 bits carry the 22-bit
+                // hi + lo pair; cscale is a power of two (exact). The all-f64 split
+                // (4 XU conversions + 2 FP64-pipe ops per value) idled the DMMA pipe
+                // ~9% per tile (ncu r02: tensor 84%, XU 12%)
+                const float x0 = col < args.N ? (float)acc[mi][f][0] * (float)args.cscale : 0.f;
+                const float x1 = col + 1 < args.N ? (float)acc[mi][f][1] * (float)args.cscale : 0.f;
+                const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+                const __half l0 = __float2half_rn(x0 - __half2float(h0));
+                const __half l1 = __float2half_rn(x1 - __half2float(h1));
                 const int64_t o = row * args.ldc + col;
                 *reinterpret_cast<__half2*>(static_cast<__half*>(args.C) + o) = __halves2half2(h0, h1);
                 *reinterpret_cast<__half2*>(static_cast<__half*>(args.C2) + o) = __halves2half2(l0, l1);
