@@ -648,9 +648,11 @@ def _min_sep_t(alpha: torch.Tensor) -> float:
 
 def _objective_t(alpha, D, T):
     P = _vander_t(alpha, T)
-    B = la.lstsq_minnorm(P, D)            # gelsd semantics (linalg.py:136-141)
+    q = []
+    B = la.lstsq_minnorm(P, D, qr_out=q)  # gelsd semantics (linalg.py:136-141)
     R = D - P @ B
-    return float(torch.linalg.vector_norm(R).item()), B, P, R
+    # P carries its orthonormal factor when the QR path ran (reused by the LM step)
+    return float(torch.linalg.vector_norm(R).item()), B, (P, q[0] if q else None), R
 
 
 def _varpro_lm_device(D: torch.Tensor, alpha0: np.ndarray, cfg: LMConfig):
@@ -669,16 +671,20 @@ def _varpro_lm_device(D: torch.Tensor, alpha0: np.ndarray, cfg: LMConfig):
     mu = cfg.init_damping
     converged = False
     eye = torch.eye(alpha.numel(), dtype=torch.complex128, device=dev)
+    jac = None
     for _ in range(cfg.max_iters):
         if f <= floor:
             converged = True
             break
-        Qp, _ = torch.linalg.qr(P, mode="reduced")
-        dphi = torch.zeros_like(P)
-        dphi[1:, :] = t[1:, None] * alpha[None, :] ** (t[1:, None] - 1)
-        Wk = dphi - Qp @ (Qp.mH @ dphi)
-        JHJ = (Wk.mH @ Wk) * (B @ B.mH).conj()
-        g = torch.diagonal(Wk.mH @ (R @ B.mH))
+        if jac is None:                   # a rejected step only changes mu: same J^H J and g
+            Pm, Qp = P
+            if Qp is None:
+                Qp, _ = torch.linalg.qr(Pm, mode="reduced")
+            dphi = torch.zeros_like(Pm)
+            dphi[1:, :] = t[1:, None] * alpha[None, :] ** (t[1:, None] - 1)
+            Wk = dphi - Qp @ (Qp.mH @ dphi)
+            jac = ((Wk.mH @ Wk) * (B @ B.mH).conj(), torch.diagonal(Wk.mH @ (R @ B.mH)))
+        JHJ, g = jac
         delta, info = torch.linalg.solve_ex(JHJ + mu * eye, g)
         if int(info.item()) != 0:
             mu *= cfg.damping_up
@@ -690,6 +696,7 @@ def _varpro_lm_device(D: torch.Tensor, alpha0: np.ndarray, cfg: LMConfig):
         if f_new < f:
             rel = (f - f_new) / max(f, 1e-300)
             alpha, f, B, P, R = cand, f_new, B_new, P_new, R_new
+            jac = None
             history.append(f)
             mu /= cfg.damping_down
             if rel < cfg.rel_tol or f <= floor:

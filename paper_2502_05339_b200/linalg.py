@@ -854,12 +854,54 @@ def _check_eig(A, w, V):
     return w, V
 
 
-def lstsq_minnorm(A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+# CholeskyQR2 is used for the small tall factors (T x r Vandermonde of the
+# variable projection) while cond(A) stays below this bound: u cond^2 <= 1e-4,
+# so the second pass restores orthogonality to O(u)
+SMALL_CHOLQR_COND = 1e6
+
+
+def thin_qr_fullrank(A: torch.Tensor):
+    """(Q, R^-1) of a numerically full-column-rank tall A (M >= N) = Q R, or
+    None when A is too close to rank deficient for the unique least-squares
+    solution to equal gelsd's minimum-norm one (the caller then takes the SVD).
+
+    On the device a Householder QR of a 200 x 150 complex128 matrix is ~150
+    latency-bound panel steps (10-15 ms; the LM loop of config 1 spent 42 ms
+    per iteration in two of them). CholeskyQR2 — Gram, potrf, triangular
+    inverse, twice — is a dozen small kernels; it runs while the Frobenius
+    bound ||R||_F ||R^-1||_F >= cond_2(A) stays under SMALL_CHOLQR_COND,
+    otherwise Householder QR decides."""
+    M, N = int(A.shape[0]), int(A.shape[1])
+    rcond = torch.finfo(torch.float64).eps * max(M, N)
+    eye = torch.eye(N, dtype=A.dtype, device=A.device)
+    G = A.mH @ A
+    L, info = torch.linalg.cholesky_ex(0.5 * (G + G.mH))
+    R1 = L.mH
+    Ri1 = torch.linalg.solve_triangular(R1, eye, upper=True)
+    bound = torch.linalg.matrix_norm(R1) * torch.linalg.matrix_norm(Ri1)
+    chk = torch.stack([info.to(torch.float64), bound.real.to(torch.float64)]).cpu()
+    if int(chk[0]) == 0 and float(chk[1]) <= SMALL_CHOLQR_COND:
+        Q1 = A @ Ri1
+        G2 = Q1.mH @ Q1
+        L2, info2 = torch.linalg.cholesky_ex(0.5 * (G2 + G2.mH))
+        if int(info2.item()) == 0:
+            Ri2 = torch.linalg.solve_triangular(L2.mH, eye, upper=True)
+            return Q1 @ Ri2, Ri1 @ Ri2
+    Qa, Ra = torch.linalg.qr(A, mode="reduced")
+    Ri = torch.linalg.solve_triangular(Ra, eye, upper=True)
+    hb = float((torch.linalg.matrix_norm(Ra) * torch.linalg.matrix_norm(Ri)).item())
+    if hb * rcond < 1e-3:
+        return Qa, Ri
+    return None
+
+
+def lstsq_minnorm(A: torch.Tensor, B: torch.Tensor, qr_out: Optional[list] = None) -> torch.Tensor:
     """Minimum-norm least-squares solution of A X = B with numpy's default
     cut (np.linalg.lstsq(rcond=None) -> LAPACK gelsd: singular values at or
     below eps * max(M, N) * s_max are treated as zero), as linalg.py:136-141.
-    CUDA `gels` is a plain QR that assumes full rank, so the solve goes
-    through the SVD of A on the device instead."""
+    CUDA `gels` is a plain QR that assumes full rank, so a rank-deficient A
+    goes through its SVD on the device instead. `qr_out` (a list) receives the
+    orthonormal factor Q of A when the QR path ran (the LM step reuses it)."""
     if A.shape[0] == 0 or A.shape[1] == 0:
         return torch.zeros((A.shape[1],) + tuple(B.shape[1:]), dtype=torch.result_type(A, B), device=A.device)
     M, N = int(A.shape[0]), int(A.shape[1])
@@ -868,11 +910,11 @@ def lstsq_minnorm(A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
         # fast path: when R of A = QR is provably well inside the cut
         # (||R||_F ||R^-1||_F >= cond_2(A)), A has full column rank numerically,
         # the least-squares solution is unique and equals the min-norm one
-        Qa, Ra = torch.linalg.qr(A, mode="reduced")
-        eye = torch.eye(N, dtype=Ra.dtype, device=Ra.device)
-        Ri = torch.linalg.solve_triangular(Ra, eye, upper=True)
-        bound = float((torch.linalg.matrix_norm(Ra) * torch.linalg.matrix_norm(Ri)).item())
-        if bound * rcond < 1e-3:
+        fac = thin_qr_fullrank(A)
+        if fac is not None:
+            Qa, Ri = fac
+            if qr_out is not None:
+                qr_out.append(Qa)
             return Ri @ (Qa.mH @ B.to(Qa.dtype))
     U, s, Vh = torch.linalg.svd(A, full_matrices=False, driver="gesvdj" if A.is_cuda else None)
     keep = s > rcond * s[0]
