@@ -795,17 +795,22 @@ int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n
   // staged chunks (2-deep basis ring) when the output rows are 16-byte aligned.
   // Measured at n = 50.3M: B = 256 18.2 ms vs 16.7 ms with register stores,
   // B = 512 equal (33.4 ms) — off by default.
-  static const bool tmao_on = [] { const char* e = getenv("FDMD_TC2_TMAO"); return e && strcmp(e, "1") == 0; }();
-  const bool tmao = !ph && tmao_on && (ldo * 4) % 16 == 0 && ((uintptr_t)out % 16) == 0;
-  auto kern = ph ? fdmd::tc_decode2_kernel<true, false, fdmd::tc2::AST>
-                 : (tmao ? fdmd::tc_decode2_kernel<false, true, 2> : fdmd::tc_decode2_kernel<false, false, fdmd::tc2::AST>);
-  const int smem = (int)(tmao ? sizeof(fdmd::TC2SmemT<2, true>) : sizeof(fdmd::TC2Smem)) + 1024;
-  static thread_local int configured[3] = {-1, -1, -1};
-  static thread_local int max_clusters[3] = {0, 0, 0};
-  const int kv = ph ? 1 : (tmao ? 2 : 0);
+  // FDMD_TC2_TMAO=2: the same staging, written out with 16-byte register stores
+  // (512 contiguous bytes of one frame per warp instruction).
+  static const int tmao_mode = [] { const char* e = getenv("FDMD_TC2_TMAO"); return e ? atoi(e) : 0; }();
+  const bool aligned = !ph && (ldo * 4) % 16 == 0 && ((uintptr_t)out % 16) == 0;
+  const int tmao = aligned && (tmao_mode == 1 || tmao_mode == 2) ? tmao_mode : 0;
+  auto kern = ph ? fdmd::tc_decode2_kernel<true, 0, fdmd::tc2::AST>
+                 : (tmao == 1 ? fdmd::tc_decode2_kernel<false, 1, 2>
+                    : tmao == 2 ? fdmd::tc_decode2_kernel<false, 2, 2>
+                                : fdmd::tc_decode2_kernel<false, 0, fdmd::tc2::AST>);
+  const int smem = (int)(tmao ? sizeof(fdmd::TC2SmemT<2, 1>) : sizeof(fdmd::TC2Smem)) + 1024;
+  static thread_local int configured[4] = {-1, -1, -1, -1};
+  static thread_local int max_clusters[4] = {0, 0, 0, 0};
+  const int kv = ph ? 1 : (tmao ? 1 + tmao : 0);
   CUtensorMap omap;
   memset(&omap, 0, sizeof(omap));
-  if (tmao) {
+  if (tmao == 1) {
     cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)nf};
     cuuint64_t strides[1] = {(cuuint64_t)(ldo * 4)};
     cuuint32_t box[2] = {(cuuint32_t)fdmd::tc2::BM, (cuuint32_t)fdmd::TMAO_FR};

@@ -52,7 +52,9 @@ constexpr int B_CHUNK_BYTES = BNH * BKC * 2;   // 16 KB per plane
 // basis ring (3 before): at 256 frames per basis tile a pair SM needs ~15 GB/s
 // of basis, covered by 64 KB in flight.
 constexpr int TMAO_FR = 8;                       // frames per staged chunk (2 buffers per part)
-template <int AST_, bool TMAO>
+// TMAO: 0 register stores, 1 staged + TMA store, 2 staged + 16-byte register
+// stores (each warp instruction writes 512 contiguous bytes of one frame)
+template <int AST_, int TMAO>
 struct TC2SmemT {
   __half A[AST_][2][tc2::BM * tc2::BKC];
   __half B[tc2::MAXKC][2][tc2::BNH * tc2::BKC];
@@ -63,7 +65,7 @@ struct TC2SmemT {
   uint64_t tfull[2], tempty[2];
   uint32_t tmem_base;
 };
-using TC2Smem = TC2SmemT<tc2::AST, false>;
+using TC2Smem = TC2SmemT<tc2::AST, 0>;
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -113,7 +115,7 @@ __device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, unsigned byte
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
-template <bool PLANES, bool TMAO, int AST_>
+template <bool PLANES, int TMAO, int AST_>
 __global__ void __launch_bounds__(tc2::THREADS, 1)
 tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_constant__ CUtensorMap amap_l,
                   const __grid_constant__ CUtensorMap bmap_h, const __grid_constant__ CUtensorMap bmap_l,
@@ -226,6 +228,7 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
     const int part = (warp - 2) / 4;
     const int c_lo = part * (tc2::BN / SPLIT), c_hi = c_lo + tc2::BN / SPLIT;
     const uint32_t tempty_l[2] = {mapa_u32(&sm.tempty[0], 0), mapa_u32(&sm.tempty[1], 0)};
+    int buf = 0;   // staging buffer parity: alternates over ALL chunks (also across tiles)
     for (int64_t t = 0; t < my_tiles; ++t) {
       const int acc = (int)(t & 1);
       mbar_wait(&sm.tfull[acc], (uint32_t)((t >> 1) & 1));
@@ -233,7 +236,6 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
       const int64_t row = (pair + t * npairs) * (2 * tc2::BM) + rank * tc2::BM + q * 32 + lane;
       if constexpr (TMAO && !PLANES) {
         const int64_t row0 = row - q * 32 - lane;              // first row of this CTA's tile half
-        int buf = 0;
 #pragma unroll 1
         for (int cb = c_lo; cb < c_hi; cb += 2 * TMAO_FR) {
           if (f0 + cb >= args.nf) break;                       // uniform over the part's 4 warps
@@ -246,6 +248,34 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
 #pragma unroll
             for (int j = 0; j < TMAO_FR; ++j)
               stg[j * tc2::BM + q * 32 + lane] = v[h * TMAO_FR + j] * sm.fs[cb + h * TMAO_FR + j];
+            if constexpr (TMAO == 2) {
+              // staged chunk -> global with 16-byte stores: warp q writes frames q, q + 4
+              // of the chunk, lane = 4 consecutive rows, so one instruction covers 512
+              // contiguous bytes of one frame (HBM absorbs 512-B runs at 6.0-6.3 TB/s
+              // against 4.5 for the 128-B runs of the lane = row layout). One barrier
+              // per chunk: the other buffer is rewritten only after every warp of the
+              // part passed the next barrier, i.e. finished reading this one.
+              asm volatile("bar.sync %0, 128;\n" ::"r"(1 + part) : "memory");
+#pragma unroll
+              for (int jj = 0; jj < TMAO_FR / 4; ++jj) {
+                const int j = q + 4 * jj;
+                const int fr = f0 + cb + h * TMAO_FR + j;
+                const int64_t r4 = row0 + 4 * lane;
+                if (fr < args.nf && r4 < args.n) {
+                  const float4 w = *reinterpret_cast<const float4*>(stg + j * tc2::BM + 4 * lane);
+                  float* o = args.out + (int64_t)fr * args.ldo + r4;
+                  if (r4 + 3 < args.n) {
+                    __stcs(reinterpret_cast<float4*>(o), w);
+                  } else {
+                    o[0] = w.x;
+                    if (r4 + 1 < args.n) o[1] = w.y;
+                    if (r4 + 2 < args.n) o[2] = w.z;
+                  }
+                }
+              }
+              buf ^= 1;
+              continue;
+            }
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             asm volatile("bar.sync %0, 128;\n" ::"r"(1 + part) : "memory");
             if (q == 0 && lane == 0) {
@@ -336,7 +366,7 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
       if (lane == 0) mbar_arrive_cluster(tempty_l[acc]);
     }
   }
-  if constexpr (TMAO && !PLANES)
+  if constexpr (TMAO == 1 && !PLANES)
     if (warp >= 2) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores complete
   __syncwarp();
   tc_fence_before();
