@@ -1,0 +1,10 @@
+# round-2 GPU session 28: full GPU suite, smoke, bench + reference arm, ncu launch list / traffic, full-size config-3 parity (HEAD)
+cd $GRAFT_REPO_ROOT
+timeout 2400 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider -rf --durations=8 > gpurun_out/r2s28_gputest.log 2>&1; echo EXIT $? >> gpurun_out/r2s28_gputest.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r2s28_smoke.log 2>&1; echo EXIT $? >> gpurun_out/r2s28_smoke.log
+timeout 900 python bench.py > gpurun_out/r2s28_bench.json 2> gpurun_out/r2s28_bench.err; echo EXIT $? >> gpurun_out/r2s28_bench.err
+timeout 600 python bench.py --impl reference > gpurun_out/r2s28_bench_ref.json 2> gpurun_out/r2s28_bench_ref.err; echo EXIT $? >> gpurun_out/r2s28_bench_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/r2s28_c3_launches.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/r2s28_ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tall_gram_panel -s 1 -c 1 -o gpurun_out/r2s28_gram_bordered python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/r2s28_ncu_full.log 2>&1
+timeout 2400 python tests/fullsize_parity.py --config c3 --out gpurun_out/r2s28_fullsize_c3.json > gpurun_out/r2s28_fullsize_c3.log 2>&1; echo EXIT $? >> gpurun_out/r2s28_fullsize_c3.log
+echo done
