@@ -37,6 +37,8 @@ CONFIGS = {
     "c3": dict(cfg=3, grid=256, r=200, p=10, q=1, lm_iters=10, times=1024, seed=3),
     "c1": dict(cfg=1, grid=128, r=150, p=10, q=1, lm_iters=10, times=1024, seed=1),
     "c3s": dict(cfg=3, grid=64, r=200, p=10, q=1, lm_iters=10, times=1024, seed=3),
+    # BASELINE config 1 as written: exact DMD r = 150 + 200 integer steps + 1 interactive frame (a side line)
+    "c1x": dict(cfg=1, grid=128, r=150, p=10, q=1, steps=200, seed=1),
     # config 2 (DMDc): augmented fit r_aug = 158 + 200 controlled frames (a side line, not the headline)
     "c2": dict(cfg=2, grid=128, r=150, r_aug=158, p=10, q=1, ell=8, steps=200, seed=2),
 }
@@ -294,6 +296,72 @@ def dmdc_flops(n, m, r_aug, r, p, q, ell):
     return sum(terms.values()), terms
 
 
+def run_c1x(args, cfg):
+    """BASELINE config 1 as written: exact DMD (randomized SVD r = 150, p = 10,
+    q = 1) of the 128^3 x 3 matrix from HBM-resident snapshots, then 200 integer
+    steps decoded in one batched device GEMM and one interactive single-frame
+    GEMV. One JSON line (a side workload; full-size parity of this fit:
+    tests/test_gpu_fullsize.py::test_config1_full_size_vs_streamed_oracle)."""
+    import warnings
+
+    import torch
+
+    import paper_2502_05339_b200 as fd
+    from paper_2502_05339_b200 import device as dv
+    from paper_2502_05339_b200 import synth, trace
+    torch.cuda.set_device(0)
+    p = synth.config_params(cfg["cfg"], seed=cfg["seed"], grid=cfg["grid"])
+    n, m, r = p.n, p.m, cfg["r"]
+    S = dv.alloc_tall(n, m, torch.float32, "row")
+    S.buf[:, m:].zero_()
+    tabs = [torch.as_tensor(np.ascontiguousarray(t), device="cuda") for t in p.sep_tables()]
+    dv.get_ops().synth3d(tabs, m, p.noise, synth.noise_key(p.seed), 0, n, S)
+    torch.cuda.synchronize()
+    data = fd.SnapshotMatrix(S, synth.DT)
+    x0 = S.buf[:n, 0].clone()
+    F, terms, l = fit_flops(n, m, r, cfg["p"], cfg["q"], modes="exact")
+    F -= terms.pop("lift U 2nlr")                       # exact DMD forms no POD lift (dmd.py:240-274)
+
+    def one():
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record()
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            model = fd.exact_dmd(data, r, svd_mode="randomized", seed=cfg["seed"], oversample=cfg["p"],
+                                 power_iters=cfg["q"])
+            e[1].record()
+            z0 = fd.encode(model, x0)
+            frames = fd.rollout(model, z0, cfg["steps"], to_host=False)
+            frames = frames[0] if isinstance(frames, tuple) else frames
+            e[2].record()
+            one_frame = fd.decode(model, fd.step_k(model, z0, 7), to_host=False)
+        e[3].record()
+        torch.cuda.synchronize()
+        del frames, one_frame, model
+        return [e[i].elapsed_time(e[i + 1]) / 1e3 for i in range(3)]
+
+    for _ in range(args.warmup):
+        one()
+    trace.enable()
+    ts = np.array([one() for _ in range(args.steps)])
+    stages = trace.summarize(trace.disable(), args.steps)
+    fit_t, roll_t, one_t = [float(x) for x in ts.mean(axis=0)]
+    line = {"metric": "config-1 exact DMD fit GFLOP/s + rollout frames/s", "value": round(F / fit_t / 1e9, 1),
+            "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round((fit_t + roll_t + one_t) * 1e3, 1), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config1 exact DMD (r=150, p=10, q=1) + 200 integer steps + 1 interactive frame",
+                       "n": n, "m": m, "r": r, "l": l, "grid": "128^3x3", "snapshot_dtype": "f32",
+                       "l2": "inputs larger than L2"},
+            "fit": {"s": round(fit_t, 4), "flops": F, "terms": terms}, "fit_stages_ms": stages,
+            "rollout": {"frames": cfg["steps"], "s": round(roll_t, 4),
+                        "frames_per_s": round(cfg["steps"] / roll_t, 1),
+                        "hbm_GBps": round((4.0 * n * r + 4.0 * n * cfg["steps"]) / roll_t / 1e9, 1)},
+            "interactive_frame": {"ms": round(one_t * 1e3, 3),
+                                  "hbm_GBps": round(4.0 * n * (r + 1) / one_t / 1e9, 1)}}
+    print(json.dumps(line), flush=True)
+
+
 def run_c2(args, cfg):
     """Config 2: the augmented DMDc fit of a 128^3 x 3 controlled system
     (synth.config2_params) from HBM-resident snapshots, then 200 controlled
@@ -339,9 +407,12 @@ def run_c2(args, cfg):
         torch.cuda.synchronize()
         return e[0].elapsed_time(e[1]) / 1e3, e[1].elapsed_time(e[2]) / 1e3, frames
 
+    from paper_2502_05339_b200 import trace
     for _ in range(args.warmup):
         one()
+    trace.enable()
     ts = [one() for _ in range(args.steps)]
+    stages = trace.summarize(trace.disable(), args.steps)
     fit_t = float(np.mean([t[0] for t in ts]))
     roll_t = float(np.mean([t[1] for t in ts]))
     frames = ts[-1][2]
@@ -354,7 +425,7 @@ def run_c2(args, cfg):
             "config": {"workload": "config2 DMDc fit ([X;Upsilon] r_aug=158, p=10, q=1; output basis r=150) + "
                                    "200 controlled steps with fresh seeded controls", "n": n, "m": m, "ell": cfg["ell"],
                        "grid": "128^3x3", "snapshot_dtype": "f32", "l2": "inputs larger than L2"},
-            "fit": {"s": round(fit_t, 4), "flops": F, "terms": terms},
+            "fit": {"s": round(fit_t, 4), "flops": F, "terms": terms}, "fit_stages_ms": stages,
             "rollout": {"frames": cfg["steps"], "s": round(roll_t, 4), "frames_per_s": round(cfg["steps"] / roll_t, 1),
                         "max_rel_err_vs_generator": err}}
     print(json.dumps(line), flush=True)
@@ -376,6 +447,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.config == "c2":
         return run_c2(args, cfg)
+    if args.config == "c1x":
+        return run_c1x(args, cfg)
     if args.impl == "reference":
         return run_reference(args, cfg)
 

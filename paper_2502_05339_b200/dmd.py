@@ -960,29 +960,33 @@ def dmdc_fit(data, controls, r_aug, r, seed=None, *, oversample=10, power_iters=
     last = shard is None or shard.row0 + n_loc == n
     extra = ell if last else 0
     # augmented tall matrix: rows [S; Upsilon | 0] (the control rows on the last shard)
-    Aug = alloc_tall(n_loc + extra, m, S.dtype, "row", device=dev, zero=False)
-    Aug.buf[:n_loc].copy_(S.buf[:n_loc])
-    if extra:
-        tail = torch.zeros((ell, Aug.ld), dtype=S.dtype, device=dev)
-        tail[:, :T] = torch.as_tensor(Ups, dtype=S.dtype, device=dev)
-        Aug.buf[n_loc:n_loc + ell].copy_(tail)
+    with stage("dmdc.aug_copy"):
+        Aug = alloc_tall(n_loc + extra, m, S.dtype, "row", device=dev, zero=False)
+        Aug.buf[:n_loc].copy_(S.buf[:n_loc])
+        if extra:
+            tail = torch.zeros((ell, Aug.ld), dtype=S.dtype, device=dev)
+            tail[:, :T] = torch.as_tensor(Ups, dtype=S.dtype, device=dev)
+            Aug.buf[n_loc:n_loc + ell].copy_(tail)
     aug_shard = None
     if shard is not None:
         aug_shard = Shard(shard.row0, n_loc + extra, n + ell, shard.group, shard.world)
     t0 = time.perf_counter()
     p1 = min(oversample, min(n + ell, T) - r_aug)
-    f1 = la.sketch_factors(Aug, T, r_aug + p1, power_iters, la.draw_omega(T, r_aug + p1, seed), aug_shard)
+    with stage("dmdc.sketch_aug"):
+        f1 = la.sketch_factors(Aug, T, r_aug + p1, power_iters, la.draw_omega(T, r_aug + p1, seed), aug_shard)
     p2 = min(oversample, min(n, T) - r)
     # rank-r sketch of X' = S[:, 1:] (column window c0 = 1 of the same resident S)
-    f2 = la.sketch_factors(S, T, r + p2, power_iters, la.draw_omega(T, r + p2, None if seed is None else seed + 1),
-                           shard, c0=1)
+    with stage("dmdc.sketch_Xp"):
+        f2 = la.sketch_factors(S, T, r + p2, power_iters,
+                               la.draw_omega(T, r + p2, None if seed is None else seed + 1), shard, c0=1)
     Ub1 = f1.Ub[:, :r_aug]
     s1 = f1.s[:r_aug]
     V1 = f1.Vh[:r_aug].t()
     Ub2 = f2.Ub[:, :r]
     # U1^T Uhat = Ub1^T (Q1[:n]^T Q2) Ub2
     Q1top = Tall(f1.Q.buf, "row", n_loc, f1.Q.k)
-    M12 = allreduce(shard, dv.get_ops().tall_gram(Q1top, f2.Q))       # l1 x l2
+    with stage("dmdc.cross_Q1tQ2"):
+        M12 = allreduce(shard, dv.get_ops().tall_gram(Q1top, f2.Q))       # l1 x l2
     if f1.fix is not None:
         M12 = f1.fix.t() @ M12
     if f2.fix is not None:
@@ -996,7 +1000,8 @@ def dmdc_fit(data, controls, r_aug, r, seed=None, *, oversample=10, power_iters=
     core = UhtXp @ (V1 / s1[None, :])                                  # r x r_aug
     Atil = core @ U1tUh                                                # r x r
     Btil = core @ U2.t()                                               # r x ell
-    lam_raw, W = _eig_device(Atil)
+    with stage("small.eig(Atil)"):
+        lam_raw, W = _eig_device(Atil)
     plan = pair_plan(lam_raw)
     Wt = torch.as_tensor(W, device=dev)
     Cmap = ((V1 / s1[None, :]) @ U1tUh).to(torch.complex128) @ Wt     # T x r
@@ -1005,16 +1010,19 @@ def dmdc_fit(data, controls, r_aug, r, seed=None, *, oversample=10, power_iters=
         torch.cuda.synchronize()
         timings["svd_s"] = time.perf_counter() - t0
     tdt = table_dtype or S.dtype
-    modes = _modes_pass(S, Cmap, plan, 1, shard, tdt, timings)
+    with stage("dmdc.modes"):
+        modes = _modes_pass(S, Cmap, plan, 1, shard, tdt, timings)
     model = ReducedModel(None, plan.lam, s1.cpu().numpy()[:r] if r <= r_aug else s1.cpu().numpy(),
                          data.dt, grid_meta=data.grid_meta,
                          provenance={"method": "dmdc", "svd": "randomized", "seed": seed,
                                      "r_aug": r_aug}, _modes=modes)
     # reduced_b = pinv(phi) U_hat B~ / dt, U_hat = Q2 Ub2
-    D, E = modes.basis()
-    DtQ2 = allreduce(shard, dv.get_ops().tall_gram(D, f2.Q, K1=E.shape[0]))   # ncol x l2
-    y = (DtQ2 @ f2.right(Ub2) @ Btil).cpu().numpy()                    # ncol x ell
-    red = modes.pinv_rows() @ y / data.dt
+    with stage("dmdc.reduced_b"):
+        D, E = modes.basis()
+        DtQ2 = allreduce(shard, dv.get_ops().tall_gram(D, f2.Q, K1=E.shape[0]))   # ncol x l2
+        y = (DtQ2 @ f2.right(Ub2) @ Btil).cpu().numpy()                    # ncol x ell
+        with stage("dmdc.pinv_rows"):
+            red = modes.pinv_rows() @ y / data.dt
     ctrl = ControlOperator([red], ["augmented"])
     model.provenance["A_tilde"] = Atil.cpu().numpy()
     model.provenance["B_tilde"] = Btil.cpu().numpy()

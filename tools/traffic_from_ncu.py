@@ -41,7 +41,7 @@ def main():
             v *= BSCALE.get(u, 1.0)
         launches[key][m] = v
         meta[key] = (r["Kernel Name"], r["Grid Size"], r["Block Size"])
-    # steps of bench.py: a step starts at the first tall_gemm after a tc_decode
+    # steps of bench.py: a step starts at the first tall_gram / tall_gemm after a tc_decode
     # (fit -> reconstruct); keep the last COMPLETE step (a later step start exists)
     ids = sorted(launches)
     starts, seen_rec = [], True
@@ -49,7 +49,7 @@ def main():
         s = short(meta[k][0])
         if "tc_decode" in s:
             seen_rec = True
-        elif "tall_gemm" in s and seen_rec:
+        elif ("tall_gemm" in s or "tall_gram" in s) and seen_rec:   # the fit's first tall kernel
             starts.append(k)
             seen_rec = False
     if "--all" not in sys.argv and len(starts) >= 2:
