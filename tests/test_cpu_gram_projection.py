@@ -61,3 +61,36 @@ def test_config1_shape_keeps_the_direct_projection(config_golden):
     assert "gram_projection" not in st and st["proj_gram_bound"] > 1e-7, st
     assert np.max(np.abs(model.sigma - g["c1s_sigma"]) / g["c1s_sigma"]) <= 1e-9
     assert match_eigs(model.lam, g["c1s_lam"]) <= 1e-7
+
+
+def test_rank_deficient_sketch_span_only_pass_avoids_householder():
+    """A numerically rank-deficient sketch (exactly rank-6 data, and rank-6 data
+    stored in fp32, sketched at l = 18, q = 1): the span-only first pass takes
+    its factor from the eigen-decomposition of the sketch Gram
+    (linalg._span_from_gram) instead of a Householder QR of the tall buffer;
+    the final orthonormalisation keeps its own fallbacks, and the identifiable
+    singular values still match the reference algorithm (oracle.sketch_svd,
+    Householder QR throughout)."""
+    import flowdmd_oracle as orc
+    from paper_2502_05339_b200 import device as dv
+    from paper_2502_05339_b200 import linalg as la
+    from cpu_ops import CpuOps
+    rng = np.random.default_rng(5)
+    n, T, r, p, q = 4000, 60, 8, 10, 1
+    base = rng.standard_normal((n, 6)) @ rng.standard_normal((6, T))
+    prev = dv.set_ops(CpuOps())
+    try:
+        for M, tol in ((base, 1e-9), (base.astype(np.float32).astype(np.float64), 1e-8)):
+            Mt = dv.Tall(torch.as_tensor(M).contiguous(), "row", n, T)
+            f = la.sketch_factors(Mt, T, r + p, q, la.draw_omega(T, r + p, 9))
+            assert f.stats.get("eigh_span_fallback", 0) + f.stats.get("shifted_cholqr3", 0) \
+                + f.stats.get("householder_fallback", 0) >= 1, f.stats
+            _, S, _ = orc.sketch_svd(M, r, p, q, 9)
+            got = f.s.cpu().numpy()
+            np.testing.assert_allclose(got[:6], S[:6], rtol=tol)
+        # exactly rank-deficient: the singular Gram takes the eigen route in the span-only pass
+        Mt = dv.Tall(torch.as_tensor(base).contiguous(), "row", n, T)
+        f = la.sketch_factors(Mt, T, r + p, q, la.draw_omega(T, r + p, 9))
+        assert f.stats.get("eigh_span_fallback", 0) >= 1 and f.stats["span_rank"][0] == 6, f.stats
+    finally:
+        dv.set_ops(prev)
