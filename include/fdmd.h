@@ -149,6 +149,14 @@ int fdmd_residual(const void* S, int s_dtype, int64_t lds, const void* D, int d_
                   const double* F, int r, int T, int64_t n, double* out,
                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* Thin SVD of a small row-major f64 device matrix B (l x T, l <= T, row stride ldb):
+ * B = Ub diag(s) Vh with ubt = Ub^T (l x l row-major), s (l, descending), vh (l x T
+ * row-major) — `np.linalg.svd(B, full_matrices=False)` of randomized_svd (reference
+ * linalg.py:87) and of the DMDc sketches. cuSOLVER gesvdp, stream-ordered (no host
+ * synchronisation); *info_dev (device int) receives cuSOLVER's info; B is destroyed. */
+int fdmd_svd_small(double* B, int64_t ldb, int l, int T, double* ubt, double* s_out, double* vh, int* info_dev,
+                   void* stream);
+
 /* Real nonsymmetric eigendecomposition (cuSOLVER Xgeev). A: n x n column-major
  * f64 (overwritten). Outputs: w_host (2n doubles: re, im interleaved),
  * vr_host (n x n column-major, LAPACK packing: a complex pair occupies columns

@@ -1401,6 +1401,37 @@ int fdmd_geev(int n, double* A, double* w_host, double* vr_host, void* stream) {
   return FDMD_OK;
 }
 
+// Thin SVD of the fit's small row-major B (l x T, l <= T, f64, device): B = Ub diag(s) Vh.
+// cuSOLVER gesvdp (polar decomposition + symmetric eigensolver; 5.8 ms at 200 x 200 where
+// the one-sided Jacobi gesvdj torch calls takes 13-15 ms, tools/svdp_probe.cu). The
+// row-major B is the column-major T x l matrix B^T = Um diag(s) Vm^T, so Vh is Um's
+// buffer as it stands (l x T row-major) and Ub^T is Vm's buffer. Stream-ordered: no
+// host synchronisation; *info_dev (device int) receives cuSOLVER's info. B is destroyed.
+int fdmd_svd_small(double* B, int64_t ldb, int l, int T, double* ubt, double* s_out, double* vh, int* info_dev,
+                   void* stream) {
+  if (!B || !ubt || !s_out || !vh || !info_dev || l <= 0 || T < l || ldb < T)
+    return fail(FDMD_ERR_INVALID, "svd_small: bad arguments (needs l <= T <= ldb)");
+  SolverCtx* c = solver_ctx();
+  if (!c) return fail(FDMD_ERR_SOLVER, "cusolverDnCreate failed");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cusolverDnSetStream(c->h, s) != CUSOLVER_STATUS_SUCCESS) return fail(FDMD_ERR_SOLVER, "set stream");
+  size_t dws = 0, hws = 0;
+  cusolverStatus_t st = cusolverDnXgesvdp_bufferSize(c->h, c->p, CUSOLVER_EIG_MODE_VECTOR, 1, T, l, CUDA_R_64F, B,
+                                                     ldb, CUDA_R_64F, s_out, CUDA_R_64F, vh, T, CUDA_R_64F, ubt, l,
+                                                     CUDA_R_64F, &dws, &hws);
+  if (st != CUSOLVER_STATUS_SUCCESS) return fail(FDMD_ERR_SOLVER, "Xgesvdp_bufferSize status %d", (int)st);
+  void* dbuf = nullptr;
+  CUDA_TRY(scratch_alloc(&dbuf, dws > 0 ? dws : 1, s));
+  std::vector<char> hbuf(hws > 0 ? hws : 1);
+  double h_err = 0.0;
+  st = cusolverDnXgesvdp(c->h, c->p, CUSOLVER_EIG_MODE_VECTOR, 1, T, l, CUDA_R_64F, B, ldb, CUDA_R_64F, s_out,
+                         CUDA_R_64F, vh, T, CUDA_R_64F, ubt, l, CUDA_R_64F, dbuf, dws, hbuf.data(), hws, info_dev,
+                         &h_err);
+  cudaFreeAsync(dbuf, s);
+  if (st != CUSOLVER_STATUS_SUCCESS) return fail(FDMD_ERR_SOLVER, "Xgesvdp status %d", (int)st);
+  return FDMD_OK;
+}
+
 int fdmd_split_basis(const float* D, int64_t ldd, int64_t n, int r, float scale, void* uh, void* ul, int64_t ldu,
                      void* stream) {
   if (!D || !uh || !ul || n <= 0 || r <= 0 || ldu < r || ldd < n || ldu % 8 || ldu > 256)

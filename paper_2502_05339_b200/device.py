@@ -509,6 +509,22 @@ class CudaOps:
         self.launches += 2
         return out
 
+    def svd_small(self, B: torch.Tensor):
+        """Thin SVD of the small device matrix B (l x T, l <= T): (Ub, s, Vh, info)
+        with info a device int32 (cuSOLVER gesvdp's status; 0 = converged).
+        Stream-ordered on the current stream, no host synchronisation."""
+        l, T = int(B.shape[0]), int(B.shape[1])
+        assert l <= T and B.is_cuda
+        A = B.to(torch.float64).clone(memory_format=torch.contiguous_format)
+        dev = B.device
+        ubt = torch.empty((l, l), dtype=torch.float64, device=dev)
+        sv = torch.empty((l,), dtype=torch.float64, device=dev)
+        vh = torch.empty((l, T), dtype=torch.float64, device=dev)
+        info = torch.zeros((), dtype=torch.int32, device=dev)
+        _lib.check(_lib.lib().fdmd_svd_small(_ptr(A), A.stride(0), l, T, _ptr(ubt), _ptr(sv), _ptr(vh), _ptr(info),
+                                             _stream()), "svd_small")
+        return ubt.t(), sv, vh, info
+
     def geev(self, K: torch.Tensor, vectors: bool = True):
         """Real nonsymmetric eig on device (cuSOLVER Xgeev). Returns host
         (w complex[n], V complex[n, n]) with LAPACK pair unpacking; V is None

@@ -703,17 +703,31 @@ def _svd_tail(Q: Tall, QtS: torch.Tensor, c0: int, T: int, pre_svd, stats: dict,
             side = _svd_stream(B.device)
             side.wait_event(ready)
             with torch.cuda.stream(side):
-                Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvdj")
+                Ub, s, Vh = _svd_small(B)
             main.wait_stream(side)
             for t in (B, Ub, s, Vh):
                 t.record_stream(side)
         else:
-            Ub, s, Vh = torch.linalg.svd(B, full_matrices=False, driver="gesvdj" if B.is_cuda else None)
+            Ub, s, Vh = _svd_small(B)
     f = SketchFactors(Q, Ub, s, Vh, QtS, stats, fix, implicit)
     f.pre = pre
     return f
 
 
+def _svd_small(B: torch.Tensor):
+    """np.linalg.svd(B, full_matrices=False) of linalg.py:87 on the device:
+    cuSOLVER gesvdp through libfdmd (5.8 ms at 200 x 200 against 13-15 ms for the
+    one-sided Jacobi gesvdj, profiles/r02_svd_probe.txt); gesvdj when gesvdp
+    reports a failure, for wide-over-tall blocks and for the CPU test harness."""
+    ops = dv.get_ops()
+    if B.is_cuda and B.shape[0] <= B.shape[1] and hasattr(ops, "svd_small") and _SVD_GESVDP:
+        Ub, s, Vh, info = ops.svd_small(B)
+        if int(info.item()) == 0 and bool(torch.isfinite(s).all()):
+            return Ub, s, Vh
+    return torch.linalg.svd(B, full_matrices=False, driver="gesvdj" if B.is_cuda else None)
+
+
+_SVD_GESVDP = os.environ.get("FDMD_SVD", "gesvdp") != "gesvdj"
 _SVD_STREAMS = {}
 
 

@@ -354,6 +354,29 @@ def test_tall_gram_bordered(dv, n, K, dt):
     np.testing.assert_allclose(G[:, K].cpu().numpy(), y.cpu().numpy(), rtol=1e-12, atol=tol)
 
 
+@pytest.mark.parametrize("l,T,cond", [(200, 200, 1.2e4), (160, 201, 1e6), (20, 100, 10.0), (1, 5, 1.0)])
+def test_svd_small_gesvdp(dv, l, T, cond):
+    """fdmd_svd_small (cuSOLVER gesvdp, stream-ordered): the thin SVD of the fit's
+    small projected matrix B (a strided column window of Q^T S) against LAPACK."""
+    rng = np.random.default_rng(l + T)
+    U0, _ = np.linalg.qr(rng.standard_normal((l, l)))
+    V0, _ = np.linalg.qr(rng.standard_normal((T, l)))
+    sv = cond ** (-np.arange(l) / max(l - 1, 1))
+    full = np.zeros((l, T + 3))
+    full[:, :T] = (U0 * sv) @ V0.T
+    Bt = torch.as_tensor(full, device="cuda")[:, :T]          # non-contiguous window, like QtS[:, :T]
+    Ub, s, Vh, info = dv.get_ops().svd_small(Bt)
+    assert int(info.item()) == 0
+    s_h = s.cpu().numpy()
+    np.testing.assert_allclose(s_h, sv, rtol=1e-10 * cond, atol=0)
+    assert np.all(np.diff(s_h) <= 0)
+    rec = (Ub * s[None, :]) @ Vh
+    assert float((rec - Bt).abs().max()) <= 1e-13
+    eye = torch.eye(l, dtype=torch.float64, device="cuda")
+    assert float((Ub.t() @ Ub - eye).abs().max()) <= 1e-12 and float((Vh @ Vh.t() - eye).abs().max()) <= 1e-12
+    assert torch.equal(Bt, torch.as_tensor(full, device="cuda")[:, :T])   # input untouched
+
+
 @pytest.mark.parametrize("nv", [1, 3, 8])
 def test_colmajor_dot(dv, nv):
     rng = np.random.default_rng(nv)
