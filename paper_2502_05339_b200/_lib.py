@@ -38,6 +38,7 @@ SIGNATURES = {
     "fdmd_tall_gemm_planes": (_i, [_vp, _i, _i64, _vp, _i64, _vp, _vp, _i64, _d, _i64, _i, _i, _i, _vp]),
     "fdmd_tall_gram_bordered_workspace": (_sz, [_i64, _i]),
     "fdmd_tall_gram_bordered": (_i, [_vp, _i, _i64, _vp, _i64, _d, _i64, _i, _vp, _sz, _vp]),
+    "fdmd_tc_decode_pairstats": (_i, [_vp, _vp, _i64, _i64, _i, _vp, _vp, _i, _i, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "fdmd_svd_small": (_i, [_vp, _i64, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "fdmd_gram_plan_info": (_i, [_i64, _i, _i, _i, _i, _vp, _vp, _i]),
     "fdmd_tall_tdot_workspace": (_sz, [_i64, _i]),

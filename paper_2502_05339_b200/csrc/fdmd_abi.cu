@@ -773,7 +773,7 @@ int launch_tc_decode_mc(const void* uh, const void* ul, int64_t ldu, int64_t n, 
 int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch,
                           const void* cl, int ldk, int nf, const float* fscale, float* out, int64_t ldo,
                           void* stream, int reserve_pairs = 0, void* ph = nullptr, void* pl = nullptr,
-                          int64_t ldp = 0, float pscale = 1.f) {
+                          int64_t ldp = 0, float pscale = 1.f, double* st = nullptr, int64_t row_offset = 0) {
   auto encode = tensor_map_encoder();
   if (!encode) return fail(FDMD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap maps[4];
@@ -799,15 +799,19 @@ int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n
   // (512 contiguous bytes of one frame per warp instruction).
   static const int tmao_mode = [] { const char* e = getenv("FDMD_TC2_TMAO"); return e ? atoi(e) : 0; }();
   const bool aligned = !ph && (ldo * 4) % 16 == 0 && ((uintptr_t)out % 16) == 0;
-  const int tmao = aligned && (tmao_mode == 1 || tmao_mode == 2) ? tmao_mode : 0;
+  // st != nullptr: the frame epilogue also keeps per column pair the max |phi|^2 and the
+  // first row attaining it (the modes product: no separate statistics pass over the table)
+  const int tmao = !st && aligned && (tmao_mode == 1 || tmao_mode == 2) ? tmao_mode : 0;
+  if (st && ph) return fail(FDMD_ERR_INVALID, "tc_decode2: statistics need the frame output");
   auto kern = ph ? fdmd::tc_decode2_kernel<true, 0, fdmd::tc2::AST>
-                 : (tmao == 1 ? fdmd::tc_decode2_kernel<false, 1, 2>
+                 : (st ? fdmd::tc_decode2_kernel<false, 0, fdmd::tc2::AST, true>
+                    : tmao == 1 ? fdmd::tc_decode2_kernel<false, 1, 2>
                     : tmao == 2 ? fdmd::tc_decode2_kernel<false, 2, 2>
                                 : fdmd::tc_decode2_kernel<false, 0, fdmd::tc2::AST>);
   const int smem = (int)(tmao ? sizeof(fdmd::TC2SmemT<2, 1>) : sizeof(fdmd::TC2Smem)) + 1024;
-  static thread_local int configured[4] = {-1, -1, -1, -1};
-  static thread_local int max_clusters[4] = {0, 0, 0, 0};
-  const int kv = ph ? 1 : (tmao ? 1 + tmao : 0);
+  static thread_local int configured[5] = {-1, -1, -1, -1, -1};
+  static thread_local int max_clusters[5] = {0, 0, 0, 0, 0};
+  const int kv = ph ? 1 : (st ? 4 : (tmao ? 1 + tmao : 0));
   CUtensorMap omap;
   memset(&omap, 0, sizeof(omap));
   if (tmao == 1) {
@@ -851,8 +855,23 @@ int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n
   const int64_t npairs =
       std::max<int64_t>(1, std::min<int64_t>(ptiles, std::max(1, max_clusters[kv] / gy - reserve_pairs)));
   cfg.gridDim = dim3((unsigned)(2 * npairs * gy), 1);
+  const int nctas = (int)(2 * npairs * gy);
+  void* stbuf = nullptr;
+  if (st) {
+    const size_t slots = (size_t)nctas * fdmd::tc2::EPI * 32;
+    CUDA_TRY(scratch_alloc(&stbuf, slots * (sizeof(long long) + sizeof(double)), (cudaStream_t)stream));
+    ta.st_idx = static_cast<long long*>(stbuf);
+    ta.st_max = reinterpret_cast<double*>(ta.st_idx + slots);
+  }
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], omap, ta));
   LAUNCH_CHECK("tc_decode2");
+  if (st) {
+    const int units = nf / 2;
+    fdmd::tc2_pair_stats_final_kernel<<<(units + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+        ta.st_max, ta.st_idx, nctas, gy, units, (long long)row_offset, st);
+    LAUNCH_CHECK("tc2_pair_stats_final");
+    cudaFreeAsync(stbuf, (cudaStream_t)stream);
+  }
   return FDMD_OK;
 }
 
@@ -1533,6 +1552,29 @@ int fdmd_tc_decode_ex(const void* uh, const void* ul, int64_t ldu, int64_t n, in
   if (ny <= 4 || mc_cap < 8)
     return launch_tc_decode_mc<128, 3, 0, 4>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
   return launch_tc_decode_mc<128, 3, 0, 8>(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream);
+}
+
+// fdmd_tc_decode of a modes product (column pairs (2u, 2u + 1) = (Re, Im) of mode u) with the
+// normalisation / phase-pivot statistics of _order_and_pair fused into the frame epilogue:
+// st[u] = {unchanged, max_i |phi_u[i]|^2, first row attaining it + row_offset}. *fused = 1 when
+// the CTA-pair kernel ran (nf > 128) and filled st; 0 = frames only (run fdmd_pair_stats).
+int fdmd_tc_decode_pairstats(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch,
+                             const void* cl, int ldk, int nf, const float* fscale, float* out, int64_t ldo,
+                             int64_t row_offset, double* st, int* fused, void* stream) {
+  if (!st || !fused || nf % 2) return fail(FDMD_ERR_INVALID, "tc_decode_pairstats: bad arguments (nf even)");
+  *fused = 0;
+  static const int pair_on = [] { const char* e = getenv("FDMD_TC_IMPL"); return e ? (strcmp(e, "mc") == 0 ? 0 : 1) : 1; }();
+  static const int fuse_on = [] { const char* e = getenv("FDMD_TC_STATS"); return e ? atoi(e) : 1; }();
+  if (nf <= 128 || !pair_on || !fuse_on)
+    return fdmd_tc_decode_ex(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, 0, stream);
+  if (!uh || !ul || !ch || !cl || !fscale || !out || n <= 0 || r <= 0 || r > fdmd::tc::BKC * fdmd::tc::MAXKC)
+    return fail(FDMD_ERR_INVALID, "tc_decode: bad arguments (r must be <= %d)", fdmd::tc::BKC * fdmd::tc::MAXKC);
+  if ((ldu * 2) % 16 || (ldk * 2) % 16 || ldu < r || ldk < r || ldo < n || n >= (int64_t)UINT32_MAX)
+    return fail(FDMD_ERR_INVALID, "tc_decode: leading dimensions must be multiples of 8 halves");
+  const int rc = launch_tc_decode_pair(uh, ul, ldu, n, r, ch, cl, ldk, nf, fscale, out, ldo, stream, 0, nullptr, nullptr,
+                                       0, 1.f, st, row_offset);
+  if (rc == FDMD_OK) *fused = 1;
+  return rc;
 }
 
 int fdmd_tc_decode_planes(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch,

@@ -131,6 +131,11 @@ struct TCArgs {
   __half* pl = nullptr;
   int64_t ldp = 0;
   float pscale = 1.f;
+  // fused column-pair statistics (CTA-pair kernel, frame output): per CTA and
+  // epilogue warp, 32 lane-owned (max |phi|^2, first row attaining it) entries
+  // for the warp's 32 column pairs; tc2_pair_stats_final_kernel combines them
+  double* st_max = nullptr;
+  long long* st_idx = nullptr;
 };
 
 // TMA maps: amap_h/amap_l over Us planes (dims {r, n}, box {64, 128 / MC}, SW128),
@@ -415,6 +420,10 @@ __global__ void split_rows_kernel(const TA* __restrict__ A, int64_t lda, int64_t
 // [sum_i |phi_i|^2, max_i |phi_i|^2, first argmax i + row_offset] — the
 // statistics tall_gemm fuses into its DMMA epilogue, for tables produced by
 // the tcgen05 kernels. Fixed-order two-stage reduction (ties -> lowest row).
+// |re + i im|^2 with one rounding order for every kernel that takes these statistics
+// (pair_stats_kernel over the table, the fused tc_decode2 epilogue): bitwise-equal maxima
+__device__ __forceinline__ double pair_mag2(double a, double b) { return __fma_rn(a, a, __dmul_rn(b, b)); }
+
 __global__ void pair_stats_kernel(const float* __restrict__ raw, int64_t ld, int64_t n, int units,
                                   int64_t rows_per_split, double* __restrict__ part) {
   const int u = blockIdx.x;
@@ -426,7 +435,7 @@ __global__ void pair_stats_kernel(const float* __restrict__ raw, int64_t ld, int
   int64_t idx = INT64_MAX;
   for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
     const double a = re[i], b = im[i];
-    const double v = a * a + b * b;
+    const double v = pair_mag2(a, b);
     sum += v;
     if (v > mx) { mx = v; idx = i; }
   }

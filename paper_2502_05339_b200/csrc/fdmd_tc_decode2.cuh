@@ -115,7 +115,7 @@ __device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, unsigned byte
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
-template <bool PLANES, int TMAO, int AST_>
+template <bool PLANES, int TMAO, int AST_, bool STATS = false>
 __global__ void __launch_bounds__(tc2::THREADS, 1)
 tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_constant__ CUtensorMap amap_l,
                   const __grid_constant__ CUtensorMap bmap_h, const __grid_constant__ CUtensorMap bmap_l,
@@ -229,6 +229,11 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
     const int c_lo = part * (tc2::BN / SPLIT), c_hi = c_lo + tc2::BN / SPLIT;
     const uint32_t tempty_l[2] = {mapa_u32(&sm.tempty[0], 0), mapa_u32(&sm.tempty[1], 0)};
     int buf = 0;   // staging buffer parity: alternates over ALL chunks (also across tiles)
+    // STATS: lane L owns column pair L of the warp's 64 columns (the (Re, Im) columns
+    // of one mode): running max of re^2 + im^2 over the warp's rows and the first
+    // row attaining it (tiles arrive in increasing row order; strict > keeps the first)
+    double st_best = -1.0;
+    long long st_row = 0;
     for (int64_t t = 0; t < my_tiles; ++t) {
       const int acc = (int)(t & 1);
       mbar_wait(&sm.tfull[acc], (uint32_t)((t >> 1) & 1));
@@ -340,6 +345,24 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
           }
           continue;
         }
+        if constexpr (STATS) {
+          const bool live = row < args.n;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            // the stored values, squared in f64 exactly as pair_stats_kernel does
+            const double a = (double)(v[2 * u] * sm.fs[cb + 2 * u]), b = (double)(v[2 * u + 1] * sm.fs[cb + 2 * u + 1]);
+            const double w = pair_mag2(a, b);
+            // w >= 0: its bits order like unsigned integers (two 32-bit redux.sync steps)
+            const unsigned hi = live ? (unsigned)__double2hiint(w) : 0u, lo = live ? (unsigned)__double2loint(w) : 0u;
+            const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+            const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+            const unsigned who = __ballot_sync(0xffffffffu, live && hi == mh && lo == ml);
+            if (lane == ((cb - c_lo) >> 1) + u && who != 0u) {
+              const double m = __hiloint2double((int)mh, (int)ml);   // a NaN wins once and stays (reported downstream)
+              if (m > st_best || m != m) { st_best = m; st_row = (long long)(row - lane) + (__ffs(who) - 1); }
+            }
+          }
+        }
         if (row < args.n) {
           float* o = args.out + (int64_t)(f0 + cb) * args.ldo + row;
           const int jn = min(32, args.nf - (f0 + cb));
@@ -365,6 +388,11 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_l[acc]);
     }
+    if constexpr (STATS && !PLANES && TMAO == 0) {
+      const size_t slot = ((size_t)blockIdx.x * tc2::EPI + (warp - 2)) * 32 + lane;
+      args.st_max[slot] = st_best;
+      args.st_idx[slot] = st_row;
+    }
   }
   if constexpr (TMAO == 1 && !PLANES)
     if (warp >= 2) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores complete
@@ -375,6 +403,33 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS));
   }
+}
+
+// Combine the fused statistics of tc_decode2_kernel<.., STATS>: column pair u
+// (columns 2u, 2u + 1) lives in frame tile ft = 2u / 256, epilogue part
+// (2u % 256) / 64, lane ((2u % 64) / 2); candidates are the 4 quadrant warps of
+// that part in every CTA of the tile (CTA x: pid = x >> 1, tile pid % gy).
+// st[u] = {untouched, max, first row attaining it + row_offset} (ties: lowest row).
+__global__ void tc2_pair_stats_final_kernel(const double* __restrict__ st_max, const long long* __restrict__ st_idx,
+                                            int nctas, int gy, int units, long long row_offset,
+                                            double* __restrict__ st) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= units) return;
+  const int f = 2 * u, ft = f / tc2::BN, part = (f % tc2::BN) / (tc2::BN / (tc2::EPI / 4)), lane = (f % 64) >> 1;
+  double best = -1.0;
+  long long row = 0;
+  for (int x = 0; x < nctas; ++x) {
+    if (((x >> 1) % gy) != ft) continue;
+    for (int q = 0; q < 4; ++q) {
+      const size_t slot = ((size_t)x * tc2::EPI + part * 4 + q) * 32 + lane;
+      const double m = st_max[slot];
+      const long long r = st_idx[slot];
+      if (best != best) continue;   // NaN seen: keep it
+      if (m != m || m > best || (m == best && r < row)) { best = m; row = r; }
+    }
+  }
+  st[3 * u + 1] = best;
+  st[3 * u + 2] = (double)(row + row_offset);
 }
 
 }  // namespace fdmd

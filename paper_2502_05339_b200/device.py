@@ -377,6 +377,35 @@ class CudaOps:
         self.launches += 2
         return out
 
+    def tc_decode_pairstats(self, tcb: dict, coef: torch.Tensor, out: torch.Tensor, units: int,
+                            row_offset: int = 0) -> Optional[torch.Tensor]:
+        """tc_decode of a modes product (columns 2u, 2u+1 = Re, Im of mode u) whose
+        frame epilogue also takes max_i |phi_u[i]|^2 and the first row attaining it
+        (the statistics pair_stats reads back from the table). Returns st (units x 3
+        f64, column 0 left at zero for the caller) or None when the batch is too
+        narrow for the CTA-pair kernel (the frames are still written)."""
+        r, n = tcb["r"], tcb["n"]
+        coef = coef.to(torch.float32).contiguous()
+        B = int(coef.shape[1])
+        assert B == 2 * units
+        ldk = round_up(r, 8)
+        dev = coef.device
+        ch = torch.empty((B, ldk), dtype=torch.float16, device=dev)
+        cl = torch.empty_like(ch)
+        fs = torch.empty((B,), dtype=torch.float32, device=dev)
+        st = torch.zeros((units, 3), dtype=torch.float64, device=dev)
+        fused = ctypes.c_int(0)
+        e0 = self._ev()
+        L = _lib.lib()
+        _lib.check(L.fdmd_split_coef(_ptr(coef), coef.stride(0), r, B, ctypes.c_float(1.0 / tcb["su"]), _ptr(ch),
+                                     _ptr(cl), ldk, _ptr(fs), _stream()), "split_coef")
+        _lib.check(L.fdmd_tc_decode_pairstats(_ptr(tcb["uh"]), _ptr(tcb["ul"]), tcb["ldu"], n, r, _ptr(ch), _ptr(cl),
+                                              ldk, B, _ptr(fs), _ptr(out), out.stride(0), int(row_offset), _ptr(st),
+                                              ctypes.byref(fused), _stream()), "tc_decode_pairstats")
+        self._done("tc_decode", 2.0 * n * r * B, e0)
+        self.launches += 3 if fused.value else 2
+        return st if fused.value else None
+
     def tc_decode_planes(self, tcb: dict, coef: torch.Tensor, bound: float = 2.0, share_sms: bool = False) -> dict:
         """basis @ coef (r x k, k <= 256) on tcgen05, written straight into the
         fp16 hi/lo planes of a row-major n x round_up(k, 8) matrix (the lift

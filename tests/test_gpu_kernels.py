@@ -354,6 +354,40 @@ def test_tall_gram_bordered(dv, n, K, dt):
     np.testing.assert_allclose(G[:, K].cpu().numpy(), y.cpu().numpy(), rtol=1e-12, atol=tol)
 
 
+@pytest.mark.parametrize("n,r,units", [(300007, 200, 100), (70001, 150, 75), (256 * 148 * 3, 64, 100), (5000, 200, 40)])
+def test_tc_decode_fused_pair_stats(dv, n, r, units):
+    """The modes product's frame epilogue also takes max_i |phi_u[i]|^2 and the
+    first row attaining it (fdmd_tc_decode_pairstats): bitwise equal to
+    pair_stats over the written table, frames identical to plain tc_decode;
+    batches of <= 128 columns report `not fused` (None)."""
+    rng = np.random.default_rng(n + units)
+    ops = dv.get_ops()
+    Ut = _tall_from(dv, rng.standard_normal((n, r)).astype(np.float32) / np.sqrt(n), "col", torch.float32)
+    tcb = ops.tc_basis(Ut)
+    coef = torch.as_tensor(rng.standard_normal((r, 2 * units)), device="cuda")
+    raw = dv.alloc_tall(n, 2 * units, torch.float32, "col")
+    ref = dv.alloc_tall(n, 2 * units, torch.float32, "col")
+    ops.tc_decode(tcb, coef, out=ref.buf[: 2 * units])
+    st = ops.tc_decode_pairstats(tcb, coef, raw.buf[: 2 * units], units, row_offset=17)
+    if 2 * units <= 128:
+        assert st is None
+        assert torch.equal(raw.buf[: 2 * units, :n], ref.buf[: 2 * units, :n])
+        return
+    assert st is not None and torch.equal(raw.buf[: 2 * units, :n], ref.buf[: 2 * units, :n])
+    want = ops.pair_stats(ref, units, row_offset=17)
+    assert torch.equal(st[:, 1], want[:, 1]) and torch.equal(st[:, 2], want[:, 2]), (st[:4], want[:4])
+    assert float(st[:, 0].abs().max()) == 0.0
+    # planted ties: the first row wins
+    raw.buf[: 2 * units].zero_()
+    Z = torch.zeros((n, r), dtype=torch.float32)
+    Z[5, 0] = Z[n - 3, 0] = 1.0
+    tz = ops.tc_basis(_tall_from(dv, Z.numpy(), "col", torch.float32))
+    c2 = torch.zeros((r, 2 * units), dtype=torch.float64, device="cuda")
+    c2[0, :] = 1.0
+    st2 = ops.tc_decode_pairstats(tz, c2, raw.buf[: 2 * units], units)
+    assert torch.all(st2[:, 2] == 5.0) and torch.all(st2[:, 1] == 2.0)
+
+
 @pytest.mark.parametrize("l,T,cond", [(200, 200, 1.2e4), (160, 201, 1e6), (20, 100, 10.0), (1, 5, 1.0)])
 def test_svd_small_gesvdp(dv, l, T, cond):
     """fdmd_svd_small (cuSOLVER gesvdp, stream-ordered): the thin SVD of the fit's
