@@ -200,9 +200,9 @@ int fdmd_tc_decode_ex(const void* uh, const void* ul, int64_t ldu, int64_t n, in
 /* fdmd_tc_decode of a modes product (columns 2u, 2u+1 = Re, Im of mode u; `U @ B.T`, reference
  * dmd.py:414) with the normalisation / phase-pivot statistics of `_order_and_pair`
  * (dmd.py:189-206: the first largest-|.| entry of each mode) taken in the frame epilogue:
- * st[3u + 1] = max_i |phi_u[i]|^2, st[3u + 2] = first row attaining it + row_offset
- * (st[3u] is left to the caller: the squared norm follows from the coefficients of an
- * orthonormal basis). *fused = 1 when the CTA-pair kernel ran (nf > 128) and filled st;
+ * st[3u] = sum_i |phi_u[i]|^2 (f64 running sums of f32 32-row partials), st[3u + 1] =
+ * max_i |phi_u[i]|^2, st[3u + 2] = first row attaining it + row_offset — what
+ * fdmd_pair_stats reads back from the table. *fused = 1 when the CTA-pair kernel ran (nf > 128) and filled st;
  * 0 = frames only (the caller then runs fdmd_pair_stats over the table). */
 int fdmd_tc_decode_pairstats(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch,
                              const void* cl, int ldk, int nf, const float* fscale, float* out, int64_t ldo,

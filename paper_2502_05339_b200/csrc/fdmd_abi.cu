@@ -859,16 +859,17 @@ int launch_tc_decode_pair(const void* uh, const void* ul, int64_t ldu, int64_t n
   void* stbuf = nullptr;
   if (st) {
     const size_t slots = (size_t)nctas * fdmd::tc2::EPI * 32;
-    CUDA_TRY(scratch_alloc(&stbuf, slots * (sizeof(long long) + sizeof(double)), (cudaStream_t)stream));
+    CUDA_TRY(scratch_alloc(&stbuf, slots * (sizeof(long long) + 2 * sizeof(double)), (cudaStream_t)stream));
     ta.st_idx = static_cast<long long*>(stbuf);
     ta.st_max = reinterpret_cast<double*>(ta.st_idx + slots);
+    ta.st_sum = ta.st_max + slots;
   }
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], omap, ta));
   LAUNCH_CHECK("tc_decode2");
   if (st) {
     const int units = nf / 2;
     fdmd::tc2_pair_stats_final_kernel<<<(units + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
-        ta.st_max, ta.st_idx, nctas, gy, units, (long long)row_offset, st);
+        ta.st_max, ta.st_idx, ta.st_sum, nctas, gy, units, (long long)row_offset, st);
     LAUNCH_CHECK("tc2_pair_stats_final");
     cudaFreeAsync(stbuf, (cudaStream_t)stream);
   }
@@ -1556,7 +1557,7 @@ int fdmd_tc_decode_ex(const void* uh, const void* ul, int64_t ldu, int64_t n, in
 
 // fdmd_tc_decode of a modes product (column pairs (2u, 2u + 1) = (Re, Im) of mode u) with the
 // normalisation / phase-pivot statistics of _order_and_pair fused into the frame epilogue:
-// st[u] = {unchanged, max_i |phi_u[i]|^2, first row attaining it + row_offset}. *fused = 1 when
+// st[u] = {sum_i |phi_u[i]|^2, max_i |phi_u[i]|^2, first row attaining it + row_offset}. *fused = 1 when
 // the CTA-pair kernel ran (nf > 128) and filled st; 0 = frames only (run fdmd_pair_stats).
 int fdmd_tc_decode_pairstats(const void* uh, const void* ul, int64_t ldu, int64_t n, int r, const void* ch,
                              const void* cl, int ldk, int nf, const float* fscale, float* out, int64_t ldo,

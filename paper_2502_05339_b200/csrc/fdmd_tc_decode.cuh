@@ -132,9 +132,10 @@ struct TCArgs {
   int64_t ldp = 0;
   float pscale = 1.f;
   // fused column-pair statistics (CTA-pair kernel, frame output): per CTA and
-  // epilogue warp, 32 lane-owned (max |phi|^2, first row attaining it) entries
+  // epilogue warp, 32 entries (sum |phi|^2, max |phi|^2, first row attaining it)
   // for the warp's 32 column pairs; tc2_pair_stats_final_kernel combines them
   double* st_max = nullptr;
+  double* st_sum = nullptr;
   long long* st_idx = nullptr;
 };
 

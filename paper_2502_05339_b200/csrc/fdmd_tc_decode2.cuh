@@ -232,7 +232,7 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
     // STATS: lane L owns column pair L of the warp's 64 columns (the (Re, Im) columns
     // of one mode): running max of re^2 + im^2 over the warp's rows and the first
     // row attaining it (tiles arrive in increasing row order; strict > keeps the first)
-    double st_best = -1.0;
+    double st_best = -1.0, st_sum0 = 0.0, st_sum1 = 0.0;   // sums: pairs lane / 2 and 16 + lane / 2
     long long st_row = 0;
     for (int64_t t = 0; t < my_tiles; ++t) {
       const int acc = (int)(t & 1);
@@ -347,6 +347,7 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
         }
         if constexpr (STATS) {
           const bool live = row < args.n;
+          float wf[16];
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
             // the stored values, squared in f64 exactly as pair_stats_kernel does
@@ -361,7 +362,23 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
               const double m = __hiloint2double((int)mh, (int)ml);   // a NaN wins once and stays (reported downstream)
               if (m > st_best || m != m) { st_best = m; st_row = (long long)(row - lane) + (__ffs(who) - 1); }
             }
+            wf[u] = live ? (float)w : 0.f;
           }
+          // sum over the warp's 32 rows of all 16 pairs at once (transposing butterfly:
+          // 16 shuffles): lanes 2p, 2p + 1 end up with pair p's total. f32 is enough
+          // for a 32-row partial (it only feeds the f64 running sum of the norm)
+#pragma unroll
+          for (int b = 4; b >= 1; --b) {
+            const int half = 1 << (b - 1);
+            const bool up = (lane >> b) & 1;
+#pragma unroll
+            for (int j = 0; j < half; ++j) {
+              const float send = up ? wf[j] : wf[j + half], keep = up ? wf[j + half] : wf[j];
+              wf[j] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << b);
+            }
+          }
+          const float tot = wf[0] + __shfl_xor_sync(0xffffffffu, wf[0], 1);
+          if (cb == c_lo) st_sum0 += (double)tot; else st_sum1 += (double)tot;
         }
         if (row < args.n) {
           float* o = args.out + (int64_t)(f0 + cb) * args.ldo + row;
@@ -392,6 +409,10 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
       const size_t slot = ((size_t)blockIdx.x * tc2::EPI + (warp - 2)) * 32 + lane;
       args.st_max[slot] = st_best;
       args.st_idx[slot] = st_row;
+      if ((lane & 1) == 0) {
+        args.st_sum[slot - lane + (lane >> 1)] = st_sum0;
+        args.st_sum[slot - lane + 16 + (lane >> 1)] = st_sum1;
+      }
     }
   }
   if constexpr (TMAO == 1 && !PLANES)
@@ -409,25 +430,27 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
 // (columns 2u, 2u + 1) lives in frame tile ft = 2u / 256, epilogue part
 // (2u % 256) / 64, lane ((2u % 64) / 2); candidates are the 4 quadrant warps of
 // that part in every CTA of the tile (CTA x: pid = x >> 1, tile pid % gy).
-// st[u] = {untouched, max, first row attaining it + row_offset} (ties: lowest row).
+// st[u] = {sum, max, first row attaining it + row_offset} (ties: lowest row).
 __global__ void tc2_pair_stats_final_kernel(const double* __restrict__ st_max, const long long* __restrict__ st_idx,
-                                            int nctas, int gy, int units, long long row_offset,
-                                            double* __restrict__ st) {
+                                            const double* __restrict__ st_sum, int nctas, int gy, int units,
+                                            long long row_offset, double* __restrict__ st) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= units) return;
   const int f = 2 * u, ft = f / tc2::BN, part = (f % tc2::BN) / (tc2::BN / (tc2::EPI / 4)), lane = (f % 64) >> 1;
-  double best = -1.0;
+  double best = -1.0, sum = 0.0;
   long long row = 0;
   for (int x = 0; x < nctas; ++x) {
     if (((x >> 1) % gy) != ft) continue;
     for (int q = 0; q < 4; ++q) {
       const size_t slot = ((size_t)x * tc2::EPI + part * 4 + q) * 32 + lane;
+      sum += st_sum[slot];                                   // fixed order: deterministic
       const double m = st_max[slot];
       const long long r = st_idx[slot];
       if (best != best) continue;   // NaN seen: keep it
       if (m != m || m > best || (m == best && r < row)) { best = m; row = r; }
     }
   }
+  st[3 * u] = sum;
   st[3 * u + 1] = best;
   st[3 * u + 2] = (double)(row + row_offset);
 }

@@ -381,9 +381,9 @@ class CudaOps:
                             row_offset: int = 0) -> Optional[torch.Tensor]:
         """tc_decode of a modes product (columns 2u, 2u+1 = Re, Im of mode u) whose
         frame epilogue also takes max_i |phi_u[i]|^2 and the first row attaining it
-        (the statistics pair_stats reads back from the table). Returns st (units x 3
-        f64, column 0 left at zero for the caller) or None when the batch is too
-        narrow for the CTA-pair kernel (the frames are still written)."""
+        and the sum of |phi_u|^2 (the statistics pair_stats reads back from the
+        table). Returns st (units x 3 f64) or None when the batch is too narrow for
+        the CTA-pair kernel (the frames are still written)."""
         r, n = tcb["r"], tcb["n"]
         coef = coef.to(torch.float32).contiguous()
         B = int(coef.shape[1])

@@ -293,7 +293,6 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
         raw = alloc_tall(n_loc, 2 * U, table_dtype, "col", device=dev)
     row0 = 0 if shard is None else shard.row0
     t0 = time.perf_counter()
-    fused_norm2 = None
     # SURVEY §8d counts F_modes = 4 n K r (real n x K times complex K x r); only
     # one column of each conjugate pair is executed, so the kernel is credited
     # with its executed 2 n K (2U) flops (the fit-level metric keeps the formula)
@@ -301,17 +300,11 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
         if tc_src is not None:
             M = Bm if tc_src.get("Umap") is None else tc_src["Umap"] @ Bm
             coef = M.to(torch.float32)                                       # (l | m) x 2U
-            st = None
-            if a_orthonormal and hasattr(ops, "tc_decode_pairstats"):
-                # max |phi|^2 and its first row come out of the frame epilogue; the
-                # squared norm is the coefficients' (phi = U c with U orthonormal:
-                # ||phi||^2 = ||c||^2), so no statistics pass re-reads the table
-                st = ops.tc_decode_pairstats(tc_src["planes"], coef, raw.buf[: 2 * U], U, row_offset=row0)
-                fused_norm2 = (Bm[:, 0::2] ** 2 + Bm[:, 1::2] ** 2).sum(dim=0) if st is not None else None
-            else:
-                ops.tc_decode(tc_src["planes"], coef, out=raw.buf[: 2 * U])
+            # sum / max / first argmax of |phi|^2 come out of the frame epilogue when
+            # the CTA-pair kernel runs (> 128 columns); otherwise a statistics pass
+            # reads the table back
+            st = ops.tc_decode_pairstats(tc_src["planes"], coef, raw.buf[: 2 * U], U, row_offset=row0)
             if st is None:
-                fused_norm2 = None
                 st = ops.pair_stats(raw, U, row_offset=row0)
         else:
             st = ops.tall_gemm(A, Bm, raw, stats=True, row_offset=row0,
@@ -319,8 +312,6 @@ def _modes_pass(A: Tall, Cmap: torch.Tensor, plan: PairPlan, row_pad_top: int, s
     post = stage("modes.post")
     post.__enter__()
     st = la._reduce_pair_stats(st, shard)
-    if fused_norm2 is not None:
-        st[:, 0] = fused_norm2            # global already (small matrices, identical on every rank)
     nrm = torch.sqrt(st[:, 0])
     idx = st[:, 2].round().long()
     # pivot values raw[idx] (gathered from the owning shard)
