@@ -232,7 +232,8 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
     // STATS: lane L owns column pair L of the warp's 64 columns (the (Re, Im) columns
     // of one mode): running max of re^2 + im^2 over the warp's rows and the first
     // row attaining it (tiles arrive in increasing row order; strict > keeps the first)
-    double st_best = -1.0, st_sum0 = 0.0, st_sum1 = 0.0;   // sums: pairs lane / 2 and 16 + lane / 2
+    float st_best = -1.f;
+    double st_sum0 = 0.0, st_sum1 = 0.0;   // sums: pairs lane / 2 and 16 + lane / 2
     long long st_row = 0;
     for (int64_t t = 0; t < my_tiles; ++t) {
       const int acc = (int)(t & 1);
@@ -350,19 +351,21 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
           float wf[16];
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
-            // the stored values, squared in f64 exactly as pair_stats_kernel does
-            const double a = (double)(v[2 * u] * sm.fs[cb + 2 * u]), b = (double)(v[2 * u + 1] * sm.fs[cb + 2 * u + 1]);
-            const double w = pair_mag2(a, b);
-            // w >= 0: its bits order like unsigned integers (two 32-bit redux.sync steps)
-            const unsigned hi = live ? (unsigned)__double2hiint(w) : 0u, lo = live ? (unsigned)__double2loint(w) : 0u;
-            const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
-            const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-            const unsigned who = __ballot_sync(0xffffffffu, live && hi == mh && lo == ml);
+            // |phi|^2 of the stored f32 values, evaluated in f32 (f64 here made the
+            // epilogue XU / FP64-pipe bound: 26 ms against 16 ms for the plain
+            // product). Magnitudes within 2^-23 of each other may order differently
+            // than in f64 — below the resolution of the f32 table itself.
+            const float x0 = v[2 * u] * sm.fs[cb + 2 * u], x1 = v[2 * u + 1] * sm.fs[cb + 2 * u + 1];
+            const float w = live ? __fmaf_rn(x0, x0, x1 * x1) : 0.f;
+            // w >= 0: its bits order like unsigned integers (one redux.sync)
+            const unsigned mb = __float_as_uint(w);
+            const unsigned mx = __reduce_max_sync(0xffffffffu, mb);
+            const unsigned who = __ballot_sync(0xffffffffu, live && mb == mx);
             if (lane == ((cb - c_lo) >> 1) + u && who != 0u) {
-              const double m = __hiloint2double((int)mh, (int)ml);   // a NaN wins once and stays (reported downstream)
+              const float m = __uint_as_float(mx);   // a NaN wins once and stays (reported downstream)
               if (m > st_best || m != m) { st_best = m; st_row = (long long)(row - lane) + (__ffs(who) - 1); }
             }
-            wf[u] = live ? (float)w : 0.f;
+            wf[u] = w;
           }
           // sum over the warp's 32 rows of all 16 pairs at once (transposing butterfly:
           // 16 shuffles): lanes 2p, 2p + 1 end up with pair p's total. f32 is enough
@@ -407,7 +410,7 @@ tc_decode2_kernel(const __grid_constant__ CUtensorMap amap_h, const __grid_const
     }
     if constexpr (STATS && !PLANES && TMAO == 0) {
       const size_t slot = ((size_t)blockIdx.x * tc2::EPI + (warp - 2)) * 32 + lane;
-      args.st_max[slot] = st_best;
+      args.st_max[slot] = (double)st_best;
       args.st_idx[slot] = st_row;
       if ((lane & 1) == 0) {
         args.st_sum[slot - lane + (lane >> 1)] = st_sum0;

@@ -375,8 +375,15 @@ def test_tc_decode_fused_pair_stats(dv, n, r, units):
         return
     assert st is not None and torch.equal(raw.buf[: 2 * units, :n], ref.buf[: 2 * units, :n])
     want = ops.pair_stats(ref, units, row_offset=17)
-    assert torch.equal(st[:, 1], want[:, 1]) and torch.equal(st[:, 2], want[:, 2]), (st[:4], want[:4])
-    np.testing.assert_allclose(st[:, 0].cpu().numpy(), want[:, 0].cpu().numpy(), rtol=2e-7)
+    # the fused magnitudes are evaluated in f32: the maximum agrees to f32 rounding and
+    # the argmax is a row whose f64 magnitude is within that rounding of the maximum
+    np.testing.assert_allclose(st[:, 1].cpu().numpy(), want[:, 1].cpu().numpy(), rtol=3e-7)
+    rows = (st[:, 2] - 17).long()
+    ar = torch.arange(units, device="cuda")
+    mag = ref.buf[2 * ar, rows].double() ** 2 + ref.buf[2 * ar + 1, rows].double() ** 2
+    assert torch.all(mag >= want[:, 1] * (1 - 3e-7))
+    assert float((st[:, 2] == want[:, 2]).double().mean()) >= 0.98
+    np.testing.assert_allclose(st[:, 0].cpu().numpy(), want[:, 0].cpu().numpy(), rtol=3e-7)
     # planted ties: the first row wins
     raw.buf[: 2 * units].zero_()
     Z = torch.zeros((n, r), dtype=torch.float32)
